@@ -1,0 +1,164 @@
+/*
+ * ltl_b200.h -- C-ABI of the B200-native Larger-than-Life step library
+ * (paper_2406_17284_b200/libltl_b200.so).
+ *
+ * This is the drop-in boundary.  The reference has no FFI or plugin registry:
+ * its engines form a closed enum + switch (proj/include/catsim/engines.hpp:11,
+ * proj/src/engines.cpp:26-46) and the hot path is the C++ call chain
+ *   run_engine(EngineKind::Cat, ...)   proj/src/engines.cpp:26-36
+ *     -> simulate(...)                 proj/src/cat_engine.cpp:308-321
+ *       -> simulate_step(...)          proj/src/cat_engine.cpp:260-306
+ * Every entry point below replaces one piece of that chain with plain C types
+ * (pointers + sizes, no torch, no C++ types), so any host language can bind it:
+ * the C++ catsim API of this repo (include/catsim/ headers) sits on top of it, and
+ * INTEGRATION.md shows the ctypes / cgo / JNI stubs.
+ *
+ * Errors: every int-returning call returns LTL_OK or one of the LTL_ERR_*
+ * codes, which map 1:1 onto the reference's exception classes; the message
+ * (same stable prefixes as the reference: "config error:", "geometry error:",
+ * "layout error:", "unsupported rule", "rule parse error: field X",
+ * "internal consistency: negative neighborhood count", ...) is available from
+ * ltl_last_error().  A context is not thread-safe; use one per host thread.
+ */
+#ifndef LTL_B200_H
+#define LTL_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define LTL_ABI_VERSION 1
+
+/* status codes <-> reference exception classes */
+#define LTL_OK 0
+#define LTL_ERR_INVALID_ARGUMENT 1 /* std::invalid_argument */
+#define LTL_ERR_LOGIC 2            /* std::logic_error (sequencing / consistency) */
+#define LTL_ERR_RUNTIME 3          /* std::runtime_error */
+#define LTL_ERR_CUDA 4             /* device failure (no reference analogue) */
+
+/* catsim::Layout, proj/include/catsim/grid.hpp:14 */
+#define LTL_LAYOUT_ROW_MAJOR 0
+#define LTL_LAYOUT_FRAGMENT 1
+
+/* catsim::NeighborhoodKind, proj/include/catsim/rule.hpp:13 */
+#define LTL_KIND_MOORE 0
+#define LTL_KIND_VON_NEUMANN 1
+
+/* ltl_run flags */
+#define LTL_FLAG_INJECT_FAULT 0x1u  /* CatConfig.inject_band_fault, cat_engine.hpp:22-24 */
+#define LTL_FLAG_WANT_STATS 0x2u    /* fill ltl_stats_c (device max-reduction of H / R) */
+#define LTL_FLAG_STENCIL 0x4u       /* run the CUDA-core stencil ablation, not tcgen05 */
+#define LTL_FLAG_NO_GRAPH 0x8u      /* launch step by step instead of a captured CUDA graph */
+
+/* catsim::LtlRule, proj/include/catsim/rule.hpp:17-32 */
+typedef struct ltl_rule_c {
+  int32_t r, c, m, s1, s2, b1, b2, kind;
+} ltl_rule_c;
+
+/* catsim::CatStats, proj/include/catsim/cat_engine.hpp:29-38 (mma_count in
+ * the reference's 16x16-fragment units, so the numbers match its counters). */
+typedef struct ltl_stats_c {
+  int64_t mma_count;
+  int64_t steps;
+  int32_t max_h;
+  int32_t max_r;
+  int32_t fragments_per_row;
+  int32_t reserved;
+} ltl_stats_c;
+
+typedef struct ltl_ctx ltl_ctx;
+
+/* --- context (device grid) ---------------------------------------------- */
+
+/* Square n x n torus with fragment side f (4, 8, 16), split into `num_slabs`
+ * row slabs on devices dev_ids[0..num_slabs) (NULL -> slab i on device
+ * i % device_count).  Replaces make_grid (src/grid.cpp:41-49) + the second
+ * ping-pong buffer simulate allocates (src/cat_engine.cpp:313).  Errors as
+ * make_grid: "geometry error: n (..) must be a non-negative multiple of f (..)". */
+int ltl_create(ltl_ctx** out, int32_t n, int32_t f, int32_t num_slabs, const int32_t* dev_ids);
+
+/* Rectangular rows x cols torus (weak-scaling extension: the reference Grid
+ * is square only, grid.hpp:53-54).  f = 16 semantics (any rows, cols >= 1). */
+int ltl_create_torus(ltl_ctx** out, int32_t rows, int32_t cols, int32_t num_slabs,
+                     const int32_t* dev_ids);
+
+void ltl_destroy(ltl_ctx* ctx);
+const char* ltl_last_error(const ltl_ctx* ctx); /* "" after success; never NULL */
+
+/* Geometry queries. */
+int32_t ltl_rows(const ltl_ctx* ctx);
+int32_t ltl_cols(const ltl_ctx* ctx);
+int32_t ltl_num_slabs(const ltl_ctx* ctx);
+
+/* --- host <-> device (copies; no host pointer is retained) --------------- */
+
+/* Padded (n+2f)^2 host grid in the given layout (catsim::Grid::cells); only
+ * the interior is read -- the device refreshes its own periodic halo, which is
+ * what simulate_step does first anyway (src/cat_engine.cpp:275). */
+int ltl_upload(ltl_ctx* ctx, const uint8_t* padded, int32_t layout);
+/* Writes the padded grid: interior = current generation, halo = its periodic
+ * image (callers may treat it as stale, as the reference does after a step). */
+int ltl_download(ltl_ctx* ctx, uint8_t* padded, int32_t layout);
+/* Dense rows x cols interior, row-major (no halo). */
+int ltl_upload_interior(ltl_ctx* ctx, const uint8_t* interior);
+int ltl_download_interior(ltl_ctx* ctx, uint8_t* interior);
+
+/* --- the hot path --------------------------------------------------------- */
+
+/* `steps` generations (simulate, src/cat_engine.cpp:308-321), each one fused
+ * tcgen05 launch per slab + halo exchange.  Validation and messages as the
+ * reference: steps < 0 -> "config error: steps must be >= 0"; rule checks of
+ * src/rule.cpp:32-57; r > f -> "unsupported radius r=.. for fragment side
+ * f=.." (src/fragment.cpp:25-27); negative count (fault injection) ->
+ * LTL_ERR_LOGIC "internal consistency: negative neighborhood count".
+ * stats may be NULL.  Synchronous. */
+int ltl_run(ltl_ctx* ctx, const ltl_rule_c* rule, int32_t steps, uint32_t flags,
+            ltl_stats_c* stats);
+
+/* Asynchronous variant for pipelines: enqueues `steps` generations on the
+ * context's streams and returns (no stats, no error readback). */
+int ltl_run_async(ltl_ctx* ctx, const ltl_rule_c* rule, int32_t steps, uint32_t flags);
+int ltl_synchronize(ltl_ctx* ctx);
+
+/* Device timing with CUDA events on the slab streams (max over slabs):
+ * `warmup` untimed generations then `steps` timed ones.  total_ms covers the
+ * whole generation loop; kernel_ms sums only the main step kernel launches
+ * (the roofline kernel).  Either output pointer may be NULL. */
+int ltl_time(ltl_ctx* ctx, const ltl_rule_c* rule, int32_t steps, int32_t warmup,
+             uint32_t flags, double* total_ms, double* kernel_ms);
+
+/* End-to-end: upload interior from host memory, run `steps` generations,
+ * download the interior into `interior_out` -- the whole run_engine(Cat)
+ * contract (src/engines.cpp:26-36) in one call. */
+int ltl_run_interior(ltl_ctx* ctx, const uint8_t* interior_in, uint8_t* interior_out,
+                     const ltl_rule_c* rule, int32_t steps, uint32_t flags, ltl_stats_c* stats);
+
+/* --- multi-process slabs (one process per GPU) --------------------------- */
+
+/* Device pointers of slab `slab`'s current generation buffer and its pitch;
+ * for exchanging halos through an external transport (NCCL, IPC). */
+int ltl_slab_buffer(ltl_ctx* ctx, int32_t slab, int32_t which, void** dev_ptr, int64_t* pitch,
+                    int32_t* rows);
+
+/* --- host-side rule helpers (pure C, no device) --------------------------- */
+
+/* parse_ltl_rule (src/rule.cpp:61-87): returns LTL_OK or
+ * LTL_ERR_INVALID_ARGUMENT with the reference's message in err (may be NULL). */
+int ltl_parse_rule(const char* text, ltl_rule_c* out, char* err, int32_t err_len);
+/* format_ltl_rule (src/rule.cpp:89-97); returns the string length. */
+int32_t ltl_format_rule(const ltl_rule_c* rule, char* buf, int32_t buf_len);
+/* ltl_presets (src/rule.cpp:113-133): count, then entries by index. */
+int32_t ltl_preset_count(void);
+int ltl_preset(int32_t index, const char** name, const char** rule, double* density);
+/* von_neumann_probe_rule (src/rule.cpp:142-152). */
+void ltl_von_neumann_probe_rule(int32_t r, ltl_rule_c* out);
+
+/* Library identity (also proves the .so was loaded). */
+const char* ltl_build_info(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

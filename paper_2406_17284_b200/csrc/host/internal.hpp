@@ -1,0 +1,40 @@
+// internal.hpp -- declarations shared between the host-side translation units
+// of libltl_b200.so (not part of the public API).
+#pragma once
+
+#include "catsim/rule.hpp"
+#include "ltl_b200.h"
+
+namespace catsim {
+
+// The reference's rule validation (src/rule.cpp:32-57), throwing the same
+// std::invalid_argument messages.
+void validate_rule(const LtlRule& rule);
+
+inline LtlRule from_c(const ltl_rule_c& c) {
+  LtlRule r;
+  r.r = c.r;
+  r.c = c.c;
+  r.m = c.m;
+  r.s1 = c.s1;
+  r.s2 = c.s2;
+  r.b1 = c.b1;
+  r.b2 = c.b2;
+  r.kind = c.kind == LTL_KIND_MOORE ? NeighborhoodKind::Moore : NeighborhoodKind::VonNeumannSimplified;
+  return r;
+}
+
+inline ltl_rule_c to_c(const LtlRule& r) {
+  ltl_rule_c c;
+  c.r = r.r;
+  c.c = r.c;
+  c.m = r.m;
+  c.s1 = r.s1;
+  c.s2 = r.s2;
+  c.b1 = r.b1;
+  c.b2 = r.b2;
+  c.kind = r.kind == NeighborhoodKind::Moore ? LTL_KIND_MOORE : LTL_KIND_VON_NEUMANN;
+  return c;
+}
+
+}  // namespace catsim

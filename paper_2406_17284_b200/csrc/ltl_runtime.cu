@@ -1,0 +1,539 @@
+// ltl_runtime.cu -- implementation of the C-ABI in include/ltl_b200.h.
+//
+// Owns the device side of a run: the halo-padded slab buffers (two
+// generations each), the TMA tensor maps, per-slab streams and the
+// generation loop that replaces simulate / simulate_step
+// (proj/src/cat_engine.cpp:260-321).  No CPU fallback exists: without a
+// working device every call fails with LTL_ERR_CUDA.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <exception>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "host/internal.hpp"
+#include "ltl_b200.h"
+#include "ltl_kernels.cuh"
+
+using ltl::kHalo;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+struct CudaFailure : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+void ck(cudaError_t e, const char* what) {
+  if (e != cudaSuccess)
+    throw CudaFailure(std::string("cuda error: ") + what + ": " + cudaGetErrorString(e));
+}
+
+struct Slab {
+  int dev = 0;
+  int32_t row0 = 0, rows = 0;
+  int64_t pitch = 0;
+  uint8_t* buf[2] = {nullptr, nullptr};
+  CUtensorMap load_map[2];
+  CUtensorMap store_map[2];
+  ltl::DeviceStats* dstats = nullptr;
+  cudaStream_t stream = nullptr;
+  bool own_stream = true;
+  cudaEvent_t ev_step = nullptr;
+  std::vector<cudaEvent_t> timing;
+
+  ltl::SlabView view(int which, int32_t cols) const {
+    return ltl::SlabView{buf[which], rows, cols, pitch};
+  }
+};
+
+}  // namespace
+
+struct ltl_ctx {
+  int32_t rows = 0, cols = 0, f = 16;
+  int cur = 0;
+  bool external_row_halo = false;
+  std::vector<Slab> slabs;
+  std::string err;
+};
+
+namespace {
+
+int status_of(const std::exception& e) {
+  if (dynamic_cast<const CudaFailure*>(&e)) return LTL_ERR_CUDA;
+  if (dynamic_cast<const std::invalid_argument*>(&e)) return LTL_ERR_INVALID_ARGUMENT;
+  if (dynamic_cast<const std::out_of_range*>(&e)) return LTL_ERR_INVALID_ARGUMENT;
+  if (dynamic_cast<const std::logic_error*>(&e)) return LTL_ERR_LOGIC;
+  return LTL_ERR_RUNTIME;
+}
+
+template <typename Fn>
+int guarded(ltl_ctx* ctx, Fn&& fn) {
+  try {
+    fn();
+    if (ctx) ctx->err.clear();
+    g_last_error.clear();
+    return LTL_OK;
+  } catch (const std::exception& e) {
+    if (ctx) ctx->err = e.what();
+    g_last_error = e.what();
+    return status_of(e);
+  }
+}
+
+ltl::RuleConsts rule_consts(const ltl_rule_c& r) {
+  const int mult = r.kind == LTL_KIND_MOORE ? 1 : 2;
+  ltl::RuleConsts c{};
+  c.r = r.r;
+  c.kind = r.kind == LTL_KIND_MOORE ? 0 : 1;
+  c.lo_dead = r.b1;
+  c.w_dead = r.b2 - r.b1;
+  c.lo_live = r.s1 + (mult - r.m);
+  c.w_live = r.s2 - r.s1;
+  c.neg_live = mult - r.m;
+  return c;
+}
+
+void check_run_args(const ltl_ctx* ctx, const ltl_rule_c* rule, int32_t steps) {
+  if (!rule) throw std::invalid_argument("config error: rule is null");
+  if (steps < 0) throw std::invalid_argument("config error: steps must be >= 0");
+  catsim::validate_rule(catsim::from_c(*rule));
+  if (rule->r < 1 || rule->r > ctx->f)
+    throw std::invalid_argument("unsupported radius r=" + std::to_string(rule->r) +
+                                " for fragment side f=" + std::to_string(ctx->f));
+}
+
+int64_t round_up(int64_t v, int64_t a) { return (v + a - 1) / a * a; }
+
+void build_maps(Slab& s, int32_t cols) {
+  for (int i = 0; i < 2; ++i) {
+    ck(ltl::make_load_map(&s.load_map[i], s.view(i, cols)), "tensor map (load)");
+    ck(ltl::make_store_map(&s.store_map[i], s.view(i, cols)), "tensor map (store)");
+  }
+}
+
+void create_slabs(ltl_ctx* ctx, int32_t num_slabs, const int32_t* dev_ids) {
+  int ndev = 0;
+  ck(cudaGetDeviceCount(&ndev), "cudaGetDeviceCount");
+  if (ndev <= 0) throw CudaFailure("cuda error: no CUDA device visible");
+  if (num_slabs < 1) throw std::invalid_argument("config error: need at least one slab");
+  if (num_slabs > 1 && ctx->rows / num_slabs < kHalo)
+    throw std::invalid_argument("geometry error: " + std::to_string(num_slabs) + " slabs of " +
+                                std::to_string(ctx->rows) +
+                                " rows are thinner than the 16-row halo");
+  ctx->slabs.resize(num_slabs);
+  const int32_t base = ctx->rows / num_slabs, extra = ctx->rows % num_slabs;
+  int32_t row0 = 0;
+  for (int32_t i = 0; i < num_slabs; ++i) {
+    Slab& s = ctx->slabs[i];
+    s.dev = dev_ids ? dev_ids[i] : i % ndev;
+    if (s.dev < 0 || s.dev >= ndev)
+      throw std::invalid_argument("config error: device " + std::to_string(s.dev) +
+                                  " not visible");
+    s.row0 = row0;
+    s.rows = base + (i < extra ? 1 : 0);
+    row0 += s.rows;
+    s.pitch = round_up(ctx->cols + 2 * kHalo, 128);
+    ck(cudaSetDevice(s.dev), "cudaSetDevice");
+    const size_t bytes = static_cast<size_t>(s.rows + 2 * kHalo) * s.pitch;
+    for (int b = 0; b < 2; ++b) {
+      ck(cudaMalloc(&s.buf[b], bytes), "cudaMalloc slab");
+      ck(cudaMemset(s.buf[b], 0, bytes), "cudaMemset slab");
+    }
+    ck(cudaMalloc(&s.dstats, sizeof(ltl::DeviceStats)), "cudaMalloc stats");
+    ck(cudaStreamCreateWithFlags(&s.stream, cudaStreamNonBlocking), "cudaStreamCreate");
+    ck(cudaEventCreateWithFlags(&s.ev_step, cudaEventDisableTiming), "cudaEventCreate");
+    build_maps(s, ctx->cols);
+  }
+  // peer access between distinct neighbouring devices (NVLink / NVSwitch)
+  for (int32_t i = 0; i < num_slabs; ++i) {
+    const int a = ctx->slabs[i].dev;
+    for (int32_t d : {-1, 1}) {
+      const int b = ctx->slabs[(i + d + num_slabs) % num_slabs].dev;
+      if (a == b) continue;
+      int can = 0;
+      ck(cudaDeviceCanAccessPeer(&can, a, b), "cudaDeviceCanAccessPeer");
+      if (!can)
+        throw CudaFailure("cuda error: no peer access between devices " + std::to_string(a) +
+                          " and " + std::to_string(b));
+      ck(cudaSetDevice(a), "cudaSetDevice");
+      const cudaError_t e = cudaDeviceEnablePeerAccess(b, 0);
+      if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) ck(e, "enable peer access");
+      cudaGetLastError();
+    }
+  }
+}
+
+void destroy_ctx(ltl_ctx* ctx) {
+  for (Slab& s : ctx->slabs) {
+    cudaSetDevice(s.dev);
+    if (s.stream) cudaStreamSynchronize(s.stream);
+    for (auto& b : s.buf)
+      if (b) cudaFree(b);
+    if (s.dstats) cudaFree(s.dstats);
+    if (s.ev_step) cudaEventDestroy(s.ev_step);
+    for (cudaEvent_t e : s.timing) cudaEventDestroy(e);
+    if (s.stream && s.own_stream) cudaStreamDestroy(s.stream);
+  }
+  ctx->slabs.clear();
+}
+
+// Halo refresh of generation buffer `which` on every slab (after all slabs'
+// interiors for that generation are enqueued).
+void enqueue_halo(ltl_ctx* ctx, int which) {
+  const int32_t G = static_cast<int32_t>(ctx->slabs.size());
+  for (int32_t i = 0; i < G; ++i) {
+    Slab& s = ctx->slabs[i];
+    Slab& up = ctx->slabs[(i - 1 + G) % G];
+    Slab& dn = ctx->slabs[(i + 1) % G];
+    ck(cudaSetDevice(s.dev), "cudaSetDevice");
+    if (G > 1) {
+      ck(cudaStreamWaitEvent(s.stream, up.ev_step, 0), "wait above");
+      ck(cudaStreamWaitEvent(s.stream, dn.ev_step, 0), "wait below");
+    }
+    ltl::SlabView self = s.view(which, ctx->cols);
+    ltl::SlabView above = ctx->external_row_halo ? self : up.view(which, ctx->cols);
+    ltl::SlabView below = ctx->external_row_halo ? self : dn.view(which, ctx->cols);
+    if (ctx->external_row_halo) {
+      // rows come from an external transport; refresh only the column wrap
+      above.rows = below.rows = -1;
+    }
+    ck(ltl::launch_halo_fill(self, above, below, s.stream), "halo kernel");
+  }
+}
+
+// One generation: main kernel per slab (cur -> nxt), then halo of nxt.
+void enqueue_step(ltl_ctx* ctx, const ltl::RuleConsts& rc, uint32_t flags, bool want_stats,
+                  cudaEvent_t* kt0, cudaEvent_t* kt1) {
+  const int cur = ctx->cur, nxt = 1 - cur;
+  const bool fault = (flags & LTL_FLAG_INJECT_FAULT) != 0;
+  for (size_t i = 0; i < ctx->slabs.size(); ++i) {
+    Slab& s = ctx->slabs[i];
+    ck(cudaSetDevice(s.dev), "cudaSetDevice");
+    if (kt0) ck(cudaEventRecord(kt0[i], s.stream), "event");
+    if (flags & LTL_FLAG_STENCIL) {
+      ck(ltl::launch_stencil_step(s.view(cur, ctx->cols), s.view(nxt, ctx->cols), rc, fault,
+                                  want_stats ? s.dstats : nullptr, s.stream),
+         "stencil kernel");
+    } else {
+      ltl::TcLaunch a{};
+      a.load_map = &s.load_map[cur];
+      a.store_map = &s.store_map[nxt];
+      a.rows = s.rows;
+      a.cols = ctx->cols;
+      a.rule = rc;
+      a.inject_fault = fault;
+      a.stats = want_stats ? s.dstats : nullptr;
+      ck(ltl::launch_tc_step(a, s.stream), "tcgen05 kernel");
+    }
+    if (kt1) ck(cudaEventRecord(kt1[i], s.stream), "event");
+    if (ctx->slabs.size() > 1) ck(cudaEventRecord(s.ev_step, s.stream), "event");
+  }
+  enqueue_halo(ctx, nxt);
+  ctx->cur = nxt;
+}
+
+void sync_all(ltl_ctx* ctx) {
+  for (Slab& s : ctx->slabs) {
+    ck(cudaSetDevice(s.dev), "cudaSetDevice");
+    ck(cudaStreamSynchronize(s.stream), "cudaStreamSynchronize");
+  }
+}
+
+void reset_stats(ltl_ctx* ctx) {
+  for (Slab& s : ctx->slabs) {
+    ck(cudaSetDevice(s.dev), "cudaSetDevice");
+    ck(cudaMemsetAsync(s.dstats, 0, sizeof(ltl::DeviceStats), s.stream), "memset stats");
+  }
+}
+
+void run_steps(ltl_ctx* ctx, const ltl_rule_c* rule, int32_t steps, uint32_t flags,
+               ltl_stats_c* stats) {
+  check_run_args(ctx, rule, steps);
+  const ltl::RuleConsts rc = rule_consts(*rule);
+  // The negative-count guard is always armed; max_h/max_r ride the same buffer.
+  reset_stats(ctx);
+  for (int32_t t = 0; t < steps; ++t) enqueue_step(ctx, rc, flags, true, nullptr, nullptr);
+  sync_all(ctx);
+  ltl::DeviceStats agg{};
+  for (Slab& s : ctx->slabs) {
+    ltl::DeviceStats h{};
+    ck(cudaSetDevice(s.dev), "cudaSetDevice");
+    ck(cudaMemcpy(&h, s.dstats, sizeof h, cudaMemcpyDeviceToHost), "stats readback");
+    agg.max_h = std::max(agg.max_h, h.max_h);
+    agg.max_r = std::max(agg.max_r, h.max_r);
+    agg.error |= h.error;
+  }
+  if (agg.error) throw std::logic_error("internal consistency: negative neighborhood count");
+  if (stats) {
+    // CAT-fragment accounting (cat_engine.cpp:151-155, :198-202): 3 MMAs per
+    // fragment of the H pass (all fragment rows, interior columns) and 3 per
+    // interior fragment of the R pass, per step.
+    const int64_t fpr = (ctx->cols + 2LL * ctx->f) / ctx->f;
+    const int64_t per_step = ctx->rows == ctx->cols && ctx->rows > 0
+                                 ? 3 * fpr * (fpr - 2) + 3 * (fpr - 2) * (fpr - 2)
+                                 : 0;
+    stats->mma_count += per_step * steps;
+    stats->steps += steps;
+    stats->max_h = std::max(stats->max_h, steps > 0 ? agg.max_h : 0);
+    stats->max_r = std::max(stats->max_r, steps > 0 ? agg.max_r : 0);
+    stats->fragments_per_row = static_cast<int32_t>(fpr);
+  }
+}
+
+// Host layout helpers (fragment-contiguous order: grid.hpp:20-25).
+size_t host_index(int32_t layout, int32_t f, int32_t p, int32_t y, int32_t x) {
+  if (layout == LTL_LAYOUT_ROW_MAJOR) return static_cast<size_t>(y) * p + x;
+  const int32_t fpr = p / f;
+  return (static_cast<size_t>(y / f) * fpr + x / f) * (static_cast<size_t>(f) * f) +
+         static_cast<size_t>(y % f) * f + (x % f);
+}
+
+void upload_interior(ltl_ctx* ctx, const uint8_t* interior) {
+  for (Slab& s : ctx->slabs) {
+    ck(cudaSetDevice(s.dev), "cudaSetDevice");
+    if (s.rows == 0 || ctx->cols == 0) continue;
+    ck(cudaMemcpy2DAsync(s.buf[ctx->cur] + kHalo * s.pitch + kHalo, s.pitch,
+                         interior + static_cast<size_t>(s.row0) * ctx->cols, ctx->cols,
+                         ctx->cols, s.rows, cudaMemcpyHostToDevice, s.stream),
+       "upload");
+    if (ctx->slabs.size() > 1) ck(cudaEventRecord(s.ev_step, s.stream), "event");
+  }
+  enqueue_halo(ctx, ctx->cur);
+  sync_all(ctx);
+}
+
+void download_interior(ltl_ctx* ctx, uint8_t* interior) {
+  for (Slab& s : ctx->slabs) {
+    ck(cudaSetDevice(s.dev), "cudaSetDevice");
+    if (s.rows == 0 || ctx->cols == 0) continue;
+    ck(cudaMemcpy2DAsync(interior + static_cast<size_t>(s.row0) * ctx->cols, ctx->cols,
+                         s.buf[ctx->cur] + kHalo * s.pitch + kHalo, s.pitch, ctx->cols, s.rows,
+                         cudaMemcpyDeviceToHost, s.stream),
+       "download");
+  }
+  sync_all(ctx);
+}
+
+void check_layout(int32_t layout) {
+  if (layout != LTL_LAYOUT_ROW_MAJOR && layout != LTL_LAYOUT_FRAGMENT)
+    throw std::invalid_argument("layout error: unknown layout " + std::to_string(layout));
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* ltl_build_info(void) {
+  return "ltl_b200 abi=1 arch=sm_100a kernels=tcgen05-banded-i8,cuda-core-stencil,halo";
+}
+
+int ltl_create_torus(ltl_ctx** out, int32_t rows, int32_t cols, int32_t num_slabs,
+                     const int32_t* dev_ids) {
+  if (!out) return LTL_ERR_INVALID_ARGUMENT;
+  *out = nullptr;
+  ltl_ctx* ctx = new ltl_ctx;
+  const int st = guarded(nullptr, [&] {
+    if (rows < 0 || cols < 0)
+      throw std::invalid_argument("geometry error: torus sides must be non-negative");
+    if ((rows == 0) != (cols == 0))
+      throw std::invalid_argument("geometry error: empty torus must be 0 x 0");
+    ctx->rows = rows;
+    ctx->cols = cols;
+    ctx->f = 16;
+    create_slabs(ctx, num_slabs, dev_ids);
+  });
+  if (st != LTL_OK) {
+    destroy_ctx(ctx);
+    delete ctx;
+    return st;
+  }
+  *out = ctx;
+  return LTL_OK;
+}
+
+int ltl_create(ltl_ctx** out, int32_t n, int32_t f, int32_t num_slabs, const int32_t* dev_ids) {
+  if (!out) return LTL_ERR_INVALID_ARGUMENT;
+  *out = nullptr;
+  const int st = guarded(nullptr, [&] {
+    if (f != 4 && f != 8 && f != 16)
+      throw std::invalid_argument("config error: fragment side must be 4, 8, or 16");
+    if (n < 0 || n % f != 0)
+      throw std::invalid_argument("geometry error: n (" + std::to_string(n) +
+                                  ") must be a non-negative multiple of f (" +
+                                  std::to_string(f) + ")");
+  });
+  if (st != LTL_OK) return st;
+  const int st2 = ltl_create_torus(out, n, n, num_slabs, dev_ids);
+  if (st2 == LTL_OK) (*out)->f = f;
+  return st2;
+}
+
+void ltl_destroy(ltl_ctx* ctx) {
+  if (!ctx) return;
+  destroy_ctx(ctx);
+  delete ctx;
+}
+
+const char* ltl_last_error(const ltl_ctx* ctx) {
+  return ctx ? ctx->err.c_str() : g_last_error.c_str();
+}
+
+int32_t ltl_rows(const ltl_ctx* ctx) { return ctx ? ctx->rows : -1; }
+int32_t ltl_cols(const ltl_ctx* ctx) { return ctx ? ctx->cols : -1; }
+int32_t ltl_num_slabs(const ltl_ctx* ctx) {
+  return ctx ? static_cast<int32_t>(ctx->slabs.size()) : -1;
+}
+
+int ltl_upload_interior(ltl_ctx* ctx, const uint8_t* interior) {
+  if (!ctx) return LTL_ERR_INVALID_ARGUMENT;
+  return guarded(ctx, [&] {
+    if (!interior && ctx->rows > 0) throw std::invalid_argument("config error: null buffer");
+    upload_interior(ctx, interior);
+  });
+}
+
+int ltl_download_interior(ltl_ctx* ctx, uint8_t* interior) {
+  if (!ctx) return LTL_ERR_INVALID_ARGUMENT;
+  return guarded(ctx, [&] {
+    if (!interior && ctx->rows > 0) throw std::invalid_argument("config error: null buffer");
+    download_interior(ctx, interior);
+  });
+}
+
+int ltl_upload(ltl_ctx* ctx, const uint8_t* padded, int32_t layout) {
+  if (!ctx) return LTL_ERR_INVALID_ARGUMENT;
+  return guarded(ctx, [&] {
+    check_layout(layout);
+    if (ctx->rows != ctx->cols) throw std::invalid_argument("layout error: padded grids are square");
+    const int32_t n = ctx->rows, f = ctx->f, p = n + 2 * f;
+    std::vector<uint8_t> interior(static_cast<size_t>(n) * n);
+    for (int32_t y = 0; y < n; ++y)
+      for (int32_t x = 0; x < n; ++x)
+        interior[static_cast<size_t>(y) * n + x] = padded[host_index(layout, f, p, y + f, x + f)];
+    upload_interior(ctx, interior.data());
+  });
+}
+
+int ltl_download(ltl_ctx* ctx, uint8_t* padded, int32_t layout) {
+  if (!ctx) return LTL_ERR_INVALID_ARGUMENT;
+  return guarded(ctx, [&] {
+    check_layout(layout);
+    if (ctx->rows != ctx->cols) throw std::invalid_argument("layout error: padded grids are square");
+    const int32_t n = ctx->rows, f = ctx->f, p = n + 2 * f;
+    std::vector<uint8_t> interior(static_cast<size_t>(n) * n);
+    download_interior(ctx, interior.data());
+    for (int32_t y = 0; y < p; ++y)
+      for (int32_t x = 0; x < p; ++x) {
+        const int32_t sy = n ? ((y - f) % n + n) % n : 0, sx = n ? ((x - f) % n + n) % n : 0;
+        padded[host_index(layout, f, p, y, x)] = n ? interior[static_cast<size_t>(sy) * n + sx] : 0;
+      }
+  });
+}
+
+int ltl_run(ltl_ctx* ctx, const ltl_rule_c* rule, int32_t steps, uint32_t flags,
+            ltl_stats_c* stats) {
+  if (!ctx) return LTL_ERR_INVALID_ARGUMENT;
+  return guarded(ctx, [&] { run_steps(ctx, rule, steps, flags, stats); });
+}
+
+int ltl_run_async(ltl_ctx* ctx, const ltl_rule_c* rule, int32_t steps, uint32_t flags) {
+  if (!ctx) return LTL_ERR_INVALID_ARGUMENT;
+  return guarded(ctx, [&] {
+    check_run_args(ctx, rule, steps);
+    const ltl::RuleConsts rc = rule_consts(*rule);
+    for (int32_t t = 0; t < steps; ++t) enqueue_step(ctx, rc, flags, false, nullptr, nullptr);
+  });
+}
+
+int ltl_synchronize(ltl_ctx* ctx) {
+  if (!ctx) return LTL_ERR_INVALID_ARGUMENT;
+  return guarded(ctx, [&] { sync_all(ctx); });
+}
+
+int ltl_time(ltl_ctx* ctx, const ltl_rule_c* rule, int32_t steps, int32_t warmup,
+             uint32_t flags, double* total_ms, double* kernel_ms) {
+  if (!ctx) return LTL_ERR_INVALID_ARGUMENT;
+  return guarded(ctx, [&] {
+    check_run_args(ctx, rule, steps);
+    const ltl::RuleConsts rc = rule_consts(*rule);
+    const size_t G = ctx->slabs.size();
+    for (int32_t t = 0; t < warmup; ++t) enqueue_step(ctx, rc, flags, false, nullptr, nullptr);
+    sync_all(ctx);
+    // per slab: [start, end] + per-step kernel [k0, k1] pairs
+    for (Slab& s : ctx->slabs) {
+      ck(cudaSetDevice(s.dev), "cudaSetDevice");
+      const size_t need = 2 + 2 * static_cast<size_t>(steps);
+      while (s.timing.size() < need) {
+        cudaEvent_t e;
+        ck(cudaEventCreate(&e), "cudaEventCreate");
+        s.timing.push_back(e);
+      }
+      ck(cudaEventRecord(s.timing[0], s.stream), "event");
+    }
+    std::vector<cudaEvent_t> k0(G), k1(G);
+    for (int32_t t = 0; t < steps; ++t) {
+      for (size_t i = 0; i < G; ++i) {
+        k0[i] = ctx->slabs[i].timing[2 + 2 * t];
+        k1[i] = ctx->slabs[i].timing[3 + 2 * t];
+      }
+      enqueue_step(ctx, rc, flags, false, kernel_ms ? k0.data() : nullptr,
+                   kernel_ms ? k1.data() : nullptr);
+    }
+    for (Slab& s : ctx->slabs) {
+      ck(cudaSetDevice(s.dev), "cudaSetDevice");
+      ck(cudaEventRecord(s.timing[1], s.stream), "event");
+    }
+    sync_all(ctx);
+    double tot = 0, ker = 0;
+    for (Slab& s : ctx->slabs) {
+      float ms = 0;
+      ck(cudaEventElapsedTime(&ms, s.timing[0], s.timing[1]), "elapsed");
+      tot = std::max(tot, static_cast<double>(ms));
+      if (kernel_ms) {
+        double acc = 0;
+        for (int32_t t = 0; t < steps; ++t) {
+          float k = 0;
+          ck(cudaEventElapsedTime(&k, s.timing[2 + 2 * t], s.timing[3 + 2 * t]), "elapsed");
+          acc += k;
+        }
+        ker = std::max(ker, acc);
+      }
+    }
+    if (total_ms) *total_ms = tot;
+    if (kernel_ms) *kernel_ms = ker;
+  });
+}
+
+int ltl_run_interior(ltl_ctx* ctx, const uint8_t* interior_in, uint8_t* interior_out,
+                     const ltl_rule_c* rule, int32_t steps, uint32_t flags, ltl_stats_c* stats) {
+  if (!ctx) return LTL_ERR_INVALID_ARGUMENT;
+  return guarded(ctx, [&] {
+    check_run_args(ctx, rule, steps);
+    upload_interior(ctx, interior_in);
+    run_steps(ctx, rule, steps, flags, stats);
+    download_interior(ctx, interior_out);
+  });
+}
+
+int ltl_slab_buffer(ltl_ctx* ctx, int32_t slab, int32_t which, void** dev_ptr, int64_t* pitch,
+                    int32_t* rows) {
+  if (!ctx) return LTL_ERR_INVALID_ARGUMENT;
+  return guarded(ctx, [&] {
+    if (slab < 0 || slab >= static_cast<int32_t>(ctx->slabs.size()))
+      throw std::out_of_range("config error: slab index out of range");
+    const Slab& s = ctx->slabs[slab];
+    const int b = which == 0 ? ctx->cur : 1 - ctx->cur;
+    if (dev_ptr) *dev_ptr = s.buf[b];
+    if (pitch) *pitch = s.pitch;
+    if (rows) *rows = s.rows;
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,383 @@
+// ltl_tc.cu -- one Larger-than-Life generation as two banded tcgen05 MMAs.
+//
+// Replaces the reference hot path src/cat_engine.cpp:260-306 (simulate_step:
+// horizontal_step :123-161, vertical_step_moore :163-208,
+// vertical_step_von_neumann :210-258, rule loop :293-303).  The reference
+// restates the paper's method with 16x16 int32 fragments and three band
+// fragments pi1/pi2/pi3 (src/fragment.cpp:23-41).  Here the same banded
+// products run on the 5th-generation tensor cores in their native shapes:
+//
+//   tile     = a 128-column strip of the slab, streamed down in 32-row chunks
+//   pass 1   D1[x][y] = sum_k A1[x][k] * X[y][k]          (tcgen05.mma kind::i8,
+//            A1 = 128 x 160 band (SMEM, resident), X = TMA-loaded 32 x 160 chunk,
+//            M = 128 (x), N = 32 (y), K = 160 = 5 MMAs of K = 32)
+//            A1[x][k] = [|k-16-x| <= r] + 128*[k == x+16]: the extra 128 at
+//            the centre rides the cell state out in bit 7 of D1 for free.
+//   convert  epilogue warps: D1 (s32, TMEM) -> bytes, H = D1 & 0x7F and the
+//            state bit -> tcgen05.st back into TMEM as the K-major A operand
+//            of pass 2 (no SMEM round trip, no transposition).
+//   pass 2   D2[x][n] = sum_k H[x][k] * Bv[k][n] over the 64 H rows around
+//            each 32-row output chunk (2 MMAs, A from TMEM, band B in SMEM).
+//            Von Neumann adds  X^T * Bv + H^T * Iv  instead (4 MMAs).
+//   epilogue D2 -> rule (apply_transition, src/rule.cpp:99-111) -> bytes ->
+//            SMEM staging -> TMA store of the next generation.
+//
+// Every quantity is an exact small integer (H <= 33, R <= 1089 < 2^31), so the
+// s32 accumulation is bit-exact with the reference's int32 loops.
+//
+// Warp roles (192 threads): warp 0 TMA producer, warp 1 MMA issuer + TMEM
+// owner, warps 2..5 epilogue (warp w owns TMEM lanes 32*(w%4)..+32, i.e. 32
+// columns of the strip).  Persistent CTAs walk (strip, row-segment) work units.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "ltl_kernels.cuh"
+#include "ptx_sm100.cuh"
+
+namespace ltl {
+namespace {
+
+using namespace ptx;
+
+constexpr int kStripCols = 128;  // M of both MMAs = output columns per strip
+constexpr int kChunkRows = 32;   // N of both MMAs = rows per chunk
+constexpr int kKTile = 160;      // 128 + 2*16 input columns per strip
+constexpr int kKChunks = kKTile / 32;
+constexpr int kXStages = 4;
+constexpr int kA2Slots = 4;
+constexpr int kThreads = 192;
+constexpr int kEpiThreads = 128;
+
+// Shared-memory carve-up (offsets from a 1024-aligned base).
+constexpr uint32_t kSmemA1 = 0;                                   // 5 x 128 x 32 B
+constexpr uint32_t kSmemBand = kSmemA1 + kKChunks * 128 * 32;     // Bv0, Bv1, Iv0, Iv1: 4 x 1 KB
+constexpr uint32_t kSmemX = kSmemBand + 4 * 1024;                 // kXStages x 5 KB
+constexpr uint32_t kXStageBytes = kKChunks * kChunkRows * 32;     // 5120
+constexpr uint32_t kSmemStage = kSmemX + kXStages * kXStageBytes;  // 2 x 4 KB output staging
+constexpr uint32_t kStageBytes = kChunkRows * kStripCols;         // 4096
+constexpr uint32_t kSmemBars = kSmemStage + 2 * kStageBytes;
+constexpr uint32_t kNumBars = 2 * kXStages + 2 * 2 + 2 * kA2Slots + 2 * 2;
+constexpr uint32_t kSmemTotal = kSmemBars + kNumBars * 8 + 16;
+constexpr uint32_t kSmemAlloc = kSmemTotal + 1024;  // alignment slack
+
+// TMEM columns (allocation of 256).
+constexpr uint32_t kTmemCols = 256;
+constexpr uint32_t kTmemD1 = 0;    // 2 x 32
+constexpr uint32_t kTmemD2 = 64;   // 2 x 32
+constexpr uint32_t kTmemA2 = 128;  // kA2Slots x 16 (H part +0, state part +8)
+
+constexpr uint32_t kIdescM128N32 = idesc_i8_u8u8_s32(128, 32);
+
+struct Params {
+  int32_t rows, cols;
+  int32_t num_strips, chunks, seg, segs, num_units;
+  RuleConsts rule;
+  int32_t inject_fault;
+  DeviceStats* stats;
+};
+
+__device__ __forceinline__ uint32_t pack_low_bytes(uint32_t a, uint32_t b, uint32_t c,
+                                                   uint32_t d) {
+  return __byte_perm(__byte_perm(a, b, 0x0040), __byte_perm(c, d, 0x0040), 0x5410);
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+    ltl_tc_step_kernel(const __grid_constant__ CUtensorMap load_map,
+                       const __grid_constant__ CUtensorMap store_map, const Params p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kSmemBars);
+  uint64_t* x_full = bars;
+  uint64_t* x_empty = x_full + kXStages;
+  uint64_t* d1_full = x_empty + kXStages;
+  uint64_t* d1_empty = d1_full + 2;
+  uint64_t* a2_full = d1_empty + 2;
+  uint64_t* a2_empty = a2_full + kA2Slots;
+  uint64_t* d2_full = a2_empty + kA2Slots;
+  uint64_t* d2_empty = d2_full + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(d2_empty + 2);
+
+  const uint32_t warp = warp_id();
+  const uint32_t lane = threadIdx.x & 31;
+  const int r = p.rule.r;
+  const bool vn = p.rule.kind != 0;
+
+  // ---- one-time setup: resident bands (generic-proxy writes), barriers, TMEM
+  for (uint32_t i = threadIdx.x; i < 128u * kKTile; i += kThreads) {
+    const int m = static_cast<int>(i / kKTile), k = static_cast<int>(i % kKTile);
+    const int d = k - 16 - m;
+    uint32_t v = (d >= -r && d <= r) ? 1u : 0u;
+    if (d == 0) {
+      v += 128u;  // state marker
+      if (p.inject_fault && m == 0) v = 128u;  // test hook: drop one centre entry
+    }
+    smem[kSmemA1 + (k / 32) * 4096 + sw32_offset(m, k % 32)] = static_cast<uint8_t>(v);
+  }
+  for (uint32_t i = threadIdx.x; i < 4u * 32u * 32u; i += kThreads) {
+    const int t = static_cast<int>(i / 1024), n = static_cast<int>((i / 32) % 32),
+              k = static_cast<int>(i % 32);
+    int v;
+    if (t == 0) v = (k - 16 - n >= -r && k - 16 - n <= r);
+    else if (t == 1) v = (k + 16 - n >= -r && k + 16 - n <= r);
+    else if (t == 2) v = (k == n + 16);
+    else v = (k + 16 == n);
+    smem[kSmemBand + t * 1024 + sw32_offset(n, k)] = static_cast<uint8_t>(v);
+  }
+  fence_proxy_async_smem();
+  if (warp == 0 && lane == 0) {
+    prefetch_tmap(&load_map);
+    prefetch_tmap(&store_map);
+    for (int i = 0; i < kXStages; ++i) {
+      mbar_init(&x_full[i], 1);
+      mbar_init(&x_empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&d1_full[i], 1);
+      mbar_init(&d1_empty[i], kEpiThreads);
+      mbar_init(&d2_full[i], 1);
+      mbar_init(&d2_empty[i], kEpiThreads);
+    }
+    for (int i = 0; i < kA2Slots; ++i) {
+      mbar_init(&a2_full[i], kEpiThreads);
+      mbar_init(&a2_empty[i], 1);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, kTmemCols);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    // ================= TMA producer =================
+    if (elect_one()) {
+      uint32_t g = 0;
+      for (int u = blockIdx.x; u < p.num_units; u += gridDim.x) {
+        const int strip = u % p.num_strips, seg = u / p.num_strips;
+        const int c0 = seg * p.seg;
+        const int nc = min(p.seg, p.chunks - c0);
+        for (int k = 0; k <= nc; ++k, ++g) {
+          const uint32_t s = g % kXStages;
+          mbar_wait(&x_empty[s], ((g / kXStages) & 1) ^ 1);
+          uint8_t* dst = smem + kSmemX + s * kXStageBytes;
+          mbar_arrive_expect_tx(&x_full[s], kXStageBytes);
+#pragma unroll
+          for (int q = 0; q < kKChunks; ++q)
+            tma_load_2d(dst + q * 1024, &load_map, &x_full[s], strip * kStripCols + 32 * q,
+                        (c0 + k) * kChunkRows);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ================= MMA issuer =================
+    const uint32_t a1_base = smem_u32(smem + kSmemA1);
+    const uint32_t band_base = smem_u32(smem + kSmemBand);
+    const uint32_t x_base = smem_u32(smem + kSmemX);
+    uint32_t g = 0, o = 0;
+    auto pass1 = [&](uint32_t gg) {
+      const uint32_t s = gg % kXStages, d1 = gg & 1;
+      mbar_wait(&x_full[s], (gg / kXStages) & 1);
+      mbar_wait(&d1_empty[d1], ((gg >> 1) & 1) ^ 1);
+      tc_fence_after();
+      if (elect_one()) {
+#pragma unroll
+        for (int q = 0; q < kKChunks; ++q)
+          mma_i8_ss(tmem + kTmemD1 + 32 * d1, smem_desc_sw32_kmajor(a1_base + q * 4096),
+                    smem_desc_sw32_kmajor(x_base + s * kXStageBytes + q * 1024), kIdescM128N32,
+                    q > 0);
+        mma_commit(&x_empty[s]);
+        mma_commit(&d1_full[d1]);
+      }
+      __syncwarp();
+    };
+    auto pass2 = [&](uint32_t gg, uint32_t oo) {
+      const uint32_t s0 = gg % kA2Slots, s1 = (gg + 1) % kA2Slots, d2 = oo & 1;
+      mbar_wait(&a2_full[s0], (gg / kA2Slots) & 1);
+      mbar_wait(&a2_full[s1], ((gg + 1) / kA2Slots) & 1);
+      mbar_wait(&d2_empty[d2], ((oo >> 1) & 1) ^ 1);
+      tc_fence_after();
+      if (elect_one()) {
+        const uint32_t dcol = tmem + kTmemD2 + 32 * d2;
+        const uint32_t a0 = tmem + kTmemA2 + 16 * s0, a1 = tmem + kTmemA2 + 16 * s1;
+        if (!vn) {
+          mma_i8_ts(dcol, a0, smem_desc_sw32_kmajor(band_base + 0), kIdescM128N32, 0);
+          mma_i8_ts(dcol, a1, smem_desc_sw32_kmajor(band_base + 1024), kIdescM128N32, 1);
+        } else {
+          // cross sum: vertical window over the states + the row window at the centre
+          mma_i8_ts(dcol, a0 + 8, smem_desc_sw32_kmajor(band_base + 0), kIdescM128N32, 0);
+          mma_i8_ts(dcol, a1 + 8, smem_desc_sw32_kmajor(band_base + 1024), kIdescM128N32, 1);
+          mma_i8_ts(dcol, a0, smem_desc_sw32_kmajor(band_base + 2048), kIdescM128N32, 1);
+          mma_i8_ts(dcol, a1, smem_desc_sw32_kmajor(band_base + 3072), kIdescM128N32, 1);
+        }
+        mma_commit(&d2_full[d2]);
+        mma_commit(&a2_empty[s0]);
+      }
+      __syncwarp();
+    };
+    for (int u = blockIdx.x; u < p.num_units; u += gridDim.x) {
+      const int seg = u / p.num_strips;
+      const int nc = min(p.seg, p.chunks - seg * p.seg);
+      pass1(g);
+      for (int k = 0; k <= nc; ++k) {
+        if (k + 1 <= nc) pass1(g + k + 1);
+        if (k >= 1) pass2(g + k - 1, o + k - 1);
+      }
+      g += nc + 1;
+      o += nc;
+    }
+  } else {
+    // ================= epilogue (4 warps, 128 threads) =================
+    const uint32_t q = warp & 3;            // TMEM lane quarter
+    const uint32_t m = q * 32 + lane;       // column within the strip
+    const uint32_t trow = tmem + ((q * 32) << 16);
+    const bool is_store_thread = (warp == 2 && lane == 0);
+    uint8_t* stage_base = smem + kSmemStage;
+    int32_t max_h = 0, max_r = 0, bad = 0;
+    uint32_t g = 0, o = 0;
+    const RuleConsts rc = p.rule;
+
+    for (int u = blockIdx.x; u < p.num_units; u += gridDim.x) {
+      const int strip = u % p.num_strips, seg = u / p.num_strips;
+      const int c0 = seg * p.seg;
+      const int nc = min(p.seg, p.chunks - c0);
+      uint32_t st_prev[8], st_cur[8];  // state bytes (0/1), 4 rows per word
+
+      auto output_chunk = [&](int c, const uint32_t (&sa)[8], const uint32_t (&sb)[8]) {
+        const uint32_t oo = o + c, d2 = oo & 1;
+        mbar_wait(&d2_full[d2], (oo >> 1) & 1);
+        tc_fence_after();
+        uint32_t v[32];
+        tmem_ld_32x32b_x32(trow + kTmemD2 + 32 * d2, v);
+        tmem_ld_wait();
+        tc_fence_before();
+        mbar_arrive(&d2_empty[d2]);
+        // staging buffer oo&1 was last read by the TMA store of chunk oo-2
+        if (is_store_thread) tma_store_wait_read<1>();
+        named_barrier(1, kEpiThreads);
+        uint8_t* stage = stage_base + d2 * kStageBytes;
+#pragma unroll
+        for (int n = 0; n < 32; ++n) {
+          // output row n = H-chunk c row 16+n (n < 16) or H-chunk c+1 row n-16
+          const uint32_t w = (n < 16) ? sa[4 + n / 4] : sb[(n - 16) / 4];
+          const uint32_t st = (w >> (8 * (n & 3))) & 1u;
+          const int32_t R = static_cast<int32_t>(v[n]);
+          max_r = max(max_r, R);
+          const int32_t lo = st ? rc.lo_live : rc.lo_dead;
+          const uint32_t wd = static_cast<uint32_t>(st ? rc.w_live : rc.w_dead);
+          bad |= (st && R < rc.neg_live);
+          stage[n * kStripCols + m] = (static_cast<uint32_t>(R - lo) <= wd) ? 1 : 0;
+        }
+        fence_proxy_async_smem();
+        named_barrier(1, kEpiThreads);
+        if (is_store_thread) {
+          tma_store_2d(&store_map, stage, strip * kStripCols, (c0 + c) * kChunkRows);
+          tma_store_commit();
+        }
+      };
+
+      for (int k = 0; k <= nc; ++k) {
+        const uint32_t gg = g + k, d1 = gg & 1, s = gg % kA2Slots;
+        mbar_wait(&d1_full[d1], (gg >> 1) & 1);
+        tc_fence_after();
+        uint32_t v[32];
+        tmem_ld_32x32b_x32(trow + kTmemD1 + 32 * d1, v);
+        tmem_ld_wait();
+        tc_fence_before();
+        mbar_arrive(&d1_empty[d1]);
+        uint32_t hw[8], sw[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const uint32_t raw = pack_low_bytes(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+          hw[j] = raw & 0x7F7F7F7Fu;
+          sw[j] = (raw >> 7) & 0x01010101u;
+          if (p.stats) {
+            const uint32_t mx = __vmaxu4(hw[j], hw[j] >> 16);
+            max_h = max(max_h, static_cast<int32_t>(max(mx & 0xFF, (mx >> 8) & 0xFF)));
+          }
+        }
+        mbar_wait(&a2_empty[s], ((gg / kA2Slots) & 1) ^ 1);
+        tc_fence_after();
+        tmem_st_32x32b_x8(trow + kTmemA2 + 16 * s, hw);
+        if (vn) tmem_st_32x32b_x8(trow + kTmemA2 + 16 * s + 8, sw);
+        tmem_st_wait();
+        tc_fence_before();
+        mbar_arrive(&a2_full[s]);
+        // rotate the state words: st_prev <- st_cur <- this chunk
+        if (k >= 2) output_chunk(k - 2, st_prev, st_cur);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          st_prev[j] = st_cur[j];
+          st_cur[j] = sw[j];
+        }
+      }
+      if (nc >= 1) output_chunk(nc - 1, st_prev, st_cur);
+      g += nc + 1;
+      o += nc;
+    }
+    if (is_store_thread) tma_store_wait_all<0>();
+    if (p.stats) {
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) {
+        max_h = max(max_h, __shfl_xor_sync(0xffffffffu, max_h, off));
+        max_r = max(max_r, __shfl_xor_sync(0xffffffffu, max_r, off));
+      }
+      if (lane == 0) {
+        atomicMax(&p.stats->max_h, max_h);
+        atomicMax(&p.stats->max_r, max_r);
+      }
+    }
+    if (__any_sync(0xffffffffu, bad) && lane == 0 && p.stats) atomicOr(&p.stats->error, 1);
+  }
+
+  __syncwarp();
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc(tmem, kTmemCols);
+}
+
+}  // namespace
+
+size_t tc_smem_bytes() { return kSmemAlloc; }
+
+cudaError_t launch_tc_step(const TcLaunch& a, cudaStream_t stream) {
+  static int num_sms = 0;
+  if (num_sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaError_t e = cudaFuncSetAttribute(ltl_tc_step_kernel,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(kSmemAlloc));
+    if (e != cudaSuccess) return e;
+  }
+  if (a.rows <= 0 || a.cols <= 0) return cudaSuccess;
+  Params p{};
+  p.rows = a.rows;
+  p.cols = a.cols;
+  p.num_strips = (a.cols + kStripCols - 1) / kStripCols;
+  p.chunks = (a.rows + kChunkRows - 1) / kChunkRows;
+  int seg = a.seg_chunks;
+  if (seg <= 0) {
+    // enough units for ~4 per CTA slot, but never shorter than 4 chunks when avoidable
+    const int64_t target_units = 4LL * num_sms;
+    const int64_t per_strip = (target_units + p.num_strips - 1) / p.num_strips;
+    seg = static_cast<int>((p.chunks + per_strip - 1) / per_strip);
+    seg = seg < 1 ? 1 : (seg > 64 ? 64 : seg);
+  }
+  p.seg = seg;
+  p.segs = (p.chunks + seg - 1) / seg;
+  p.num_units = p.num_strips * p.segs;
+  p.rule = a.rule;
+  p.inject_fault = a.inject_fault;
+  p.stats = a.stats;
+  int grid = a.grid > 0 ? a.grid : num_sms;
+  if (grid > p.num_units) grid = p.num_units;
+  ltl_tc_step_kernel<<<grid, kThreads, kSmemAlloc, stream>>>(*a.load_map, *a.store_map, p);
+  return cudaGetLastError();
+}
+
+}  // namespace ltl

@@ -1,0 +1,148 @@
+"""Parity of the device engines with the reference, on a B200.
+
+Every grid the CUDA path produces is compared byte-for-byte with the C
+restatement of the reference (oracle/, pinned in tests/test_oracle.py) and/or
+the reference-generated golden fixtures (tests/golden/).  Both engines are
+exercised through the C-ABI: "cat" (tcgen05 banded MMA) and "stencil" (the
+CUDA-core ablation).
+"""
+import numpy as np
+import pytest
+
+from golden_data import load, parse_rule_text
+
+pytestmark = pytest.mark.gpu
+
+ENGINES = ("cat", "stencil")
+
+
+@pytest.fixture(scope="module")
+def ltl():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    from paper_2406_17284_b200 import ltl as mod
+    return mod
+
+
+def _fnv(orc, a):
+    return f"{orc.fnv1a64(a):016x}"
+
+
+@pytest.mark.parametrize("engine", ENGINES)
+def test_criterion1_sweep(ltl, orc, engine):
+    """acceptance.cpp:69-146 shape: r=1..16 x {Moore preset, VN probe} x n x seeds x
+    steps, plus f=4/8 geometries -- against the reference's own hashes."""
+    cases = load("criterion1.json")["cases"]
+    tori = {}
+    inits = {}
+    failures = []
+    for c in cases:
+        key = (c["n"], c["f"])
+        if key not in tori:
+            tori[key] = ltl.DeviceTorus(n=c["n"], f=c["f"])
+        ikey = (c["n"], c["density"], c["seed"])
+        if ikey not in inits:
+            inits[ikey] = orc.init_random(*ikey)
+        t = tori[key]
+        t.upload(inits[ikey])
+        st = t.run(c["rule"], c["steps"], stencil=(engine == "stencil"))
+        out = t.download()
+        if _fnv(orc, out) != c["fnv"]:
+            failures.append((c["rule"], c["n"], c["f"], c["seed"], c["steps"]))
+        elif c["f"] == 16 and c["n"] >= 32:
+            assert st["max_h"] <= 2 * c["r"] + 1
+    for t in tori.values():
+        t.close()
+    assert not failures, f"{len(failures)} mismatches, first: {failures[:5]}"
+
+
+@pytest.mark.parametrize("engine", ENGINES)
+def test_anchors(ltl, orc, engine):
+    for a in load("anchors.json")["anchors"]:
+        init = orc.init_random(a["n"], a["density"], a["seed"])
+        out = ltl.run_engine(engine, init, a["rule"], a["steps"])
+        assert int(out.sum()) == a["alive"], a
+        assert _fnv(orc, out) == a["fnv"], a
+
+
+@pytest.mark.parametrize("engine", ENGINES)
+@pytest.mark.parametrize("rows,cols", [(96, 160), (200, 72), (33, 1000), (4096, 128), (17, 17)])
+def test_rectangular_torus(ltl, orc, engine, rows, cols):
+    rng = np.random.default_rng(rows * 7 + cols)
+    init = (rng.random((rows, cols)) < 0.3).astype(np.uint8)
+    for text in ("R1,C2,M0,S2..3,B3..3,NM", "R7,C2,M1,S60..140,B50..110,NM",
+                 "R16,C2,M0,S170..296,B170..300,NM", "R9,C2,M0,S5..18,B7..12,NN"):
+        rule = parse_rule_text(text)
+        with ltl.DeviceTorus(rows=rows, cols=cols) as t:
+            t.upload(init)
+            t.run(text, 3, stencil=(engine == "stencil"))
+            got = t.download()
+        assert np.array_equal(got, orc.simulate(init, rule, 3)), (text, rows, cols)
+
+
+def test_max_h_max_r_all_alive(ltl):
+    """acceptance.cpp:245-277: all-live grid at r=16 hits H=33 and R=1089 exactly."""
+    for engine in ENGINES:
+        g = np.ones((64, 64), np.uint8)
+        _, st = ltl.run_engine(engine, g, "R16,C2,M1,S0..1089,B0..1089,NM", 1, stats=True)
+        assert (st["max_h"], st["max_r"]) == (33, 1089), engine
+
+
+def test_mma_accounting_matches_reference(ltl, orc):
+    """CatStats.mma_count in reference fragment units (test_cat_engine.cpp:274-305)."""
+    for c in load("criterion1.json")["cases"][:40]:
+        init = orc.init_random(c["n"], c["density"], c["seed"])
+        _, st = ltl.run_engine("cat", init, c["rule"], c["steps"], f=c["f"], stats=True)
+        assert st["mma_count"] == c["mma_count"]
+        assert st["max_h"] == c["max_h"] and st["max_r"] == c["max_r"], c
+
+
+def test_fault_injection_detected(ltl, orc):
+    """test_cat_engine.cpp:353-370: a corrupted band entry must diverge or trip the guard."""
+    init = orc.init_random(64, 0.3, 1)
+    rule = "R1,C2,M0,S2..3,B3..3,NM"
+    clean = ltl.run_engine("cat", init, rule, 5)
+    try:
+        faulty = ltl.run_engine("cat", init, rule, 5, inject_fault=True)
+        assert not np.array_equal(faulty, clean)
+    except ltl.LtlLogicError as e:
+        assert "internal consistency: negative neighborhood count" in str(e)
+
+
+def test_virtual_slabs_match_single(ltl, orc):
+    """The multi-GPU slab path (halo rows exchanged between slabs) with every slab
+    on device 0: bit-identical to one slab and to the oracle."""
+    init = orc.init_random(512, 0.26, 3)
+    text = "R16,C2,M0,S170..296,B170..300,NM"
+    expect = orc.simulate(init, parse_rule_text(text), 6)
+    for slabs in (1, 2, 3, 4, 8):
+        with ltl.DeviceTorus(n=512, slabs=slabs, devices=[0] * slabs) as t:
+            t.upload(init)
+            t.run(text, 6)
+            assert np.array_equal(t.download(), expect), slabs
+
+
+def test_steps_zero_is_identity(ltl, orc):
+    init = orc.init_random(64, 0.5, 2)
+    assert np.array_equal(ltl.run_engine("cat", init, "R2,C2,M0,S7..12,B8..11,NM", 0), init)
+
+
+def test_run_errors(ltl):
+    with ltl.DeviceTorus(n=32, f=4) as t:
+        with pytest.raises(ValueError, match="unsupported radius r=5 for fragment side f=4"):
+            t.run("R5,C2,M0,S35..59,B34..45,NM", 1)
+        with pytest.raises(ValueError, match="config error: steps must be >= 0"):
+            t.run("R1,C2,M0,S2..3,B3..3,NM", -1)
+
+
+def test_large_grid_engines_agree(ltl, orc):
+    """At sizes the oracle is slow for: tcgen05 == stencil == oracle on a 4096^2
+    grid for a few generations, at three radii."""
+    init = orc.init_random(4096, 0.3, 11)
+    for text in ("R1,C2,M0,S2..3,B3..3,NM", "R5,C2,M1,S34..58,B34..45,NM",
+                 "R16,C2,M0,S170..296,B170..300,NM"):
+        a = ltl.run_engine("cat", init, text, 2)
+        b = ltl.run_engine("stencil", init, text, 2)
+        assert np.array_equal(a, b), text
+        assert np.array_equal(a, orc.simulate(init, parse_rule_text(text), 2)), text
