@@ -105,6 +105,14 @@ int ltl_download(ltl_ctx* ctx, uint8_t* padded, int32_t layout);
 int ltl_upload_interior(ltl_ctx* ctx, const uint8_t* interior);
 int ltl_download_interior(ltl_ctx* ctx, uint8_t* interior);
 
+/* Deterministic random fill generated on the device, bit-identical to
+ * init_random (src/grid.cpp:61-73): splitmix64 draw k = y * fill + x for the
+ * top-left fill x fill block (fill_n < 0: the whole torus, row-major), alive
+ * iff alive_threshold(draw, density) (src/grid.cpp:21-39); the rest dead.
+ * Errors as the reference ("init_random: density must be in [0, 1]",
+ * "init_random: fill_n exceeds n"). */
+int ltl_init_random(ltl_ctx* ctx, double density, uint64_t seed, int32_t fill_n);
+
 /* --- the hot path --------------------------------------------------------- */
 
 /* `steps` generations (simulate, src/cat_engine.cpp:308-321), each one fused
@@ -137,8 +145,26 @@ int ltl_run_interior(ltl_ctx* ctx, const uint8_t* interior_in, uint8_t* interior
 
 /* --- multi-process slabs (one process per GPU) --------------------------- */
 
-/* Device pointers of slab `slab`'s current generation buffer and its pitch;
- * for exchanging halos through an external transport (NCCL, IPC). */
+/* One slab of a torus that is partitioned across processes (one per GPU):
+ * rows_local x cols interior on `device`, holding global rows
+ * [row0, row0 + rows_local) (used by ltl_init_random).  Its column wrap is refreshed
+ * locally; its 16 halo rows above / below are filled by the caller's
+ * transport (NCCL send/recv, CUDA IPC) from the neighbouring ranks. */
+int ltl_create_part(ltl_ctx** out, int32_t rows_local, int32_t cols, int32_t row0,
+                    int32_t device);
+/* Run slab `slab`'s work on an external CUDA stream (e.g. the one NCCL uses),
+ * so kernels and the halo transport are ordered without host syncs. */
+int ltl_set_stream(ltl_ctx* ctx, int32_t slab, void* stream);
+/* Enqueue exactly one generation (main kernel + local halo refresh), then
+ * flip the generation buffers.  Asynchronous. */
+int ltl_step_part(ltl_ctx* ctx, const ltl_rule_c* rule, uint32_t flags);
+/* Enqueue a halo refresh of the current generation (local column wrap, and
+ * row wrap / peer rows unless the context is a part). */
+int ltl_fill_halo(ltl_ctx* ctx);
+
+/* Device pointers of slab `slab`'s current (which = 0) or other (1)
+ * generation buffer, its pitch and interior row count; for exchanging halos
+ * through an external transport (NCCL, IPC). */
 int ltl_slab_buffer(ltl_ctx* ctx, int32_t slab, int32_t which, void** dev_ptr, int64_t* pitch,
                     int32_t* rows);
 

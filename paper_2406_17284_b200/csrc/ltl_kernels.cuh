@@ -64,6 +64,13 @@ cudaError_t make_store_map(CUtensorMap* map, const SlabView& s);
 cudaError_t launch_stencil_step(const SlabView& in, const SlabView& out, const RuleConsts& rule,
                                 int32_t inject_fault, DeviceStats* stats, cudaStream_t stream);
 
+// ---- device init_random (ltl_init.cu): cell (gy, x) of the global torus gets
+// splitmix64 draw number gy * fill_cols + x when gy < fill_rows and x < fill_cols.
+void density_threshold(double density, int32_t* mode, uint64_t* threshold);
+cudaError_t launch_init_random(const SlabView& s, int32_t row0, int32_t fill_rows,
+                               int32_t fill_cols, double density, uint64_t seed,
+                               cudaStream_t stream);
+
 // ---- periodic halo refresh (ltl_halo.cu)
 // Fills the halo of `self` from the interiors of `above` (rows over the top
 // edge), `below` (rows under the bottom edge) and `self` (column wrap).  For a

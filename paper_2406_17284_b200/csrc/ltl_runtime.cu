@@ -522,6 +522,68 @@ int ltl_run_interior(ltl_ctx* ctx, const uint8_t* interior_in, uint8_t* interior
   });
 }
 
+int ltl_create_part(ltl_ctx** out, int32_t rows_local, int32_t cols, int32_t row0,
+                    int32_t device) {
+  const int32_t dev = device;
+  const int st = ltl_create_torus(out, rows_local, cols, 1, &dev);
+  if (st == LTL_OK) {
+    (*out)->external_row_halo = true;
+    (*out)->slabs[0].row0 = row0;  // global row of the first local row (init_random)
+  }
+  return st;
+}
+
+int ltl_set_stream(ltl_ctx* ctx, int32_t slab, void* stream) {
+  if (!ctx) return LTL_ERR_INVALID_ARGUMENT;
+  return guarded(ctx, [&] {
+    if (slab < 0 || slab >= static_cast<int32_t>(ctx->slabs.size()))
+      throw std::out_of_range("config error: slab index out of range");
+    Slab& s = ctx->slabs[slab];
+    ck(cudaSetDevice(s.dev), "cudaSetDevice");
+    ck(cudaStreamSynchronize(s.stream), "cudaStreamSynchronize");
+    if (s.own_stream) ck(cudaStreamDestroy(s.stream), "cudaStreamDestroy");
+    s.stream = static_cast<cudaStream_t>(stream);
+    s.own_stream = false;
+  });
+}
+
+int ltl_step_part(ltl_ctx* ctx, const ltl_rule_c* rule, uint32_t flags) {
+  if (!ctx) return LTL_ERR_INVALID_ARGUMENT;
+  return guarded(ctx, [&] {
+    check_run_args(ctx, rule, 1);
+    enqueue_step(ctx, rule_consts(*rule), flags, false, nullptr, nullptr);
+  });
+}
+
+int ltl_init_random(ltl_ctx* ctx, double density, uint64_t seed, int32_t fill_n) {
+  if (!ctx) return LTL_ERR_INVALID_ARGUMENT;
+  return guarded(ctx, [&] {
+    if (!(density >= 0.0 && density <= 1.0))
+      throw std::invalid_argument("init_random: density must be in [0, 1]");
+    int32_t fill_rows = ctx->external_row_halo ? ctx->slabs[0].row0 + ctx->rows : ctx->rows;
+    int32_t fill_cols = ctx->cols;
+    if (fill_n >= 0) {
+      if (fill_n > ctx->rows || fill_n > ctx->cols)
+        throw std::invalid_argument("init_random: fill_n exceeds n");
+      fill_rows = fill_cols = fill_n;
+    }
+    for (Slab& s : ctx->slabs) {
+      ck(cudaSetDevice(s.dev), "cudaSetDevice");
+      ck(ltl::launch_init_random(s.view(ctx->cur, ctx->cols), s.row0, fill_rows, fill_cols,
+                                 density, seed, s.stream),
+         "init kernel");
+      if (ctx->slabs.size() > 1) ck(cudaEventRecord(s.ev_step, s.stream), "event");
+    }
+    enqueue_halo(ctx, ctx->cur);
+    sync_all(ctx);
+  });
+}
+
+int ltl_fill_halo(ltl_ctx* ctx) {
+  if (!ctx) return LTL_ERR_INVALID_ARGUMENT;
+  return guarded(ctx, [&] { enqueue_halo(ctx, ctx->cur); });
+}
+
 int ltl_slab_buffer(ltl_ctx* ctx, int32_t slab, int32_t which, void** dev_ptr, int64_t* pitch,
                     int32_t* rows) {
   if (!ctx) return LTL_ERR_INVALID_ARGUMENT;

@@ -194,7 +194,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       __syncwarp();
     };
-    auto pass2 = [&](uint32_t gg, uint32_t oo) {
+    auto pass2 = [&](uint32_t gg, uint32_t oo, bool last) {
       const uint32_t s0 = gg % kA2Slots, s1 = (gg + 1) % kA2Slots, d2 = oo & 1;
       mbar_wait(&a2_full[s0], (gg / kA2Slots) & 1);
       mbar_wait(&a2_full[s1], ((gg + 1) / kA2Slots) & 1);
@@ -215,6 +215,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         mma_commit(&d2_full[d2]);
         mma_commit(&a2_empty[s0]);
+        // the unit's final H chunk is only ever the second operand: free it here
+        if (last) mma_commit(&a2_empty[s1]);
       }
       __syncwarp();
     };
@@ -224,7 +226,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       pass1(g);
       for (int k = 0; k <= nc; ++k) {
         if (k + 1 <= nc) pass1(g + k + 1);
-        if (k >= 1) pass2(g + k - 1, o + k - 1);
+        if (k >= 1) pass2(g + k - 1, o + k - 1, k == nc);
       }
       g += nc + 1;
       o += nc;

@@ -59,7 +59,8 @@ EXPORTS = (
     "ltl_create", "ltl_create_torus", "ltl_destroy", "ltl_last_error", "ltl_rows", "ltl_cols",
     "ltl_num_slabs", "ltl_upload", "ltl_download", "ltl_upload_interior",
     "ltl_download_interior", "ltl_run", "ltl_run_async", "ltl_synchronize", "ltl_time",
-    "ltl_run_interior", "ltl_slab_buffer", "ltl_parse_rule", "ltl_format_rule",
+    "ltl_run_interior", "ltl_create_part", "ltl_set_stream", "ltl_step_part", "ltl_fill_halo",
+    "ltl_slab_buffer", "ltl_init_random", "ltl_parse_rule", "ltl_format_rule",
     "ltl_preset_count", "ltl_preset", "ltl_von_neumann_probe_rule", "ltl_build_info",
 )
 
@@ -99,6 +100,12 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
                       P(ctypes.c_double), P(ctypes.c_double)], ctypes.c_int),
         "ltl_run_interior": ([vp, u8p, u8p, P(ltl_rule_c), ctypes.c_int32, ctypes.c_uint32,
                               P(ltl_stats_c)], ctypes.c_int),
+        "ltl_create_part": ([P(vp), ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32],
+                            ctypes.c_int),
+        "ltl_set_stream": ([vp, ctypes.c_int32, vp], ctypes.c_int),
+        "ltl_step_part": ([vp, P(ltl_rule_c), ctypes.c_uint32], ctypes.c_int),
+        "ltl_fill_halo": ([vp], ctypes.c_int),
+        "ltl_init_random": ([vp, ctypes.c_double, ctypes.c_uint64, ctypes.c_int32], ctypes.c_int),
         "ltl_slab_buffer": ([vp, ctypes.c_int32, ctypes.c_int32, P(vp), P(ctypes.c_int64),
                              P(ctypes.c_int32)], ctypes.c_int),
         "ltl_parse_rule": ([ctypes.c_char_p, P(ltl_rule_c), ctypes.c_char_p, ctypes.c_int32],
@@ -203,13 +210,20 @@ class DeviceTorus:
     """A device-resident torus (one ltl_ctx): row slabs over one or more GPUs."""
 
     def __init__(self, n: int | None = None, f: int = 16, rows: int | None = None,
-                 cols: int | None = None, slabs: int = 1, devices=None):
+                 cols: int | None = None, slabs: int = 1, devices=None,
+                 part_device: int | None = None, part_row0: int = 0):
+        """n (square, fragment side f) or rows x cols (rectangular torus), split
+        into `slabs` row slabs on `devices`.  part_device=d makes this context
+        one rank's slab of a torus partitioned across processes: the rows above
+        and below come from the caller's transport (see step_part)."""
         self.lib = load_library()
         self._ctx = ctypes.c_void_p()
         devs = None
         if devices is not None:
             devs = (ctypes.c_int32 * len(devices))(*devices)
-        if n is not None:
+        if part_device is not None:
+            st = self.lib.ltl_create_part(ctypes.byref(self._ctx), rows, cols, part_row0, part_device)
+        elif n is not None:
             st = self.lib.ltl_create(ctypes.byref(self._ctx), n, f, slabs, devs)
         else:
             st = self.lib.ltl_create_torus(ctypes.byref(self._ctx), rows, cols, slabs, devs)
@@ -251,6 +265,10 @@ class DeviceTorus:
             out = np.empty((self.rows, self.cols), np.uint8)
         self._check(self.lib.ltl_download_interior(self._ctx, _u8(out)))
         return out
+
+    def init_random(self, density: float, seed: int, fill_n: int = -1) -> None:
+        """Device-side init_random (bit-identical to src/grid.cpp:61-73)."""
+        self._check(self.lib.ltl_init_random(self._ctx, density, seed, fill_n))
 
     def upload_padded(self, padded: np.ndarray, layout: int = LAYOUT_ROW_MAJOR) -> None:
         a = np.ascontiguousarray(padded, np.uint8)
@@ -302,6 +320,17 @@ class DeviceTorus:
                                               steps, self._flags(stencil, False),
                                               ctypes.byref(st)))
         return out
+
+    def set_stream(self, stream_ptr: int, slab: int = 0) -> None:
+        self._check(self.lib.ltl_set_stream(self._ctx, slab, ctypes.c_void_p(stream_ptr)))
+
+    def step_part(self, rule, stencil: bool = False) -> None:
+        """Enqueue one generation + local column-halo refresh (async)."""
+        r = as_rule(rule).to_c()
+        self._check(self.lib.ltl_step_part(self._ctx, ctypes.byref(r), self._flags(stencil, False)))
+
+    def fill_halo(self) -> None:
+        self._check(self.lib.ltl_fill_halo(self._ctx))
 
     def slab_buffer(self, slab: int = 0, which: int = 0):
         ptr, pitch, rows = ctypes.c_void_p(), ctypes.c_int64(), ctypes.c_int32()

@@ -146,3 +146,35 @@ def test_large_grid_engines_agree(ltl, orc):
         b = ltl.run_engine("stencil", init, text, 2)
         assert np.array_equal(a, b), text
         assert np.array_equal(a, orc.simulate(init, parse_rule_text(text), 2)), text
+
+
+def test_device_init_random_matches_reference(ltl, orc):
+    """Device init_random == the reference's splitmix64 grid (src/grid.cpp:61-73),
+    including fill_n padding and density edges."""
+    from golden_data import unpack_grid
+    for e in load("kats.json")["init_grids"]:
+        with ltl.DeviceTorus(n=e["n"], f=e["f"]) as t:
+            t.init_random(e["density"], e["seed"], e["fill_n"])
+            assert np.array_equal(t.download(), unpack_grid(e)), e
+    for n, d, seed in ((1024, 0.5, 1), (333, 0.37, 99), (64, 0.0, 5), (64, 1.0, 5),
+                       (128, 2.0 ** -70, 0)):
+        with ltl.DeviceTorus(rows=n, cols=n) as t:
+            t.init_random(d, seed)
+            assert np.array_equal(t.download(), orc.init_random(n, d, seed)), (n, d, seed)
+
+
+def test_partition_single_rank_matches_torus(ltl, orc):
+    """The multi-process slab path (ltl_create_part + ltl_step_part + the row
+    exchange of paper_2406_17284_b200.dist) at world size 1."""
+    from paper_2406_17284_b200.dist import PartitionedTorus
+    part = PartitionedTorus(256, 192, 0, 1, 0)
+    part.init_random(0.21, 1)
+    text = "R5,C2,M1,S34..58,B34..45,NM"
+    for _ in range(5):
+        part.step(text)
+    part.torus.synchronize()
+    init = np.zeros((256, 192), np.uint8)
+    with ltl.DeviceTorus(rows=256, cols=192) as t:
+        t.init_random(0.21, 1)
+        init = t.download()
+    assert np.array_equal(part.torus.download(), orc.simulate(init, parse_rule_text(text), 5))

@@ -11,7 +11,7 @@ from paper_2406_17284_b200 import ltl  # noqa: E402
 
 orc = oracle.Oracle()
 for n, text in ((128, "R1,C2,M0,S2..3,B3..3,NM"), (256, "R5,C2,M1,S34..58,B34..45,NM"),
-                (64, "R2,C2,M0,S4..9,B5..8,NN")):
+                (64, "R2,C2,M0,S2..6,B3..5,NN")):
     rule = ltl.parse_ltl_rule(text)
     init = orc.init_random(n, 0.4, 1)
     exp = orc.simulate(init, rule.ints(), 1)
