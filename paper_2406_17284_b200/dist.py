@@ -100,6 +100,9 @@ class PartitionedTorus:
         self.cols = cols
         self.torus = DeviceTorus(rows=self.rows, cols=cols, part_device=device,
                                  part_row0=self.row0)
+        # kernels and the halo transport must share one stream (no host syncs)
+        import torch
+        self.torus.set_stream(torch.cuda.current_stream(device).cuda_stream)
 
     def use_stream(self, stream_ptr: int) -> None:
         self.torus.set_stream(stream_ptr)
