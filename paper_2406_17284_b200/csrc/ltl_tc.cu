@@ -7,31 +7,40 @@
 // fragments pi1/pi2/pi3 (src/fragment.cpp:23-41).  Here the same banded
 // products run on the 5th-generation tensor cores in their native shapes:
 //
-//   tile     = a 128-column strip of the slab, streamed down in 32-row chunks
-//   pass 1   D1[x][y] = sum_k A1[x][k] * X[y][k]          (tcgen05.mma kind::i8,
-//            A1 = 128 x 160 band (SMEM, resident), X = TMA-loaded 32 x 160 chunk,
-//            M = 128 (x), N = 32 (y), K = 160 = 5 MMAs of K = 32)
-//            A1[x][k] = [|k-16-x| <= r] + 128*[k == x+16]: the extra 128 at
-//            the centre rides the cell state out in bit 7 of D1 for free.
-//   convert  epilogue warps: D1 (s32, TMEM) -> bytes, H = D1 & 0x7F and the
-//            state bit -> tcgen05.st back into TMEM as the K-major A operand
-//            of pass 2 (no SMEM round trip, no transposition).
-//   pass 2   D2[x][n] = sum_k H[x][k] * Bv[k][n] over the 64 H rows around
-//            each 32-row output chunk (2 MMAs, A from TMEM, band B in SMEM).
-//            Von Neumann adds  X^T * Bv + H^T * Iv  instead (4 MMAs).
-//   epilogue D2 -> rule (apply_transition, src/rule.cpp:99-111) -> bytes ->
-//            SMEM staging -> TMA store of the next generation.
+//   tile     a 128-column strip of the slab, streamed down in 32-row chunks
+//   pass 1   D1[x][y] = sum_k A1[x][k] * X[y][k]            tcgen05.mma kind::i8
+//            A1 = 128 x 160 band, resident in SMEM; X = TMA-loaded 32 x 160
+//            chunk (K-major, SWIZZLE_32B); M = 128 (x), N = 32 (y), K = 5 x 32.
+//            A1[x][k] = [|k-16-x| <= r] + 128*[k == x+16]: the extra 128 on
+//            the centre carries the cell state out in bit 7 (H <= 33 < 128).
+//   convert  epilogue: D1 (s32 in TMEM) -> two byte planes written back into
+//            TMEM as K-major A operands of pass 2 (no SMEM round trip):
+//              Moore: H = D1 & 0x7F and S = D1 & 0x80 (state * 128)
+//              VN   : H' = D1 (= H + 128*state) and s = state
+//   pass 2   D2[x][j] = sum over the 64 H rows around output chunk c
+//              Moore: H*Bv + S*(16*Iv)  = R_box   + 2048*state
+//              VN   : H'*Iv + s*Bv      = R_cross + 128*state
+//            4 MMAs (A from TMEM, band B from SMEM).  Folding the state into
+//            the accumulator makes the birth/survival rule (apply_transition,
+//            src/rule.cpp:99-111) a pure function of one 12-bit number Z.
+//   rule     Z is read back two cells per register (16-bit lanes); the two
+//            range tests (dead: b1..b2, live: K+s1'..K+s2') are four biased
+//            adds and two LOP3s per register (bit 15 of each lane = result).
+//   store    the D2 columns are permuted (pi, below) so that stmatrix.trans
+//            writes each 16x256b TMEM fragment straight into a row-major,
+//            SWIZZLE_128B staging tile -> TMA store of the next generation.
 //
-// Every quantity is an exact small integer (H <= 33, R <= 1089 < 2^31), so the
-// s32 accumulation is bit-exact with the reference's int32 loops.
+// Every quantity is an exact small integer (H <= 33, R <= 1089, Z < 4096), so
+// the result is bit-identical to the reference's int32 loops.
 //
 // Warp roles (192 threads): warp 0 TMA producer, warp 1 MMA issuer + TMEM
 // owner, warps 2..5 epilogue (warp w owns TMEM lanes 32*(w%4)..+32, i.e. 32
-// columns of the strip).  Persistent CTAs walk (strip, row-segment) work units.
+// columns of the strip).  Persistent CTAs (2 per SM) walk (strip, segment) units.
 #include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 
 #include "ltl_kernels.cuh"
 #include "ptx_sm100.cuh"
@@ -49,24 +58,26 @@ constexpr int kXStages = 4;
 constexpr int kA2Slots = 4;
 constexpr int kThreads = 192;
 constexpr int kEpiThreads = 128;
+constexpr int kNumBands = 6;  // Bv0, Bv1, Iv0, Iv1, 16*Iv0, 16*Iv1
 
 // Shared-memory carve-up (offsets from a 1024-aligned base).
-constexpr uint32_t kSmemA1 = 0;                                   // 5 x 128 x 32 B
-constexpr uint32_t kSmemBand = kSmemA1 + kKChunks * 128 * 32;     // Bv0, Bv1, Iv0, Iv1: 4 x 1 KB
-constexpr uint32_t kSmemX = kSmemBand + 4 * 1024;                 // kXStages x 5 KB
-constexpr uint32_t kXStageBytes = kKChunks * kChunkRows * 32;     // 5120
-constexpr uint32_t kSmemStage = kSmemX + kXStages * kXStageBytes;  // 2 x 4 KB output staging
-constexpr uint32_t kStageBytes = kChunkRows * kStripCols;         // 4096
+constexpr uint32_t kSmemA1 = 0;                                    // 5 x 128 x 32 B
+constexpr uint32_t kSmemBand = kSmemA1 + kKChunks * 128 * 32;      // 6 x 1 KB
+constexpr uint32_t kSmemX = kSmemBand + kNumBands * 1024;          // kXStages x 5 KB
+constexpr uint32_t kXStageBytes = kKChunks * kChunkRows * 32;      // 5120
+constexpr uint32_t kSmemStage = kSmemX + kXStages * kXStageBytes;  // 2 x 4 KB staging (SW128)
+constexpr uint32_t kStageBytes = kChunkRows * kStripCols;          // 4096
 constexpr uint32_t kSmemBars = kSmemStage + 2 * kStageBytes;
 constexpr uint32_t kNumBars = 2 * kXStages + 2 * 2 + 2 * kA2Slots + 2 * 2;
 constexpr uint32_t kSmemTotal = kSmemBars + kNumBars * 8 + 16;
 constexpr uint32_t kSmemAlloc = kSmemTotal + 1024;  // alignment slack
+static_assert(kSmemStage % 1024 == 0, "SWIZZLE_128B staging needs 1024-byte alignment");
 
-// TMEM columns (allocation of 256).
+// TMEM columns (allocation of 256 -> two CTAs per SM).
 constexpr uint32_t kTmemCols = 256;
 constexpr uint32_t kTmemD1 = 0;    // 2 x 32
 constexpr uint32_t kTmemD2 = 64;   // 2 x 32
-constexpr uint32_t kTmemA2 = 128;  // kA2Slots x 16 (H part +0, state part +8)
+constexpr uint32_t kTmemA2 = 128;  // kA2Slots x 16 (plane 0 at +0, plane 1 at +8)
 
 constexpr uint32_t kIdescM128N32 = idesc_i8_u8u8_s32(128, 32);
 
@@ -78,12 +89,34 @@ struct Params {
   DeviceStats* stats;
 };
 
-__device__ __forceinline__ uint32_t pack_low_bytes(uint32_t a, uint32_t b, uint32_t c,
-                                                   uint32_t d) {
-  return __byte_perm(__byte_perm(a, b, 0x0040), __byte_perm(c, d, 0x0040), 0x5410);
+// D2 column j holds output row pi(j).  With j = [e, m, a0, a1, v] (bit 0
+// first), pi(j) = [e, a0, a1, m, v]: the stmatrix fragment of column group
+// (m, v) then covers the 8 consecutive output rows 8*(m + 2v) .. +7.
+__host__ __device__ constexpr int out_row_of_col(int j) {
+  return (j & 1) | (((j >> 2) & 3) << 1) | (((j >> 1) & 1) << 3) | (j & 16);
 }
 
-__global__ void __launch_bounds__(kThreads, 1)
+__device__ __forceinline__ uint32_t pack_pairs(uint32_t p0, uint32_t p1) {
+  return __byte_perm(p0, p1, 0x6420);  // low bytes of four 16-bit lanes
+}
+
+// Two cells per register: lanes hold Z = R + K*state (< 4096).  Bit 15 (31)
+// of the result is the next state of the low (high) cell.
+struct SimdRule {
+  uint32_t ca, cb, cc, cd;
+};
+
+__device__ __forceinline__ uint32_t rule_pair(uint32_t z, const SimdRule& k) {
+  const uint32_t a = z + k.ca;  // Z >= b1
+  const uint32_t b = z + k.cb;  // Z >  b2
+  const uint32_t c = z + k.cc;  // Z >= K + s1'
+  const uint32_t d = z + k.cd;  // Z >  K + s2'
+  const uint32_t e = lop3<0xBA>(a, b, c);  // (a & ~b) | c
+  return lop3<0x70>(e, c, d);             // e & ~(c & d)
+}
+
+template <bool kChecked>
+__global__ void __launch_bounds__(kThreads, 2)
     ltl_tc_step_kernel(const __grid_constant__ CUtensorMap load_map,
                        const __grid_constant__ CUtensorMap store_map, const Params p) {
   extern __shared__ uint8_t smem_raw[];
@@ -116,15 +149,20 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     smem[kSmemA1 + (k / 32) * 4096 + sw32_offset(m, k % 32)] = static_cast<uint8_t>(v);
   }
-  for (uint32_t i = threadIdx.x; i < 4u * 32u * 32u; i += kThreads) {
-    const int t = static_cast<int>(i / 1024), n = static_cast<int>((i / 32) % 32),
+  for (uint32_t i = threadIdx.x; i < kNumBands * 32u * 32u; i += kThreads) {
+    const int t = static_cast<int>(i / 1024), j = static_cast<int>((i / 32) % 32),
               k = static_cast<int>(i % 32);
+    const int n = out_row_of_col(j);  // output row of D2 column j (row 16+n of the window)
     int v;
-    if (t == 0) v = (k - 16 - n >= -r && k - 16 - n <= r);
-    else if (t == 1) v = (k + 16 - n >= -r && k + 16 - n <= r);
-    else if (t == 2) v = (k == n + 16);
-    else v = (k + 16 == n);
-    smem[kSmemBand + t * 1024 + sw32_offset(n, k)] = static_cast<uint8_t>(v);
+    switch (t) {
+      case 0: v = (k - 16 - n >= -r && k - 16 - n <= r); break;  // H rows of chunk c
+      case 1: v = (k + 16 - n >= -r && k + 16 - n <= r); break;  // H rows of chunk c+1
+      case 2: v = (k == n + 16); break;                          // centre row, chunk c
+      case 3: v = (k + 16 == n); break;                          // centre row, chunk c+1
+      case 4: v = 16 * (k == n + 16); break;                     // 16 * centre (state*2048)
+      default: v = 16 * (k + 16 == n); break;
+    }
+    smem[kSmemBand + t * 1024 + sw32_offset(j, k)] = static_cast<uint8_t>(v);
   }
   fence_proxy_async_smem();
   if (warp == 0 && lane == 0) {
@@ -175,8 +213,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else if (warp == 1) {
     // ================= MMA issuer =================
     const uint32_t a1_base = smem_u32(smem + kSmemA1);
-    const uint32_t band_base = smem_u32(smem + kSmemBand);
+    const uint32_t band = smem_u32(smem + kSmemBand);
     const uint32_t x_base = smem_u32(smem + kSmemX);
+    // pass-2 operand pairing: {A plane, B band} for the 4 MMAs of a chunk
+    const uint32_t p0_b0 = band + (vn ? 2048 : 0), p0_b1 = band + (vn ? 3072 : 1024);
+    const uint32_t p1_b0 = band + (vn ? 0 : 4096), p1_b1 = band + (vn ? 1024 : 5120);
     uint32_t g = 0, o = 0;
     auto pass1 = [&](uint32_t gg) {
       const uint32_t s = gg % kXStages, d1 = gg & 1;
@@ -203,16 +244,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (elect_one()) {
         const uint32_t dcol = tmem + kTmemD2 + 32 * d2;
         const uint32_t a0 = tmem + kTmemA2 + 16 * s0, a1 = tmem + kTmemA2 + 16 * s1;
-        if (!vn) {
-          mma_i8_ts(dcol, a0, smem_desc_sw32_kmajor(band_base + 0), kIdescM128N32, 0);
-          mma_i8_ts(dcol, a1, smem_desc_sw32_kmajor(band_base + 1024), kIdescM128N32, 1);
-        } else {
-          // cross sum: vertical window over the states + the row window at the centre
-          mma_i8_ts(dcol, a0 + 8, smem_desc_sw32_kmajor(band_base + 0), kIdescM128N32, 0);
-          mma_i8_ts(dcol, a1 + 8, smem_desc_sw32_kmajor(band_base + 1024), kIdescM128N32, 1);
-          mma_i8_ts(dcol, a0, smem_desc_sw32_kmajor(band_base + 2048), kIdescM128N32, 1);
-          mma_i8_ts(dcol, a1, smem_desc_sw32_kmajor(band_base + 3072), kIdescM128N32, 1);
-        }
+        mma_i8_ts(dcol, a0, smem_desc_sw32_kmajor(p0_b0), kIdescM128N32, 0);
+        mma_i8_ts(dcol, a1, smem_desc_sw32_kmajor(p0_b1), kIdescM128N32, 1);
+        mma_i8_ts(dcol, a0 + 8, smem_desc_sw32_kmajor(p1_b0), kIdescM128N32, 1);
+        mma_i8_ts(dcol, a1 + 8, smem_desc_sw32_kmajor(p1_b1), kIdescM128N32, 1);
         mma_commit(&d2_full[d2]);
         mma_commit(&a2_empty[s0]);
         // the unit's final H chunk is only ever the second operand: free it here
@@ -233,50 +268,77 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else {
     // ================= epilogue (4 warps, 128 threads) =================
-    const uint32_t q = warp & 3;            // TMEM lane quarter
-    const uint32_t m = q * 32 + lane;       // column within the strip
+    const uint32_t q = warp & 3;  // TMEM lane quarter = 32 strip columns
     const uint32_t trow = tmem + ((q * 32) << 16);
     const bool is_store_thread = (warp == 2 && lane == 0);
-    uint8_t* stage_base = smem + kSmemStage;
-    int32_t max_h = 0, max_r = 0, bad = 0;
-    uint32_t g = 0, o = 0;
+    const uint32_t stage_base = smem_u32(smem + kSmemStage);
     const RuleConsts rc = p.rule;
+    const uint32_t K = vn ? 128u : 2048u;
+    SimdRule sr;
+    sr.ca = (0x8000u - rc.lo_dead) * 0x10001u;
+    sr.cb = (0x7FFFu - (rc.lo_dead + rc.w_dead)) * 0x10001u;
+    sr.cc = (0x8000u - (K + rc.lo_live)) * 0x10001u;
+    sr.cd = (0x7FFFu - (K + rc.lo_live + rc.w_live)) * 0x10001u;
+    const uint32_t g_live = (0x8000u - K) * 0x10001u;
+    const uint32_t g_neg = (0x8000u - (K + rc.neg_live)) * 0x10001u;
+    const uint32_t r_mask = (K - 1) * 0x10001u;
+    uint32_t max_h = 0, max_r = 0, bad = 0;
+    // stmatrix row address of this thread: staging row `lane`, 16-byte chunk
+    // (2q + h) of the 128-byte row, SWIZZLE_128B (chunk ^= row % 8)
+    const uint32_t row_off = lane * 128;
+    const uint32_t chunk_h0 = ((2 * q + 0) ^ (lane & 7)) << 4;
+    const uint32_t chunk_h1 = ((2 * q + 1) ^ (lane & 7)) << 4;
+    uint32_t g = 0, o = 0;
 
     for (int u = blockIdx.x; u < p.num_units; u += gridDim.x) {
       const int strip = u % p.num_strips, seg = u / p.num_strips;
       const int c0 = seg * p.seg;
       const int nc = min(p.seg, p.chunks - c0);
-      uint32_t st_prev[8], st_cur[8];  // state bytes (0/1), 4 rows per word
 
-      auto output_chunk = [&](int c, const uint32_t (&sa)[8], const uint32_t (&sb)[8]) {
+      auto output_chunk = [&](int c) {
         const uint32_t oo = o + c, d2 = oo & 1;
         mbar_wait(&d2_full[d2], (oo >> 1) & 1);
         tc_fence_after();
-        uint32_t v[32];
-        tmem_ld_32x32b_x32(trow + kTmemD2 + 32 * d2, v);
+        uint32_t z0[8], z1[8];
+        tmem_ld_16x256b_x2_pack16(trow + kTmemD2 + 32 * d2, z0);
+        tmem_ld_16x256b_x2_pack16(trow + (16u << 16) + kTmemD2 + 32 * d2, z1);
         tmem_ld_wait();
         tc_fence_before();
         mbar_arrive(&d2_empty[d2]);
+        uint32_t w0[4], w1[4];
+#pragma unroll
+        for (int v = 0; v < 2; ++v) {
+          const uint32_t a0 = rule_pair(z0[4 * v + 0], sr), b0 = rule_pair(z0[4 * v + 1], sr);
+          const uint32_t a2 = rule_pair(z0[4 * v + 2], sr), b2 = rule_pair(z0[4 * v + 3], sr);
+          w0[2 * v + 0] = prmt(a0, a2, 0xFDB9) & 0x01010101u;
+          w0[2 * v + 1] = prmt(b0, b2, 0xFDB9) & 0x01010101u;
+          const uint32_t c0r = rule_pair(z1[4 * v + 0], sr), d0r = rule_pair(z1[4 * v + 1], sr);
+          const uint32_t c2r = rule_pair(z1[4 * v + 2], sr), d2r = rule_pair(z1[4 * v + 3], sr);
+          w1[2 * v + 0] = prmt(c0r, c2r, 0xFDB9) & 0x01010101u;
+          w1[2 * v + 1] = prmt(d0r, d2r, 0xFDB9) & 0x01010101u;
+        }
+        if constexpr (kChecked) {
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const uint32_t z = h ? z1[i] : z0[i];
+              max_r = __vmaxu2(max_r, z & r_mask);
+              bad |= (z + g_live) & ~(z + g_neg) & 0x80008000u;  // live and count < 0
+            }
+          }
+        }
         // staging buffer oo&1 was last read by the TMA store of chunk oo-2
         if (is_store_thread) tma_store_wait_read<1>();
         named_barrier(1, kEpiThreads);
-        uint8_t* stage = stage_base + d2 * kStageBytes;
-#pragma unroll
-        for (int n = 0; n < 32; ++n) {
-          // output row n = H-chunk c row 16+n (n < 16) or H-chunk c+1 row n-16
-          const uint32_t w = (n < 16) ? sa[4 + n / 4] : sb[(n - 16) / 4];
-          const uint32_t st = (w >> (8 * (n & 3))) & 1u;
-          const int32_t R = static_cast<int32_t>(v[n]);
-          max_r = max(max_r, R);
-          const int32_t lo = st ? rc.lo_live : rc.lo_dead;
-          const uint32_t wd = static_cast<uint32_t>(st ? rc.w_live : rc.w_dead);
-          bad |= (st && R < rc.neg_live);
-          stage[n * kStripCols + m] = (static_cast<uint32_t>(R - lo) <= wd) ? 1 : 0;
-        }
+        const uint32_t stage = stage_base + d2 * kStageBytes + row_off;
+        stmatrix_x4_trans_b8(stage + chunk_h0, w0[0], w0[1], w0[2], w0[3]);
+        stmatrix_x4_trans_b8(stage + chunk_h1, w1[0], w1[1], w1[2], w1[3]);
         fence_proxy_async_smem();
         named_barrier(1, kEpiThreads);
         if (is_store_thread) {
-          tma_store_2d(&store_map, stage, strip * kStripCols, (c0 + c) * kChunkRows);
+          tma_store_2d(&store_map, smem + kSmemStage + d2 * kStageBytes, strip * kStripCols,
+                       (c0 + c) * kChunkRows);
           tma_store_commit();
         }
       };
@@ -285,54 +347,53 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t gg = g + k, d1 = gg & 1, s = gg % kA2Slots;
         mbar_wait(&d1_full[d1], (gg >> 1) & 1);
         tc_fence_after();
-        uint32_t v[32];
-        tmem_ld_32x32b_x32(trow + kTmemD1 + 32 * d1, v);
+        uint32_t v[16];
+        tmem_ld_32x32b_x16_pack16(trow + kTmemD1 + 32 * d1, v);
         tmem_ld_wait();
         tc_fence_before();
         mbar_arrive(&d1_empty[d1]);
-        uint32_t hw[8], sw[8];
+        uint32_t plane0[8], plane1[8];
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
-          const uint32_t raw = pack_low_bytes(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
-          hw[j] = raw & 0x7F7F7F7Fu;
-          sw[j] = (raw >> 7) & 0x01010101u;
-          if (p.stats) {
-            const uint32_t mx = __vmaxu4(hw[j], hw[j] >> 16);
-            max_h = max(max_h, static_cast<int32_t>(max(mx & 0xFF, (mx >> 8) & 0xFF)));
+          const uint32_t raw = pack_pairs(v[2 * j], v[2 * j + 1]);  // 4 rows of H + 128*state
+          if (vn) {
+            plane0[j] = raw;
+            plane1[j] = (raw >> 7) & 0x01010101u;
+          } else {
+            plane0[j] = raw & 0x7F7F7F7Fu;
+            plane1[j] = raw & 0x80808080u;
           }
+          if constexpr (kChecked) max_h = __vmaxu4(max_h, raw & 0x7F7F7F7Fu);
         }
         mbar_wait(&a2_empty[s], ((gg / kA2Slots) & 1) ^ 1);
         tc_fence_after();
-        tmem_st_32x32b_x8(trow + kTmemA2 + 16 * s, hw);
-        if (vn) tmem_st_32x32b_x8(trow + kTmemA2 + 16 * s + 8, sw);
+        tmem_st_32x32b_x8(trow + kTmemA2 + 16 * s, plane0);
+        tmem_st_32x32b_x8(trow + kTmemA2 + 16 * s + 8, plane1);
         tmem_st_wait();
         tc_fence_before();
         mbar_arrive(&a2_full[s]);
-        // rotate the state words: st_prev <- st_cur <- this chunk
-        if (k >= 2) output_chunk(k - 2, st_prev, st_cur);
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          st_prev[j] = st_cur[j];
-          st_cur[j] = sw[j];
-        }
+        if (k >= 2) output_chunk(k - 2);
       }
-      if (nc >= 1) output_chunk(nc - 1, st_prev, st_cur);
+      if (nc >= 1) output_chunk(nc - 1);
       g += nc + 1;
       o += nc;
     }
     if (is_store_thread) tma_store_wait_all<0>();
-    if (p.stats) {
+    if constexpr (kChecked) {
+      int32_t mh = static_cast<int32_t>(max(max(max_h & 0xFF, (max_h >> 8) & 0xFF),
+                                            max((max_h >> 16) & 0xFF, max_h >> 24)));
+      int32_t mr = static_cast<int32_t>(max(max_r & 0xFFFF, max_r >> 16));
 #pragma unroll
       for (int off = 16; off > 0; off >>= 1) {
-        max_h = max(max_h, __shfl_xor_sync(0xffffffffu, max_h, off));
-        max_r = max(max_r, __shfl_xor_sync(0xffffffffu, max_r, off));
+        mh = max(mh, __shfl_xor_sync(0xffffffffu, mh, off));
+        mr = max(mr, __shfl_xor_sync(0xffffffffu, mr, off));
       }
       if (lane == 0) {
-        atomicMax(&p.stats->max_h, max_h);
-        atomicMax(&p.stats->max_r, max_r);
+        atomicMax(&p.stats->max_h, mh);
+        atomicMax(&p.stats->max_r, mr);
       }
+      if (__any_sync(0xffffffffu, bad != 0) && lane == 0) atomicOr(&p.stats->error, 1);
     }
-    if (__any_sync(0xffffffffu, bad) && lane == 0 && p.stats) atomicOr(&p.stats->error, 1);
   }
 
   __syncwarp();
@@ -346,15 +407,17 @@ __global__ void __launch_bounds__(kThreads, 1)
 size_t tc_smem_bytes() { return kSmemAlloc; }
 
 cudaError_t launch_tc_step(const TcLaunch& a, cudaStream_t stream) {
-  static int num_sms = 0;
+  static int num_sms = 0, ctas_per_sm = 2;
   if (num_sms == 0) {
     int dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaError_t e = cudaFuncSetAttribute(ltl_tc_step_kernel,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(kSmemAlloc));
-    if (e != cudaSuccess) return e;
+    if (const char* e = std::getenv("LTL_TC_CTAS_PER_SM")) ctas_per_sm = std::atoi(e) > 1 ? 2 : 1;
+    for (auto fn : {ltl_tc_step_kernel<false>, ltl_tc_step_kernel<true>}) {
+      cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           static_cast<int>(kSmemAlloc));
+      if (e != cudaSuccess) return e;
+    }
   }
   if (a.rows <= 0 || a.cols <= 0) return cudaSuccess;
   Params p{};
@@ -362,10 +425,12 @@ cudaError_t launch_tc_step(const TcLaunch& a, cudaStream_t stream) {
   p.cols = a.cols;
   p.num_strips = (a.cols + kStripCols - 1) / kStripCols;
   p.chunks = (a.rows + kChunkRows - 1) / kChunkRows;
+  const int slots = num_sms * ctas_per_sm;
   int seg = a.seg_chunks;
   if (seg <= 0) {
-    // enough units for ~4 per CTA slot, but never shorter than 4 chunks when avoidable
-    const int64_t target_units = 4LL * num_sms;
+    // ~4 units per CTA slot for balance, segments as long as that allows (the
+    // extra halo chunk per unit costs 1/seg of the input traffic)
+    const int64_t target_units = 4LL * slots;
     const int64_t per_strip = (target_units + p.num_strips - 1) / p.num_strips;
     seg = static_cast<int>((p.chunks + per_strip - 1) / per_strip);
     seg = seg < 1 ? 1 : (seg > 64 ? 64 : seg);
@@ -376,9 +441,12 @@ cudaError_t launch_tc_step(const TcLaunch& a, cudaStream_t stream) {
   p.rule = a.rule;
   p.inject_fault = a.inject_fault;
   p.stats = a.stats;
-  int grid = a.grid > 0 ? a.grid : num_sms;
+  int grid = a.grid > 0 ? a.grid : slots;
   if (grid > p.num_units) grid = p.num_units;
-  ltl_tc_step_kernel<<<grid, kThreads, kSmemAlloc, stream>>>(*a.load_map, *a.store_map, p);
+  if (a.stats)
+    ltl_tc_step_kernel<true><<<grid, kThreads, kSmemAlloc, stream>>>(*a.load_map, *a.store_map, p);
+  else
+    ltl_tc_step_kernel<false><<<grid, kThreads, kSmemAlloc, stream>>>(*a.load_map, *a.store_map, p);
   return cudaGetLastError();
 }
 
