@@ -28,14 +28,15 @@
 //            adds and two LOP3s per register (bit 15 of each lane = result).
 //   store    the D2 columns are permuted (pi, below) so that stmatrix.trans
 //            writes each 16x256b TMEM fragment straight into a row-major,
-//            SWIZZLE_128B staging tile -> TMA store of the next generation.
+//            SWIZZLE_32B 32x32 staging tile per warp -> TMA store of the next
+//            generation (no CTA-wide barrier on the output path).
 //
 // Every quantity is an exact small integer (H <= 33, R <= 1089, Z < 4096), so
 // the result is bit-identical to the reference's int32 loops.
 //
-// Warp roles (192 threads): warp 0 TMA producer, warp 1 MMA issuer + TMEM
-// owner, warps 2..5 epilogue (warp w owns TMEM lanes 32*(w%4)..+32, i.e. 32
-// columns of the strip).  Persistent CTAs (2 per SM) walk (strip, segment) units.
+// Warp roles (320 threads): warp 0 TMA producer, warp 1 MMA issuer + TMEM
+// owner, warps 2..5 convert D1, warps 6..9 rule + store D2 (warp w owns TMEM
+// lanes 32*(w%4)..+32, i.e. 32 columns of the strip).  Persistent CTAs (2 per SM) walk (strip, segment) units.
 #include <cuda.h>
 #include <cuda_runtime.h>
 
@@ -56,8 +57,9 @@ constexpr int kKTile = 160;      // 128 + 2*16 input columns per strip
 constexpr int kKChunks = kKTile / 32;
 constexpr int kXStages = 4;
 constexpr int kA2Slots = 4;
-constexpr int kThreads = 192;
-constexpr int kEpiThreads = 128;
+constexpr int kGroupWarps = 4;   // warps per epilogue group (one per TMEM lane quarter)
+constexpr int kThreads = 64 + 2 * 32 * kGroupWarps;  // producer, MMA, convert x4, output x4
+constexpr int kEpiThreads = 32 * kGroupWarps;
 constexpr int kNumBands = 6;  // Bv0, Bv1, Iv0, Iv1, 16*Iv0, 16*Iv1
 
 // Shared-memory carve-up (offsets from a 1024-aligned base).
@@ -66,12 +68,12 @@ constexpr uint32_t kSmemBand = kSmemA1 + kKChunks * 128 * 32;      // 6 x 1 KB
 constexpr uint32_t kSmemX = kSmemBand + kNumBands * 1024;          // kXStages x 5 KB
 constexpr uint32_t kXStageBytes = kKChunks * kChunkRows * 32;      // 5120
 constexpr uint32_t kSmemStage = kSmemX + kXStages * kXStageBytes;  // 2 x 4 KB staging (SW128)
-constexpr uint32_t kStageBytes = kChunkRows * kStripCols;          // 4096
+constexpr uint32_t kStageBytes = kChunkRows * kStripCols;          // 4096 (4 warps x 1 KB)
 constexpr uint32_t kSmemBars = kSmemStage + 2 * kStageBytes;
 constexpr uint32_t kNumBars = 2 * kXStages + 2 * 2 + 2 * kA2Slots + 2 * 2;
 constexpr uint32_t kSmemTotal = kSmemBars + kNumBars * 8 + 16;
 constexpr uint32_t kSmemAlloc = kSmemTotal + 1024;  // alignment slack
-static_assert(kSmemStage % 1024 == 0, "SWIZZLE_128B staging needs 1024-byte alignment");
+static_assert(kSmemStage % 1024 == 0, "swizzled staging needs aligned slots");
 
 // TMEM columns (allocation of 256 -> two CTAs per SM).
 constexpr uint32_t kTmemCols = 256;
@@ -266,12 +268,58 @@ __global__ void __launch_bounds__(kThreads, 2)
       g += nc + 1;
       o += nc;
     }
-  } else {
-    // ================= epilogue (4 warps, 128 threads) =================
+  } else if (warp < 2 + kGroupWarps) {
+    // ================= convert warps (D1 -> pass-2 A planes) =================
     const uint32_t q = warp & 3;  // TMEM lane quarter = 32 strip columns
     const uint32_t trow = tmem + ((q * 32) << 16);
-    const bool is_store_thread = (warp == 2 && lane == 0);
-    const uint32_t stage_base = smem_u32(smem + kSmemStage);
+    uint32_t max_h = 0, g = 0;
+    for (int u = blockIdx.x; u < p.num_units; u += gridDim.x) {
+      const int seg = u / p.num_strips;
+      const int nc = min(p.seg, p.chunks - seg * p.seg);
+      for (int k = 0; k <= nc; ++k, ++g) {
+        const uint32_t d1 = g & 1, s = g % kA2Slots;
+        mbar_wait(&d1_full[d1], (g >> 1) & 1);
+        tc_fence_after();
+        uint32_t v[16];
+        tmem_ld_32x32b_x16_pack16(trow + kTmemD1 + 32 * d1, v);
+        tmem_ld_wait();
+        tc_fence_before();
+        mbar_arrive(&d1_empty[d1]);
+        uint32_t plane0[8], plane1[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const uint32_t raw = pack_pairs(v[2 * j], v[2 * j + 1]);  // 4 rows of H + 128*state
+          if (vn) {
+            plane0[j] = raw;
+            plane1[j] = (raw >> 7) & 0x01010101u;
+          } else {
+            plane0[j] = raw & 0x7F7F7F7Fu;
+            plane1[j] = raw & 0x80808080u;
+          }
+          if constexpr (kChecked) max_h = __vmaxu4(max_h, raw & 0x7F7F7F7Fu);
+        }
+        mbar_wait(&a2_empty[s], ((g / kA2Slots) & 1) ^ 1);
+        tc_fence_after();
+        tmem_st_32x32b_x8(trow + kTmemA2 + 16 * s, plane0);
+        tmem_st_32x32b_x8(trow + kTmemA2 + 16 * s + 8, plane1);
+        tmem_st_wait();
+        tc_fence_before();
+        mbar_arrive(&a2_full[s]);
+      }
+    }
+    if constexpr (kChecked) {
+      int32_t mh = static_cast<int32_t>(max(max(max_h & 0xFF, (max_h >> 8) & 0xFF),
+                                            max((max_h >> 16) & 0xFF, max_h >> 24)));
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) mh = max(mh, __shfl_xor_sync(0xffffffffu, mh, off));
+      if (lane == 0) atomicMax(&p.stats->max_h, mh);
+    }
+  } else {
+    // ================= output warps (D2 -> rule -> next generation) ==========
+    // Each warp owns 32 strip columns and its own staging slots and TMA
+    // stores, so the output path needs no CTA-wide barrier.
+    const uint32_t q = warp & 3;
+    const uint32_t trow = tmem + ((q * 32) << 16);
     const RuleConsts rc = p.rule;
     const uint32_t K = vn ? 128u : 2048u;
     SimdRule sr;
@@ -282,22 +330,21 @@ __global__ void __launch_bounds__(kThreads, 2)
     const uint32_t g_live = (0x8000u - K) * 0x10001u;
     const uint32_t g_neg = (0x8000u - (K + rc.neg_live)) * 0x10001u;
     const uint32_t r_mask = (K - 1) * 0x10001u;
-    uint32_t max_h = 0, max_r = 0, bad = 0;
-    // stmatrix row address of this thread: staging row `lane`, 16-byte chunk
-    // (2q + h) of the 128-byte row, SWIZZLE_128B (chunk ^= row % 8)
-    const uint32_t row_off = lane * 128;
-    const uint32_t chunk_h0 = ((2 * q + 0) ^ (lane & 7)) << 4;
-    const uint32_t chunk_h1 = ((2 * q + 1) ^ (lane & 7)) << 4;
-    uint32_t g = 0, o = 0;
-
+    uint32_t max_r = 0, bad = 0;
+    // staging: per warp 2 slots of [32 rows][32 B], SWIZZLE_32B (16-byte
+    // chunk ^= (row >> 2) & 1); this thread addresses row `lane`.
+    uint8_t* my_stage = smem + kSmemStage + q * 1024;
+    const uint32_t stage_u32 = smem_u32(my_stage);
+    const uint32_t addr_h0 = lane * 32 + ((0u ^ ((lane >> 2) & 1)) << 4);
+    const uint32_t addr_h1 = lane * 32 + ((1u ^ ((lane >> 2) & 1)) << 4);
+    uint32_t o = 0;
     for (int u = blockIdx.x; u < p.num_units; u += gridDim.x) {
       const int strip = u % p.num_strips, seg = u / p.num_strips;
       const int c0 = seg * p.seg;
       const int nc = min(p.seg, p.chunks - c0);
-
-      auto output_chunk = [&](int c) {
-        const uint32_t oo = o + c, d2 = oo & 1;
-        mbar_wait(&d2_full[d2], (oo >> 1) & 1);
+      for (int c = 0; c < nc; ++c, ++o) {
+        const uint32_t d2 = o & 1;
+        mbar_wait(&d2_full[d2], (o >> 1) & 1);
         tc_fence_after();
         uint32_t z0[8], z1[8];
         tmem_ld_16x256b_x2_pack16(trow + kTmemD2 + 32 * d2, z0);
@@ -328,70 +375,27 @@ __global__ void __launch_bounds__(kThreads, 2)
             }
           }
         }
-        // staging buffer oo&1 was last read by the TMA store of chunk oo-2
-        if (is_store_thread) tma_store_wait_read<1>();
-        named_barrier(1, kEpiThreads);
-        const uint32_t stage = stage_base + d2 * kStageBytes + row_off;
-        stmatrix_x4_trans_b8(stage + chunk_h0, w0[0], w0[1], w0[2], w0[3]);
-        stmatrix_x4_trans_b8(stage + chunk_h1, w1[0], w1[1], w1[2], w1[3]);
+        // this warp's slot d2 was last read by its TMA store of chunk o-2
+        if (lane == 0) tma_store_wait_read<1>();
+        __syncwarp();
+        const uint32_t slot = stage_u32 + d2 * kStageBytes;
+        stmatrix_x4_trans_b8(slot + addr_h0, w0[0], w0[1], w0[2], w0[3]);
+        stmatrix_x4_trans_b8(slot + addr_h1, w1[0], w1[1], w1[2], w1[3]);
         fence_proxy_async_smem();
-        named_barrier(1, kEpiThreads);
-        if (is_store_thread) {
-          tma_store_2d(&store_map, smem + kSmemStage + d2 * kStageBytes, strip * kStripCols,
+        __syncwarp();
+        if (lane == 0) {
+          tma_store_2d(&store_map, my_stage + d2 * kStageBytes, strip * kStripCols + 32 * q,
                        (c0 + c) * kChunkRows);
           tma_store_commit();
         }
-      };
-
-      for (int k = 0; k <= nc; ++k) {
-        const uint32_t gg = g + k, d1 = gg & 1, s = gg % kA2Slots;
-        mbar_wait(&d1_full[d1], (gg >> 1) & 1);
-        tc_fence_after();
-        uint32_t v[16];
-        tmem_ld_32x32b_x16_pack16(trow + kTmemD1 + 32 * d1, v);
-        tmem_ld_wait();
-        tc_fence_before();
-        mbar_arrive(&d1_empty[d1]);
-        uint32_t plane0[8], plane1[8];
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          const uint32_t raw = pack_pairs(v[2 * j], v[2 * j + 1]);  // 4 rows of H + 128*state
-          if (vn) {
-            plane0[j] = raw;
-            plane1[j] = (raw >> 7) & 0x01010101u;
-          } else {
-            plane0[j] = raw & 0x7F7F7F7Fu;
-            plane1[j] = raw & 0x80808080u;
-          }
-          if constexpr (kChecked) max_h = __vmaxu4(max_h, raw & 0x7F7F7F7Fu);
-        }
-        mbar_wait(&a2_empty[s], ((gg / kA2Slots) & 1) ^ 1);
-        tc_fence_after();
-        tmem_st_32x32b_x8(trow + kTmemA2 + 16 * s, plane0);
-        tmem_st_32x32b_x8(trow + kTmemA2 + 16 * s + 8, plane1);
-        tmem_st_wait();
-        tc_fence_before();
-        mbar_arrive(&a2_full[s]);
-        if (k >= 2) output_chunk(k - 2);
       }
-      if (nc >= 1) output_chunk(nc - 1);
-      g += nc + 1;
-      o += nc;
     }
-    if (is_store_thread) tma_store_wait_all<0>();
+    if (lane == 0) tma_store_wait_all<0>();
     if constexpr (kChecked) {
-      int32_t mh = static_cast<int32_t>(max(max(max_h & 0xFF, (max_h >> 8) & 0xFF),
-                                            max((max_h >> 16) & 0xFF, max_h >> 24)));
       int32_t mr = static_cast<int32_t>(max(max_r & 0xFFFF, max_r >> 16));
 #pragma unroll
-      for (int off = 16; off > 0; off >>= 1) {
-        mh = max(mh, __shfl_xor_sync(0xffffffffu, mh, off));
-        mr = max(mr, __shfl_xor_sync(0xffffffffu, mr, off));
-      }
-      if (lane == 0) {
-        atomicMax(&p.stats->max_h, mh);
-        atomicMax(&p.stats->max_r, mr);
-      }
+      for (int off = 16; off > 0; off >>= 1) mr = max(mr, __shfl_xor_sync(0xffffffffu, mr, off));
+      if (lane == 0) atomicMax(&p.stats->max_r, mr);
       if (__any_sync(0xffffffffu, bad != 0) && lane == 0) atomicOr(&p.stats->error, 1);
     }
   }

@@ -56,13 +56,13 @@ cudaError_t make_load_map(CUtensorMap* map, const SlabView& s) {
 }
 
 // Interior only: stores of partial strips / chunks are clipped to the torus.
-// The 32 x 128 staging tile is SWIZZLE_128B so the epilogue's stmatrix rows
-// land conflict-free.
+// Each epilogue warp stores its own 32 x 32 tile, SWIZZLE_32B so the
+// stmatrix rows land conflict-free.
 cudaError_t make_store_map(CUtensorMap* map, const SlabView& s) {
   if (s.rows <= 0 || s.cols <= 0) return cudaSuccess;
   return encode(map, s.buf + kHalo * s.pitch + kHalo, static_cast<uint64_t>(s.cols),
-                static_cast<uint64_t>(s.rows), static_cast<uint64_t>(s.pitch), 128, 32,
-                CU_TENSOR_MAP_SWIZZLE_128B);
+                static_cast<uint64_t>(s.rows), static_cast<uint64_t>(s.pitch), 32, 32,
+                CU_TENSOR_MAP_SWIZZLE_32B);
 }
 
 }  // namespace ltl
