@@ -7,6 +7,11 @@
 // over NVLink straight out of the peer's HBM (peer access / IPC mappings).
 // With one slab all three views are the same buffer and this is exactly the
 // reference's single-grid fill, including n < 16 where images wrap repeatedly.
+//
+// All sources are interior cells (never other halo cells), so the three parts
+// below run concurrently without ordering: side columns of the interior rows,
+// and the 16-row bands above and below (full padded width, interior part
+// copied 16 bytes at a time).
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -23,39 +28,38 @@ __device__ __forceinline__ int wrap(int v, int n) {
 
 __global__ void ltl_halo_kernel(SlabView self, SlabView above, SlabView below) {
   const int rows = self.rows, cols = self.cols;
-  const int64_t band = static_cast<int64_t>(kHalo) * (cols + 2 * kHalo);  // cells per row band
-  const int64_t side = static_cast<int64_t>(rows) * 2 * kHalo;            // left+right columns
-  // rows < 0 on the neighbour views: row bands come from an external transport
-  const bool rows_too = above.rows >= 0 && below.rows >= 0;
-  const int64_t total = 2 * band + side;
-  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
-       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    if (!rows_too && i < 2 * band) continue;
-    int py, px;
-    if (i < 2 * band) {
-      const int64_t b = i % band;
-      py = static_cast<int>(b / (cols + 2 * kHalo)) + (i < band ? 0 : rows + kHalo);
-      px = static_cast<int>(b % (cols + 2 * kHalo));
-    } else {
-      const int64_t s = i - 2 * band;
-      py = static_cast<int>(s / (2 * kHalo)) + kHalo;
-      const int c = static_cast<int>(s % (2 * kHalo));
-      px = c < kHalo ? c : cols + c;  // left: 0..15, right: cols+16..cols+31
+  const int tid = blockIdx.x * blockDim.x + threadIdx.x;
+  const int nthreads = gridDim.x * blockDim.x;
+  if (blockIdx.y == 0) {
+    // side columns: 32 bytes per interior row, one warp per row
+    for (int i = tid; i < rows * 2 * kHalo; i += nthreads) {
+      const int y = i / (2 * kHalo), c = i % (2 * kHalo);
+      const int px = c < kHalo ? c : cols + c;  // left 0..15, right cols+16..cols+31
+      const int sx = wrap(px - kHalo, cols);
+      uint8_t* row = self.buf + static_cast<int64_t>(y + kHalo) * self.pitch;
+      row[px] = row[sx + kHalo];
     }
-    const int sx = wrap(px - kHalo, cols);
-    const SlabView* src;
-    int sy;
-    if (py < kHalo) {
-      src = &above;
-      sy = wrap(py - kHalo, above.rows);
-    } else if (py >= rows + kHalo) {
-      src = &below;
-      sy = wrap(py - kHalo - rows, below.rows);
+    return;
+  }
+  // row bands: blockIdx.y == 1 -> 16 rows above (from `above`), 2 -> below
+  const bool top = blockIdx.y == 1;
+  const SlabView& src = top ? above : below;
+  if (src.rows < 0) return;  // rows come from an external transport
+  const bool vec = (cols % 16) == 0;
+  const int per_row = vec ? cols / 16 + 2 * kHalo : cols + 2 * kHalo;
+  for (int i = tid; i < kHalo * per_row; i += nthreads) {
+    const int t = i / per_row, e = i % per_row;
+    const int py = top ? t : rows + kHalo + t;
+    const int sy = top ? wrap(t - kHalo, src.rows) : wrap(t, src.rows);
+    uint8_t* drow = self.buf + static_cast<int64_t>(py) * self.pitch;
+    const uint8_t* srow = src.buf + static_cast<int64_t>(sy + kHalo) * src.pitch + kHalo;
+    if (vec && e < cols / 16) {
+      reinterpret_cast<uint4*>(drow + kHalo)[e] = reinterpret_cast<const uint4*>(srow)[e];
     } else {
-      src = &self;
-      sy = py - kHalo;
+      const int b = vec ? e - cols / 16 : e;  // vec: 0..31 edge bytes; else all bytes
+      const int px = vec ? (b < kHalo ? b : cols + b) : b;
+      drow[px] = srow[wrap(px - kHalo, cols)];
     }
-    self.buf[py * self.pitch + px] = src->buf[(sy + kHalo) * src->pitch + (sx + kHalo)];
   }
 }
 
@@ -64,10 +68,12 @@ __global__ void ltl_halo_kernel(SlabView self, SlabView above, SlabView below) {
 cudaError_t launch_halo_fill(const SlabView& self, const SlabView& above, const SlabView& below,
                              cudaStream_t stream) {
   if (self.rows <= 0 || self.cols <= 0) return cudaSuccess;
-  const int64_t total = 2LL * kHalo * (self.cols + 2 * kHalo) + 2LL * kHalo * self.rows;
-  int blocks = static_cast<int>((total + 255) / 256);
-  if (blocks > 148 * 16) blocks = 148 * 16;
-  ltl_halo_kernel<<<blocks, 256, 0, stream>>>(self, above, below);
+  const int64_t side = 2LL * kHalo * self.rows;
+  const int64_t band = kHalo * (self.cols / 16 + 2LL * kHalo);
+  int64_t work = side > band ? side : band;
+  int blocks = static_cast<int>((work + 255) / 256);
+  if (blocks > 148 * 4) blocks = 148 * 4;
+  ltl_halo_kernel<<<dim3(blocks, 3), 256, 0, stream>>>(self, above, below);
   return cudaGetLastError();
 }
 

@@ -55,7 +55,9 @@ constexpr int kStripCols = 128;  // M of both MMAs = output columns per strip
 constexpr int kChunkRows = 32;   // N of both MMAs = rows per chunk
 constexpr int kKTile = 160;      // 128 + 2*16 input columns per strip
 constexpr int kKChunks = kKTile / 32;
-constexpr int kXStages = 4;
+// Loads in flight per CTA: HBM needs ~bandwidth x loaded latency (~10 MB
+// chip-wide) of outstanding reads; 12 stages x 5 KB x 296 CTAs ~ 18 MB.
+constexpr int kXStages = 12;
 constexpr int kA2Slots = 4;
 constexpr int kGroupWarps = 4;   // warps per epilogue group (one per TMEM lane quarter)
 constexpr int kThreads = 64 + 2 * 32 * kGroupWarps;  // producer, MMA, convert x4, output x4
@@ -85,10 +87,33 @@ constexpr uint32_t kIdescM128N32 = idesc_i8_u8u8_s32(128, 32);
 
 struct Params {
   int32_t rows, cols;
-  int32_t num_strips, chunks, seg, segs, num_units;
+  int32_t num_strips, chunks;  // strips of 128 columns, 32-row output chunks per strip
   RuleConsts rule;
   int32_t inject_fault;
   DeviceStats* stats;
+};
+
+// Static balanced schedule: the strip-major sequence of all output chunks is
+// cut into gridDim.x equal contiguous ranges; a range is walked as "units"
+// (maximal runs inside one strip), each costing one extra H chunk of halo.
+// Every role of the CTA iterates the same units in the same order.
+struct UnitIter {
+  int64_t a, b;
+  int32_t chunks;
+  __device__ UnitIter(const Params& p) : chunks(p.chunks) {
+    const int64_t total = static_cast<int64_t>(p.num_strips) * p.chunks;
+    a = total * blockIdx.x / gridDim.x;
+    b = total * (blockIdx.x + 1) / gridDim.x;
+  }
+  __device__ bool next(int& strip, int& c0, int& nc) {
+    if (a >= b) return false;
+    strip = static_cast<int>(a / chunks);
+    c0 = static_cast<int>(a - static_cast<int64_t>(strip) * chunks);
+    const int64_t end = min(b, static_cast<int64_t>(strip + 1) * chunks);
+    nc = static_cast<int>(end - a);
+    a = end;
+    return true;
+  }
 };
 
 // D2 column j holds output row pi(j).  With j = [e, m, a0, a1, v] (bit 0
@@ -141,30 +166,44 @@ __global__ void __launch_bounds__(kThreads, 2)
   const bool vn = p.rule.kind != 0;
 
   // ---- one-time setup: resident bands (generic-proxy writes), barriers, TMEM
-  for (uint32_t i = threadIdx.x; i < 128u * kKTile; i += kThreads) {
-    const int m = static_cast<int>(i / kKTile), k = static_cast<int>(i % kKTile);
-    const int d = k - 16 - m;
-    uint32_t v = (d >= -r && d <= r) ? 1u : 0u;
-    if (d == 0) {
-      v += 128u;  // state marker
-      if (p.inject_fault && m == 0) v = 128u;  // test hook: drop one centre entry
+  // (built a 32-bit word -- 4 consecutive k -- at a time; the swizzle moves
+  // whole 16-byte chunks, so a word stays contiguous)
+  for (uint32_t w = threadIdx.x; w < 128u * kKTile / 4; w += kThreads) {
+    const int m = static_cast<int>(w / (kKTile / 4)), k0 = 4 * static_cast<int>(w % (kKTile / 4));
+    uint32_t word = 0;
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const int d = k0 + b - 16 - m;
+      uint32_t v = (d >= -r && d <= r) ? 1u : 0u;
+      if (d == 0) {
+        v += 128u;  // state marker
+        if (p.inject_fault && m == 0) v = 128u;  // test hook: drop one centre entry
+      }
+      word |= v << (8 * b);
     }
-    smem[kSmemA1 + (k / 32) * 4096 + sw32_offset(m, k % 32)] = static_cast<uint8_t>(v);
+    *reinterpret_cast<uint32_t*>(smem + kSmemA1 + (k0 / 32) * 4096 + sw32_offset(m, k0 % 32)) =
+        word;
   }
-  for (uint32_t i = threadIdx.x; i < kNumBands * 32u * 32u; i += kThreads) {
-    const int t = static_cast<int>(i / 1024), j = static_cast<int>((i / 32) % 32),
-              k = static_cast<int>(i % 32);
+  for (uint32_t w = threadIdx.x; w < kNumBands * 32u * 8u; w += kThreads) {
+    const int t = static_cast<int>(w / 256), j = static_cast<int>((w / 8) % 32),
+              k0 = 4 * static_cast<int>(w % 8);
     const int n = out_row_of_col(j);  // output row of D2 column j (row 16+n of the window)
-    int v;
-    switch (t) {
-      case 0: v = (k - 16 - n >= -r && k - 16 - n <= r); break;  // H rows of chunk c
-      case 1: v = (k + 16 - n >= -r && k + 16 - n <= r); break;  // H rows of chunk c+1
-      case 2: v = (k == n + 16); break;                          // centre row, chunk c
-      case 3: v = (k + 16 == n); break;                          // centre row, chunk c+1
-      case 4: v = 16 * (k == n + 16); break;                     // 16 * centre (state*2048)
-      default: v = 16 * (k + 16 == n); break;
+    uint32_t word = 0;
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const int k = k0 + b;
+      int v;
+      switch (t) {
+        case 0: v = (k - 16 - n >= -r && k - 16 - n <= r); break;  // H rows of chunk c
+        case 1: v = (k + 16 - n >= -r && k + 16 - n <= r); break;  // H rows of chunk c+1
+        case 2: v = (k == n + 16); break;                          // centre row, chunk c
+        case 3: v = (k + 16 == n); break;                          // centre row, chunk c+1
+        case 4: v = 16 * (k == n + 16); break;                     // 16 * centre (state*2048)
+        default: v = 16 * (k + 16 == n); break;
+      }
+      word |= static_cast<uint32_t>(v) << (8 * b);
     }
-    smem[kSmemBand + t * 1024 + sw32_offset(j, k)] = static_cast<uint8_t>(v);
+    *reinterpret_cast<uint32_t*>(smem + kSmemBand + t * 1024 + sw32_offset(j, k0)) = word;
   }
   fence_proxy_async_smem();
   if (warp == 0 && lane == 0) {
@@ -196,10 +235,9 @@ __global__ void __launch_bounds__(kThreads, 2)
     // ================= TMA producer =================
     if (elect_one()) {
       uint32_t g = 0;
-      for (int u = blockIdx.x; u < p.num_units; u += gridDim.x) {
-        const int strip = u % p.num_strips, seg = u / p.num_strips;
-        const int c0 = seg * p.seg;
-        const int nc = min(p.seg, p.chunks - c0);
+      UnitIter it(p);
+      int strip, c0, nc;
+      while (it.next(strip, c0, nc)) {
         for (int k = 0; k <= nc; ++k, ++g) {
           const uint32_t s = g % kXStages;
           mbar_wait(&x_empty[s], ((g / kXStages) & 1) ^ 1);
@@ -257,9 +295,9 @@ __global__ void __launch_bounds__(kThreads, 2)
       }
       __syncwarp();
     };
-    for (int u = blockIdx.x; u < p.num_units; u += gridDim.x) {
-      const int seg = u / p.num_strips;
-      const int nc = min(p.seg, p.chunks - seg * p.seg);
+    UnitIter it(p);
+    int strip, c0, nc;
+    while (it.next(strip, c0, nc)) {
       pass1(g);
       for (int k = 0; k <= nc; ++k) {
         if (k + 1 <= nc) pass1(g + k + 1);
@@ -273,9 +311,9 @@ __global__ void __launch_bounds__(kThreads, 2)
     const uint32_t q = warp & 3;  // TMEM lane quarter = 32 strip columns
     const uint32_t trow = tmem + ((q * 32) << 16);
     uint32_t max_h = 0, g = 0;
-    for (int u = blockIdx.x; u < p.num_units; u += gridDim.x) {
-      const int seg = u / p.num_strips;
-      const int nc = min(p.seg, p.chunks - seg * p.seg);
+    UnitIter it(p);
+    int strip, c0, nc;
+    while (it.next(strip, c0, nc)) {
       for (int k = 0; k <= nc; ++k, ++g) {
         const uint32_t d1 = g & 1, s = g % kA2Slots;
         mbar_wait(&d1_full[d1], (g >> 1) & 1);
@@ -338,10 +376,9 @@ __global__ void __launch_bounds__(kThreads, 2)
     const uint32_t addr_h0 = lane * 32 + ((0u ^ ((lane >> 2) & 1)) << 4);
     const uint32_t addr_h1 = lane * 32 + ((1u ^ ((lane >> 2) & 1)) << 4);
     uint32_t o = 0;
-    for (int u = blockIdx.x; u < p.num_units; u += gridDim.x) {
-      const int strip = u % p.num_strips, seg = u / p.num_strips;
-      const int c0 = seg * p.seg;
-      const int nc = min(p.seg, p.chunks - c0);
+    UnitIter it(p);
+    int strip, c0, nc;
+    while (it.next(strip, c0, nc)) {
       for (int c = 0; c < nc; ++c, ++o) {
         const uint32_t d2 = o & 1;
         mbar_wait(&d2_full[d2], (o >> 1) & 1);
@@ -430,23 +467,16 @@ cudaError_t launch_tc_step(const TcLaunch& a, cudaStream_t stream) {
   p.num_strips = (a.cols + kStripCols - 1) / kStripCols;
   p.chunks = (a.rows + kChunkRows - 1) / kChunkRows;
   const int slots = num_sms * ctas_per_sm;
-  int seg = a.seg_chunks;
-  if (seg <= 0) {
-    // ~4 units per CTA slot for balance, segments as long as that allows (the
-    // extra halo chunk per unit costs 1/seg of the input traffic)
-    const int64_t target_units = 4LL * slots;
-    const int64_t per_strip = (target_units + p.num_strips - 1) / p.num_strips;
-    seg = static_cast<int>((p.chunks + per_strip - 1) / per_strip);
-    seg = seg < 1 ? 1 : (seg > 64 ? 64 : seg);
-  }
-  p.seg = seg;
-  p.segs = (p.chunks + seg - 1) / seg;
-  p.num_units = p.num_strips * p.segs;
   p.rule = a.rule;
   p.inject_fault = a.inject_fault;
   p.stats = a.stats;
-  int grid = a.grid > 0 ? a.grid : slots;
-  if (grid > p.num_units) grid = p.num_units;
+  // Every CTA gets an equal share of the strip-major chunk sequence (UnitIter);
+  // small grids keep >= 2 chunks per CTA so the per-unit halo chunk and the
+  // CTA prologue stay amortised.
+  const int64_t total = static_cast<int64_t>(p.num_strips) * p.chunks;
+  int64_t grid = a.grid > 0 ? a.grid : slots;
+  if (grid > (total + 1) / 2) grid = (total + 1) / 2;
+  if (grid < 1) grid = 1;
   if (a.stats)
     ltl_tc_step_kernel<true><<<grid, kThreads, kSmemAlloc, stream>>>(*a.load_map, *a.store_map, p);
   else
