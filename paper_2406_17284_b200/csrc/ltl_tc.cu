@@ -88,30 +88,31 @@ constexpr uint32_t kIdescM128N32 = idesc_i8_u8u8_s32(128, 32);
 struct Params {
   int32_t rows, cols;
   int32_t num_strips, chunks;  // strips of 128 columns, 32-row output chunks per strip
+  int32_t segs;                // row segments per strip (units = num_strips * segs)
   RuleConsts rule;
   int32_t inject_fault;
   DeviceStats* stats;
 };
 
-// Static balanced schedule: the strip-major sequence of all output chunks is
-// cut into gridDim.x equal contiguous ranges; a range is walked as "units"
-// (maximal runs inside one strip), each costing one extra H chunk of halo.
+// Static schedule.  A unit is (strip, row segment); unit u is strip u % S,
+// segment u / S, and CTA b walks units b, b + G, b + 2G, ...  The host picks
+// segs and G so that every CTA gets the same work (G = S * segs, or several
+// whole strips each when S exceeds the CTA slots).  Consecutive CTAs then
+// stream neighbouring strips down the same rows at the same time, so the
+// 32 overlapping halo columns and the 256-byte L2 promotion of each strip's
+// loads are shared through L2 instead of being fetched twice from HBM.
 // Every role of the CTA iterates the same units in the same order.
 struct UnitIter {
-  int64_t a, b;
-  int32_t chunks;
-  __device__ UnitIter(const Params& p) : chunks(p.chunks) {
-    const int64_t total = static_cast<int64_t>(p.num_strips) * p.chunks;
-    a = total * blockIdx.x / gridDim.x;
-    b = total * (blockIdx.x + 1) / gridDim.x;
-  }
+  int32_t u;
+  const Params& p;
+  __device__ explicit UnitIter(const Params& pp) : u(blockIdx.x), p(pp) {}
   __device__ bool next(int& strip, int& c0, int& nc) {
-    if (a >= b) return false;
-    strip = static_cast<int>(a / chunks);
-    c0 = static_cast<int>(a - static_cast<int64_t>(strip) * chunks);
-    const int64_t end = min(b, static_cast<int64_t>(strip + 1) * chunks);
-    nc = static_cast<int>(end - a);
-    a = end;
+    if (u >= p.num_strips * p.segs) return false;
+    strip = u % p.num_strips;
+    const int seg = u / p.num_strips;
+    c0 = static_cast<int>(static_cast<int64_t>(p.chunks) * seg / p.segs);
+    nc = static_cast<int>(static_cast<int64_t>(p.chunks) * (seg + 1) / p.segs) - c0;
+    u += gridDim.x;
     return true;
   }
 };
@@ -470,13 +471,23 @@ cudaError_t launch_tc_step(const TcLaunch& a, cudaStream_t stream) {
   p.rule = a.rule;
   p.inject_fault = a.inject_fault;
   p.stats = a.stats;
-  // Every CTA gets an equal share of the strip-major chunk sequence (UnitIter);
-  // small grids keep >= 2 chunks per CTA so the per-unit halo chunk and the
-  // CTA prologue stay amortised.
-  const int64_t total = static_cast<int64_t>(p.num_strips) * p.chunks;
-  int64_t grid = a.grid > 0 ? a.grid : slots;
-  if (grid > (total + 1) / 2) grid = (total + 1) / 2;
-  if (grid < 1) grid = 1;
+  // Balanced units (UnitIter): with S <= slots, split every strip into
+  // segs = slots / S row segments (>= 2 chunks each) and run one unit per
+  // CTA; with S > slots, give each CTA the same number of whole strips.
+  const int S = p.num_strips;
+  int64_t grid;
+  if (S <= slots) {
+    int segs = slots / S;
+    const int max_segs = p.chunks / 2 > 1 ? p.chunks / 2 : 1;
+    if (segs > max_segs) segs = max_segs;
+    p.segs = segs;
+    grid = static_cast<int64_t>(S) * segs;
+  } else {
+    p.segs = 1;
+    const int per_cta = (S + slots - 1) / slots;
+    grid = (S + per_cta - 1) / per_cta;
+  }
+  if (a.grid > 0 && a.grid < grid) grid = a.grid;
   if (a.stats)
     ltl_tc_step_kernel<true><<<grid, kThreads, kSmemAlloc, stream>>>(*a.load_map, *a.store_map, p);
   else
