@@ -51,7 +51,8 @@ struct TcLaunch {
   int32_t inject_fault;
   DeviceStats* stats;  // nullptr -> no stats reduction
   int32_t grid;        // CTAs (0 = auto)
-  int32_t seg_chunks;  // output chunks (32 rows) per work unit (0 = auto)
+  int32_t seg_chunks;  // unused (kept for ABI of the launch struct)
+  long long* trace;    // debug timeline (LTL_TC_TRACE), nullptr = off
 };
 cudaError_t launch_tc_step(const TcLaunch& a, cudaStream_t stream);
 size_t tc_smem_bytes();

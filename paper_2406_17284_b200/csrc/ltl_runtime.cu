@@ -10,6 +10,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <exception>
 #include <stdexcept>
@@ -230,7 +231,32 @@ void enqueue_step(ltl_ctx* ctx, const ltl::RuleConsts& rc, uint32_t flags, bool 
       a.rule = rc;
       a.inject_fault = fault;
       a.stats = want_stats ? s.dstats : nullptr;
+      // Debug: LTL_TC_TRACE=<file> dumps the pipeline timeline of CTA 0 of
+      // the first traced launch (12 event kinds x 64 chunks of clock64 stamps).
+      static bool traced = false;
+      const char* trace_path = std::getenv("LTL_TC_TRACE");
+      long long* dtrace = nullptr;
+      if (trace_path && !traced && !want_stats) {
+        ck(cudaMalloc(&dtrace, 12 * 64 * sizeof(long long)), "trace alloc");
+        ck(cudaMemsetAsync(dtrace, 0, 12 * 64 * sizeof(long long), s.stream), "trace memset");
+        a.trace = dtrace;
+      }
       ck(ltl::launch_tc_step(a, s.stream), "tcgen05 kernel");
+      if (dtrace) {
+        std::vector<long long> h(12 * 64);
+        ck(cudaStreamSynchronize(s.stream), "trace sync");
+        ck(cudaMemcpy(h.data(), dtrace, h.size() * sizeof(long long), cudaMemcpyDeviceToHost),
+           "trace copy");
+        cudaFree(dtrace);
+        if (FILE* fh = std::fopen(trace_path, "w")) {
+          for (int e = 0; e < 12; ++e) {
+            for (int k = 0; k < 64; ++k) std::fprintf(fh, "%s%lld", k ? "," : "", h[e * 64 + k]);
+            std::fprintf(fh, "\n");
+          }
+          std::fclose(fh);
+        }
+        traced = true;
+      }
     }
     if (kt1) ck(cudaEventRecord(kt1[i], s.stream), "event");
     if (ctx->slabs.size() > 1) ck(cudaEventRecord(s.ev_step, s.stream), "event");

@@ -92,7 +92,11 @@ struct Params {
   RuleConsts rule;
   int32_t inject_fault;
   DeviceStats* stats;
+  long long* trace;  // debug timeline of CTA 0 (nullptr: off)
 };
+
+#define LTL_TRACE(ev, idx) \
+  do { if (p.trace && blockIdx.x == 0 && (idx) < 64) p.trace[(ev) * 64 + (idx)] = clock64(); } while (0)
 
 // Static schedule.  A unit is (strip, row segment); unit u is strip u % S,
 // segment u / S, and CTA b walks units b, b + G, b + 2G, ...  The host picks
@@ -242,6 +246,7 @@ __global__ void __launch_bounds__(kThreads, 2)
         for (int k = 0; k <= nc; ++k, ++g) {
           const uint32_t s = g % kXStages;
           mbar_wait(&x_empty[s], ((g / kXStages) & 1) ^ 1);
+          LTL_TRACE(0, g);
           uint8_t* dst = smem + kSmemX + s * kXStageBytes;
           mbar_arrive_expect_tx(&x_full[s], kXStageBytes);
 #pragma unroll
@@ -264,6 +269,7 @@ __global__ void __launch_bounds__(kThreads, 2)
       const uint32_t s = gg % kXStages, d1 = gg & 1;
       mbar_wait(&x_full[s], (gg / kXStages) & 1);
       mbar_wait(&d1_empty[d1], ((gg >> 1) & 1) ^ 1);
+      if (lane == 0) LTL_TRACE(1, gg);
       tc_fence_after();
       if (elect_one()) {
 #pragma unroll
@@ -273,6 +279,7 @@ __global__ void __launch_bounds__(kThreads, 2)
                     q > 0);
         mma_commit(&x_empty[s]);
         mma_commit(&d1_full[d1]);
+        LTL_TRACE(2, gg);
       }
       __syncwarp();
     };
@@ -280,7 +287,9 @@ __global__ void __launch_bounds__(kThreads, 2)
       const uint32_t s0 = gg % kA2Slots, s1 = (gg + 1) % kA2Slots, d2 = oo & 1;
       mbar_wait(&a2_full[s0], (gg / kA2Slots) & 1);
       mbar_wait(&a2_full[s1], ((gg + 1) / kA2Slots) & 1);
+      if (lane == 0) LTL_TRACE(3, oo);
       mbar_wait(&d2_empty[d2], ((oo >> 1) & 1) ^ 1);
+      if (lane == 0) LTL_TRACE(4, oo);
       tc_fence_after();
       if (elect_one()) {
         const uint32_t dcol = tmem + kTmemD2 + 32 * d2;
@@ -318,6 +327,7 @@ __global__ void __launch_bounds__(kThreads, 2)
       for (int k = 0; k <= nc; ++k, ++g) {
         const uint32_t d1 = g & 1, s = g % kA2Slots;
         mbar_wait(&d1_full[d1], (g >> 1) & 1);
+        if (warp == 2 && lane == 0) LTL_TRACE(5, g);
         tc_fence_after();
         uint32_t v[16];
         tmem_ld_32x32b_x16_pack16(trow + kTmemD1 + 32 * d1, v);
@@ -337,11 +347,14 @@ __global__ void __launch_bounds__(kThreads, 2)
           }
           if constexpr (kChecked) max_h = __vmaxu4(max_h, raw & 0x7F7F7F7Fu);
         }
+        if (warp == 2 && lane == 0) LTL_TRACE(6, g);
         mbar_wait(&a2_empty[s], ((g / kA2Slots) & 1) ^ 1);
+        if (warp == 2 && lane == 0) LTL_TRACE(7, g);
         tc_fence_after();
         tmem_st_32x32b_x8(trow + kTmemA2 + 16 * s, plane0);
         tmem_st_32x32b_x8(trow + kTmemA2 + 16 * s + 8, plane1);
         tmem_st_wait();
+        if (warp == 2 && lane == 0) LTL_TRACE(8, g);
         tc_fence_before();
         mbar_arrive(&a2_full[s]);
       }
@@ -383,6 +396,7 @@ __global__ void __launch_bounds__(kThreads, 2)
       for (int c = 0; c < nc; ++c, ++o) {
         const uint32_t d2 = o & 1;
         mbar_wait(&d2_full[d2], (o >> 1) & 1);
+        if (warp == 6 && lane == 0) LTL_TRACE(9, o);
         tc_fence_after();
         uint32_t z0[8], z1[8];
         tmem_ld_16x256b_x2_pack16(trow + kTmemD2 + 32 * d2, z0);
@@ -425,6 +439,7 @@ __global__ void __launch_bounds__(kThreads, 2)
           tma_store_2d(&store_map, my_stage + d2 * kStageBytes, strip * kStripCols + 32 * q,
                        (c0 + c) * kChunkRows);
           tma_store_commit();
+          if (warp == 6) LTL_TRACE(11, o);
         }
       }
     }
@@ -471,6 +486,7 @@ cudaError_t launch_tc_step(const TcLaunch& a, cudaStream_t stream) {
   p.rule = a.rule;
   p.inject_fault = a.inject_fault;
   p.stats = a.stats;
+  p.trace = a.trace;
   // Balanced units (UnitIter): with S <= slots, split every strip into
   // segs = slots / S row segments (>= 2 chunks each) and run one unit per
   // CTA; with S > slots, give each CTA the same number of whole strips.
