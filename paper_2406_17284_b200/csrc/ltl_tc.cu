@@ -34,9 +34,10 @@
 // Every quantity is an exact small integer (H <= 33, R <= 1089, Z < 4096), so
 // the result is bit-identical to the reference's int32 loops.
 //
-// Warp roles (320 threads): warp 0 TMA producer, warp 1 MMA issuer + TMEM
-// owner, warps 2..5 convert D1, warps 6..9 rule + store D2 (warp w owns TMEM
-// lanes 32*(w%4)..+32, i.e. 32 columns of the strip).  Persistent CTAs (2 per SM) walk (strip, segment) units.
+// Warp roles (352 threads): warp 0 TMA producer, warp 1 pass-1 MMA issuer +
+// TMEM owner, warps 2..5 convert D1, warps 6..9 rule + store D2 (warp w owns
+// TMEM lanes 32*(w%4)..+32, i.e. 32 columns of the strip), warp 10 pass-2
+// MMA issuer.  Persistent CTAs (2 per SM) walk (strip, segment) units.
 #include <cuda.h>
 #include <cuda_runtime.h>
 
@@ -59,8 +60,10 @@ constexpr int kKChunks = kKTile / 32;
 // chip-wide) of outstanding reads; 12 stages x 5 KB x 296 CTAs ~ 18 MB.
 constexpr int kXStages = 12;
 constexpr int kA2Slots = 4;
+constexpr int kD1Slots = 3;  // pass-1 accumulators in flight
+constexpr int kD2Slots = 3;  // pass-2 accumulators in flight
 constexpr int kGroupWarps = 4;   // warps per epilogue group (one per TMEM lane quarter)
-constexpr int kThreads = 64 + 2 * 32 * kGroupWarps;  // producer, MMA, convert x4, output x4
+constexpr int kThreads = 96 + 2 * 32 * kGroupWarps;  // TMA, P1 MMA, convert x4, output x4, P2 MMA
 constexpr int kEpiThreads = 32 * kGroupWarps;
 constexpr int kNumBands = 6;  // Bv0, Bv1, Iv0, Iv1, 16*Iv0, 16*Iv1
 
@@ -72,16 +75,16 @@ constexpr uint32_t kXStageBytes = kKChunks * kChunkRows * 32;      // 5120
 constexpr uint32_t kSmemStage = kSmemX + kXStages * kXStageBytes;  // 2 x 4 KB staging (SW128)
 constexpr uint32_t kStageBytes = kChunkRows * kStripCols;          // 4096 (4 warps x 1 KB)
 constexpr uint32_t kSmemBars = kSmemStage + 2 * kStageBytes;
-constexpr uint32_t kNumBars = 2 * kXStages + 2 * 2 + 2 * kA2Slots + 2 * 2;
+constexpr uint32_t kNumBars = 2 * kXStages + 2 * kD1Slots + 2 * kA2Slots + 2 * kD2Slots;
 constexpr uint32_t kSmemTotal = kSmemBars + kNumBars * 8 + 16;
 constexpr uint32_t kSmemAlloc = kSmemTotal + 1024;  // alignment slack
 static_assert(kSmemStage % 1024 == 0, "swizzled staging needs aligned slots");
 
 // TMEM columns (allocation of 256 -> two CTAs per SM).
 constexpr uint32_t kTmemCols = 256;
-constexpr uint32_t kTmemD1 = 0;    // 2 x 32
-constexpr uint32_t kTmemD2 = 64;   // 2 x 32
-constexpr uint32_t kTmemA2 = 128;  // kA2Slots x 16 (plane 0 at +0, plane 1 at +8)
+constexpr uint32_t kTmemD1 = 0;    // kD1Slots x 32
+constexpr uint32_t kTmemD2 = 96;   // kD2Slots x 32
+constexpr uint32_t kTmemA2 = 192;  // kA2Slots x 16 (plane 0 at +0, plane 1 at +8)
 
 constexpr uint32_t kIdescM128N32 = idesc_i8_u8u8_s32(128, 32);
 
@@ -158,12 +161,12 @@ __global__ void __launch_bounds__(kThreads, 2)
   uint64_t* x_full = bars;
   uint64_t* x_empty = x_full + kXStages;
   uint64_t* d1_full = x_empty + kXStages;
-  uint64_t* d1_empty = d1_full + 2;
-  uint64_t* a2_full = d1_empty + 2;
+  uint64_t* d1_empty = d1_full + kD1Slots;
+  uint64_t* a2_full = d1_empty + kD1Slots;
   uint64_t* a2_empty = a2_full + kA2Slots;
   uint64_t* d2_full = a2_empty + kA2Slots;
-  uint64_t* d2_empty = d2_full + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(d2_empty + 2);
+  uint64_t* d2_empty = d2_full + kD2Slots;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(d2_empty + kD2Slots);
 
   const uint32_t warp = warp_id();
   const uint32_t lane = threadIdx.x & 31;
@@ -218,9 +221,11 @@ __global__ void __launch_bounds__(kThreads, 2)
       mbar_init(&x_full[i], 1);
       mbar_init(&x_empty[i], 1);
     }
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < kD1Slots; ++i) {
       mbar_init(&d1_full[i], 1);
       mbar_init(&d1_empty[i], kEpiThreads);
+    }
+    for (int i = 0; i < kD2Slots; ++i) {
       mbar_init(&d2_full[i], 1);
       mbar_init(&d2_empty[i], kEpiThreads);
     }
@@ -257,64 +262,33 @@ __global__ void __launch_bounds__(kThreads, 2)
       }
     }
   } else if (warp == 1) {
-    // ================= MMA issuer =================
+    // ================= pass-1 MMA issuer =================
+    // Runs ahead of everything downstream as far as the X ring and the D1
+    // ring allow; pass 2 has its own issuer warp so neither waits on the other.
     const uint32_t a1_base = smem_u32(smem + kSmemA1);
-    const uint32_t band = smem_u32(smem + kSmemBand);
     const uint32_t x_base = smem_u32(smem + kSmemX);
-    // pass-2 operand pairing: {A plane, B band} for the 4 MMAs of a chunk
-    const uint32_t p0_b0 = band + (vn ? 2048 : 0), p0_b1 = band + (vn ? 3072 : 1024);
-    const uint32_t p1_b0 = band + (vn ? 0 : 4096), p1_b1 = band + (vn ? 1024 : 5120);
-    uint32_t g = 0, o = 0;
-    auto pass1 = [&](uint32_t gg) {
-      const uint32_t s = gg % kXStages, d1 = gg & 1;
-      mbar_wait(&x_full[s], (gg / kXStages) & 1);
-      mbar_wait(&d1_empty[d1], ((gg >> 1) & 1) ^ 1);
-      if (lane == 0) LTL_TRACE(1, gg);
-      tc_fence_after();
-      if (elect_one()) {
-#pragma unroll
-        for (int q = 0; q < kKChunks; ++q)
-          mma_i8_ss(tmem + kTmemD1 + 32 * d1, smem_desc_sw32_kmajor(a1_base + q * 4096),
-                    smem_desc_sw32_kmajor(x_base + s * kXStageBytes + q * 1024), kIdescM128N32,
-                    q > 0);
-        mma_commit(&x_empty[s]);
-        mma_commit(&d1_full[d1]);
-        LTL_TRACE(2, gg);
-      }
-      __syncwarp();
-    };
-    auto pass2 = [&](uint32_t gg, uint32_t oo, bool last) {
-      const uint32_t s0 = gg % kA2Slots, s1 = (gg + 1) % kA2Slots, d2 = oo & 1;
-      mbar_wait(&a2_full[s0], (gg / kA2Slots) & 1);
-      mbar_wait(&a2_full[s1], ((gg + 1) / kA2Slots) & 1);
-      if (lane == 0) LTL_TRACE(3, oo);
-      mbar_wait(&d2_empty[d2], ((oo >> 1) & 1) ^ 1);
-      if (lane == 0) LTL_TRACE(4, oo);
-      tc_fence_after();
-      if (elect_one()) {
-        const uint32_t dcol = tmem + kTmemD2 + 32 * d2;
-        const uint32_t a0 = tmem + kTmemA2 + 16 * s0, a1 = tmem + kTmemA2 + 16 * s1;
-        mma_i8_ts(dcol, a0, smem_desc_sw32_kmajor(p0_b0), kIdescM128N32, 0);
-        mma_i8_ts(dcol, a1, smem_desc_sw32_kmajor(p0_b1), kIdescM128N32, 1);
-        mma_i8_ts(dcol, a0 + 8, smem_desc_sw32_kmajor(p1_b0), kIdescM128N32, 1);
-        mma_i8_ts(dcol, a1 + 8, smem_desc_sw32_kmajor(p1_b1), kIdescM128N32, 1);
-        mma_commit(&d2_full[d2]);
-        mma_commit(&a2_empty[s0]);
-        // the unit's final H chunk is only ever the second operand: free it here
-        if (last) mma_commit(&a2_empty[s1]);
-      }
-      __syncwarp();
-    };
+    uint32_t g = 0;
     UnitIter it(p);
     int strip, c0, nc;
     while (it.next(strip, c0, nc)) {
-      pass1(g);
-      for (int k = 0; k <= nc; ++k) {
-        if (k + 1 <= nc) pass1(g + k + 1);
-        if (k >= 1) pass2(g + k - 1, o + k - 1, k == nc);
+      for (int k = 0; k <= nc; ++k, ++g) {
+        const uint32_t s = g % kXStages, d1 = g % kD1Slots;
+        mbar_wait(&x_full[s], (g / kXStages) & 1);
+        mbar_wait(&d1_empty[d1], ((g / kD1Slots) & 1) ^ 1);
+        if (lane == 0) LTL_TRACE(1, g);
+        tc_fence_after();
+        if (elect_one()) {
+#pragma unroll
+          for (int q = 0; q < kKChunks; ++q)
+            mma_i8_ss(tmem + kTmemD1 + 32 * d1, smem_desc_sw32_kmajor(a1_base + q * 4096),
+                      smem_desc_sw32_kmajor(x_base + s * kXStageBytes + q * 1024),
+                      kIdescM128N32, q > 0);
+          mma_commit(&x_empty[s]);
+          mma_commit(&d1_full[d1]);
+          LTL_TRACE(2, g);
+        }
+        __syncwarp();
       }
-      g += nc + 1;
-      o += nc;
     }
   } else if (warp < 2 + kGroupWarps) {
     // ================= convert warps (D1 -> pass-2 A planes) =================
@@ -325,8 +299,8 @@ __global__ void __launch_bounds__(kThreads, 2)
     int strip, c0, nc;
     while (it.next(strip, c0, nc)) {
       for (int k = 0; k <= nc; ++k, ++g) {
-        const uint32_t d1 = g & 1, s = g % kA2Slots;
-        mbar_wait(&d1_full[d1], (g >> 1) & 1);
+        const uint32_t d1 = g % kD1Slots, s = g % kA2Slots;
+        mbar_wait(&d1_full[d1], (g / kD1Slots) & 1);
         if (warp == 2 && lane == 0) LTL_TRACE(5, g);
         tc_fence_after();
         uint32_t v[16];
@@ -366,6 +340,41 @@ __global__ void __launch_bounds__(kThreads, 2)
       for (int off = 16; off > 0; off >>= 1) mh = max(mh, __shfl_xor_sync(0xffffffffu, mh, off));
       if (lane == 0) atomicMax(&p.stats->max_h, mh);
     }
+  } else if (warp == 2 + 2 * kGroupWarps) {
+    // ================= pass-2 MMA issuer =================
+    const uint32_t band = smem_u32(smem + kSmemBand);
+    // operand pairing {A plane, B band} for the 4 MMAs of an output chunk
+    const uint32_t p0_b0 = band + (vn ? 2048 : 0), p0_b1 = band + (vn ? 3072 : 1024);
+    const uint32_t p1_b0 = band + (vn ? 0 : 4096), p1_b1 = band + (vn ? 1024 : 5120);
+    uint32_t g = 0, o = 0;
+    UnitIter it(p);
+    int strip, c0, nc;
+    while (it.next(strip, c0, nc)) {
+      for (int c = 0; c < nc; ++c, ++o) {
+        const uint32_t gg = g + c;
+        const uint32_t s0 = gg % kA2Slots, s1 = (gg + 1) % kA2Slots, d2 = o % kD2Slots;
+        mbar_wait(&a2_full[s0], (gg / kA2Slots) & 1);
+        mbar_wait(&a2_full[s1], ((gg + 1) / kA2Slots) & 1);
+        if (lane == 0) LTL_TRACE(3, o);
+        mbar_wait(&d2_empty[d2], ((o / kD2Slots) & 1) ^ 1);
+        if (lane == 0) LTL_TRACE(4, o);
+        tc_fence_after();
+        if (elect_one()) {
+          const uint32_t dcol = tmem + kTmemD2 + 32 * d2;
+          const uint32_t a0 = tmem + kTmemA2 + 16 * s0, a1 = tmem + kTmemA2 + 16 * s1;
+          mma_i8_ts(dcol, a0, smem_desc_sw32_kmajor(p0_b0), kIdescM128N32, 0);
+          mma_i8_ts(dcol, a1, smem_desc_sw32_kmajor(p0_b1), kIdescM128N32, 1);
+          mma_i8_ts(dcol, a0 + 8, smem_desc_sw32_kmajor(p1_b0), kIdescM128N32, 1);
+          mma_i8_ts(dcol, a1 + 8, smem_desc_sw32_kmajor(p1_b1), kIdescM128N32, 1);
+          mma_commit(&d2_full[d2]);
+          mma_commit(&a2_empty[s0]);
+          // the unit's final H chunk is only ever the second operand: free it too
+          if (c == nc - 1) mma_commit(&a2_empty[s1]);
+        }
+        __syncwarp();
+      }
+      g += nc + 1;
+    }
   } else {
     // ================= output warps (D2 -> rule -> next generation) ==========
     // Each warp owns 32 strip columns and its own staging slots and TMA
@@ -394,8 +403,8 @@ __global__ void __launch_bounds__(kThreads, 2)
     int strip, c0, nc;
     while (it.next(strip, c0, nc)) {
       for (int c = 0; c < nc; ++c, ++o) {
-        const uint32_t d2 = o & 1;
-        mbar_wait(&d2_full[d2], (o >> 1) & 1);
+        const uint32_t d2 = o % kD2Slots, slot_idx = o & 1;
+        mbar_wait(&d2_full[d2], (o / kD2Slots) & 1);
         if (warp == 6 && lane == 0) LTL_TRACE(9, o);
         tc_fence_after();
         uint32_t z0[8], z1[8];
@@ -430,13 +439,13 @@ __global__ void __launch_bounds__(kThreads, 2)
         // this warp's slot d2 was last read by its TMA store of chunk o-2
         if (lane == 0) tma_store_wait_read<1>();
         __syncwarp();
-        const uint32_t slot = stage_u32 + d2 * kStageBytes;
+        const uint32_t slot = stage_u32 + slot_idx * kStageBytes;
         stmatrix_x4_trans_b8(slot + addr_h0, w0[0], w0[1], w0[2], w0[3]);
         stmatrix_x4_trans_b8(slot + addr_h1, w1[0], w1[1], w1[2], w1[3]);
         fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) {
-          tma_store_2d(&store_map, my_stage + d2 * kStageBytes, strip * kStripCols + 32 * q,
+          tma_store_2d(&store_map, my_stage + slot_idx * kStageBytes, strip * kStripCols + 32 * q,
                        (c0 + c) * kChunkRows);
           tma_store_commit();
           if (warp == 6) LTL_TRACE(11, o);
