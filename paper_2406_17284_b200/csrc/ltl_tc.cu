@@ -7,37 +7,40 @@
 // fragments pi1/pi2/pi3 (src/fragment.cpp:23-41).  Here the same banded
 // products run on the 5th-generation tensor cores in their native shapes:
 //
-//   tile     a 128-column strip of the slab, streamed down in 32-row chunks
+//   tile     a 128-column strip of the slab, streamed down in 64-row chunks
 //   pass 1   D1[x][y] = sum_k A1[x][k] * X[y][k]            tcgen05.mma kind::i8
-//            A1 = 128 x 160 band, resident in SMEM; X = TMA-loaded 32 x 160
-//            chunk (K-major, SWIZZLE_32B); M = 128 (x), N = 32 (y), K = 5 x 32.
+//            A1 = 128 x 160 band, resident in SMEM; X = TMA-loaded 64 x 160
+//            chunk (K-major, SWIZZLE_32B); M = 128 (x), N = 64 (y), K = 5 x 32.
 //            A1[x][k] = [|k-16-x| <= r] + 128*[k == x+16]: the extra 128 on
 //            the centre carries the cell state out in bit 7 (H <= 33 < 128).
 //   convert  epilogue: D1 (s32 in TMEM) -> two byte planes written back into
 //            TMEM as K-major A operands of pass 2 (no SMEM round trip):
 //              Moore: H = D1 & 0x7F and S = D1 & 0x80 (state * 128)
 //              VN   : H' = D1 (= H + 128*state) and s = state
-//   pass 2   D2[x][j] = sum over the 64 H rows around output chunk c
+//   pass 2   D2[x][j] = sum over the 96 H rows around output chunk c
 //              Moore: H*Bv + S*(16*Iv)  = R_box   + 2048*state
 //              VN   : H'*Iv + s*Bv      = R_cross + 128*state
-//            4 MMAs (A from TMEM, band B from SMEM).  Folding the state into
+//            6 MMAs (A from TMEM, band B from SMEM).  Folding the state into
 //            the accumulator makes the birth/survival rule (apply_transition,
 //            src/rule.cpp:99-111) a pure function of one 12-bit number Z.
 //   rule     Z is read back two cells per register (16-bit lanes); the two
 //            range tests (dead: b1..b2, live: K+s1'..K+s2') are four biased
 //            adds and two LOP3s per register (bit 15 of each lane = result).
-//   store    the D2 columns are permuted (pi, below) so that stmatrix.trans
-//            writes each 16x256b TMEM fragment straight into a row-major,
-//            SWIZZLE_32B 32x32 staging tile per warp -> TMA store of the next
-//            generation (no CTA-wide barrier on the output path).
+//   store    the D2 columns are permuted (out_row_of_col) so that
+//            stmatrix.trans writes each 16x256b TMEM fragment straight into a
+//            row-major SWIZZLE_32B 32x32 staging tile per warp -> TMA store of
+//            the next generation (no CTA-wide barrier on the output path).
 //
 // Every quantity is an exact small integer (H <= 33, R <= 1089, Z < 4096), so
 // the result is bit-identical to the reference's int32 loops.
 //
-// Warp roles (352 threads): warp 0 TMA producer, warp 1 pass-1 MMA issuer +
-// TMEM owner, warps 2..5 convert D1, warps 6..9 rule + store D2 (warp w owns
-// TMEM lanes 32*(w%4)..+32, i.e. 32 columns of the strip), warp 10 pass-2
-// MMA issuer.  Persistent CTAs (2 per SM) walk (strip, segment) units.
+// One persistent CTA per SM (all 512 TMEM columns), 15 warps:
+//   warp 0        TMA producer            warp 1   pass-1 MMA issuer, TMEM owner
+//   warps 2..5    convert D1 (warp w: TMEM lane quarter w%4 = 32 strip columns)
+//   warps 6..13   rule + store D2 (quarter w%4, 32 of the 64 chunk rows each)
+//   warp 14       pass-2 MMA issuer
+// Every stage hands over through mbarrier rings, so TMA, both MMA passes and
+// both epilogue groups overlap across chunks.
 #include <cuda.h>
 #include <cuda_runtime.h>
 
@@ -53,53 +56,59 @@ namespace {
 using namespace ptx;
 
 constexpr int kStripCols = 128;  // M of both MMAs = output columns per strip
-constexpr int kChunkRows = 32;   // N of both MMAs = rows per chunk
+constexpr int kRows = 64;        // N of both MMAs = rows per chunk
 constexpr int kKTile = 160;      // 128 + 2*16 input columns per strip
 constexpr int kKChunks = kKTile / 32;
-// Loads in flight per CTA: HBM needs ~bandwidth x loaded latency (~10 MB
-// chip-wide) of outstanding reads; 12 stages x 5 KB x 296 CTAs ~ 18 MB.
-constexpr int kXStages = 12;
+constexpr int kXStages = 10;  // 10 KB each: ~100 KB of loads in flight per SM
 constexpr int kA2Slots = 4;
-constexpr int kD1Slots = 3;  // pass-1 accumulators in flight
-constexpr int kD2Slots = 3;  // pass-2 accumulators in flight
-constexpr int kGroupWarps = 4;   // warps per epilogue group (one per TMEM lane quarter)
-constexpr int kThreads = 96 + 2 * 32 * kGroupWarps;  // TMA, P1 MMA, convert x4, output x4, P2 MMA
-constexpr int kEpiThreads = 32 * kGroupWarps;
-constexpr int kNumBands = 6;  // Bv0, Bv1, Iv0, Iv1, 16*Iv0, 16*Iv1
+constexpr int kD1Slots = 2;
+constexpr int kD2Slots = 2;
+constexpr int kConvWarps = 4;
+constexpr int kOutWarps = 8;
+constexpr int kThreads = 32 * (3 + kConvWarps + kOutWarps);  // 480
+constexpr int kConvThreads = 32 * kConvWarps;
+constexpr int kOutThreads = 32 * kOutWarps;
+constexpr int kWarpP2 = 2 + kConvWarps + kOutWarps;  // 14
+constexpr int kNumBands = 9;  // Bv_j, Iv_j, 16*Iv_j for the 3 K chunks of pass 2
 
 // Shared-memory carve-up (offsets from a 1024-aligned base).
 constexpr uint32_t kSmemA1 = 0;                                    // 5 x 128 x 32 B
-constexpr uint32_t kSmemBand = kSmemA1 + kKChunks * 128 * 32;      // 6 x 1 KB
-constexpr uint32_t kSmemX = kSmemBand + kNumBands * 1024;          // kXStages x 5 KB
-constexpr uint32_t kXStageBytes = kKChunks * kChunkRows * 32;      // 5120
-constexpr uint32_t kSmemStage = kSmemX + kXStages * kXStageBytes;  // 2 x 4 KB staging (SW128)
-constexpr uint32_t kStageBytes = kChunkRows * kStripCols;          // 4096 (4 warps x 1 KB)
-constexpr uint32_t kSmemBars = kSmemStage + 2 * kStageBytes;
-constexpr uint32_t kNumBars = 2 * kXStages + 2 * kD1Slots + 2 * kA2Slots + 2 * kD2Slots;
+constexpr uint32_t kBandBytes = kRows * 32;                        // 2 KB: [64 n][32 k]
+constexpr uint32_t kSmemBand = kSmemA1 + kKChunks * 128 * 32;      // 9 x 2 KB
+constexpr uint32_t kSmemX = kSmemBand + kNumBands * kBandBytes;    // kXStages x 10 KB
+constexpr uint32_t kXChunkBytes = kRows * 32;                      // one 32-column box
+constexpr uint32_t kXStageBytes = kKChunks * kXChunkBytes;         // 10240
+constexpr uint32_t kSmemStage = kSmemX + kXStages * kXStageBytes;  // 8 warps x 2 x 1 KB
+constexpr uint32_t kSmemBars = kSmemStage + kOutWarps * 2 * 1024;
+constexpr uint32_t kNumBars = 2 * (kXStages + kD1Slots + kA2Slots + kD2Slots);
 constexpr uint32_t kSmemTotal = kSmemBars + kNumBars * 8 + 16;
 constexpr uint32_t kSmemAlloc = kSmemTotal + 1024;  // alignment slack
-static_assert(kSmemStage % 1024 == 0, "swizzled staging needs aligned slots");
+static_assert(kSmemAlloc <= 227 * 1024, "shared memory budget");
 
-// TMEM columns (allocation of 256 -> two CTAs per SM).
-constexpr uint32_t kTmemCols = 256;
-constexpr uint32_t kTmemD1 = 0;    // kD1Slots x 32
-constexpr uint32_t kTmemD2 = 96;   // kD2Slots x 32
-constexpr uint32_t kTmemA2 = 192;  // kA2Slots x 16 (plane 0 at +0, plane 1 at +8)
+// TMEM columns: the whole 512 of the SM.
+constexpr uint32_t kTmemCols = 512;
+constexpr uint32_t kTmemD1 = 0;    // kD1Slots x 64
+constexpr uint32_t kTmemD2 = 128;  // kD2Slots x 64
+constexpr uint32_t kTmemA2 = 256;  // kA2Slots x 32 (plane 0 at +0, plane 1 at +16)
 
-constexpr uint32_t kIdescM128N32 = idesc_i8_u8u8_s32(128, 32);
+constexpr uint32_t kIdesc = idesc_i8_u8u8_s32(128, kRows);
 
 struct Params {
   int32_t rows, cols;
-  int32_t num_strips, chunks;  // strips of 128 columns, 32-row output chunks per strip
+  int32_t num_strips, chunks;  // strips of 128 columns, 64-row chunks per strip
   int32_t segs;                // row segments per strip (units = num_strips * segs)
   RuleConsts rule;
   int32_t inject_fault;
   DeviceStats* stats;
-  long long* trace;  // debug timeline of CTA 0 (nullptr: off)
+  long long* trace;  // debug timeline of CTA 0 (only with -DLTL_TC_TRACE_BUILD)
 };
 
+#ifdef LTL_TC_TRACE_BUILD
 #define LTL_TRACE(ev, idx) \
   do { if (p.trace && blockIdx.x == 0 && (idx) < 64) p.trace[(ev) * 64 + (idx)] = clock64(); } while (0)
+#else
+#define LTL_TRACE(ev, idx) do { } while (0)
+#endif
 
 // Static schedule.  A unit is (strip, row segment); unit u is strip u % S,
 // segment u / S, and CTA b walks units b, b + G, b + 2G, ...  The host picks
@@ -124,11 +133,12 @@ struct UnitIter {
   }
 };
 
-// D2 column j holds output row pi(j).  With j = [e, m, a0, a1, v] (bit 0
-// first), pi(j) = [e, a0, a1, m, v]: the stmatrix fragment of column group
-// (m, v) then covers the 8 consecutive output rows 8*(m + 2v) .. +7.
+// D2 column j holds chunk row out_row_of_col(j).  Within each 32-column half,
+// with j = [e, m, a0, a1, v] (bit 0 first) the row is [e, a0, a1, m, v]: the
+// stmatrix fragment of column group (m, v) of a 16x256b load then covers the 8
+// consecutive rows 8*(m + 2v) .. +7 of that half.
 __host__ __device__ constexpr int out_row_of_col(int j) {
-  return (j & 1) | (((j >> 2) & 3) << 1) | (((j >> 1) & 1) << 3) | (j & 16);
+  return (j & 32) | (j & 1) | (((j >> 2) & 3) << 1) | (((j >> 1) & 1) << 3) | (j & 16);
 }
 
 __device__ __forceinline__ uint32_t pack_pairs(uint32_t p0, uint32_t p1) {
@@ -151,7 +161,7 @@ __device__ __forceinline__ uint32_t rule_pair(uint32_t z, const SimdRule& k) {
 }
 
 template <bool kChecked>
-__global__ void __launch_bounds__(kThreads, 2)
+__global__ void __launch_bounds__(kThreads, 1)
     ltl_tc_step_kernel(const __grid_constant__ CUtensorMap load_map,
                        const __grid_constant__ CUtensorMap store_map, const Params p) {
   extern __shared__ uint8_t smem_raw[];
@@ -192,26 +202,24 @@ __global__ void __launch_bounds__(kThreads, 2)
     *reinterpret_cast<uint32_t*>(smem + kSmemA1 + (k0 / 32) * 4096 + sw32_offset(m, k0 % 32)) =
         word;
   }
-  for (uint32_t w = threadIdx.x; w < kNumBands * 32u * 8u; w += kThreads) {
-    const int t = static_cast<int>(w / 256), j = static_cast<int>((w / 8) % 32),
+  // pass-2 B tiles [64 n][32 k]: tile t = kind * 3 + j, K chunk j covers rows
+  // 32j .. 32j+31 of the 96-row H window; output row rho sits at window row 16 + rho
+  for (uint32_t w = threadIdx.x; w < kNumBands * kRows * 8u; w += kThreads) {
+    const int t = static_cast<int>(w / (kRows * 8)), j = static_cast<int>((w / 8) % kRows),
               k0 = 4 * static_cast<int>(w % 8);
-    const int n = out_row_of_col(j);  // output row of D2 column j (row 16+n of the window)
+    const int kind = t / 3, kc = t % 3;
+    const int rho = out_row_of_col(j);
     uint32_t word = 0;
 #pragma unroll
     for (int b = 0; b < 4; ++b) {
-      const int k = k0 + b;
+      const int d = 32 * kc + k0 + b - 16 - rho;  // window row - centre row
       int v;
-      switch (t) {
-        case 0: v = (k - 16 - n >= -r && k - 16 - n <= r); break;  // H rows of chunk c
-        case 1: v = (k + 16 - n >= -r && k + 16 - n <= r); break;  // H rows of chunk c+1
-        case 2: v = (k == n + 16); break;                          // centre row, chunk c
-        case 3: v = (k + 16 == n); break;                          // centre row, chunk c+1
-        case 4: v = 16 * (k == n + 16); break;                     // 16 * centre (state*2048)
-        default: v = 16 * (k + 16 == n); break;
-      }
+      if (kind == 0) v = (d >= -r && d <= r);      // band
+      else if (kind == 1) v = (d == 0);            // centre
+      else v = 16 * (d == 0);                      // 16 * centre (state * 2048)
       word |= static_cast<uint32_t>(v) << (8 * b);
     }
-    *reinterpret_cast<uint32_t*>(smem + kSmemBand + t * 1024 + sw32_offset(j, k0)) = word;
+    *reinterpret_cast<uint32_t*>(smem + kSmemBand + t * kBandBytes + sw32_offset(j, k0)) = word;
   }
   fence_proxy_async_smem();
   if (warp == 0 && lane == 0) {
@@ -223,15 +231,15 @@ __global__ void __launch_bounds__(kThreads, 2)
     }
     for (int i = 0; i < kD1Slots; ++i) {
       mbar_init(&d1_full[i], 1);
-      mbar_init(&d1_empty[i], kEpiThreads);
+      mbar_init(&d1_empty[i], kConvThreads);
+    }
+    for (int i = 0; i < kA2Slots; ++i) {
+      mbar_init(&a2_full[i], kConvThreads);
+      mbar_init(&a2_empty[i], 1);
     }
     for (int i = 0; i < kD2Slots; ++i) {
       mbar_init(&d2_full[i], 1);
-      mbar_init(&d2_empty[i], kEpiThreads);
-    }
-    for (int i = 0; i < kA2Slots; ++i) {
-      mbar_init(&a2_full[i], kEpiThreads);
-      mbar_init(&a2_empty[i], 1);
+      mbar_init(&d2_empty[i], kOutThreads);
     }
     fence_barrier_init();
   }
@@ -256,17 +264,15 @@ __global__ void __launch_bounds__(kThreads, 2)
           mbar_arrive_expect_tx(&x_full[s], kXStageBytes);
 #pragma unroll
           for (int q = 0; q < kKChunks; ++q)
-            tma_load_2d(dst + q * 1024, &load_map, &x_full[s], strip * kStripCols + 32 * q,
-                        (c0 + k) * kChunkRows);
+            tma_load_2d(dst + q * kXChunkBytes, &load_map, &x_full[s],
+                        strip * kStripCols + 32 * q, (c0 + k) * kRows);
         }
       }
     }
   } else if (warp == 1) {
     // ================= pass-1 MMA issuer =================
-    // Runs ahead of everything downstream as far as the X ring and the D1
-    // ring allow; pass 2 has its own issuer warp so neither waits on the other.
-    const uint32_t a1_base = smem_u32(smem + kSmemA1);
-    const uint32_t x_base = smem_u32(smem + kSmemX);
+    const uint64_t a1_desc = smem_desc_sw32_kmajor(smem_u32(smem + kSmemA1));
+    const uint64_t x_desc = smem_desc_sw32_kmajor(smem_u32(smem + kSmemX));
     uint32_t g = 0;
     UnitIter it(p);
     int strip, c0, nc;
@@ -275,22 +281,21 @@ __global__ void __launch_bounds__(kThreads, 2)
         const uint32_t s = g % kXStages, d1 = g % kD1Slots;
         mbar_wait(&x_full[s], (g / kXStages) & 1);
         mbar_wait(&d1_empty[d1], ((g / kD1Slots) & 1) ^ 1);
-        if (lane == 0) LTL_TRACE(1, g);
+        LTL_TRACE(1, g);
         tc_fence_after();
         if (elect_one()) {
+          const uint64_t xd = x_desc + ((s * kXStageBytes) >> 4);
 #pragma unroll
           for (int q = 0; q < kKChunks; ++q)
-            mma_i8_ss(tmem + kTmemD1 + 32 * d1, smem_desc_sw32_kmajor(a1_base + q * 4096),
-                      smem_desc_sw32_kmajor(x_base + s * kXStageBytes + q * 1024),
-                      kIdescM128N32, q > 0);
+            mma_i8_ss(tmem + kTmemD1 + kRows * d1, a1_desc + ((q * 4096) >> 4),
+                      xd + ((q * kXChunkBytes) >> 4), kIdesc, q > 0);
           mma_commit(&x_empty[s]);
           mma_commit(&d1_full[d1]);
-          LTL_TRACE(2, g);
         }
         __syncwarp();
       }
     }
-  } else if (warp < 2 + kGroupWarps) {
+  } else if (warp < 2 + kConvWarps) {
     // ================= convert warps (D1 -> pass-2 A planes) =================
     const uint32_t q = warp & 3;  // TMEM lane quarter = 32 strip columns
     const uint32_t trow = tmem + ((q * 32) << 16);
@@ -301,16 +306,15 @@ __global__ void __launch_bounds__(kThreads, 2)
       for (int k = 0; k <= nc; ++k, ++g) {
         const uint32_t d1 = g % kD1Slots, s = g % kA2Slots;
         mbar_wait(&d1_full[d1], (g / kD1Slots) & 1);
-        if (warp == 2 && lane == 0) LTL_TRACE(5, g);
         tc_fence_after();
-        uint32_t v[16];
-        tmem_ld_32x32b_x16_pack16(trow + kTmemD1 + 32 * d1, v);
+        uint32_t v[32];
+        tmem_ld_32x32b_x32_pack16(trow + kTmemD1 + kRows * d1, v);
         tmem_ld_wait();
         tc_fence_before();
         mbar_arrive(&d1_empty[d1]);
-        uint32_t plane0[8], plane1[8];
+        uint32_t plane0[16], plane1[16];
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
+        for (int j = 0; j < 16; ++j) {
           const uint32_t raw = pack_pairs(v[2 * j], v[2 * j + 1]);  // 4 rows of H + 128*state
           if (vn) {
             plane0[j] = raw;
@@ -321,14 +325,11 @@ __global__ void __launch_bounds__(kThreads, 2)
           }
           if constexpr (kChecked) max_h = __vmaxu4(max_h, raw & 0x7F7F7F7Fu);
         }
-        if (warp == 2 && lane == 0) LTL_TRACE(6, g);
         mbar_wait(&a2_empty[s], ((g / kA2Slots) & 1) ^ 1);
-        if (warp == 2 && lane == 0) LTL_TRACE(7, g);
         tc_fence_after();
-        tmem_st_32x32b_x8(trow + kTmemA2 + 16 * s, plane0);
-        tmem_st_32x32b_x8(trow + kTmemA2 + 16 * s + 8, plane1);
+        tmem_st_32x32b_x16(trow + kTmemA2 + 32 * s, plane0);
+        tmem_st_32x32b_x16(trow + kTmemA2 + 32 * s + 16, plane1);
         tmem_st_wait();
-        if (warp == 2 && lane == 0) LTL_TRACE(8, g);
         tc_fence_before();
         mbar_arrive(&a2_full[s]);
       }
@@ -340,12 +341,14 @@ __global__ void __launch_bounds__(kThreads, 2)
       for (int off = 16; off > 0; off >>= 1) mh = max(mh, __shfl_xor_sync(0xffffffffu, mh, off));
       if (lane == 0) atomicMax(&p.stats->max_h, mh);
     }
-  } else if (warp == 2 + 2 * kGroupWarps) {
+  } else if (warp == kWarpP2) {
     // ================= pass-2 MMA issuer =================
-    const uint32_t band = smem_u32(smem + kSmemBand);
-    // operand pairing {A plane, B band} for the 4 MMAs of an output chunk
-    const uint32_t p0_b0 = band + (vn ? 2048 : 0), p0_b1 = band + (vn ? 3072 : 1024);
-    const uint32_t p1_b0 = band + (vn ? 0 : 4096), p1_b1 = band + (vn ? 1024 : 5120);
+    // K chunk j of the 96-row window: H chunk c rows 0..31 (j=0), 32..63 (j=1),
+    // H chunk c+1 rows 0..31 (j=2) = TMEM column offsets +0, +8, next slot +0.
+    const uint64_t band_desc = smem_desc_sw32_kmajor(smem_u32(smem + kSmemBand));
+    auto tile = [&](int t) { return band_desc + ((t * kBandBytes) >> 4); };
+    // plane 0 pairs with band (Moore) / centre (VN); plane 1 with 16*centre / band
+    const int t_p0 = vn ? 3 : 0, t_p1 = vn ? 0 : 6;
     uint32_t g = 0, o = 0;
     UnitIter it(p);
     int strip, c0, nc;
@@ -355,17 +358,18 @@ __global__ void __launch_bounds__(kThreads, 2)
         const uint32_t s0 = gg % kA2Slots, s1 = (gg + 1) % kA2Slots, d2 = o % kD2Slots;
         mbar_wait(&a2_full[s0], (gg / kA2Slots) & 1);
         mbar_wait(&a2_full[s1], ((gg + 1) / kA2Slots) & 1);
-        if (lane == 0) LTL_TRACE(3, o);
         mbar_wait(&d2_empty[d2], ((o / kD2Slots) & 1) ^ 1);
-        if (lane == 0) LTL_TRACE(4, o);
+        LTL_TRACE(4, o);
         tc_fence_after();
         if (elect_one()) {
-          const uint32_t dcol = tmem + kTmemD2 + 32 * d2;
-          const uint32_t a0 = tmem + kTmemA2 + 16 * s0, a1 = tmem + kTmemA2 + 16 * s1;
-          mma_i8_ts(dcol, a0, smem_desc_sw32_kmajor(p0_b0), kIdescM128N32, 0);
-          mma_i8_ts(dcol, a1, smem_desc_sw32_kmajor(p0_b1), kIdescM128N32, 1);
-          mma_i8_ts(dcol, a0 + 8, smem_desc_sw32_kmajor(p1_b0), kIdescM128N32, 1);
-          mma_i8_ts(dcol, a1 + 8, smem_desc_sw32_kmajor(p1_b1), kIdescM128N32, 1);
+          const uint32_t dcol = tmem + kTmemD2 + kRows * d2;
+          const uint32_t a0 = tmem + kTmemA2 + 32 * s0, a1 = tmem + kTmemA2 + 32 * s1;
+          mma_i8_ts(dcol, a0, tile(t_p0 + 0), kIdesc, 0);
+          mma_i8_ts(dcol, a0 + 8, tile(t_p0 + 1), kIdesc, 1);
+          mma_i8_ts(dcol, a1, tile(t_p0 + 2), kIdesc, 1);
+          mma_i8_ts(dcol, a0 + 16, tile(t_p1 + 0), kIdesc, 1);
+          mma_i8_ts(dcol, a0 + 24, tile(t_p1 + 1), kIdesc, 1);
+          mma_i8_ts(dcol, a1 + 16, tile(t_p1 + 2), kIdesc, 1);
           mma_commit(&d2_full[d2]);
           mma_commit(&a2_empty[s0]);
           // the unit's final H chunk is only ever the second operand: free it too
@@ -377,10 +381,11 @@ __global__ void __launch_bounds__(kThreads, 2)
     }
   } else {
     // ================= output warps (D2 -> rule -> next generation) ==========
-    // Each warp owns 32 strip columns and its own staging slots and TMA
-    // stores, so the output path needs no CTA-wide barrier.
+    // Warp w owns strip columns 32*(w%4)..+32 and chunk rows 32*half..+32 (its
+    // own staging slots and TMA stores: no CTA-wide barrier on this path).
     const uint32_t q = warp & 3;
-    const uint32_t trow = tmem + ((q * 32) << 16);
+    const uint32_t half = (warp - (2 + kConvWarps)) >> 2;
+    const uint32_t trow = tmem + ((q * 32) << 16) + 32 * half;
     const RuleConsts rc = p.rule;
     const uint32_t K = vn ? 128u : 2048u;
     SimdRule sr;
@@ -394,7 +399,8 @@ __global__ void __launch_bounds__(kThreads, 2)
     uint32_t max_r = 0, bad = 0;
     // staging: per warp 2 slots of [32 rows][32 B], SWIZZLE_32B (16-byte
     // chunk ^= (row >> 2) & 1); this thread addresses row `lane`.
-    uint8_t* my_stage = smem + kSmemStage + q * 1024;
+    const uint32_t wslot = warp - (2 + kConvWarps);
+    uint8_t* my_stage = smem + kSmemStage + wslot * 2048;
     const uint32_t stage_u32 = smem_u32(my_stage);
     const uint32_t addr_h0 = lane * 32 + ((0u ^ ((lane >> 2) & 1)) << 4);
     const uint32_t addr_h1 = lane * 32 + ((1u ^ ((lane >> 2) & 1)) << 4);
@@ -403,13 +409,12 @@ __global__ void __launch_bounds__(kThreads, 2)
     int strip, c0, nc;
     while (it.next(strip, c0, nc)) {
       for (int c = 0; c < nc; ++c, ++o) {
-        const uint32_t d2 = o % kD2Slots, slot_idx = o & 1;
+        const uint32_t d2 = o % kD2Slots, slot = o & 1;
         mbar_wait(&d2_full[d2], (o / kD2Slots) & 1);
-        if (warp == 6 && lane == 0) LTL_TRACE(9, o);
         tc_fence_after();
         uint32_t z0[8], z1[8];
-        tmem_ld_16x256b_x2_pack16(trow + kTmemD2 + 32 * d2, z0);
-        tmem_ld_16x256b_x2_pack16(trow + (16u << 16) + kTmemD2 + 32 * d2, z1);
+        tmem_ld_16x256b_x2_pack16(trow + kTmemD2 + kRows * d2, z0);
+        tmem_ld_16x256b_x2_pack16(trow + (16u << 16) + kTmemD2 + kRows * d2, z1);
         tmem_ld_wait();
         tc_fence_before();
         mbar_arrive(&d2_empty[d2]);
@@ -436,19 +441,19 @@ __global__ void __launch_bounds__(kThreads, 2)
             }
           }
         }
-        // this warp's slot d2 was last read by its TMA store of chunk o-2
+        // this warp's staging slot was last read by its TMA store of chunk o-2
         if (lane == 0) tma_store_wait_read<1>();
         __syncwarp();
-        const uint32_t slot = stage_u32 + slot_idx * kStageBytes;
-        stmatrix_x4_trans_b8(slot + addr_h0, w0[0], w0[1], w0[2], w0[3]);
-        stmatrix_x4_trans_b8(slot + addr_h1, w1[0], w1[1], w1[2], w1[3]);
+        const uint32_t sa = stage_u32 + slot * 1024;
+        stmatrix_x4_trans_b8(sa + addr_h0, w0[0], w0[1], w0[2], w0[3]);
+        stmatrix_x4_trans_b8(sa + addr_h1, w1[0], w1[1], w1[2], w1[3]);
         fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) {
-          tma_store_2d(&store_map, my_stage + slot_idx * kStageBytes, strip * kStripCols + 32 * q,
-                       (c0 + c) * kChunkRows);
+          tma_store_2d(&store_map, my_stage + slot * 1024, strip * kStripCols + 32 * q,
+                       (c0 + c) * kRows + 32 * half);
           tma_store_commit();
-          if (warp == 6) LTL_TRACE(11, o);
+          if (warp == 2 + kConvWarps) LTL_TRACE(11, o);
         }
       }
     }
@@ -473,12 +478,11 @@ __global__ void __launch_bounds__(kThreads, 2)
 size_t tc_smem_bytes() { return kSmemAlloc; }
 
 cudaError_t launch_tc_step(const TcLaunch& a, cudaStream_t stream) {
-  static int num_sms = 0, ctas_per_sm = 2;
+  static int num_sms = 0;
   if (num_sms == 0) {
     int dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
-    if (const char* e = std::getenv("LTL_TC_CTAS_PER_SM")) ctas_per_sm = std::atoi(e) > 1 ? 2 : 1;
     for (auto fn : {ltl_tc_step_kernel<false>, ltl_tc_step_kernel<true>}) {
       cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            static_cast<int>(kSmemAlloc));
@@ -490,8 +494,7 @@ cudaError_t launch_tc_step(const TcLaunch& a, cudaStream_t stream) {
   p.rows = a.rows;
   p.cols = a.cols;
   p.num_strips = (a.cols + kStripCols - 1) / kStripCols;
-  p.chunks = (a.rows + kChunkRows - 1) / kChunkRows;
-  const int slots = num_sms * ctas_per_sm;
+  p.chunks = (a.rows + kRows - 1) / kRows;
   p.rule = a.rule;
   p.inject_fault = a.inject_fault;
   p.stats = a.stats;
@@ -499,6 +502,7 @@ cudaError_t launch_tc_step(const TcLaunch& a, cudaStream_t stream) {
   // Balanced units (UnitIter): with S <= slots, split every strip into
   // segs = slots / S row segments (>= 2 chunks each) and run one unit per
   // CTA; with S > slots, give each CTA the same number of whole strips.
+  const int slots = num_sms;
   const int S = p.num_strips;
   int64_t grid;
   if (S <= slots) {

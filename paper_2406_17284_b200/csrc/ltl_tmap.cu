@@ -46,13 +46,13 @@ cudaError_t encode(CUtensorMap* map, void* base, uint64_t w, uint64_t h, uint64_
 
 }  // namespace
 
-// Whole padded slab; 32 x 32 boxes in the SWIZZLE_32B K-major layout the
-// pass-1 B operand descriptor expects (ptx::smem_desc_sw32_kmajor).
+// Whole padded slab; 32-column x 64-row boxes in the SWIZZLE_32B K-major
+// layout the pass-1 B operand descriptor expects (ptx::smem_desc_sw32_kmajor).
 cudaError_t make_load_map(CUtensorMap* map, const SlabView& s) {
   if (s.rows <= 0 || s.cols <= 0) return cudaSuccess;
   return encode(map, s.buf, static_cast<uint64_t>(s.cols) + 2 * kHalo,
                 static_cast<uint64_t>(s.rows) + 2 * kHalo, static_cast<uint64_t>(s.pitch), 32,
-                32, CU_TENSOR_MAP_SWIZZLE_32B);
+                64, CU_TENSOR_MAP_SWIZZLE_32B);
 }
 
 // Interior only: stores of partial strips / chunks are clipped to the torus.
