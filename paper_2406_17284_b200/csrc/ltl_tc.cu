@@ -499,13 +499,25 @@ cudaError_t launch_tc_step(const TcLaunch& a, cudaStream_t stream) {
   p.inject_fault = a.inject_fault;
   p.stats = a.stats;
   p.trace = a.trace;
-  // Balanced units (UnitIter): with S <= slots, split every strip into
-  // segs = slots / S row segments (>= 2 chunks each) and run one unit per
-  // CTA; with S > slots, give each CTA the same number of whole strips.
+  // Balanced units (UnitIter).  Preferred: the smallest segs for which the
+  // S * segs units divide evenly over every SM (e.g. 128 strips x 37 segments
+  // = 32 units per CTA on 148 SMs) while segments stay >= 4 chunks -- all SMs
+  // busy, equal work, and the unit-order keeps neighbouring strips in flight
+  // together.  Otherwise: with S <= slots, segs = slots / S and one unit per
+  // CTA; with S > slots, the same number of whole strips per CTA.
   const int slots = num_sms;
   const int S = p.num_strips;
   int64_t grid;
-  if (S <= slots) {
+  int even_segs = 0;
+  for (int segs = 1; segs <= p.chunks / 4; ++segs)
+    if ((static_cast<int64_t>(S) * segs) % slots == 0) {
+      even_segs = segs;
+      break;
+    }
+  if (even_segs > 0) {
+    p.segs = even_segs;
+    grid = slots;
+  } else if (S <= slots) {
     int segs = slots / S;
     const int max_segs = p.chunks / 2 > 1 ? p.chunks / 2 : 1;
     if (segs > max_segs) segs = max_segs;
