@@ -529,6 +529,20 @@ cudaError_t launch_tc_step(const TcLaunch& a, cudaStream_t stream) {
     grid = (S + per_cta - 1) / per_cta;
   }
   if (a.grid > 0 && a.grid < grid) grid = a.grid;
+  // tuning knobs (benchmark sweeps only): LTL_TC_SEGS=<segments per strip>,
+  // LTL_TC_GRID=<CTAs>
+  if (const char* e = std::getenv("LTL_TC_SEGS")) {
+    const int v = std::atoi(e);
+    if (v >= 1 && v <= p.chunks) {
+      p.segs = v;
+      grid = static_cast<int64_t>(S) * v;
+      if (grid > slots) grid = slots;
+    }
+  }
+  if (const char* e = std::getenv("LTL_TC_GRID")) {
+    const int v = std::atoi(e);
+    if (v >= 1 && v <= slots) grid = v;
+  }
   if (a.stats)
     ltl_tc_step_kernel<true><<<grid, kThreads, kSmemAlloc, stream>>>(*a.load_map, *a.store_map, p);
   else
