@@ -499,24 +499,27 @@ cudaError_t launch_tc_step(const TcLaunch& a, cudaStream_t stream) {
   p.inject_fault = a.inject_fault;
   p.stats = a.stats;
   p.trace = a.trace;
-  // Balanced units (UnitIter).  Preferred: the smallest segs for which the
-  // S * segs units divide evenly over every SM (e.g. 128 strips x 37 segments
-  // = 32 units per CTA on 148 SMs) while segments stay >= 4 chunks -- all SMs
-  // busy, equal work, and the unit-order keeps neighbouring strips in flight
-  // together.  Otherwise: with S <= slots, segs = slots / S and one unit per
-  // CTA; with S > slots, the same number of whole strips per CTA.
+  // Balanced units (UnitIter).  Measured on B200 (tools/ubench_stream2.cu,
+  // profiles/): streaming whole strips with every CTA on the same rows and the
+  // in-flight strips covering an aligned power-of-two span of each row runs
+  // at ~4.7-5 TB/s, while 148 concurrent strips (an unaligned 148/256 of the
+  // row) or many short segments drop to ~2.6-3.1 TB/s.  So for wide grids
+  // (S >= 64 strips) use the largest divisor G of S with G <= SMs, one whole
+  // strip per unit (CTA b streams strips b, b + G, ...).  Small grids split
+  // strips into row segments to fill the GPU.
   const int slots = num_sms;
   const int S = p.num_strips;
   int64_t grid;
-  int even_segs = 0;
-  for (int segs = 1; segs <= p.chunks / 4; ++segs)
-    if ((static_cast<int64_t>(S) * segs) % slots == 0) {
-      even_segs = segs;
-      break;
-    }
-  if (even_segs > 0) {
-    p.segs = even_segs;
-    grid = slots;
+  int wide_grid = 0;
+  if (S >= 64)
+    for (int g = slots; g >= 1; --g)
+      if (S % g == 0) {
+        wide_grid = g;
+        break;
+      }
+  if (wide_grid >= slots / 2) {
+    p.segs = 1;
+    grid = wide_grid;
   } else if (S <= slots) {
     int segs = slots / S;
     const int max_segs = p.chunks / 2 > 1 ? p.chunks / 2 : 1;

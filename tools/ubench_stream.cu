@@ -14,11 +14,11 @@
 
 using namespace ltl::ptx;
 
-constexpr int kStages = 10;
+constexpr int kStages = 8;
 constexpr int kRows = 64;
 
 struct Cfg {
-  int strips, chunks, segs, box_w, nbox;
+  int strips, chunks, segs, box_w, nbox, wide;  // wide: strips (128 cols) per unit
 };
 
 __global__ void __launch_bounds__(128, 1) stream_kernel(const __grid_constant__ CUtensorMap lmap,
@@ -26,7 +26,7 @@ __global__ void __launch_bounds__(128, 1) stream_kernel(const __grid_constant__ 
                                                         Cfg c) {
   extern __shared__ uint8_t raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(raw) + 1023) & ~uintptr_t(1023));
-  const uint32_t stage_bytes = 160 * kRows;
+  const uint32_t stage_bytes = 288 * kRows;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * stage_bytes);
   uint64_t* empty = full + kStages;
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
@@ -50,7 +50,7 @@ __global__ void __launch_bounds__(128, 1) stream_kernel(const __grid_constant__ 
         mbar_arrive_expect_tx(&full[s], c.nbox * c.box_w * kRows);
         for (int b = 0; b < c.nbox; ++b)
           tma_load_2d(smem + s * stage_bytes + b * c.box_w * kRows, &lmap, &full[s],
-                      strip * 128 + b * c.box_w, k * kRows);
+                      strip * 128 * c.wide + b * c.box_w, k * kRows);
       }
     }
   } else if (warp == 1 && lane == 0) {
@@ -62,9 +62,9 @@ __global__ void __launch_bounds__(128, 1) stream_kernel(const __grid_constant__ 
         const uint32_t s = g % kStages;
         mbar_wait(&full[s], (g / kStages) & 1);
         if (k < c1) {
-          for (int b = 0; b < 4; ++b)
-            tma_store_2d(&smap, smem + s * stage_bytes + b * 32 * kRows, strip * 128 + 32 * b,
-                         k * kRows);
+          for (int b = 0; b < 4 * c.wide; ++b)
+            tma_store_2d(&smap, smem + s * stage_bytes + b * 32 * kRows,
+                         strip * 128 * c.wide + 32 * b, k * kRows);
           tma_store_commit();
           tma_store_wait_read<0>();
         }
@@ -80,8 +80,14 @@ using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, voi
                               CUtensorMapInterleave, CUtensorMapSwizzle, CUtensorMapL2promotion,
                               CUtensorMapFloatOOBfill);
 
+int run(int n);
 int main() {
-  const int n = 16384, pad = n + 32, pitch = (pad + 127) / 128 * 128;
+  run(16384);
+  run(32768);
+  return 0;
+}
+int run(int n) {
+  const int pad = n + 32, pitch = (pad + 127) / 128 * 128;
   uint8_t *a, *b;
   cudaMalloc(&a, (size_t)pad * pitch);
   cudaMalloc(&b, (size_t)pad * pitch);
@@ -92,16 +98,14 @@ int main() {
   EncodeFn enc = reinterpret_cast<EncodeFn>(fp);
   int sms;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-  const size_t smem = kStages * 160 * kRows + 2 * kStages * 8 + 1024;
+  const size_t smem = kStages * 288 * kRows + 2 * kStages * 8 + 1024;
   cudaFuncSetAttribute(stream_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  struct V { int box_w; CUtensorMapSwizzle swz; CUtensorMapL2promotion promo; int grid; int segs; const char* name; };
+  struct V { int box_w; CUtensorMapSwizzle swz; CUtensorMapL2promotion promo; int wide; const char* name; };
   V vars[] = {
-      {32, CU_TENSOR_MAP_SWIZZLE_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, 148, 37, "box32 sw32 promo256 148x(128*37)"},
-      {32, CU_TENSOR_MAP_SWIZZLE_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, 128, 1, "box32 sw32 promo256 128 strips"},
-      {32, CU_TENSOR_MAP_SWIZZLE_32B, CU_TENSOR_MAP_L2_PROMOTION_NONE, 148, 37, "box32 sw32 nopromo 148"},
-      {32, CU_TENSOR_MAP_SWIZZLE_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B, 148, 37, "box32 sw32 promo128 148"},
-      {160, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, 148, 37, "box160 noswz promo256 148"},
-      {32, CU_TENSOR_MAP_SWIZZLE_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, 296, 37, "box32 2 CTAs/SM"},
+      {32, CU_TENSOR_MAP_SWIZZLE_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, 1, "box32 x5, 1 strip/unit"},
+      {32, CU_TENSOR_MAP_SWIZZLE_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, 2, "box32 x9, 2 strips/unit"},
+      {32, CU_TENSOR_MAP_SWIZZLE_32B, CU_TENSOR_MAP_L2_PROMOTION_NONE, 1, "box32 x5 nopromo"},
+      {96, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, 2, "box96 x3, 2 strips/unit"},
   };
   for (const V& v : vars) {
     CUtensorMap lmap, smap;
@@ -114,21 +118,28 @@ int main() {
     enc(&smap, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, b + 16 * pitch + 16, sd, str, sbox, es,
         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    Cfg c{128, n / 64, v.segs, v.box_w, 160 / v.box_w};
+    const int strips = n / 128 / v.wide;
+    int segs = 1;
+    while ((strips * segs) % sms != 0 && segs < 200) ++segs;
+    if (segs >= 200) segs = 1;
+    const int grid = strips * segs < sms ? strips * segs : sms;
+    Cfg c{strips, n / 64, segs, v.box_w, (128 * v.wide + 32) / v.box_w, v.wide};
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
-    for (int w = 0; w < 3; ++w) stream_kernel<<<v.grid, 128, smem>>>(lmap, smap, c);
+    for (int w = 0; w < 3; ++w) stream_kernel<<<grid, 128, smem>>>(lmap, smap, c);
     cudaEventRecord(e0);
     const int it = 20;
-    for (int w = 0; w < it; ++w) stream_kernel<<<v.grid, 128, smem>>>(lmap, smap, c);
+    for (int w = 0; w < it; ++w) stream_kernel<<<grid, 128, smem>>>(lmap, smap, c);
     cudaEventRecord(e1);
     cudaError_t err = cudaEventSynchronize(e1);
     float ms;
     cudaEventElapsedTime(&ms, e0, e1);
     const double us = ms * 1000 / it;
-    std::printf("%-40s %8.1f us/pass  %7.0f GB/s (2 B/cell)  %s\n", v.name, us,
+    std::printf("n=%d %-34s segs=%d grid=%d %8.1f us/pass  %7.0f GB/s (2 B/cell)  %s\n", n, v.name, segs, grid, us,
                 2.0 * n * n / (us * 1e3), cudaGetErrorString(err));
   }
+  cudaFree(a);
+  cudaFree(b);
   return 0;
 }
