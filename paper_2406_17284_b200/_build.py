@@ -28,6 +28,8 @@ NVCC = os.environ.get("NVCC", shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc"
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-Wall",
           "-I", os.path.join(ROOT, "include"), "-I", CSRC]
+# extra nvcc flags for diagnostics builds, e.g. LTL_NVCC_FLAGS=-DLTL_TC_TRACE_BUILD
+COMMON += os.environ.get("LTL_NVCC_FLAGS", "").split()
 
 
 def sources():

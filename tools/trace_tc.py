@@ -14,8 +14,8 @@ rule = sys.argv[2] if len(sys.argv) > 2 else "R5,C2,M1,S34..58,B34..45,NM"
 t = ltl.DeviceTorus(rows=n, cols=n)
 t.init_random(0.21, 1)
 t.time(rule, 2, 0)
-names = ["tma issue", "p1 issue", "p1 committed", "p2 a2 ready", "p2 issue", "conv d1 ready",
-         "conv computed", "conv a2 slot", "conv stored", "out d2 ready", "-", "out stored"]
+
+names = ["tma issue", "p1 issue", "-", "-", "p2 issue", "-", "-", "-", "-", "-", "-", "out stored"]
 rows = [[int(v) for v in line.split(",")] for line in open(path)]
 t0 = min(v for r in rows for v in r if v > 0)
 print("chunk " + " ".join(f"{nm[:12]:>12s}" for nm in names))
