@@ -283,9 +283,14 @@ void run_steps(ltl_ctx* ctx, const ltl_rule_c* rule, int32_t steps, uint32_t fla
                ltl_stats_c* stats) {
   check_run_args(ctx, rule, steps);
   const ltl::RuleConsts rc = rule_consts(*rule);
-  // The negative-count guard is always armed; max_h/max_r ride the same buffer.
+  // Checked launches (device max-reduction of H / R plus the negative-count
+  // guard of src/rule.cpp:104-107) run when stats are requested or a band
+  // fault is injected.  With intact bands the guard cannot fire -- every
+  // reduction contains the centre `mult` times, so count >= 0 by
+  // construction -- which is why the fast path may skip it.
+  const bool checked = (flags & LTL_FLAG_INJECT_FAULT) || (stats && (flags & LTL_FLAG_WANT_STATS));
   reset_stats(ctx);
-  for (int32_t t = 0; t < steps; ++t) enqueue_step(ctx, rc, flags, true, nullptr, nullptr);
+  for (int32_t t = 0; t < steps; ++t) enqueue_step(ctx, rc, flags, checked, nullptr, nullptr);
   sync_all(ctx);
   ltl::DeviceStats agg{};
   for (Slab& s : ctx->slabs) {

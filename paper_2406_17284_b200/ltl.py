@@ -284,12 +284,17 @@ class DeviceTorus:
     def _flags(stencil: bool, inject_fault: bool) -> int:
         return (FLAG_STENCIL if stencil else 0) | (FLAG_INJECT_FAULT if inject_fault else 0)
 
-    def run(self, rule, steps: int, stencil: bool = False, inject_fault: bool = False) -> dict:
+    def run(self, rule, steps: int, stencil: bool = False, inject_fault: bool = False,
+            stats: bool = False):
+        """`steps` generations.  stats=True returns the CatStats analogue (and
+        runs the checked kernel variant that max-reduces H / R on the device)."""
         r = as_rule(rule).to_c()
         st = ltl_stats_c()
-        self._check(self.lib.ltl_run(self._ctx, ctypes.byref(r), steps,
-                                     self._flags(stencil, inject_fault) | FLAG_WANT_STATS,
-                                     ctypes.byref(st)))
+        flags = self._flags(stencil, inject_fault) | (FLAG_WANT_STATS if stats else 0)
+        self._check(self.lib.ltl_run(self._ctx, ctypes.byref(r), steps, flags,
+                                     ctypes.byref(st) if stats else None))
+        if not stats:
+            return None
         return {k: getattr(st, k) for k, _ in ltl_stats_c._fields_ if k != "reserved"}
 
     def run_async(self, rule, steps: int, stencil: bool = False) -> None:
@@ -357,6 +362,7 @@ def run_engine(engine: str, initial: np.ndarray, rule, steps: int, f: int = 16,
         raise ValueError("geometry error: expected a square grid")
     with DeviceTorus(n=g.shape[0], f=f, slabs=slabs) as t:
         t.upload(g)
-        st = t.run(rule, steps, stencil=(engine == "stencil"), inject_fault=inject_fault)
+        st = t.run(rule, steps, stencil=(engine == "stencil"), inject_fault=inject_fault,
+                   stats=stats)
         out = t.download()
     return (out, st) if stats else out
