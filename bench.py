@@ -329,6 +329,8 @@ def main():
     ap.add_argument("--rule", default=RULE)
     ap.add_argument("--cpu-gens", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--dist", action="store_true",
+                    help="use the multi-process slab path even at world size 1 (testing)")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
 
@@ -338,7 +340,7 @@ def main():
     if args.impl == "reference":
         reference_arm(args, rank)
         return
-    if world > 1:
+    if world > 1 or args.dist:
         import torch.distributed as dist
         dist.init_process_group("nccl")
         try:
