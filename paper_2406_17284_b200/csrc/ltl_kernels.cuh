@@ -53,6 +53,8 @@ struct TcLaunch {
   int32_t grid;        // CTAs (0 = auto)
   int32_t seg_chunks;  // unused (kept for ABI of the launch struct)
   long long* trace;    // debug timeline (LTL_TC_TRACE), nullptr = off
+  uint32_t* pace;      // 65 zeroed words for CTA pacing (nullptr = off); the
+                       // kernel leaves them zeroed again when it exits
 };
 cudaError_t launch_tc_step(const TcLaunch& a, cudaStream_t stream);
 size_t tc_smem_bytes();

@@ -44,6 +44,7 @@ struct Slab {
   CUtensorMap load_map[2];
   CUtensorMap store_map[2];
   ltl::DeviceStats* dstats = nullptr;
+  uint32_t* pace = nullptr;  // CTA pacing words; only when the slab has its device alone
   cudaStream_t stream = nullptr;
   bool own_stream = true;
   cudaEvent_t ev_step = nullptr;
@@ -148,6 +149,13 @@ void create_slabs(ltl_ctx* ctx, int32_t num_slabs, const int32_t* dev_ids) {
       ck(cudaMemset(s.buf[b], 0, bytes), "cudaMemset slab");
     }
     ck(cudaMalloc(&s.dstats, sizeof(ltl::DeviceStats)), "cudaMalloc stats");
+    int sharing = 0;
+    for (int32_t j = 0; j < num_slabs; ++j)
+      sharing += (dev_ids ? dev_ids[j] : j % ndev) == s.dev ? 1 : 0;
+    if (sharing == 1) {  // concurrent kernels on one device would defeat pacing
+      ck(cudaMalloc(&s.pace, 65 * sizeof(uint32_t)), "cudaMalloc pace");
+      ck(cudaMemset(s.pace, 0, 65 * sizeof(uint32_t)), "cudaMemset pace");
+    }
     ck(cudaStreamCreateWithFlags(&s.stream, cudaStreamNonBlocking), "cudaStreamCreate");
     ck(cudaEventCreateWithFlags(&s.ev_step, cudaEventDisableTiming), "cudaEventCreate");
     build_maps(s, ctx->cols);
@@ -178,6 +186,7 @@ void destroy_ctx(ltl_ctx* ctx) {
     for (auto& b : s.buf)
       if (b) cudaFree(b);
     if (s.dstats) cudaFree(s.dstats);
+    if (s.pace) cudaFree(s.pace);
     if (s.ev_step) cudaEventDestroy(s.ev_step);
     for (cudaEvent_t e : s.timing) cudaEventDestroy(e);
     if (s.stream && s.own_stream) cudaStreamDestroy(s.stream);
@@ -231,6 +240,7 @@ void enqueue_step(ltl_ctx* ctx, const ltl::RuleConsts& rc, uint32_t flags, bool 
       a.rule = rc;
       a.inject_fault = fault;
       a.stats = want_stats ? s.dstats : nullptr;
+      a.pace = s.pace;
       // Debug: LTL_TC_TRACE=<file> dumps the pipeline timeline of CTA 0 of
       // the first traced launch (12 event kinds x 64 chunks of clock64 stamps).
       static bool traced = false;

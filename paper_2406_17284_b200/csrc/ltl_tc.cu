@@ -101,7 +101,44 @@ struct Params {
   int32_t inject_fault;
   DeviceStats* stats;
   long long* trace;  // debug timeline of CTA 0 (only with -DLTL_TC_TRACE_BUILD)
+  uint32_t* pace;    // 65 words of zeroed global memory, or nullptr (pacing off)
 };
+
+// Soft pacing of the CTAs' TMA producers.  Streaming strips runs near the HBM
+// copy rate only while every CTA reads the same rows at the same time (DRAM
+// page / TLB locality, tools/ubench_stream2.cu); small per-SM speed
+// differences otherwise accumulate into drift over hundreds of chunks.  Every
+// kPaceEvery H chunks a producer publishes its epoch and waits (bounded) until
+// all CTAs have reached epoch - kPaceWindow.  It is only a hint: a wait that
+// exceeds kPaceTimeout cycles disables pacing for that CTA, so co-residency is
+// never required for correctness.
+constexpr int kPaceEvery = 8;
+constexpr int kPaceWindow = 2;
+constexpr long long kPaceTimeout = 400000;  // ~200 us
+
+__device__ __forceinline__ bool pace(uint32_t* pace_buf, uint32_t g) {
+  const uint32_t epoch = g / kPaceEvery;
+  atomicAdd(pace_buf + epoch % 64, 1u);
+  if (epoch < kPaceWindow) return true;
+  const uint32_t e = epoch - kPaceWindow;
+  const uint32_t need = gridDim.x * (e / 64 + 1);
+  volatile uint32_t* slot = pace_buf + e % 64;
+  const long long t0 = clock64();
+  while (*slot < need) {
+    if (clock64() - t0 > kPaceTimeout) return false;
+    __nanosleep(256);
+  }
+  return true;
+}
+
+__device__ __forceinline__ void pace_reset(uint32_t* pace_buf) {
+  // last CTA out zeroes the slots for the next launch (stream-ordered)
+  __threadfence();
+  if (atomicAdd(pace_buf + 64, 1u) == gridDim.x - 1) {
+    for (int i = 0; i < 65; ++i) pace_buf[i] = 0;
+    __threadfence();
+  }
+}
 
 #ifdef LTL_TC_TRACE_BUILD
 #define LTL_TRACE(ev, idx) \
@@ -253,12 +290,14 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ================= TMA producer =================
     if (elect_one()) {
       uint32_t g = 0;
+      bool pacing = p.pace != nullptr;
       UnitIter it(p);
       int strip, c0, nc;
       while (it.next(strip, c0, nc)) {
         for (int k = 0; k <= nc; ++k, ++g) {
           const uint32_t s = g % kXStages;
           mbar_wait(&x_empty[s], ((g / kXStages) & 1) ^ 1);
+          if (pacing && g % kPaceEvery == 0) pacing = pace(p.pace, g);
           LTL_TRACE(0, g);
           uint8_t* dst = smem + kSmemX + s * kXStageBytes;
           mbar_arrive_expect_tx(&x_full[s], kXStageBytes);
@@ -268,6 +307,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                         strip * kStripCols + 32 * q, (c0 + k) * kRows);
         }
       }
+      if (p.pace) pace_reset(p.pace);
     }
   } else if (warp == 1) {
     // ================= pass-1 MMA issuer =================
@@ -499,6 +539,8 @@ cudaError_t launch_tc_step(const TcLaunch& a, cudaStream_t stream) {
   p.inject_fault = a.inject_fault;
   p.stats = a.stats;
   p.trace = a.trace;
+  p.pace = a.pace;
+  if (std::getenv("LTL_TC_NO_PACE")) p.pace = nullptr;
   // Balanced units (UnitIter).  Measured on B200 (tools/ubench_stream2.cu,
   // profiles/): streaming whole strips with every CTA on the same rows and the
   // in-flight strips covering an aligned power-of-two span of each row runs

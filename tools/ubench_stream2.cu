@@ -19,6 +19,8 @@ constexpr int kStages = 8;
 constexpr uint32_t kStageMax = 96 * 288;
 
 struct Cfg {
+  int sync_every;  // >0: CTAs keep within one window of `sync_every` steps of each other
+  unsigned int* progress;
   int mode;        // 0 = V, 1 = H
   int n;           // interior side
   int units;       // strips (V) or bands (H)
@@ -51,6 +53,15 @@ __global__ void __launch_bounds__(128, 1) kern(const __grid_constant__ CUtensorM
       for (int k = 0; k < c.steps; ++k, ++g) {
         const uint32_t s = g % kStages;
         mbar_wait(&empty[s], ((g / kStages) & 1) ^ 1);
+        if (c.sync_every > 0 && g % c.sync_every == 0) {
+          // publish my progress, then wait until every CTA reached g - window
+          const unsigned int epoch = g / c.sync_every;
+          atomicAdd(c.progress + epoch % 64, 1u);
+          if (epoch >= 2) {
+            volatile unsigned int* slot = c.progress + (epoch - 2) % 64;
+            while (*slot < gridDim.x) __nanosleep(200);
+          }
+        }
         mbar_arrive_expect_tx(&full[s], nbox * box_bytes);
         const int x0 = c.mode == 0 ? u * (c.in_cols - 32) : k * 128;
         const int y0 = c.mode == 0 ? k * 64 : u * 64;
@@ -82,7 +93,7 @@ using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, voi
 
 static EncodeFn enc;
 
-void run(int n, int mode, int wide, int grid, const char* name) {
+void run(int n, int mode, int wide, int grid, const char* name, int sync_every = 0) {
   const int pad = n + 32, pitch = (pad + 127) / 128 * 128;
   uint8_t *a, *b;
   cudaMalloc(&a, (size_t)pad * pitch);
@@ -100,6 +111,8 @@ void run(int n, int mode, int wide, int grid, const char* name) {
       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   Cfg c;
+  c.sync_every = sync_every;
+  cudaMalloc(&c.progress, 64 * sizeof(unsigned int));
   c.mode = mode;
   c.n = n;
   c.in_rows = in_rows;
@@ -112,10 +125,16 @@ void run(int n, int mode, int wide, int grid, const char* name) {
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
-  for (int w = 0; w < 2; ++w) kern<<<grid, 128, smem>>>(lmap, smap, c);
+  for (int w = 0; w < 2; ++w) {
+    cudaMemset(c.progress, 0, 64 * sizeof(unsigned int));
+    kern<<<grid, 128, smem>>>(lmap, smap, c);
+  }
   cudaEventRecord(e0);
   const int it = 10;
-  for (int w = 0; w < it; ++w) kern<<<grid, 128, smem>>>(lmap, smap, c);
+  for (int w = 0; w < it; ++w) {
+    cudaMemsetAsync(c.progress, 0, 64 * sizeof(unsigned int));
+    kern<<<grid, 128, smem>>>(lmap, smap, c);
+  }
   cudaEventRecord(e1);
   cudaError_t err = cudaEventSynchronize(e1);
   float ms;
@@ -133,11 +152,11 @@ int main() {
   cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fp, cudaEnableDefault, &q);
   enc = reinterpret_cast<EncodeFn>(fp);
   for (int n : {16384, 32768}) {
-    run(n, 0, 1, 148, "V strip128");
     run(n, 0, 1, n / 128 < 148 ? n / 128 : 128, "V strip128 (<=128 CTAs)");
-    run(n, 0, 2, 148, "V strip256");
-    run(n, 1, 1, 148, "H band64 (96 rows in)");
-    run(n, 1, 1, 296, "H band64 2 CTAs/SM");
+    run(n, 0, 1, n / 128 < 148 ? n / 128 : 128, "V strip128 synced/8", 8);
+    run(n, 0, 1, n / 128 < 148 ? n / 128 : 128, "V strip128 synced/32", 32);
   }
+  run(32768, 0, 1, 148, "V strip128 148 CTAs");
+  run(32768, 0, 1, 148, "V strip128 148 CTAs synced/8", 8);
   return 0;
 }
