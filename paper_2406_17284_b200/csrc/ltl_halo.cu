@@ -27,6 +27,9 @@ __device__ __forceinline__ int wrap(int v, int n) {
 }
 
 __global__ void ltl_halo_kernel(SlabView self, SlabView above, SlabView below) {
+  // PDL: start early, but read the interiors only once the step is complete
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   const int rows = self.rows, cols = self.cols;
   const int tid = blockIdx.x * blockDim.x + threadIdx.x;
   const int nthreads = gridDim.x * blockDim.x;
@@ -73,8 +76,16 @@ cudaError_t launch_halo_fill(const SlabView& self, const SlabView& above, const 
   int64_t work = side > band ? side : band;
   int blocks = static_cast<int>((work + 255) / 256);
   if (blocks > 148 * 4) blocks = 148 * 4;
-  ltl_halo_kernel<<<dim3(blocks, 3), 256, 0, stream>>>(self, above, below);
-  return cudaGetLastError();
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(blocks, 3);
+  cfg.blockDim = dim3(256);
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, ltl_halo_kernel, self, above, below);
 }
 
 }  // namespace ltl

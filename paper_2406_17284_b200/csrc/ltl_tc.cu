@@ -285,6 +285,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  // Everything above only touched this CTA's SMEM/TMEM, so it overlapped the
+  // previous kernel's tail (PDL).  The grid is read from here on.
+  pdl_launch_dependents();
+  pdl_wait_prerequisites();
 
   if (warp == 0) {
     // ================= TMA producer =================
@@ -588,11 +592,19 @@ cudaError_t launch_tc_step(const TcLaunch& a, cudaStream_t stream) {
     const int v = std::atoi(e);
     if (v >= 1 && v <= slots) grid = v;
   }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(static_cast<unsigned>(grid));
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = kSmemAlloc;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
   if (a.stats)
-    ltl_tc_step_kernel<true><<<grid, kThreads, kSmemAlloc, stream>>>(*a.load_map, *a.store_map, p);
-  else
-    ltl_tc_step_kernel<false><<<grid, kThreads, kSmemAlloc, stream>>>(*a.load_map, *a.store_map, p);
-  return cudaGetLastError();
+    return cudaLaunchKernelEx(&cfg, ltl_tc_step_kernel<true>, *a.load_map, *a.store_map, p);
+  return cudaLaunchKernelEx(&cfg, ltl_tc_step_kernel<false>, *a.load_map, *a.store_map, p);
 }
 
 }  // namespace ltl
