@@ -29,7 +29,7 @@
 extern "C" {
 #endif
 
-#define LTL_ABI_VERSION 1
+#define LTL_ABI_VERSION 2
 
 /* status codes <-> reference exception classes */
 #define LTL_OK 0
@@ -162,11 +162,23 @@ int ltl_step_part(ltl_ctx* ctx, const ltl_rule_c* rule, uint32_t flags);
  * row wrap / peer rows unless the context is a part). */
 int ltl_fill_halo(ltl_ctx* ctx);
 
-/* Device pointers of slab `slab`'s current (which = 0) or other (1)
- * generation buffer, its pitch and interior row count; for exchanging halos
- * through an external transport (NCCL, IPC). */
-int ltl_slab_buffer(ltl_ctx* ctx, int32_t slab, int32_t which, void** dev_ptr, int64_t* pitch,
-                    int32_t* rows);
+/* Packed edge rows for an external halo transport (NCCL send/recv, CUDA
+ * IPC), enqueued on the context's stream; device buffers of 16 x cols bytes,
+ * row-major.  ltl_pack_edges: top <- interior rows [0, 16), bot <- interior
+ * rows [rows-16, rows) of the current generation.  ltl_unpack_halo: the 16
+ * halo rows above <- top_halo (the rows just above this slab, i.e. the upper
+ * neighbour's bottom edge), below <- bot_halo, each with its column wrap. */
+int ltl_pack_edges(ltl_ctx* ctx, void* top, void* bot);
+int ltl_unpack_halo(ltl_ctx* ctx, const void* top_halo, const void* bot_halo);
+
+/* Device pointer of slab `slab`'s current (which = 0) or other (1)
+ * generation buffer, its strip size in bytes and interior row count.  The
+ * device layout is column strips: logical column x in [-128, 128 * (strips-1))
+ * of padded row y (interior rows at [16, 16 + rows)) is byte
+ * ((x + 128) / 128) * strip_bytes + y * 128 + (x + 128) % 128, with
+ * strip_bytes = (rows + 32) * 128 and strips = ceil(cols / 128) + 2. */
+int ltl_slab_buffer(ltl_ctx* ctx, int32_t slab, int32_t which, void** dev_ptr,
+                    int64_t* strip_bytes, int32_t* rows);
 
 /* --- host-side rule helpers (pure C, no device) --------------------------- */
 

@@ -4,14 +4,17 @@
 // cell receives its modular interior image.  Column wrap is local to the slab;
 // the rows above / below the slab come from the interiors of the neighbouring
 // slabs (`above`, `below`), which may live on peer GPUs -- the reads then go
-// over NVLink straight out of the peer's HBM (peer access / IPC mappings).
-// With one slab all three views are the same buffer and this is exactly the
-// reference's single-grid fill, including n < 16 where images wrap repeatedly.
+// over NVLink straight out of the peer's HBM (peer access).  With one slab all
+// three views are the same buffer and this is exactly the reference's
+// single-grid fill, including n < 16 where images wrap repeatedly.
 //
-// All sources are interior cells (never other halo cells), so the three parts
-// below run concurrently without ordering: side columns of the interior rows,
-// and the 16-row bands above and below (full padded width, interior part
-// copied 16 bytes at a time).
+// All sources are interior cells (never other halo cells), so the parts below
+// run concurrently without ordering:
+//   blockIdx.y == 0  side columns of the interior rows (32 cells per row)
+//   blockIdx.y == 1  the 16 rows above, all logical columns [-16, cols + 16)
+//   blockIdx.y == 2  the 16 rows below
+// In the strip layout (ltl_kernels.cuh) a 16-row halo band of one strip is a
+// contiguous 2 KB block; interior columns move 16 bytes at a time.
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -34,34 +37,34 @@ __global__ void ltl_halo_kernel(SlabView self, SlabView above, SlabView below) {
   const int tid = blockIdx.x * blockDim.x + threadIdx.x;
   const int nthreads = gridDim.x * blockDim.x;
   if (blockIdx.y == 0) {
-    // side columns: 32 bytes per interior row, one warp per row
     for (int i = tid; i < rows * 2 * kHalo; i += nthreads) {
       const int y = i / (2 * kHalo), c = i % (2 * kHalo);
-      const int px = c < kHalo ? c : cols + c;  // left 0..15, right cols+16..cols+31
-      const int sx = wrap(px - kHalo, cols);
-      uint8_t* row = self.buf + static_cast<int64_t>(y + kHalo) * self.pitch;
-      row[px] = row[sx + kHalo];
+      const int px = c < kHalo ? c - kHalo : cols + (c - kHalo);  // [-16, 0) or [cols, cols+16)
+      const int py = y + kHalo;
+      self.buf[self.offset(py, px)] = self.buf[self.offset(py, wrap(px, cols))];
     }
     return;
   }
-  // row bands: blockIdx.y == 1 -> 16 rows above (from `above`), 2 -> below
   const bool top = blockIdx.y == 1;
   const SlabView& src = top ? above : below;
   if (src.rows < 0) return;  // rows come from an external transport
+  // interior columns in 16-byte groups (cols % 16 == 0), edge cells one by one
   const bool vec = (cols % 16) == 0;
-  const int per_row = vec ? cols / 16 + 2 * kHalo : cols + 2 * kHalo;
+  const int groups = vec ? cols / 16 : 0;
+  const int edge = vec ? 2 * kHalo : cols + 2 * kHalo;
+  const int per_row = groups + edge;
   for (int i = tid; i < kHalo * per_row; i += nthreads) {
     const int t = i / per_row, e = i % per_row;
     const int py = top ? t : rows + kHalo + t;
-    const int sy = top ? wrap(t - kHalo, src.rows) : wrap(t, src.rows);
-    uint8_t* drow = self.buf + static_cast<int64_t>(py) * self.pitch;
-    const uint8_t* srow = src.buf + static_cast<int64_t>(sy + kHalo) * src.pitch + kHalo;
-    if (vec && e < cols / 16) {
-      reinterpret_cast<uint4*>(drow + kHalo)[e] = reinterpret_cast<const uint4*>(srow)[e];
+    const int sy = (top ? wrap(t - kHalo, src.rows) : wrap(t, src.rows)) + kHalo;
+    if (e < groups) {
+      const int px = 16 * e;
+      *reinterpret_cast<uint4*>(self.buf + self.offset(py, px)) =
+          *reinterpret_cast<const uint4*>(src.buf + src.offset(sy, px));
     } else {
-      const int b = vec ? e - cols / 16 : e;  // vec: 0..31 edge bytes; else all bytes
-      const int px = vec ? (b < kHalo ? b : cols + b) : b;
-      drow[px] = srow[wrap(px - kHalo, cols)];
+      const int b = e - groups;
+      const int px = vec ? (b < kHalo ? b - kHalo : cols + b - kHalo) : b - kHalo;
+      self.buf[self.offset(py, px)] = src.buf[src.offset(sy, wrap(px, cols))];
     }
   }
 }
@@ -72,7 +75,7 @@ cudaError_t launch_halo_fill(const SlabView& self, const SlabView& above, const 
                              cudaStream_t stream) {
   if (self.rows <= 0 || self.cols <= 0) return cudaSuccess;
   const int64_t side = 2LL * kHalo * self.rows;
-  const int64_t band = kHalo * (self.cols / 16 + 2LL * kHalo);
+  const int64_t band = kHalo * (self.cols / 4 + 2LL * kHalo);
   int64_t work = side > band ? side : band;
   int blocks = static_cast<int>((work + 255) / 256);
   if (blocks > 148 * 4) blocks = 148 * 4;

@@ -29,10 +29,9 @@ __global__ void ltl_init_kernel(SlabView s, int32_t row0, int32_t fill_rows, int
                                 uint64_t seed, uint64_t threshold, int32_t mode) {
   // mode 0: never alive, 1: always alive, 2: z < threshold.  Rows over
   // blockIdx.y (grid-stride), four consecutive cells per thread (one 32-bit
-  // store; the interior starts 16 bytes into a 128-byte aligned row).
+  // store; four aligned cells never straddle a 128-column strip).
   for (int32_t y = blockIdx.y; y < s.rows; y += gridDim.y) {
     const int32_t gy = row0 + y;
-    uint8_t* row = s.buf + static_cast<int64_t>(y + kHalo) * s.pitch + kHalo;
     for (int32_t x0 = 4 * (blockIdx.x * blockDim.x + threadIdx.x); x0 < s.cols;
          x0 += 4 * gridDim.x * blockDim.x) {
       uint32_t word = 0;
@@ -47,10 +46,11 @@ __global__ void ltl_init_kernel(SlabView s, int32_t row0, int32_t fill_rows, int
         }
         word |= v << (8 * b);
       }
+      uint8_t* cell = s.buf + s.offset(y + kHalo, x0);
       if (x0 + 4 <= s.cols) {
-        *reinterpret_cast<uint32_t*>(row + x0) = word;
+        *reinterpret_cast<uint32_t*>(cell) = word;
       } else {
-        for (int b = 0; x0 + b < s.cols; ++b) row[x0 + b] = static_cast<uint8_t>(word >> (8 * b));
+        for (int b = 0; x0 + b < s.cols; ++b) cell[b] = static_cast<uint8_t>(word >> (8 * b));
       }
     }
   }

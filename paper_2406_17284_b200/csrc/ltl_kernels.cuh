@@ -13,6 +13,9 @@ namespace ltl {
 // whatever f is, because r <= 16 always and the halo only has to hold r.
 constexpr int kHalo = 16;
 
+// Column-strip width of the device layout (= the M of the tcgen05 MMAs).
+constexpr int kStrip = 128;
+
 // Rule constants the epilogues need, pre-reduced on the host from LtlRule
 // (include/catsim/rule.hpp:17-32) and apply_transition (src/rule.cpp:99-111):
 //   dead cell:  next = (unsigned)(R - lo_dead) <= w_dead       (count = R)
@@ -26,14 +29,40 @@ struct RuleConsts {
   int32_t neg_live;  // mult - m
 };
 
-// One device slab: rows [row0, row0 + rows) of the global torus, all cols.
-// Buffer geometry: (rows + 2*kHalo) x pitch bytes, interior at (kHalo, kHalo).
+// One device slab: rows [row0, row0 + rows) of the global torus, all cols,
+// stored as column STRIPS (the reference's Grid::cells is one row-major
+// vector, grid.hpp:60; on the device the layout is chosen for HBM streaming).
+//
+//   logical column px in [-128, 128 * (strips - 1)) lives in storage strip
+//   (px + 128) / 128 at byte (px + 128) % 128 of its row; strip 0 and the
+//   strip after the last interior one are padding that hold the 16 halo
+//   columns.  Each strip is a contiguous block of (rows + 32) rows x 128 B:
+//   padded row py in [0, rows + 32), interior rows at [16, 16 + rows).
+//
+// A 64..256-row piece of one strip is therefore ONE contiguous HBM block,
+// which is what lets the step kernel stream at copy bandwidth
+// (tools/ubench_stream3.cu; profiles/).
 struct SlabView {
   uint8_t* buf;
   int32_t rows;
   int32_t cols;
-  int64_t pitch;
+  int32_t strips;       // storage strips = interior strips + 2
+  int64_t strip_bytes;  // (rows + 2 * kHalo) * kStrip
+
+  __host__ __device__ __forceinline__ int64_t offset(int32_t py, int32_t px) const {
+    const int32_t sx = px + kStrip;
+    return static_cast<int64_t>(sx >> 7) * strip_bytes + static_cast<int64_t>(py) * kStrip +
+           (sx & (kStrip - 1));
+  }
+  __host__ __device__ __forceinline__ int64_t bytes() const { return strips * strip_bytes; }
 };
+
+__host__ __device__ inline int32_t interior_strips(int32_t cols) {
+  return (cols + kStrip - 1) / kStrip;
+}
+__host__ __device__ inline int32_t storage_strips(int32_t cols) {
+  return interior_strips(cols) + 2;
+}
 
 struct DeviceStats {
   int32_t max_h;
@@ -44,17 +73,14 @@ struct DeviceStats {
 
 // ---- tcgen05 banded-MMA step (ltl_tc.cu)
 struct TcLaunch {
-  const CUtensorMap* load_map;   // padded slab, box {32, 32}, SWIZZLE_32B
-  const CUtensorMap* store_map;  // interior of the destination slab, box {128, 32}
+  const CUtensorMap* load_map;   // whole source slab, {128, 256, 1} boxes, SWIZZLE_128B
+  const CUtensorMap* store_map;  // destination interior rows, {32, 32, 1} boxes, SWIZZLE_32B
   int32_t rows, cols;
   RuleConsts rule;
   int32_t inject_fault;
   DeviceStats* stats;  // nullptr -> no stats reduction
   int32_t grid;        // CTAs (0 = auto)
-  int32_t seg_chunks;  // unused (kept for ABI of the launch struct)
   long long* trace;    // debug timeline (LTL_TC_TRACE), nullptr = off
-  uint32_t* pace;      // 65 zeroed words for CTA pacing (nullptr = off); the
-                       // kernel leaves them zeroed again when it exits
 };
 cudaError_t launch_tc_step(const TcLaunch& a, cudaStream_t stream);
 size_t tc_smem_bytes();
@@ -77,8 +103,20 @@ cudaError_t launch_init_random(const SlabView& s, int32_t row0, int32_t fill_row
 // ---- periodic halo refresh (ltl_halo.cu)
 // Fills the halo of `self` from the interiors of `above` (rows over the top
 // edge), `below` (rows under the bottom edge) and `self` (column wrap).  For a
-// single slab all three are the same buffer.
+// single slab all three are the same buffer.  above.rows < 0: refresh only
+// the column wrap (the row halo comes from an external transport).
 cudaError_t launch_halo_fill(const SlabView& self, const SlabView& above, const SlabView& below,
                              cudaStream_t stream);
+
+// ---- layout conversion and edge exchange (ltl_layout.cu)
+// Dense row-major rows x cols interior <-> strip slab interior.
+cudaError_t launch_to_strips(const uint8_t* dense, const SlabView& s, cudaStream_t stream);
+cudaError_t launch_from_strips(const SlabView& s, uint8_t* dense, cudaStream_t stream);
+// top[16][cols] <- interior rows [0, 16); bot[16][cols] <- rows [rows-16, rows).
+cudaError_t launch_pack_edges(const SlabView& s, uint8_t* top, uint8_t* bot, cudaStream_t stream);
+// halo rows above <- top_halo[16][cols], below <- bot_halo[16][cols] (with the
+// column wrap of those rows, i.e. the corners).
+cudaError_t launch_unpack_halo(const SlabView& s, const uint8_t* top_halo,
+                               const uint8_t* bot_halo, cudaStream_t stream);
 
 }  // namespace ltl

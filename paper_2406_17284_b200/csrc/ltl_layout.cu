@@ -1,0 +1,107 @@
+// ltl_layout.cu -- conversions between the host's row-major grid and the
+// device's column-strip slab (ltl_kernels.cuh), and the packed edge rows the
+// multi-process halo exchange sends.
+//
+// The reference keeps one row-major (or fragment-contiguous) vector per grid
+// (grid.hpp:53-78) and permutes it around every run (to_fragment_layout /
+// to_row_major, src/layout.cpp:23-44).  Here the host format is untouched:
+// uploads land dense in HBM (one contiguous H2D copy) and are scattered into
+// strips on the device, downloads gather on the device and leave in one D2H
+// copy.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "ltl_kernels.cuh"
+
+namespace ltl {
+namespace {
+
+__device__ __forceinline__ int wrap(int v, int n) {
+  const int m = v % n;
+  return m < 0 ? m + n : m;
+}
+
+// dense [rows][cols] <-> interior of the slab; 16 bytes per thread when
+// cols % 16 == 0 (a 16-byte group never straddles a strip), else bytes.
+template <bool kToStrips>
+__global__ void relayout_kernel(uint8_t* dense, SlabView s) {
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  const int64_t tid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (s.cols % 16 == 0) {
+    const int64_t gpr = s.cols / 16, total = gpr * s.rows;
+    for (int64_t i = tid; i < total; i += stride) {
+      const int y = static_cast<int>(i / gpr), x = 16 * static_cast<int>(i % gpr);
+      uint4* d = reinterpret_cast<uint4*>(dense + static_cast<int64_t>(y) * s.cols + x);
+      uint4* c = reinterpret_cast<uint4*>(s.buf + s.offset(y + kHalo, x));
+      if (kToStrips) *c = *d;
+      else *d = *c;
+    }
+  } else {
+    const int64_t total = static_cast<int64_t>(s.cols) * s.rows;
+    for (int64_t i = tid; i < total; i += stride) {
+      const int y = static_cast<int>(i / s.cols), x = static_cast<int>(i % s.cols);
+      uint8_t* d = dense + i;
+      uint8_t* c = s.buf + s.offset(y + kHalo, x);
+      if (kToStrips) *c = *d;
+      else *d = *c;
+    }
+  }
+}
+
+__global__ void pack_edges_kernel(SlabView s, uint8_t* top, uint8_t* bot) {
+  const int n = kHalo * s.cols;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < 2 * n; i += gridDim.x * blockDim.x) {
+    const int which = i / n, k = i % n, r = k / s.cols, x = k % s.cols;
+    const int py = which == 0 ? kHalo + r : s.rows + r;  // interior rows [0,16) / [rows-16, rows)
+    (which == 0 ? top : bot)[k] = s.buf[s.offset(py, x)];
+  }
+}
+
+__global__ void unpack_halo_kernel(SlabView s, const uint8_t* top, const uint8_t* bot) {
+  const int w = s.cols + 2 * kHalo;
+  const int n = kHalo * w;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < 2 * n; i += gridDim.x * blockDim.x) {
+    const int which = i / n, k = i % n, r = k / w, px = k % w - kHalo;
+    const int py = which == 0 ? r : s.rows + kHalo + r;
+    s.buf[s.offset(py, px)] = (which == 0 ? top : bot)[r * s.cols + wrap(px, s.cols)];
+  }
+}
+
+int blocks_for(int64_t work) {
+  int64_t b = (work + 255) / 256;
+  if (b > 148 * 8) b = 148 * 8;
+  return b < 1 ? 1 : static_cast<int>(b);
+}
+
+}  // namespace
+
+cudaError_t launch_to_strips(const uint8_t* dense, const SlabView& s, cudaStream_t stream) {
+  if (s.rows <= 0 || s.cols <= 0) return cudaSuccess;
+  const int64_t work = static_cast<int64_t>(s.rows) * (s.cols % 16 == 0 ? s.cols / 16 : s.cols);
+  relayout_kernel<true><<<blocks_for(work), 256, 0, stream>>>(const_cast<uint8_t*>(dense), s);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_from_strips(const SlabView& s, uint8_t* dense, cudaStream_t stream) {
+  if (s.rows <= 0 || s.cols <= 0) return cudaSuccess;
+  const int64_t work = static_cast<int64_t>(s.rows) * (s.cols % 16 == 0 ? s.cols / 16 : s.cols);
+  relayout_kernel<false><<<blocks_for(work), 256, 0, stream>>>(dense, s);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_pack_edges(const SlabView& s, uint8_t* top, uint8_t* bot, cudaStream_t stream) {
+  if (s.rows <= 0 || s.cols <= 0) return cudaSuccess;
+  pack_edges_kernel<<<blocks_for(2LL * kHalo * s.cols), 256, 0, stream>>>(s, top, bot);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_unpack_halo(const SlabView& s, const uint8_t* top_halo,
+                               const uint8_t* bot_halo, cudaStream_t stream) {
+  if (s.rows <= 0 || s.cols <= 0) return cudaSuccess;
+  unpack_halo_kernel<<<blocks_for(2LL * kHalo * (s.cols + 2 * kHalo)), 256, 0, stream>>>(
+      s, top_halo, bot_halo);
+  return cudaGetLastError();
+}
+
+}  // namespace ltl

@@ -39,19 +39,19 @@ void ck(cudaError_t e, const char* what) {
 struct Slab {
   int dev = 0;
   int32_t row0 = 0, rows = 0;
-  int64_t pitch = 0;
+  int64_t strip_bytes = 0;
+  int32_t strips = 0;
   uint8_t* buf[2] = {nullptr, nullptr};
   CUtensorMap load_map[2];
   CUtensorMap store_map[2];
   ltl::DeviceStats* dstats = nullptr;
-  uint32_t* pace = nullptr;  // CTA pacing words; only when the slab has its device alone
   cudaStream_t stream = nullptr;
   bool own_stream = true;
   cudaEvent_t ev_step = nullptr;
   std::vector<cudaEvent_t> timing;
 
   ltl::SlabView view(int which, int32_t cols) const {
-    return ltl::SlabView{buf[which], rows, cols, pitch};
+    return ltl::SlabView{buf[which], rows, cols, strips, strip_bytes};
   }
 };
 
@@ -111,8 +111,6 @@ void check_run_args(const ltl_ctx* ctx, const ltl_rule_c* rule, int32_t steps) {
                                 " for fragment side f=" + std::to_string(ctx->f));
 }
 
-int64_t round_up(int64_t v, int64_t a) { return (v + a - 1) / a * a; }
-
 void build_maps(Slab& s, int32_t cols) {
   for (int i = 0; i < 2; ++i) {
     ck(ltl::make_load_map(&s.load_map[i], s.view(i, cols)), "tensor map (load)");
@@ -141,21 +139,15 @@ void create_slabs(ltl_ctx* ctx, int32_t num_slabs, const int32_t* dev_ids) {
     s.row0 = row0;
     s.rows = base + (i < extra ? 1 : 0);
     row0 += s.rows;
-    s.pitch = round_up(ctx->cols + 2 * kHalo, 128);
+    s.strips = ltl::storage_strips(ctx->cols);
+    s.strip_bytes = static_cast<int64_t>(s.rows + 2 * kHalo) * ltl::kStrip;
     ck(cudaSetDevice(s.dev), "cudaSetDevice");
-    const size_t bytes = static_cast<size_t>(s.rows + 2 * kHalo) * s.pitch;
+    const size_t bytes = static_cast<size_t>(s.strips) * s.strip_bytes;
     for (int b = 0; b < 2; ++b) {
       ck(cudaMalloc(&s.buf[b], bytes), "cudaMalloc slab");
       ck(cudaMemset(s.buf[b], 0, bytes), "cudaMemset slab");
     }
     ck(cudaMalloc(&s.dstats, sizeof(ltl::DeviceStats)), "cudaMalloc stats");
-    int sharing = 0;
-    for (int32_t j = 0; j < num_slabs; ++j)
-      sharing += (dev_ids ? dev_ids[j] : j % ndev) == s.dev ? 1 : 0;
-    if (sharing == 1) {  // concurrent kernels on one device would defeat pacing
-      ck(cudaMalloc(&s.pace, 65 * sizeof(uint32_t)), "cudaMalloc pace");
-      ck(cudaMemset(s.pace, 0, 65 * sizeof(uint32_t)), "cudaMemset pace");
-    }
     ck(cudaStreamCreateWithFlags(&s.stream, cudaStreamNonBlocking), "cudaStreamCreate");
     ck(cudaEventCreateWithFlags(&s.ev_step, cudaEventDisableTiming), "cudaEventCreate");
     build_maps(s, ctx->cols);
@@ -186,7 +178,6 @@ void destroy_ctx(ltl_ctx* ctx) {
     for (auto& b : s.buf)
       if (b) cudaFree(b);
     if (s.dstats) cudaFree(s.dstats);
-    if (s.pace) cudaFree(s.pace);
     if (s.ev_step) cudaEventDestroy(s.ev_step);
     for (cudaEvent_t e : s.timing) cudaEventDestroy(e);
     if (s.stream && s.own_stream) cudaStreamDestroy(s.stream);
@@ -240,7 +231,6 @@ void enqueue_step(ltl_ctx* ctx, const ltl::RuleConsts& rc, uint32_t flags, bool 
       a.rule = rc;
       a.inject_fault = fault;
       a.stats = want_stats ? s.dstats : nullptr;
-      a.pace = s.pace;
       // Debug: LTL_TC_TRACE=<file> dumps the pipeline timeline of CTA 0 of
       // the first traced launch (12 event kinds x 64 chunks of clock64 stamps).
       static bool traced = false;
@@ -336,27 +326,35 @@ size_t host_index(int32_t layout, int32_t f, int32_t p, int32_t y, int32_t x) {
          static_cast<size_t>(y % f) * f + (x % f);
 }
 
+// Host rows land dense in the other generation buffer (one contiguous H2D
+// copy), then the device scatters them into strips; downloads mirror that.
+// The other buffer's contents are dead at these points (the next step
+// rewrites its interior, and its pad bytes only ever meet zero band weights).
 void upload_interior(ltl_ctx* ctx, const uint8_t* interior) {
+  const int cur = ctx->cur;
   for (Slab& s : ctx->slabs) {
     ck(cudaSetDevice(s.dev), "cudaSetDevice");
     if (s.rows == 0 || ctx->cols == 0) continue;
-    ck(cudaMemcpy2DAsync(s.buf[ctx->cur] + kHalo * s.pitch + kHalo, s.pitch,
-                         interior + static_cast<size_t>(s.row0) * ctx->cols, ctx->cols,
-                         ctx->cols, s.rows, cudaMemcpyHostToDevice, s.stream),
+    const size_t n = static_cast<size_t>(s.rows) * ctx->cols;
+    ck(cudaMemcpyAsync(s.buf[1 - cur], interior + static_cast<size_t>(s.row0) * ctx->cols, n,
+                       cudaMemcpyHostToDevice, s.stream),
        "upload");
+    ck(ltl::launch_to_strips(s.buf[1 - cur], s.view(cur, ctx->cols), s.stream), "to_strips");
     if (ctx->slabs.size() > 1) ck(cudaEventRecord(s.ev_step, s.stream), "event");
   }
-  enqueue_halo(ctx, ctx->cur);
+  enqueue_halo(ctx, cur);
   sync_all(ctx);
 }
 
 void download_interior(ltl_ctx* ctx, uint8_t* interior) {
+  const int cur = ctx->cur;
   for (Slab& s : ctx->slabs) {
     ck(cudaSetDevice(s.dev), "cudaSetDevice");
     if (s.rows == 0 || ctx->cols == 0) continue;
-    ck(cudaMemcpy2DAsync(interior + static_cast<size_t>(s.row0) * ctx->cols, ctx->cols,
-                         s.buf[ctx->cur] + kHalo * s.pitch + kHalo, s.pitch, ctx->cols, s.rows,
-                         cudaMemcpyDeviceToHost, s.stream),
+    const size_t n = static_cast<size_t>(s.rows) * ctx->cols;
+    ck(ltl::launch_from_strips(s.view(cur, ctx->cols), s.buf[1 - cur], s.stream), "from_strips");
+    ck(cudaMemcpyAsync(interior + static_cast<size_t>(s.row0) * ctx->cols, s.buf[1 - cur], n,
+                       cudaMemcpyDeviceToHost, s.stream),
        "download");
   }
   sync_all(ctx);
@@ -372,7 +370,8 @@ void check_layout(int32_t layout) {
 extern "C" {
 
 const char* ltl_build_info(void) {
-  return "ltl_b200 abi=1 arch=sm_100a kernels=tcgen05-banded-i8,cuda-core-stencil,halo";
+  return "ltl_b200 abi=2 arch=sm_100a layout=column-strips-128 "
+         "kernels=tcgen05-banded-i8,cuda-core-stencil,halo,relayout";
 }
 
 int ltl_create_torus(ltl_ctx** out, int32_t rows, int32_t cols, int32_t num_slabs,
@@ -625,8 +624,8 @@ int ltl_fill_halo(ltl_ctx* ctx) {
   return guarded(ctx, [&] { enqueue_halo(ctx, ctx->cur); });
 }
 
-int ltl_slab_buffer(ltl_ctx* ctx, int32_t slab, int32_t which, void** dev_ptr, int64_t* pitch,
-                    int32_t* rows) {
+int ltl_slab_buffer(ltl_ctx* ctx, int32_t slab, int32_t which, void** dev_ptr,
+                    int64_t* strip_bytes, int32_t* rows) {
   if (!ctx) return LTL_ERR_INVALID_ARGUMENT;
   return guarded(ctx, [&] {
     if (slab < 0 || slab >= static_cast<int32_t>(ctx->slabs.size()))
@@ -634,8 +633,37 @@ int ltl_slab_buffer(ltl_ctx* ctx, int32_t slab, int32_t which, void** dev_ptr, i
     const Slab& s = ctx->slabs[slab];
     const int b = which == 0 ? ctx->cur : 1 - ctx->cur;
     if (dev_ptr) *dev_ptr = s.buf[b];
-    if (pitch) *pitch = s.pitch;
+    if (strip_bytes) *strip_bytes = s.strip_bytes;
     if (rows) *rows = s.rows;
+  });
+}
+
+int ltl_pack_edges(ltl_ctx* ctx, void* top, void* bot) {
+  if (!ctx) return LTL_ERR_INVALID_ARGUMENT;
+  return guarded(ctx, [&] {
+    if (ctx->slabs.size() != 1)
+      throw std::invalid_argument("config error: edge exchange needs a single-slab context");
+    Slab& s = ctx->slabs[0];
+    if (s.rows < kHalo)
+      throw std::invalid_argument("geometry error: slab thinner than the 16-row halo");
+    ck(cudaSetDevice(s.dev), "cudaSetDevice");
+    ck(ltl::launch_pack_edges(s.view(ctx->cur, ctx->cols), static_cast<uint8_t*>(top),
+                              static_cast<uint8_t*>(bot), s.stream),
+       "pack kernel");
+  });
+}
+
+int ltl_unpack_halo(ltl_ctx* ctx, const void* top_halo, const void* bot_halo) {
+  if (!ctx) return LTL_ERR_INVALID_ARGUMENT;
+  return guarded(ctx, [&] {
+    if (ctx->slabs.size() != 1)
+      throw std::invalid_argument("config error: edge exchange needs a single-slab context");
+    Slab& s = ctx->slabs[0];
+    ck(cudaSetDevice(s.dev), "cudaSetDevice");
+    ck(ltl::launch_unpack_halo(s.view(ctx->cur, ctx->cols),
+                               static_cast<const uint8_t*>(top_halo),
+                               static_cast<const uint8_t*>(bot_halo), s.stream),
+       "unpack kernel");
   });
 }
 

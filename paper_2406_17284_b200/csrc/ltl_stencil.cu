@@ -1,7 +1,7 @@
 // ltl_stencil.cu -- the classical CUDA-core ablation: shared-memory out-halo
 // stencil that sums the whole (2r+1)^2 box (Moore) or the 2(2r+1) cross (VN)
 // per cell, i.e. the paper's SHARED baseline, on the same
-// device slab layout as the tensor-core path.  It is also the engine the
+// device slab layout (column strips) as the tensor-core path.  It is also the engine the
 // parity tests run next to the tcgen05 kernel: same inputs, same bytes out.
 //
 // Work per cell grows as (2r+1)^2 -- that radius dependence is exactly what
@@ -22,18 +22,18 @@ constexpr int kSX = kTX + 2 * kHalo;  // 96
 constexpr int kSY = kTY + 2 * kHalo;  // 64
 
 __global__ void __launch_bounds__(kBX* kBY)
-    ltl_stencil_kernel(const uint8_t* __restrict__ in, int64_t in_pitch, uint8_t* __restrict__ out,
-                       int64_t out_pitch, int rows, int cols, RuleConsts rc, int inject_fault,
+    ltl_stencil_kernel(const SlabView in, const SlabView out, RuleConsts rc, int inject_fault,
                        DeviceStats* stats) {
   __shared__ uint8_t tile[kSY][kSX];
   const int x0 = blockIdx.x * kTX, y0 = blockIdx.y * kTY;
   const int tid = threadIdx.y * kBX + threadIdx.x;
-  const int rows_pad = rows + 2 * kHalo, cols_pad = cols + 2 * kHalo;
-  // out-halo load: padded rows [y0, y0+kSY), padded cols [x0, x0+kSX)
+  const int rows = in.rows, cols = in.cols;
+  const int rows_pad = rows + 2 * kHalo;
+  // out-halo load: padded rows [y0, y0+kSY), logical cols [x0-16, x0-16+kSX)
   for (int i = tid; i < kSY * kSX; i += kBX * kBY) {
     const int ty = i / kSX, tx = i % kSX;
-    const int py = y0 + ty, px = x0 + tx;
-    tile[ty][tx] = (py < rows_pad && px < cols_pad) ? in[py * in_pitch + px] : 0;
+    const int py = y0 + ty, px = x0 - kHalo + tx;
+    tile[ty][tx] = (py < rows_pad && px < cols + kHalo) ? in.buf[in.offset(py, px)] : 0;
   }
   __syncthreads();
   const int r = rc.r;
@@ -64,7 +64,7 @@ __global__ void __launch_bounds__(kBX* kBY)
         bad |= (st && red < rc.neg_live);
         const int32_t lo = st ? rc.lo_live : rc.lo_dead;
         const uint32_t w = static_cast<uint32_t>(st ? rc.w_live : rc.w_dead);
-        out[(y + kHalo) * out_pitch + (x + kHalo)] = (static_cast<uint32_t>(red - lo) <= w) ? 1 : 0;
+        out.buf[out.offset(y + kHalo, x)] = (static_cast<uint32_t>(red - lo) <= w) ? 1 : 0;
       }
     }
   }
@@ -87,9 +87,7 @@ cudaError_t launch_stencil_step(const SlabView& in, const SlabView& out, const R
                                 int32_t inject_fault, DeviceStats* stats, cudaStream_t stream) {
   if (in.rows <= 0 || in.cols <= 0) return cudaSuccess;
   dim3 grid((in.cols + kTX - 1) / kTX, (in.rows + kTY - 1) / kTY);
-  ltl_stencil_kernel<<<grid, dim3(kBX, kBY), 0, stream>>>(in.buf, in.pitch, out.buf, out.pitch,
-                                                          in.rows, in.cols, rule, inject_fault,
-                                                          stats);
+  ltl_stencil_kernel<<<grid, dim3(kBX, kBY), 0, stream>>>(in, out, rule, inject_fault, stats);
   return cudaGetLastError();
 }
 

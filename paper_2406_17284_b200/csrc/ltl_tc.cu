@@ -5,24 +5,33 @@
 // vertical_step_von_neumann :210-258, rule loop :293-303).  The reference
 // restates the paper's method with 16x16 int32 fragments and three band
 // fragments pi1/pi2/pi3 (src/fragment.cpp:23-41).  Here the same banded
-// products run on the 5th-generation tensor cores in their native shapes:
+// products run on the 5th-generation tensor cores in their native shapes, over
+// the strip-contiguous slab layout of ltl_kernels.cuh:
 //
-//   tile     a 128-column strip of the slab, streamed down in 64-row chunks
-//   pass 1   D1[x][y] = sum_k A1[x][k] * X[y][k]            tcgen05.mma kind::i8
-//            A1 = 128 x 160 band, resident in SMEM; X = TMA-loaded 64 x 160
-//            chunk (K-major, SWIZZLE_32B); M = 128 (x), N = 64 (y), K = 5 x 32.
-//            A1[x][k] = [|k-16-x| <= r] + 128*[k == x+16]: the extra 128 on
-//            the centre carries the cell state out in bit 7 (H <= 33 < 128).
-//   convert  epilogue: D1 (s32 in TMEM) -> two byte planes written back into
-//            TMEM as K-major A operands of pass 2 (no SMEM round trip):
-//              Moore: H = D1 & 0x7F and S = D1 & 0x80 (state * 128)
-//              VN   : H' = D1 (= H + 128*state) and s = state
-//   pass 2   D2[x][j] = sum over the 96 H rows around output chunk c
-//              Moore: H*Bv + S*(16*Iv)  = R_box   + 2048*state
-//              VN   : H'*Iv + s*Bv      = R_cross + 128*state
-//            6 MMAs (A from TMEM, band B from SMEM).  Folding the state into
-//            the accumulator makes the birth/survival rule (apply_transition,
-//            src/rule.cpp:99-111) a pure function of one 12-bit number Z.
+//   unit     (band, strip): output rows [224 b, 224 b + 224) x the 128
+//            columns of strip t.  A CTA owns a contiguous run of units in
+//            band-major order and walks its band left to right.
+//   box      one TMA load per unit: padded rows [224 b, 224 b + 256) of
+//            strip t = ONE contiguous 32 KB block (SWIZZLE_128B).  The 16 halo
+//            rows above and below come with it; the 16 halo columns on each
+//            side are the previous / next box, still resident in SMEM.
+//   pass 1   per 64-row block j of the box:
+//            D1[x][y] = sum_k A1[x][k] * X[y][k]        tcgen05.mma kind::i8
+//            M = 128 (x), N = 64 (y), K = 6 x 32 = columns [-32, 160) of the
+//            strip (box t-1 chunk 3, box t chunks 0..3, box t+1 chunk 0).
+//            A1[x][k] = [|k-32-x| <= r] + 128*[k == x+32], resident in SMEM:
+//            the row window sums (the reference's H) with the cell state in
+//            bit 7 (H <= 33 < 128).
+//   convert  D1 (s32 in TMEM) -> two byte planes written back into TMEM as
+//            K-major A operands of pass 2 (no SMEM round trip):
+//              Moore: Pb = H            Pi = 128 * state
+//              VN   : Pb = state        Pi = H + 128 * state
+//   pass 2   per 32-row output sub-block i (window = box rows [32i, 32i+64)):
+//            D2[x][j] = Pb . Bv + Pi . c*Iv        (4 MMAs, N = 32, A in TMEM)
+//              Moore: R_box + 2048*state      VN: R_cross + 128*state
+//            Folding the state into the accumulator makes the birth/survival
+//            rule (apply_transition, src/rule.cpp:99-111) a pure function of
+//            one 12-bit number Z.
 //   rule     Z is read back two cells per register (16-bit lanes); the two
 //            range tests (dead: b1..b2, live: K+s1'..K+s2') are four biased
 //            adds and two LOP3s per register (bit 15 of each lane = result).
@@ -37,10 +46,10 @@
 // One persistent CTA per SM (all 512 TMEM columns), 15 warps:
 //   warp 0        TMA producer            warp 1   pass-1 MMA issuer, TMEM owner
 //   warps 2..5    convert D1 (warp w: TMEM lane quarter w%4 = 32 strip columns)
-//   warps 6..13   rule + store D2 (quarter w%4, 32 of the 64 chunk rows each)
+//   warps 6..13   rule + store D2: two groups of four, alternate sub-blocks
 //   warp 14       pass-2 MMA issuer
 // Every stage hands over through mbarrier rings, so TMA, both MMA passes and
-// both epilogue groups overlap across chunks.
+// both epilogue groups overlap across blocks, sub-blocks and units.
 #include <cuda.h>
 #include <cuda_runtime.h>
 
@@ -55,90 +64,62 @@ namespace {
 
 using namespace ptx;
 
-constexpr int kStripCols = 128;  // M of both MMAs = output columns per strip
-constexpr int kRows = 64;        // N of both MMAs = rows per chunk
-constexpr int kKTile = 160;      // 128 + 2*16 input columns per strip
-constexpr int kKChunks = kKTile / 32;
-constexpr int kXStages = 10;  // 10 KB each: ~100 KB of loads in flight per SM
-constexpr int kA2Slots = 4;
-constexpr int kD1Slots = 2;
-constexpr int kD2Slots = 2;
+constexpr int kBand = 224;              // output rows per unit
+constexpr int kBox = kBand + 2 * kHalo;  // 256 box rows (one TMA box)
+constexpr int kBlk = 64;                // pass-1 N: H rows per block
+constexpr int kBlocks = kBox / kBlk;    // 4
+constexpr int kSub = 32;                // pass-2 N: output rows per sub-block
+constexpr int kSubs = kBand / kSub;     // 7
+constexpr int kKChunks = 6;             // pass-1 K = 192 columns [-32, 160)
+constexpr int kXStages = 5;             // 3 boxes in use + 2 prefetched
+constexpr uint32_t kBoxBytes = kBox * kStrip;  // 32 KB
+constexpr int kD1Slots = 3;
+constexpr int kA2Slots = kBlocks;  // one box of H rows per plane ring
+constexpr int kD2Slots = 4;
 constexpr int kConvWarps = 4;
 constexpr int kOutWarps = 8;
 constexpr int kThreads = 32 * (3 + kConvWarps + kOutWarps);  // 480
 constexpr int kConvThreads = 32 * kConvWarps;
-constexpr int kOutThreads = 32 * kOutWarps;
-constexpr int kWarpP2 = 2 + kConvWarps + kOutWarps;  // 14
-constexpr int kNumBands = 9;  // Bv_j, Iv_j, 16*Iv_j for the 3 K chunks of pass 2
+constexpr int kGroupThreads = 128;  // one output group
+constexpr int kWarpOut0 = 2 + kConvWarps;
+constexpr int kWarpP2 = kWarpOut0 + kOutWarps;  // 14
+constexpr int kNumTiles = 6;  // Bv0, Bv1, Iv0, Iv1, 16Iv0, 16Iv1
+
+static_assert(kBox == 256, "one TMA box (max 256 rows)");
+static_assert(kBand % kSub == 0 && kBox % kBlk == 0, "tiling");
 
 // Shared-memory carve-up (offsets from a 1024-aligned base).
-constexpr uint32_t kSmemA1 = 0;                                    // 5 x 128 x 32 B
-constexpr uint32_t kBandBytes = kRows * 32;                        // 2 KB: [64 n][32 k]
-constexpr uint32_t kSmemBand = kSmemA1 + kKChunks * 128 * 32;      // 9 x 2 KB
-constexpr uint32_t kSmemX = kSmemBand + kNumBands * kBandBytes;    // kXStages x 10 KB
-constexpr uint32_t kXChunkBytes = kRows * 32;                      // one 32-column box
-constexpr uint32_t kXStageBytes = kKChunks * kXChunkBytes;         // 10240
-constexpr uint32_t kSmemStage = kSmemX + kXStages * kXStageBytes;  // 8 warps x 2 x 1 KB
+constexpr uint32_t kSmemX = 0;                                        // 5 x 32 KB
+constexpr uint32_t kSmemA1 = kSmemX + kXStages * kBoxBytes;           // 6 x [128][32]
+constexpr uint32_t kSmemBand = kSmemA1 + kKChunks * 128 * 32;         // 6 x [32][32]
+constexpr uint32_t kTileBytes = kSub * 32;                            // 1 KB
+constexpr uint32_t kSmemStage = kSmemBand + kNumTiles * kTileBytes;   // 8 warps x 2 x 1 KB
 constexpr uint32_t kSmemBars = kSmemStage + kOutWarps * 2 * 1024;
 constexpr uint32_t kNumBars = 2 * (kXStages + kD1Slots + kA2Slots + kD2Slots);
 constexpr uint32_t kSmemTotal = kSmemBars + kNumBars * 8 + 16;
 constexpr uint32_t kSmemAlloc = kSmemTotal + 1024;  // alignment slack
 static_assert(kSmemAlloc <= 227 * 1024, "shared memory budget");
 
-// TMEM columns: the whole 512 of the SM.
+// TMEM columns (all 512 of the SM are allocated).
 constexpr uint32_t kTmemCols = 512;
-constexpr uint32_t kTmemD1 = 0;    // kD1Slots x 64
-constexpr uint32_t kTmemD2 = 128;  // kD2Slots x 64
-constexpr uint32_t kTmemA2 = 256;  // kA2Slots x 32 (plane 0 at +0, plane 1 at +16)
+constexpr uint32_t kTmemD1 = 0;                               // 3 x 64
+constexpr uint32_t kTmemPb = kTmemD1 + kD1Slots * kBlk;       // 64: 256 rows x 1 B
+constexpr uint32_t kTmemPi = kTmemPb + kBox / 4;              // 64
+constexpr uint32_t kTmemD2 = kTmemPi + kBox / 4;              // 4 x 32
+static_assert(kTmemD2 + kD2Slots * kSub <= kTmemCols, "TMEM budget");
 
-constexpr uint32_t kIdesc = idesc_i8_u8u8_s32(128, kRows);
+constexpr uint32_t kIdesc1 = idesc_i8_u8u8_s32(128, kBlk);
+constexpr uint32_t kIdesc2 = idesc_i8_u8u8_s32(128, kSub);
 
 struct Params {
   int32_t rows, cols;
-  int32_t num_strips, chunks;  // strips of 128 columns, 64-row chunks per strip
-  int32_t segs;                // row segments per strip (units = num_strips * segs)
+  int32_t strips;  // interior strips
+  int32_t bands;
   RuleConsts rule;
   int32_t inject_fault;
   DeviceStats* stats;
   long long* trace;  // debug timeline of CTA 0 (only with -DLTL_TC_TRACE_BUILD)
-  uint32_t* pace;    // 65 words of zeroed global memory, or nullptr (pacing off)
 };
-
-// Soft pacing of the CTAs' TMA producers.  Streaming strips runs near the HBM
-// copy rate only while every CTA reads the same rows at the same time (DRAM
-// page / TLB locality, tools/ubench_stream2.cu); small per-SM speed
-// differences otherwise accumulate into drift over hundreds of chunks.  Every
-// kPaceEvery H chunks a producer publishes its epoch and waits (bounded) until
-// all CTAs have reached epoch - kPaceWindow.  It is only a hint: a wait that
-// exceeds kPaceTimeout cycles disables pacing for that CTA, so co-residency is
-// never required for correctness.
-constexpr int kPaceEvery = 8;
-constexpr int kPaceWindow = 2;
-constexpr long long kPaceTimeout = 400000;  // ~200 us
-
-__device__ __forceinline__ bool pace(uint32_t* pace_buf, uint32_t g) {
-  const uint32_t epoch = g / kPaceEvery;
-  atomicAdd(pace_buf + epoch % 64, 1u);
-  if (epoch < kPaceWindow) return true;
-  const uint32_t e = epoch - kPaceWindow;
-  const uint32_t need = gridDim.x * (e / 64 + 1);
-  volatile uint32_t* slot = pace_buf + e % 64;
-  const long long t0 = clock64();
-  while (*slot < need) {
-    if (clock64() - t0 > kPaceTimeout) return false;
-    __nanosleep(256);
-  }
-  return true;
-}
-
-__device__ __forceinline__ void pace_reset(uint32_t* pace_buf) {
-  // last CTA out zeroes the slots for the next launch (stream-ordered)
-  __threadfence();
-  if (atomicAdd(pace_buf + 64, 1u) == gridDim.x - 1) {
-    for (int i = 0; i < 65; ++i) pace_buf[i] = 0;
-    __threadfence();
-  }
-}
 
 #ifdef LTL_TC_TRACE_BUILD
 #define LTL_TRACE(ev, idx) \
@@ -147,35 +128,39 @@ __device__ __forceinline__ void pace_reset(uint32_t* pace_buf) {
 #define LTL_TRACE(ev, idx) do { } while (0)
 #endif
 
-// Static schedule.  A unit is (strip, row segment); unit u is strip u % S,
-// segment u / S, and CTA b walks units b, b + G, b + 2G, ...  The host picks
-// segs and G so that every CTA gets the same work (G = S * segs, or several
-// whole strips each when S exceeds the CTA slots).  Consecutive CTAs then
-// stream neighbouring strips down the same rows at the same time, so the
-// 32 overlapping halo columns and the 256-byte L2 promotion of each strip's
-// loads are shared through L2 instead of being fetched twice from HBM.
-// Every role of the CTA iterates the same units in the same order.
-struct UnitIter {
-  int32_t u;
-  const Params& p;
-  __device__ explicit UnitIter(const Params& pp) : u(blockIdx.x), p(pp) {}
-  __device__ bool next(int& strip, int& c0, int& nc) {
-    if (u >= p.num_strips * p.segs) return false;
-    strip = u % p.num_strips;
-    const int seg = u / p.num_strips;
-    c0 = static_cast<int>(static_cast<int64_t>(p.chunks) * seg / p.segs);
-    nc = static_cast<int>(static_cast<int64_t>(p.chunks) * (seg + 1) / p.segs) - c0;
-    u += gridDim.x;
+// Static schedule: the bands * strips units in band-major order, CTA b takes
+// the contiguous run [b * U / G, (b + 1) * U / G), cut into segments at band
+// boundaries.  A segment [t0, t1) of band `band` streams boxes t0-1 .. t1
+// (its 16-column side halos included).  With U a multiple of G every CTA has
+// the same work (16384^2: 74 x 128 units = 64 per CTA on 148 SMs), and CTAs
+// working on neighbouring bands walk the same strips at the same time, so the
+// 32 rows their boxes share are mostly L2 hits.  Every role of the CTA
+// iterates the same segments in the same order.
+struct SegIter {
+  int64_t u, u_end;
+  int32_t S;
+  __device__ explicit SegIter(const Params& p) : S(p.strips) {
+    const int64_t U = static_cast<int64_t>(p.bands) * p.strips;
+    u = U * blockIdx.x / gridDim.x;
+    u_end = U * (blockIdx.x + 1) / gridDim.x;
+  }
+  __device__ bool next(int& band, int& t0, int& t1) {
+    if (u >= u_end) return false;
+    band = static_cast<int>(u / S);
+    t0 = static_cast<int>(u % S);
+    const int64_t e = min(u_end, static_cast<int64_t>(band + 1) * S);
+    t1 = t0 + static_cast<int>(e - u);
+    u = e;
     return true;
   }
 };
 
-// D2 column j holds chunk row out_row_of_col(j).  Within each 32-column half,
-// with j = [e, m, a0, a1, v] (bit 0 first) the row is [e, a0, a1, m, v]: the
-// stmatrix fragment of column group (m, v) of a 16x256b load then covers the 8
-// consecutive rows 8*(m + 2v) .. +7 of that half.
+// D2 column j holds sub-block row out_row_of_col(j).  With j = [e, m, a0, a1,
+// v] (bit 0 first) the row is [e, a0, a1, m, v]: the stmatrix fragment of
+// column group (m, v) of a 16x256b load then covers the 8 consecutive rows
+// 8*(m + 2v) .. +7.
 __host__ __device__ constexpr int out_row_of_col(int j) {
-  return (j & 32) | (j & 1) | (((j >> 2) & 3) << 1) | (((j >> 1) & 1) << 3) | (j & 16);
+  return (j & 1) | (((j >> 2) & 3) << 1) | (((j >> 1) & 1) << 3) | (j & 16);
 }
 
 __device__ __forceinline__ uint32_t pack_pairs(uint32_t p0, uint32_t p1) {
@@ -221,14 +206,15 @@ __global__ void __launch_bounds__(kThreads, 1)
   const bool vn = p.rule.kind != 0;
 
   // ---- one-time setup: resident bands (generic-proxy writes), barriers, TMEM
-  // (built a 32-bit word -- 4 consecutive k -- at a time; the swizzle moves
-  // whole 16-byte chunks, so a word stays contiguous)
-  for (uint32_t w = threadIdx.x; w < 128u * kKTile / 4; w += kThreads) {
-    const int m = static_cast<int>(w / (kKTile / 4)), k0 = 4 * static_cast<int>(w % (kKTile / 4));
+  // pass-1 A1 [128 x][192 k], SWIZZLE_32B per 32-column K chunk, built a
+  // 32-bit word (4 consecutive k) at a time; the swizzle moves whole 16-byte
+  // chunks, so a word stays contiguous
+  for (uint32_t w = threadIdx.x; w < 128u * kKChunks * 8; w += kThreads) {
+    const int m = static_cast<int>(w / (kKChunks * 8)), k0 = 4 * static_cast<int>(w % (kKChunks * 8));
     uint32_t word = 0;
 #pragma unroll
     for (int b = 0; b < 4; ++b) {
-      const int d = k0 + b - 16 - m;
+      const int d = k0 + b - 32 - m;
       uint32_t v = (d >= -r && d <= r) ? 1u : 0u;
       if (d == 0) {
         v += 128u;  // state marker
@@ -239,24 +225,24 @@ __global__ void __launch_bounds__(kThreads, 1)
     *reinterpret_cast<uint32_t*>(smem + kSmemA1 + (k0 / 32) * 4096 + sw32_offset(m, k0 % 32)) =
         word;
   }
-  // pass-2 B tiles [64 n][32 k]: tile t = kind * 3 + j, K chunk j covers rows
-  // 32j .. 32j+31 of the 96-row H window; output row rho sits at window row 16 + rho
-  for (uint32_t w = threadIdx.x; w < kNumBands * kRows * 8u; w += kThreads) {
-    const int t = static_cast<int>(w / (kRows * 8)), j = static_cast<int>((w / 8) % kRows),
+  // pass-2 B tiles [32 n][32 k]: tile t = kind * 2 + c, K chunk c covers
+  // window rows 32c .. 32c+31; output row rho sits at window row 16 + rho
+  for (uint32_t w = threadIdx.x; w < kNumTiles * kSub * 8u; w += kThreads) {
+    const int t = static_cast<int>(w / (kSub * 8)), j = static_cast<int>((w / 8) % kSub),
               k0 = 4 * static_cast<int>(w % 8);
-    const int kind = t / 3, kc = t % 3;
+    const int kind = t / 2, kc = t % 2;
     const int rho = out_row_of_col(j);
     uint32_t word = 0;
 #pragma unroll
     for (int b = 0; b < 4; ++b) {
       const int d = 32 * kc + k0 + b - 16 - rho;  // window row - centre row
       int v;
-      if (kind == 0) v = (d >= -r && d <= r);      // band
-      else if (kind == 1) v = (d == 0);            // centre
-      else v = 16 * (d == 0);                      // 16 * centre (state * 2048)
+      if (kind == 0) v = (d >= -r && d <= r);  // band
+      else if (kind == 1) v = (d == 0);        // centre
+      else v = 16 * (d == 0);                  // 16 * centre (state * 2048)
       word |= static_cast<uint32_t>(v) << (8 * b);
     }
-    *reinterpret_cast<uint32_t*>(smem + kSmemBand + t * kBandBytes + sw32_offset(j, k0)) = word;
+    *reinterpret_cast<uint32_t*>(smem + kSmemBand + t * kTileBytes + sw32_offset(j, k0)) = word;
   }
   fence_proxy_async_smem();
   if (warp == 0 && lane == 0) {
@@ -276,7 +262,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int i = 0; i < kD2Slots; ++i) {
       mbar_init(&d2_full[i], 1);
-      mbar_init(&d2_empty[i], kOutThreads);
+      mbar_init(&d2_empty[i], kGroupThreads);
     }
     fence_barrier_init();
   }
@@ -291,145 +277,173 @@ __global__ void __launch_bounds__(kThreads, 1)
   pdl_wait_prerequisites();
 
   if (warp == 0) {
-    // ================= TMA producer =================
+    // ================= TMA producer: boxes t0-1 .. t1 of every segment =======
     if (elect_one()) {
       uint32_t g = 0;
-      bool pacing = p.pace != nullptr;
-      UnitIter it(p);
-      int strip, c0, nc;
-      while (it.next(strip, c0, nc)) {
-        for (int k = 0; k <= nc; ++k, ++g) {
+      SegIter it(p);
+      int band, t0, t1;
+      while (it.next(band, t0, t1)) {
+        for (int k = 0; k < t1 - t0 + 2; ++k, ++g) {
           const uint32_t s = g % kXStages;
           mbar_wait(&x_empty[s], ((g / kXStages) & 1) ^ 1);
-          if (pacing && g % kPaceEvery == 0) pacing = pace(p.pace, g);
           LTL_TRACE(0, g);
-          uint8_t* dst = smem + kSmemX + s * kXStageBytes;
-          mbar_arrive_expect_tx(&x_full[s], kXStageBytes);
-#pragma unroll
-          for (int q = 0; q < kKChunks; ++q)
-            tma_load_2d(dst + q * kXChunkBytes, &load_map, &x_full[s],
-                        strip * kStripCols + 32 * q, (c0 + k) * kRows);
+          mbar_arrive_expect_tx(&x_full[s], kBoxBytes);
+          // logical strip t0-1+k = storage strip t0+k
+          tma_load_3d(smem + kSmemX + s * kBoxBytes, &load_map, &x_full[s], 0, band * kBand,
+                      t0 + k);
         }
       }
-      if (p.pace) pace_reset(p.pace);
     }
   } else if (warp == 1) {
     // ================= pass-1 MMA issuer =================
     const uint64_t a1_desc = smem_desc_sw32_kmajor(smem_u32(smem + kSmemA1));
-    const uint64_t x_desc = smem_desc_sw32_kmajor(smem_u32(smem + kSmemX));
-    uint32_t g = 0;
-    UnitIter it(p);
-    int strip, c0, nc;
-    while (it.next(strip, c0, nc)) {
-      for (int k = 0; k <= nc; ++k, ++g) {
-        const uint32_t s = g % kXStages, d1 = g % kD1Slots;
-        mbar_wait(&x_full[s], (g / kXStages) & 1);
-        mbar_wait(&d1_empty[d1], ((g / kD1Slots) & 1) ^ 1);
-        LTL_TRACE(1, g);
-        tc_fence_after();
-        if (elect_one()) {
-          const uint64_t xd = x_desc + ((s * kXStageBytes) >> 4);
+    const uint64_t x_desc = smem_desc_sw128_kmajor(smem_u32(smem + kSmemX));
+    auto box = [&](uint32_t idx) { return x_desc + (((idx % kXStages) * kBoxBytes) >> 4); };
+    uint32_t g = 0, h = 0;
+    SegIter it(p);
+    int band, t0, t1;
+    while (it.next(band, t0, t1)) {
+      for (int t = t0; t < t1; ++t) {
+        const uint32_t gl = g + (t - t0), go = gl + 1, gr = gl + 2;
+        mbar_wait(&x_full[gl % kXStages], (gl / kXStages) & 1);
+        mbar_wait(&x_full[go % kXStages], (go / kXStages) & 1);
+        mbar_wait(&x_full[gr % kXStages], (gr / kXStages) & 1);
+        const uint64_t bl = box(gl), bo = box(go), br = box(gr);
+        for (int j = 0; j < kBlocks; ++j, ++h) {
+          const uint32_t d1 = h % kD1Slots;
+          mbar_wait(&d1_empty[d1], ((h / kD1Slots) & 1) ^ 1);
+          LTL_TRACE(1, h);
+          tc_fence_after();
+          if (elect_one()) {
+            const uint32_t dcol = tmem + kTmemD1 + kBlk * d1;
+            const uint32_t rowoff = (j * kBlk * kStrip) >> 4;  // 8 KB per block
+            mma_i8_ss(dcol, a1_desc, bl + rowoff + (96 >> 4), kIdesc1, 0);
 #pragma unroll
-          for (int q = 0; q < kKChunks; ++q)
-            mma_i8_ss(tmem + kTmemD1 + kRows * d1, a1_desc + ((q * 4096) >> 4),
-                      xd + ((q * kXChunkBytes) >> 4), kIdesc, q > 0);
-          mma_commit(&x_empty[s]);
-          mma_commit(&d1_full[d1]);
+            for (int q = 1; q <= 4; ++q)
+              mma_i8_ss(dcol, a1_desc + ((q * 4096) >> 4), bo + rowoff + ((32 * (q - 1)) >> 4),
+                        kIdesc1, 1);
+            mma_i8_ss(dcol, a1_desc + ((5 * 4096) >> 4), br + rowoff, kIdesc1, 1);
+            mma_commit(&d1_full[d1]);
+            if (j == kBlocks - 1) {
+              mma_commit(&x_empty[gl % kXStages]);  // box t-1 is done
+              if (t == t1 - 1) {
+                mma_commit(&x_empty[go % kXStages]);
+                mma_commit(&x_empty[gr % kXStages]);
+              }
+            }
+          }
+          __syncwarp();
         }
-        __syncwarp();
       }
+      g += (t1 - t0) + 2;
     }
-  } else if (warp < 2 + kConvWarps) {
+  } else if (warp < kWarpOut0) {
     // ================= convert warps (D1 -> pass-2 A planes) =================
     const uint32_t q = warp & 3;  // TMEM lane quarter = 32 strip columns
     const uint32_t trow = tmem + ((q * 32) << 16);
-    uint32_t max_h = 0, g = 0;
-    UnitIter it(p);
-    int strip, c0, nc;
-    while (it.next(strip, c0, nc)) {
-      for (int k = 0; k <= nc; ++k, ++g) {
-        const uint32_t d1 = g % kD1Slots, s = g % kA2Slots;
-        mbar_wait(&d1_full[d1], (g / kD1Slots) & 1);
-        tc_fence_after();
-        uint32_t v[32];
-        tmem_ld_32x32b_x32_pack16(trow + kTmemD1 + kRows * d1, v);
-        tmem_ld_wait();
-        tc_fence_before();
-        mbar_arrive(&d1_empty[d1]);
-        uint32_t plane0[16], plane1[16];
+    uint32_t max_h = 0, h = 0;
+    SegIter it(p);
+    int band, t0, t1;
+    while (it.next(band, t0, t1)) {
+      for (int t = t0; t < t1; ++t) {
+        const bool x_ok = !kChecked || (t * kStrip + 32 * static_cast<int>(q) +
+                                        static_cast<int>(lane)) < p.cols;
+        for (int j = 0; j < kBlocks; ++j, ++h) {
+          const uint32_t d1 = h % kD1Slots;
+          mbar_wait(&d1_full[d1], (h / kD1Slots) & 1);
+          tc_fence_after();
+          uint32_t v[32];
+          tmem_ld_32x32b_x32_pack16(trow + kTmemD1 + kBlk * d1, v);
+          tmem_ld_wait();
+          tc_fence_before();
+          mbar_arrive(&d1_empty[d1]);
+          uint32_t pb[16], pi[16];
 #pragma unroll
-        for (int j = 0; j < 16; ++j) {
-          const uint32_t raw = pack_pairs(v[2 * j], v[2 * j + 1]);  // 4 rows of H + 128*state
-          if (vn) {
-            plane0[j] = raw;
-            plane1[j] = (raw >> 7) & 0x01010101u;
-          } else {
-            plane0[j] = raw & 0x7F7F7F7Fu;
-            plane1[j] = raw & 0x80808080u;
+          for (int i = 0; i < 16; ++i) {
+            const uint32_t raw = pack_pairs(v[2 * i], v[2 * i + 1]);  // 4 rows of H + 128*state
+            if (vn) {
+              pb[i] = (raw >> 7) & 0x01010101u;
+              pi[i] = raw;
+            } else {
+              pb[i] = raw & 0x7F7F7F7Fu;
+              pi[i] = raw & 0x80808080u;
+            }
           }
-          if constexpr (kChecked) max_h = __vmaxu4(max_h, raw & 0x7F7F7F7Fu);
+          if constexpr (kChecked) {
+            // rows of this block: padded rows band*224 + 64j + c, interior
+            // iff 16 <= padded < rows + 16 (halo rows hold images anyway)
+            const int prow0 = band * kBand + j * kBlk;
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+#pragma unroll
+              for (int hh = 0; hh < 2; ++hh) {
+                const int prow = prow0 + 2 * i + hh;
+                const uint32_t hv = (v[i] >> (16 * hh)) & 0x7Fu;
+                if (x_ok && prow >= kHalo && prow < p.rows + kHalo) max_h = max(max_h, hv);
+              }
+            }
+          }
+          const uint32_t s = h % kA2Slots;
+          mbar_wait(&a2_empty[s], ((h / kA2Slots) & 1) ^ 1);
+          tc_fence_after();
+          tmem_st_32x32b_x16(trow + kTmemPb + 16 * s, pb);
+          tmem_st_32x32b_x16(trow + kTmemPi + 16 * s, pi);
+          tmem_st_wait();
+          tc_fence_before();
+          mbar_arrive(&a2_full[s]);
         }
-        mbar_wait(&a2_empty[s], ((g / kA2Slots) & 1) ^ 1);
-        tc_fence_after();
-        tmem_st_32x32b_x16(trow + kTmemA2 + 32 * s, plane0);
-        tmem_st_32x32b_x16(trow + kTmemA2 + 32 * s + 16, plane1);
-        tmem_st_wait();
-        tc_fence_before();
-        mbar_arrive(&a2_full[s]);
       }
     }
     if constexpr (kChecked) {
-      int32_t mh = static_cast<int32_t>(max(max(max_h & 0xFF, (max_h >> 8) & 0xFF),
-                                            max((max_h >> 16) & 0xFF, max_h >> 24)));
+      int32_t mh = static_cast<int32_t>(max_h);
 #pragma unroll
       for (int off = 16; off > 0; off >>= 1) mh = max(mh, __shfl_xor_sync(0xffffffffu, mh, off));
       if (lane == 0) atomicMax(&p.stats->max_h, mh);
     }
   } else if (warp == kWarpP2) {
     // ================= pass-2 MMA issuer =================
-    // K chunk j of the 96-row window: H chunk c rows 0..31 (j=0), 32..63 (j=1),
-    // H chunk c+1 rows 0..31 (j=2) = TMEM column offsets +0, +8, next slot +0.
+    // sub-block i reads K chunks i and i+1 (box rows 32i .. 32i+63) of both
+    // planes = TMEM columns 8i, 8i+8 of each ring; chunk c was written by the
+    // convert of block c/2.
     const uint64_t band_desc = smem_desc_sw32_kmajor(smem_u32(smem + kSmemBand));
-    auto tile = [&](int t) { return band_desc + ((t * kBandBytes) >> 4); };
-    // plane 0 pairs with band (Moore) / centre (VN); plane 1 with 16*centre / band
-    const int t_p0 = vn ? 3 : 0, t_p1 = vn ? 0 : 6;
-    uint32_t g = 0, o = 0;
-    UnitIter it(p);
-    int strip, c0, nc;
-    while (it.next(strip, c0, nc)) {
-      for (int c = 0; c < nc; ++c, ++o) {
-        const uint32_t gg = g + c;
-        const uint32_t s0 = gg % kA2Slots, s1 = (gg + 1) % kA2Slots, d2 = o % kD2Slots;
-        mbar_wait(&a2_full[s0], (gg / kA2Slots) & 1);
-        mbar_wait(&a2_full[s1], ((gg + 1) / kA2Slots) & 1);
-        mbar_wait(&d2_empty[d2], ((o / kD2Slots) & 1) ^ 1);
-        LTL_TRACE(4, o);
-        tc_fence_after();
-        if (elect_one()) {
-          const uint32_t dcol = tmem + kTmemD2 + kRows * d2;
-          const uint32_t a0 = tmem + kTmemA2 + 32 * s0, a1 = tmem + kTmemA2 + 32 * s1;
-          mma_i8_ts(dcol, a0, tile(t_p0 + 0), kIdesc, 0);
-          mma_i8_ts(dcol, a0 + 8, tile(t_p0 + 1), kIdesc, 1);
-          mma_i8_ts(dcol, a1, tile(t_p0 + 2), kIdesc, 1);
-          mma_i8_ts(dcol, a0 + 16, tile(t_p1 + 0), kIdesc, 1);
-          mma_i8_ts(dcol, a0 + 24, tile(t_p1 + 1), kIdesc, 1);
-          mma_i8_ts(dcol, a1 + 16, tile(t_p1 + 2), kIdesc, 1);
-          mma_commit(&d2_full[d2]);
-          mma_commit(&a2_empty[s0]);
-          // the unit's final H chunk is only ever the second operand: free it too
-          if (c == nc - 1) mma_commit(&a2_empty[s1]);
+    auto tile = [&](int t) { return band_desc + ((t * kTileBytes) >> 4); };
+    const int ti = vn ? 2 : 4;  // Pi pairs with centre (VN) / 16 * centre (Moore)
+    uint32_t hs = 0, o = 0;
+    SegIter it(p);
+    int band, t0, t1;
+    while (it.next(band, t0, t1)) {
+      for (int t = t0; t < t1; ++t, ++hs) {
+        for (int i = 0; i < kSubs; ++i, ++o) {
+          const uint32_t ja = i / 2, jb = (i + 1) / 2, d2 = o % kD2Slots;
+          mbar_wait(&a2_full[ja], hs & 1);
+          mbar_wait(&a2_full[jb], hs & 1);
+          mbar_wait(&d2_empty[d2], ((o / kD2Slots) & 1) ^ 1);
+          LTL_TRACE(4, o);
+          tc_fence_after();
+          if (elect_one()) {
+            const uint32_t dcol = tmem + kTmemD2 + kSub * d2;
+            const uint32_t c0 = 8 * i, c1 = 8 * i + 8;
+            mma_i8_ts(dcol, tmem + kTmemPb + c0, tile(0), kIdesc2, 0);
+            mma_i8_ts(dcol, tmem + kTmemPb + c1, tile(1), kIdesc2, 1);
+            mma_i8_ts(dcol, tmem + kTmemPi + c0, tile(ti), kIdesc2, 1);
+            mma_i8_ts(dcol, tmem + kTmemPi + c1, tile(ti + 1), kIdesc2, 1);
+            mma_commit(&d2_full[d2]);
+            // block j is read by sub-blocks 2j-1, 2j, 2j+1
+            if (i & 1) mma_commit(&a2_empty[(i - 1) / 2]);
+            if (i == kSubs - 1) mma_commit(&a2_empty[kBlocks - 1]);
+          }
+          __syncwarp();
         }
-        __syncwarp();
       }
-      g += nc + 1;
     }
   } else {
     // ================= output warps (D2 -> rule -> next generation) ==========
-    // Warp w owns strip columns 32*(w%4)..+32 and chunk rows 32*half..+32 (its
-    // own staging slots and TMA stores: no CTA-wide barrier on this path).
+    // Group grp = 0 / 1 takes the even / odd sub-blocks; warp w owns strip
+    // columns 32*(w%4)..+32 of them (its own staging slots and TMA stores: no
+    // CTA-wide barrier on this path).
     const uint32_t q = warp & 3;
-    const uint32_t half = (warp - (2 + kConvWarps)) >> 2;
-    const uint32_t trow = tmem + ((q * 32) << 16) + 32 * half;
+    const uint32_t grp = (warp - kWarpOut0) >> 2;
+    const uint32_t trow = tmem + ((q * 32) << 16);
     const RuleConsts rc = p.rule;
     const uint32_t K = vn ? 128u : 2048u;
     SimdRule sr;
@@ -443,61 +457,74 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t max_r = 0, bad = 0;
     // staging: per warp 2 slots of [32 rows][32 B], SWIZZLE_32B (16-byte
     // chunk ^= (row >> 2) & 1); this thread addresses row `lane`.
-    const uint32_t wslot = warp - (2 + kConvWarps);
+    const uint32_t wslot = warp - kWarpOut0;
     uint8_t* my_stage = smem + kSmemStage + wslot * 2048;
     const uint32_t stage_u32 = smem_u32(my_stage);
     const uint32_t addr_h0 = lane * 32 + ((0u ^ ((lane >> 2) & 1)) << 4);
     const uint32_t addr_h1 = lane * 32 + ((1u ^ ((lane >> 2) & 1)) << 4);
-    uint32_t o = 0;
-    UnitIter it(p);
-    int strip, c0, nc;
-    while (it.next(strip, c0, nc)) {
-      for (int c = 0; c < nc; ++c, ++o) {
-        const uint32_t d2 = o % kD2Slots, slot = o & 1;
-        mbar_wait(&d2_full[d2], (o / kD2Slots) & 1);
-        tc_fence_after();
-        uint32_t z0[8], z1[8];
-        tmem_ld_16x256b_x2_pack16(trow + kTmemD2 + kRows * d2, z0);
-        tmem_ld_16x256b_x2_pack16(trow + (16u << 16) + kTmemD2 + kRows * d2, z1);
-        tmem_ld_wait();
-        tc_fence_before();
-        mbar_arrive(&d2_empty[d2]);
-        uint32_t w0[4], w1[4];
+    uint32_t o = 0, mine = 0;
+    SegIter it(p);
+    int band, t0, t1;
+    while (it.next(band, t0, t1)) {
+      for (int t = t0; t < t1; ++t) {
+        for (int i = 0; i < kSubs; ++i, ++o) {
+          if ((o & 1) != grp) continue;
+          const uint32_t d2 = o % kD2Slots, slot = mine & 1;
+          ++mine;
+          mbar_wait(&d2_full[d2], (o / kD2Slots) & 1);
+          tc_fence_after();
+          uint32_t z0[8], z1[8];
+          tmem_ld_16x256b_x2_pack16(trow + kTmemD2 + kSub * d2, z0);
+          tmem_ld_16x256b_x2_pack16(trow + (16u << 16) + kTmemD2 + kSub * d2, z1);
+          tmem_ld_wait();
+          tc_fence_before();
+          mbar_arrive(&d2_empty[d2]);
+          uint32_t w0[4], w1[4];
 #pragma unroll
-        for (int v = 0; v < 2; ++v) {
-          const uint32_t a0 = rule_pair(z0[4 * v + 0], sr), b0 = rule_pair(z0[4 * v + 1], sr);
-          const uint32_t a2 = rule_pair(z0[4 * v + 2], sr), b2 = rule_pair(z0[4 * v + 3], sr);
-          w0[2 * v + 0] = prmt(a0, a2, 0xFDB9) & 0x01010101u;
-          w0[2 * v + 1] = prmt(b0, b2, 0xFDB9) & 0x01010101u;
-          const uint32_t c0r = rule_pair(z1[4 * v + 0], sr), d0r = rule_pair(z1[4 * v + 1], sr);
-          const uint32_t c2r = rule_pair(z1[4 * v + 2], sr), d2r = rule_pair(z1[4 * v + 3], sr);
-          w1[2 * v + 0] = prmt(c0r, c2r, 0xFDB9) & 0x01010101u;
-          w1[2 * v + 1] = prmt(d0r, d2r, 0xFDB9) & 0x01010101u;
-        }
-        if constexpr (kChecked) {
+          for (int v = 0; v < 2; ++v) {
+            const uint32_t a0 = rule_pair(z0[4 * v + 0], sr), b0 = rule_pair(z0[4 * v + 1], sr);
+            const uint32_t a2 = rule_pair(z0[4 * v + 2], sr), b2 = rule_pair(z0[4 * v + 3], sr);
+            w0[2 * v + 0] = prmt(a0, a2, 0xFDB9) & 0x01010101u;
+            w0[2 * v + 1] = prmt(b0, b2, 0xFDB9) & 0x01010101u;
+            const uint32_t c0r = rule_pair(z1[4 * v + 0], sr), d0r = rule_pair(z1[4 * v + 1], sr);
+            const uint32_t c2r = rule_pair(z1[4 * v + 2], sr), d2r = rule_pair(z1[4 * v + 3], sr);
+            w1[2 * v + 0] = prmt(c0r, c2r, 0xFDB9) & 0x01010101u;
+            w1[2 * v + 1] = prmt(d0r, d2r, 0xFDB9) & 0x01010101u;
+          }
+          if constexpr (kChecked) {
+            // register jj of load hh: strip column 16hh + lane/4 + 8((jj>>1)&1)
+            // of this quarter, D2 columns c, c+1 with c = 4(lane%4) + 2(jj&1) + 16(jj>>2)
+            const int y0 = band * kBand + i * kSub;
 #pragma unroll
-          for (int i = 0; i < 8; ++i) {
+            for (int hh = 0; hh < 2; ++hh) {
 #pragma unroll
-            for (int h = 0; h < 2; ++h) {
-              const uint32_t z = h ? z1[i] : z0[i];
-              max_r = __vmaxu2(max_r, z & r_mask);
-              bad |= (z + g_live) & ~(z + g_neg) & 0x80008000u;  // live and count < 0
+              for (int jj = 0; jj < 8; ++jj) {
+                const int xl = 16 * hh + static_cast<int>(lane >> 2) + 8 * ((jj >> 1) & 1);
+                const int c = 4 * static_cast<int>(lane & 3) + 2 * (jj & 1) + 16 * (jj >> 2);
+                const bool xv = t * kStrip + 32 * static_cast<int>(q) + xl < p.cols;
+                const bool v0 = xv && y0 + out_row_of_col(c) < p.rows;
+                const bool v1 = xv && y0 + out_row_of_col(c + 1) < p.rows;
+                const uint32_t mask = (v0 ? 0xFFFFu : 0u) | (v1 ? 0xFFFF0000u : 0u);
+                const uint32_t z = hh ? z1[jj] : z0[jj];
+                max_r = __vmaxu2(max_r, z & r_mask & mask);
+                bad |= (z + g_live) & ~(z + g_neg) & 0x80008000u & mask;  // live and count < 0
+              }
             }
           }
-        }
-        // this warp's staging slot was last read by its TMA store of chunk o-2
-        if (lane == 0) tma_store_wait_read<1>();
-        __syncwarp();
-        const uint32_t sa = stage_u32 + slot * 1024;
-        stmatrix_x4_trans_b8(sa + addr_h0, w0[0], w0[1], w0[2], w0[3]);
-        stmatrix_x4_trans_b8(sa + addr_h1, w1[0], w1[1], w1[2], w1[3]);
-        fence_proxy_async_smem();
-        __syncwarp();
-        if (lane == 0) {
-          tma_store_2d(&store_map, my_stage + slot * 1024, strip * kStripCols + 32 * q,
-                       (c0 + c) * kRows + 32 * half);
-          tma_store_commit();
-          if (warp == 2 + kConvWarps) LTL_TRACE(11, o);
+          // this warp's staging slot was last read by its TMA store two sub-blocks ago
+          if (lane == 0) tma_store_wait_read<1>();
+          __syncwarp();
+          const uint32_t sa = stage_u32 + slot * 1024;
+          stmatrix_x4_trans_b8(sa + addr_h0, w0[0], w0[1], w0[2], w0[3]);
+          stmatrix_x4_trans_b8(sa + addr_h1, w1[0], w1[1], w1[2], w1[3]);
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            tma_store_3d(&store_map, my_stage + slot * 1024, 32 * q, band * kBand + i * kSub,
+                         t + 1);
+            tma_store_commit();
+            if (warp == kWarpOut0) LTL_TRACE(11, o);
+          }
         }
       }
     }
@@ -537,60 +564,19 @@ cudaError_t launch_tc_step(const TcLaunch& a, cudaStream_t stream) {
   Params p{};
   p.rows = a.rows;
   p.cols = a.cols;
-  p.num_strips = (a.cols + kStripCols - 1) / kStripCols;
-  p.chunks = (a.rows + kRows - 1) / kRows;
+  p.strips = interior_strips(a.cols);
+  p.bands = (a.rows + kBand - 1) / kBand;
   p.rule = a.rule;
   p.inject_fault = a.inject_fault;
   p.stats = a.stats;
   p.trace = a.trace;
-  p.pace = a.pace;
-  if (std::getenv("LTL_TC_NO_PACE")) p.pace = nullptr;
-  // Balanced units (UnitIter).  Measured on B200 (tools/ubench_stream2.cu,
-  // profiles/): streaming whole strips with every CTA on the same rows and the
-  // in-flight strips covering an aligned power-of-two span of each row runs
-  // at ~4.7-5 TB/s, while 148 concurrent strips (an unaligned 148/256 of the
-  // row) or many short segments drop to ~2.6-3.1 TB/s.  So for wide grids
-  // (S >= 64 strips) use the largest divisor G of S with G <= SMs, one whole
-  // strip per unit (CTA b streams strips b, b + G, ...).  Small grids split
-  // strips into row segments to fill the GPU.
-  const int slots = num_sms;
-  const int S = p.num_strips;
-  int64_t grid;
-  int wide_grid = 0;
-  if (S >= 64)
-    for (int g = slots; g >= 1; --g)
-      if (S % g == 0) {
-        wide_grid = g;
-        break;
-      }
-  if (wide_grid >= slots / 2) {
-    p.segs = 1;
-    grid = wide_grid;
-  } else if (S <= slots) {
-    int segs = slots / S;
-    const int max_segs = p.chunks / 2 > 1 ? p.chunks / 2 : 1;
-    if (segs > max_segs) segs = max_segs;
-    p.segs = segs;
-    grid = static_cast<int64_t>(S) * segs;
-  } else {
-    p.segs = 1;
-    const int per_cta = (S + slots - 1) / slots;
-    grid = (S + per_cta - 1) / per_cta;
-  }
+  // One persistent CTA per SM over the units (fewer for small grids).
+  const int64_t units = static_cast<int64_t>(p.bands) * p.strips;
+  int64_t grid = units < num_sms ? units : num_sms;
   if (a.grid > 0 && a.grid < grid) grid = a.grid;
-  // tuning knobs (benchmark sweeps only): LTL_TC_SEGS=<segments per strip>,
-  // LTL_TC_GRID=<CTAs>
-  if (const char* e = std::getenv("LTL_TC_SEGS")) {
+  if (const char* e = std::getenv("LTL_TC_GRID")) {  // tuning knob (sweeps only)
     const int v = std::atoi(e);
-    if (v >= 1 && v <= p.chunks) {
-      p.segs = v;
-      grid = static_cast<int64_t>(S) * v;
-      if (grid > slots) grid = slots;
-    }
-  }
-  if (const char* e = std::getenv("LTL_TC_GRID")) {
-    const int v = std::atoi(e);
-    if (v >= 1 && v <= slots) grid = v;
+    if (v >= 1 && v <= num_sms && v <= units) grid = v;
   }
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(static_cast<unsigned>(grid));

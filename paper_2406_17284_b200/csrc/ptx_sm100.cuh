@@ -116,6 +116,25 @@ __device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void*
       : "memory");
 }
 
+// 3-D forms (strip-contiguous slabs: {column in strip, padded row, strip}).
+__device__ __forceinline__ void tma_load_3d(void* smem_dst, const CUtensorMap* map, uint64_t* bar,
+                                            int32_t c0, int32_t c1, int32_t c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, const void* smem_src,
+                                             int32_t c0, int32_t c1, int32_t c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
+          reinterpret_cast<uint64_t>(map)),
+      "r"(smem_u32(smem_src)), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+
 __device__ __forceinline__ void tma_store_commit() {
   asm volatile("cp.async.bulk.commit_group;" ::: "memory");
 }
@@ -297,6 +316,20 @@ __device__ __forceinline__ uint64_t smem_desc_sw32_kmajor(uint32_t smem_addr) {
   d |= static_cast<uint64_t>(256 >> 4) << 32;   // SBO = 8 rows x 32 B
   d |= static_cast<uint64_t>(1) << 46;          // version (SM100)
   d |= static_cast<uint64_t>(6) << 61;          // SWIZZLE_32B
+  return d;
+}
+
+// K-major SWIZZLE_128B: 128-byte rows, 8-row (1 KB) swizzle atoms, SBO = 1 KB.
+// A K offset inside the 128-byte row is added to the start address (the
+// hardware applies the XOR swizzle to the final address bits, so the 1 KB
+// atom base must stay 1024-aligned; base offset 0).
+__device__ __forceinline__ uint64_t smem_desc_sw128_kmajor(uint32_t smem_addr) {
+  uint64_t d = 0;
+  d |= static_cast<uint64_t>((smem_addr >> 4) & 0x3FFF);
+  d |= static_cast<uint64_t>(1) << 16;          // LBO (unused for swizzled K-major)
+  d |= static_cast<uint64_t>(1024 >> 4) << 32;  // SBO = 8 rows x 128 B
+  d |= static_cast<uint64_t>(1) << 46;          // version (SM100)
+  d |= static_cast<uint64_t>(2) << 61;          // SWIZZLE_128B
   return d;
 }
 

@@ -5,12 +5,14 @@ One generation = the fused step kernel on every rank (ltl_step_part: main
 kernel + local column wrap), then the only exchange the stencil needs: the
 16 boundary rows of each slab go to the ring neighbours' halos
 
-    my interior rows [16, 32)        -> rank-1's bottom halo rows [R+16, R+32)
-    my interior rows [R, R+16)       -> rank+1's top halo rows    [0, 16)
+    my first 16 interior rows   -> rank-1's 16 halo rows below
+    my last 16 interior rows    -> rank+1's 16 halo rows above
 
-as full padded-width rows (their column halos already refreshed), over NCCL
-send/recv on the same stream as the kernels -- no host synchronisation.  The
-same plan drives CPU tensors over gloo in the world-size-2 tests.
+packed on the device into contiguous 16 x cols buffers (ltl_pack_edges),
+sent with NCCL send/recv on the same stream as the kernels -- no host
+synchronisation -- and unpacked into the strip layout with their column wrap
+(ltl_unpack_halo).  The same plan drives CPU tensors over gloo in the
+world-size-2 tests.
 """
 from __future__ import annotations
 
@@ -39,28 +41,29 @@ def slab_rows(global_rows: int, world: int, rank: int):
     return row0, rows
 
 
-def exchange_rows(buf, pitch: int, rows: int, plan: HaloPlan, dist_mod=None) -> None:
-    """Fill the 16 halo rows above / below a slab from its ring neighbours.
+def exchange_edges(send_top, send_bot, recv_top, recv_bot, plan: HaloPlan, dist_mod=None) -> None:
+    """The per-generation exchange of a row-slab partition.
 
-    buf: flat tensor (CUDA for NCCL, CPU for gloo) of (rows + 32) * pitch bytes
-    holding the padded slab, interior rows at [16, 16 + rows).
+    send_top: my first 16 interior rows   -> the upper neighbour's bottom halo
+    send_bot: my last 16 interior rows    -> the lower neighbour's top halo
+    recv_top: <- the upper neighbour's last 16 rows  (my 16 halo rows above)
+    recv_bot: <- the lower neighbour's first 16 rows (my 16 halo rows below)
+
+    All four are contiguous 16 x cols byte tensors (CUDA for NCCL, CPU for
+    gloo); the device packs / unpacks them from its strip layout
+    (ltl_pack_edges / ltl_unpack_halo).
     """
     if dist_mod is None:
         import torch.distributed as dist_mod  # noqa: N813
-    band = HALO * pitch
-    top_send = buf[HALO * pitch: HALO * pitch + band]
-    bot_send = buf[rows * pitch: rows * pitch + band]
-    top_recv = buf[0: band]
-    bot_recv = buf[(rows + HALO) * pitch: (rows + HALO) * pitch + band]
     if plan.world == 1:
-        top_recv.copy_(bot_send)
-        bot_recv.copy_(top_send)
+        recv_top.copy_(send_bot)
+        recv_bot.copy_(send_top)
         return
     ops = [
-        dist_mod.P2POp(dist_mod.isend, top_send, plan.up),
-        dist_mod.P2POp(dist_mod.irecv, bot_recv, plan.down),
-        dist_mod.P2POp(dist_mod.isend, bot_send, plan.down),
-        dist_mod.P2POp(dist_mod.irecv, top_recv, plan.up),
+        dist_mod.P2POp(dist_mod.isend, send_top, plan.up),
+        dist_mod.P2POp(dist_mod.irecv, recv_bot, plan.down),
+        dist_mod.P2POp(dist_mod.isend, send_bot, plan.down),
+        dist_mod.P2POp(dist_mod.irecv, recv_top, plan.up),
     ]
     # With world == 2 both neighbours are the same rank; messages between a
     # pair match in issue order, and every rank issues (top, bottom) sends and
@@ -68,24 +71,6 @@ def exchange_rows(buf, pitch: int, rows: int, plan: HaloPlan, dist_mod=None) -> 
     # halo and vice versa.
     for req in dist_mod.batch_isend_irecv(ops):
         req.wait()
-
-
-class _CudaArray:
-    """Zero-copy torch view of a device allocation owned by libltl_b200."""
-
-    def __init__(self, ptr: int, nbytes: int):
-        self.__cuda_array_interface__ = {
-            "shape": (nbytes,), "typestr": "|u1", "data": (ptr, False), "version": 3,
-            "strides": None,
-        }
-
-
-def slab_tensor(torus, which: int = 0):
-    """torch.uint8 CUDA tensor aliasing the current padded slab buffer."""
-    import torch
-    ptr, pitch, rows = torus.slab_buffer(0, which)
-    t = torch.as_tensor(_CudaArray(ptr, (rows + 2 * HALO) * pitch), device="cuda")
-    return t, pitch, rows
 
 
 class PartitionedTorus:
@@ -103,13 +88,18 @@ class PartitionedTorus:
         # kernels and the halo transport must share one stream (no host syncs)
         import torch
         self.torus.set_stream(torch.cuda.current_stream(device).cuda_stream)
+        # packed edge rows: send top / bottom, receive top / bottom halo
+        self.edges = [torch.empty(HALO * cols, dtype=torch.uint8, device=f"cuda:{device}")
+                      for _ in range(4)]
 
     def use_stream(self, stream_ptr: int) -> None:
         self.torus.set_stream(stream_ptr)
 
     def exchange(self) -> None:
-        buf, pitch, rows = slab_tensor(self.torus)
-        exchange_rows(buf, pitch, rows, self.plan)
+        send_top, send_bot, recv_top, recv_bot = self.edges
+        self.torus.pack_edges(send_top.data_ptr(), send_bot.data_ptr())
+        exchange_edges(send_top, send_bot, recv_top, recv_bot, self.plan)
+        self.torus.unpack_halo(recv_top.data_ptr(), recv_bot.data_ptr())
 
     def init_random(self, density: float, seed: int) -> None:
         self.torus.init_random(density, seed)

@@ -60,7 +60,7 @@ EXPORTS = (
     "ltl_num_slabs", "ltl_upload", "ltl_download", "ltl_upload_interior",
     "ltl_download_interior", "ltl_run", "ltl_run_async", "ltl_synchronize", "ltl_time",
     "ltl_run_interior", "ltl_create_part", "ltl_set_stream", "ltl_step_part", "ltl_fill_halo",
-    "ltl_slab_buffer", "ltl_init_random", "ltl_parse_rule", "ltl_format_rule",
+    "ltl_slab_buffer", "ltl_pack_edges", "ltl_unpack_halo", "ltl_init_random", "ltl_parse_rule", "ltl_format_rule",
     "ltl_preset_count", "ltl_preset", "ltl_von_neumann_probe_rule", "ltl_build_info",
 )
 
@@ -108,6 +108,8 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
         "ltl_init_random": ([vp, ctypes.c_double, ctypes.c_uint64, ctypes.c_int32], ctypes.c_int),
         "ltl_slab_buffer": ([vp, ctypes.c_int32, ctypes.c_int32, P(vp), P(ctypes.c_int64),
                              P(ctypes.c_int32)], ctypes.c_int),
+        "ltl_pack_edges": ([vp, vp, vp], ctypes.c_int),
+        "ltl_unpack_halo": ([vp, vp, vp], ctypes.c_int),
         "ltl_parse_rule": ([ctypes.c_char_p, P(ltl_rule_c), ctypes.c_char_p, ctypes.c_int32],
                            ctypes.c_int),
         "ltl_format_rule": ([P(ltl_rule_c), ctypes.c_char_p, ctypes.c_int32], ctypes.c_int32),
@@ -338,10 +340,22 @@ class DeviceTorus:
         self._check(self.lib.ltl_fill_halo(self._ctx))
 
     def slab_buffer(self, slab: int = 0, which: int = 0):
-        ptr, pitch, rows = ctypes.c_void_p(), ctypes.c_int64(), ctypes.c_int32()
+        """(device pointer, strip bytes, interior rows) of a generation buffer
+        (column-strip layout, include/ltl_b200.h)."""
+        ptr, strip_bytes, rows = ctypes.c_void_p(), ctypes.c_int64(), ctypes.c_int32()
         self._check(self.lib.ltl_slab_buffer(self._ctx, slab, which, ctypes.byref(ptr),
-                                             ctypes.byref(pitch), ctypes.byref(rows)))
-        return ptr.value, pitch.value, rows.value
+                                             ctypes.byref(strip_bytes), ctypes.byref(rows)))
+        return ptr.value, strip_bytes.value, rows.value
+
+    def pack_edges(self, top_ptr: int, bot_ptr: int) -> None:
+        """Enqueue: device buffers top/bot (16 x cols) <- first / last 16 interior rows."""
+        self._check(self.lib.ltl_pack_edges(self._ctx, ctypes.c_void_p(top_ptr),
+                                            ctypes.c_void_p(bot_ptr)))
+
+    def unpack_halo(self, top_ptr: int, bot_ptr: int) -> None:
+        """Enqueue: halo rows above / below <- device buffers (16 x cols each)."""
+        self._check(self.lib.ltl_unpack_halo(self._ctx, ctypes.c_void_p(top_ptr),
+                                             ctypes.c_void_p(bot_ptr)))
 
 
 ENGINES = ("cat", "stencil")

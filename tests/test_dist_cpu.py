@@ -2,7 +2,7 @@
 
 Each rank owns a row slab of one torus with 16 halo rows, advances it with
 the oracle on the padded slab, and exchanges boundary rows through
-paper_2406_17284_b200.dist.exchange_rows -- the same plan the GPU ranks run
+paper_2406_17284_b200.dist.exchange_edges -- the same plan the GPU ranks run
 over NCCL.  The assembled grid must equal the single-process oracle run.
 """
 import os
@@ -40,7 +40,7 @@ def _worker(rank, world, port, global_rows, cols, steps, rule, result_q):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     import oracle
-    from paper_2406_17284_b200.dist import HaloPlan, exchange_rows, slab_rows
+    from paper_2406_17284_b200.dist import HaloPlan, exchange_edges, slab_rows
     orc = oracle.Oracle()
     rng = np.random.default_rng(3)
     full = (rng.random((global_rows, cols)) < 0.3).astype(np.uint8)
@@ -51,11 +51,20 @@ def _worker(rank, world, port, global_rows, cols, steps, rule, result_q):
     plan = HaloPlan.ring(rank, world)
 
     def refresh():
-        # local column wrap (ltl_halo.cu for a part), then the row exchange
+        # local column wrap (ltl_halo.cu for a part), then the packed edge
+        # exchange (ltl_pack_edges -> send/recv -> ltl_unpack_halo)
         padded[HALO:HALO + rows, :HALO] = padded[HALO:HALO + rows, cols:cols + HALO]
         padded[HALO:HALO + rows, cols + HALO:] = padded[HALO:HALO + rows, HALO:2 * HALO]
-        t = torch.from_numpy(padded.reshape(-1))
-        exchange_rows(t, pitch, rows, plan, dist)
+        send_top = torch.from_numpy(padded[HALO:2 * HALO, HALO:HALO + cols].copy())
+        send_bot = torch.from_numpy(padded[rows:rows + HALO, HALO:HALO + cols].copy())
+        recv_top, recv_bot = torch.empty_like(send_top), torch.empty_like(send_bot)
+        exchange_edges(send_top, send_bot, recv_top, recv_bot, plan, dist)
+        for rows_dst, got in ((slice(0, HALO), recv_top),
+                              (slice(rows + HALO, rows + 2 * HALO), recv_bot)):
+            g = got.numpy()
+            padded[rows_dst, HALO:HALO + cols] = g
+            padded[rows_dst, :HALO] = g[:, cols - HALO:]
+            padded[rows_dst, cols + HALO:] = g[:, :HALO]
 
     refresh()
     for _ in range(steps):
