@@ -73,9 +73,10 @@ constexpr int kSubs = kBand / kSub;     // 7
 constexpr int kKChunks = 6;             // pass-1 K = 192 columns [-32, 160)
 constexpr int kXStages = 5;             // 3 boxes in use + 2 prefetched
 constexpr uint32_t kBoxBytes = kBox * kStrip;  // 32 KB
-constexpr int kD1Slots = 3;
-constexpr int kA2Slots = kBlocks;  // one box of H rows per plane ring
-constexpr int kD2Slots = 4;
+constexpr int kD1Slots = 2;
+constexpr int kA2Boxes = 2;                  // plane rings hold two boxes of H rows
+constexpr int kA2Slots = kA2Boxes * kBlocks;  // so convert runs a box ahead of pass 2
+constexpr int kD2Slots = 4;                  // two per output group: hides the MMA queue latency
 constexpr int kConvWarps = 4;
 constexpr int kOutWarps = 8;
 constexpr int kThreads = 32 * (3 + kConvWarps + kOutWarps);  // 480
@@ -102,10 +103,10 @@ static_assert(kSmemAlloc <= 227 * 1024, "shared memory budget");
 
 // TMEM columns (all 512 of the SM are allocated).
 constexpr uint32_t kTmemCols = 512;
-constexpr uint32_t kTmemD1 = 0;                               // 3 x 64
-constexpr uint32_t kTmemPb = kTmemD1 + kD1Slots * kBlk;       // 64: 256 rows x 1 B
-constexpr uint32_t kTmemPi = kTmemPb + kBox / 4;              // 64
-constexpr uint32_t kTmemD2 = kTmemPi + kBox / 4;              // 4 x 32
+constexpr uint32_t kTmemD1 = 0;                               // 2 x 64
+constexpr uint32_t kTmemPb = kTmemD1 + kD1Slots * kBlk;       // 2 boxes x 256 rows x 1 B
+constexpr uint32_t kTmemPi = kTmemPb + kA2Boxes * kBox / 4;   // 128
+constexpr uint32_t kTmemD2 = kTmemPi + kA2Boxes * kBox / 4;   // 4 x 32
 static_assert(kTmemD2 + kD2Slots * kSub <= kTmemCols, "TMEM budget");
 
 constexpr uint32_t kIdesc1 = idesc_i8_u8u8_s32(128, kBlk);
@@ -351,6 +352,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int j = 0; j < kBlocks; ++j, ++h) {
           const uint32_t d1 = h % kD1Slots;
           mbar_wait(&d1_full[d1], (h / kD1Slots) & 1);
+          if (warp == 2 && lane == 0) LTL_TRACE(2, h);
           tc_fence_after();
           uint32_t v[32];
           tmem_ld_32x32b_x32_pack16(trow + kTmemD1 + kBlk * d1, v);
@@ -385,6 +387,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           const uint32_t s = h % kA2Slots;
           mbar_wait(&a2_empty[s], ((h / kA2Slots) & 1) ^ 1);
+          if (warp == 2 && lane == 0) LTL_TRACE(3, h);
           tc_fence_after();
           tmem_st_32x32b_x16(trow + kTmemPb + 16 * s, pb);
           tmem_st_32x32b_x16(trow + kTmemPi + 16 * s, pi);
@@ -414,23 +417,25 @@ __global__ void __launch_bounds__(kThreads, 1)
     while (it.next(band, t0, t1)) {
       for (int t = t0; t < t1; ++t, ++hs) {
         for (int i = 0; i < kSubs; ++i, ++o) {
-          const uint32_t ja = i / 2, jb = (i + 1) / 2, d2 = o % kD2Slots;
-          mbar_wait(&a2_full[ja], hs & 1);
-          mbar_wait(&a2_full[jb], hs & 1);
+          const uint32_t half = hs % kA2Boxes, ph = (hs / kA2Boxes) & 1;
+          const uint32_t ja = kBlocks * half + i / 2, jb = kBlocks * half + (i + 1) / 2;
+          const uint32_t d2 = o % kD2Slots;
+          mbar_wait(&a2_full[ja], ph);
+          mbar_wait(&a2_full[jb], ph);
           mbar_wait(&d2_empty[d2], ((o / kD2Slots) & 1) ^ 1);
           LTL_TRACE(4, o);
           tc_fence_after();
           if (elect_one()) {
             const uint32_t dcol = tmem + kTmemD2 + kSub * d2;
-            const uint32_t c0 = 8 * i, c1 = 8 * i + 8;
+            const uint32_t c0 = (kBox / 4) * half + 8 * i, c1 = c0 + 8;
             mma_i8_ts(dcol, tmem + kTmemPb + c0, tile(0), kIdesc2, 0);
             mma_i8_ts(dcol, tmem + kTmemPb + c1, tile(1), kIdesc2, 1);
             mma_i8_ts(dcol, tmem + kTmemPi + c0, tile(ti), kIdesc2, 1);
             mma_i8_ts(dcol, tmem + kTmemPi + c1, tile(ti + 1), kIdesc2, 1);
             mma_commit(&d2_full[d2]);
             // block j is read by sub-blocks 2j-1, 2j, 2j+1
-            if (i & 1) mma_commit(&a2_empty[(i - 1) / 2]);
-            if (i == kSubs - 1) mma_commit(&a2_empty[kBlocks - 1]);
+            if (i & 1) mma_commit(&a2_empty[kBlocks * half + (i - 1) / 2]);
+            if (i == kSubs - 1) mma_commit(&a2_empty[kBlocks * half + kBlocks - 1]);
           }
           __syncwarp();
         }
@@ -468,15 +473,18 @@ __global__ void __launch_bounds__(kThreads, 1)
     while (it.next(band, t0, t1)) {
       for (int t = t0; t < t1; ++t) {
         for (int i = 0; i < kSubs; ++i, ++o) {
-          if ((o & 1) != grp) continue;
+          if ((o & 1) != grp) continue;  // group g owns D2 slots g, g + 2
           const uint32_t d2 = o % kD2Slots, slot = mine & 1;
           ++mine;
           mbar_wait(&d2_full[d2], (o / kD2Slots) & 1);
+          if (lane == 0 && warp == kWarpOut0) LTL_TRACE(5, mine - 1);
+          if (lane == 0 && warp == kWarpOut0 + 4) LTL_TRACE(7, mine - 1);
           tc_fence_after();
           uint32_t z0[8], z1[8];
           tmem_ld_16x256b_x2_pack16(trow + kTmemD2 + kSub * d2, z0);
           tmem_ld_16x256b_x2_pack16(trow + (16u << 16) + kTmemD2 + kSub * d2, z1);
           tmem_ld_wait();
+          if (lane == 0 && warp == kWarpOut0) LTL_TRACE(6, mine - 1);
           tc_fence_before();
           mbar_arrive(&d2_empty[d2]);
           uint32_t w0[4], w1[4];
