@@ -72,8 +72,10 @@ struct DeviceStats {
 };
 
 // ---- tcgen05 banded-MMA step (ltl_tc.cu)
+constexpr int kTcBand = 128;                  // output rows per unit
+constexpr int kTcBox = kTcBand + 2 * kHalo;   // rows per TMA box (160)
 struct TcLaunch {
-  const CUtensorMap* load_map;   // whole source slab, {128, 256, 1} boxes, SWIZZLE_128B
+  const CUtensorMap* load_map;   // whole source slab, {128, kTcBox, 1} boxes, SWIZZLE_128B
   const CUtensorMap* store_map;  // destination interior rows, {32, 32, 1} boxes, SWIZZLE_32B
   int32_t rows, cols;
   RuleConsts rule;

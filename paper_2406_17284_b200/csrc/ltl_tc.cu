@@ -6,29 +6,35 @@
 // restates the paper's method with 16x16 int32 fragments and three band
 // fragments pi1/pi2/pi3 (src/fragment.cpp:23-41).  Here the same banded
 // products run on the 5th-generation tensor cores in their native shapes, over
-// the strip-contiguous slab layout of ltl_kernels.cuh:
+// the strip-contiguous slab layout of ltl_kernels.cuh.
 //
-//   unit     (band, strip): output rows [224 b, 224 b + 224) x the 128
+// Design rule (measured, tools/ubench_mma.cu, profiles/): every tcgen05.mma
+// costs >= ~85 SM cycles whatever its N up to 128 (any kind); only N = 256
+// reaches the tensor peak.  So the step is organised to issue as FEW, as WIDE
+// MMAs as TMEM allows -- 16 per 128 x 128 output tile:
+//
+//   unit     (band, strip): output rows [128 b, 128 b + 128) x the 128
 //            columns of strip t.  A CTA owns a contiguous run of units in
 //            band-major order and walks its band left to right.
-//   box      one TMA load per unit: padded rows [224 b, 224 b + 256) of
-//            strip t = ONE contiguous 32 KB block (SWIZZLE_128B).  The 16 halo
+//   box      one TMA load per unit: padded rows [128 b, 128 b + 160) of
+//            strip t = ONE contiguous 20 KB block (SWIZZLE_128B).  The 16 halo
 //            rows above and below come with it; the 16 halo columns on each
 //            side are the previous / next box, still resident in SMEM.
-//   pass 1   per 64-row block j of the box:
-//            D1[x][y] = sum_k A1[x][k] * X[y][k]        tcgen05.mma kind::i8
-//            M = 128 (x), N = 64 (y), K = 6 x 32 = columns [-32, 160) of the
-//            strip (box t-1 chunk 3, box t chunks 0..3, box t+1 chunk 0).
-//            A1[x][k] = [|k-32-x| <= r] + 128*[k == x+32], resident in SMEM:
-//            the row window sums (the reference's H) with the cell state in
-//            bit 7 (H <= 33 < 128).
+//   pass 1   D1[x][y] = sum_k A1[x][k] * X[y][k]        6 x tcgen05.mma kind::i8
+//            M = 128 (x), N = 160 (all box rows), K = 6 x 32 = columns
+//            [-32, 160) of the strip (box t-1 chunk 3, box t chunks 0..3,
+//            box t+1 chunk 0).  A1[x][k] = [|k-32-x| <= r] + 128*[k == x+32],
+//            resident in SMEM: the row window sums (the reference's H) with
+//            the cell state in bit 7 (H <= 33 < 128).
 //   convert  D1 (s32 in TMEM) -> two byte planes written back into TMEM as
 //            K-major A operands of pass 2 (no SMEM round trip):
 //              Moore: Pb = H            Pi = 128 * state
 //              VN   : Pb = state        Pi = H + 128 * state
-//   pass 2   per 32-row output sub-block i (window = box rows [32i, 32i+64)):
-//            D2[x][j] = Pb . Bv + Pi . c*Iv        (4 MMAs, N = 32, A in TMEM)
-//              Moore: R_box + 2048*state      VN: R_cross + 128*state
+//            Pi is stored 16 rows up (row y at byte y - 16), so the centre
+//            rows of every 64-row output sub-block are two aligned K chunks.
+//   pass 2   per 64-row output sub-block s (window = box rows [64s, 64s+96)):
+//            D2[x][j] = Pb . Bv (3 chunks) + Pi . c*Iv (2 chunks), N = 64,
+//            A in TMEM:  Moore: R_box + 2048*state   VN: R_cross + 128*state
 //            Folding the state into the accumulator makes the birth/survival
 //            rule (apply_transition, src/rule.cpp:99-111) a pure function of
 //            one 12-bit number Z.
@@ -46,10 +52,10 @@
 // One persistent CTA per SM (all 512 TMEM columns), 15 warps:
 //   warp 0        TMA producer            warp 1   pass-1 MMA issuer, TMEM owner
 //   warps 2..5    convert D1 (warp w: TMEM lane quarter w%4 = 32 strip columns)
-//   warps 6..13   rule + store D2: two groups of four, alternate sub-blocks
+//   warps 6..13   rule + store D2: group g = 0 / 1 takes sub-block g of every unit
 //   warp 14       pass-2 MMA issuer
 // Every stage hands over through mbarrier rings, so TMA, both MMA passes and
-// both epilogue groups overlap across blocks, sub-blocks and units.
+// both epilogue groups overlap across sub-blocks and units.
 #include <cuda.h>
 #include <cuda_runtime.h>
 
@@ -64,19 +70,14 @@ namespace {
 
 using namespace ptx;
 
-constexpr int kBand = 224;              // output rows per unit
-constexpr int kBox = kBand + 2 * kHalo;  // 256 box rows (one TMA box)
-constexpr int kBlk = 64;                // pass-1 N: H rows per block
-constexpr int kBlocks = kBox / kBlk;    // 4
-constexpr int kSub = 32;                // pass-2 N: output rows per sub-block
-constexpr int kSubs = kBand / kSub;     // 7
-constexpr int kKChunks = 6;             // pass-1 K = 192 columns [-32, 160)
-constexpr int kXStages = 5;             // 3 boxes in use + 2 prefetched
-constexpr uint32_t kBoxBytes = kBox * kStrip;  // 32 KB
-constexpr int kD1Slots = 2;
-constexpr int kA2Boxes = 2;                  // plane rings hold two boxes of H rows
-constexpr int kA2Slots = kA2Boxes * kBlocks;  // so convert runs a box ahead of pass 2
-constexpr int kD2Slots = 4;                  // two per output group: hides the MMA queue latency
+constexpr int kBand = kTcBand;            // 128 output rows per unit
+constexpr int kBox = kTcBox;              // 160 box rows (one TMA box)
+constexpr int kSub = 64;                  // pass-2 N: output rows per sub-block
+constexpr int kSubs = kBand / kSub;       // 2
+constexpr int kKChunks = 6;               // pass-1 K = 192 columns [-32, 160)
+constexpr int kXStages = 8;               // 3 boxes in use + 5 prefetched
+constexpr uint32_t kBoxBytes = kBox * kStrip;  // 20 KB
+constexpr int kA2Boxes = 2;               // plane rings hold two units
 constexpr int kConvWarps = 4;
 constexpr int kOutWarps = 8;
 constexpr int kThreads = 32 * (3 + kConvWarps + kOutWarps);  // 480
@@ -84,32 +85,35 @@ constexpr int kConvThreads = 32 * kConvWarps;
 constexpr int kGroupThreads = 128;  // one output group
 constexpr int kWarpOut0 = 2 + kConvWarps;
 constexpr int kWarpP2 = kWarpOut0 + kOutWarps;  // 14
-constexpr int kNumTiles = 6;  // Bv0, Bv1, Iv0, Iv1, 16Iv0, 16Iv1
+constexpr int kNumTiles = 7;  // Bv0..2, Iv0..1, 16Iv0..1
 
-static_assert(kBox == 256, "one TMA box (max 256 rows)");
-static_assert(kBand % kSub == 0 && kBox % kBlk == 0, "tiling");
+static_assert(kBox % 32 == 0 && kBox <= 256, "box rows: whole K chunks, one TMA box");
+static_assert(kSubs == 2, "one output group per sub-block");
 
 // Shared-memory carve-up (offsets from a 1024-aligned base).
-constexpr uint32_t kSmemX = 0;                                        // 5 x 32 KB
+constexpr uint32_t kSmemX = 0;                                        // 8 x 20 KB
 constexpr uint32_t kSmemA1 = kSmemX + kXStages * kBoxBytes;           // 6 x [128][32]
-constexpr uint32_t kSmemBand = kSmemA1 + kKChunks * 128 * 32;         // 6 x [32][32]
-constexpr uint32_t kTileBytes = kSub * 32;                            // 1 KB
+constexpr uint32_t kSmemBand = kSmemA1 + kKChunks * 128 * 32;         // 7 x [64][32]
+constexpr uint32_t kTileBytes = kSub * 32;                            // 2 KB
 constexpr uint32_t kSmemStage = kSmemBand + kNumTiles * kTileBytes;   // 8 warps x 2 x 1 KB
 constexpr uint32_t kSmemBars = kSmemStage + kOutWarps * 2 * 1024;
-constexpr uint32_t kNumBars = 2 * (kXStages + kD1Slots + kA2Slots + kD2Slots);
+constexpr uint32_t kNumBars = 2 * (kXStages + 1 + kA2Boxes + kSubs);
 constexpr uint32_t kSmemTotal = kSmemBars + kNumBars * 8 + 16;
 constexpr uint32_t kSmemAlloc = kSmemTotal + 1024;  // alignment slack
 static_assert(kSmemAlloc <= 227 * 1024, "shared memory budget");
 
 // TMEM columns (all 512 of the SM are allocated).
 constexpr uint32_t kTmemCols = 512;
-constexpr uint32_t kTmemD1 = 0;                               // 2 x 64
-constexpr uint32_t kTmemPb = kTmemD1 + kD1Slots * kBlk;       // 2 boxes x 256 rows x 1 B
-constexpr uint32_t kTmemPi = kTmemPb + kA2Boxes * kBox / 4;   // 128
-constexpr uint32_t kTmemD2 = kTmemPi + kA2Boxes * kBox / 4;   // 4 x 32
-static_assert(kTmemD2 + kD2Slots * kSub <= kTmemCols, "TMEM budget");
+constexpr uint32_t kPbCols = kBox / 4;          // 40: one byte per box row
+constexpr uint32_t kPiCols = kBand / 4;         // 32: one byte per centre row
+constexpr uint32_t kTmemD1 = 0;                 // 160
+constexpr uint32_t kTmemPb = kTmemD1 + kBox;    // 2 x 40
+constexpr uint32_t kTmemPi = kTmemPb + kA2Boxes * kPbCols;  // 2 x 32
+constexpr uint32_t kTmemD2 = kTmemPi + kA2Boxes * kPiCols;  // 2 x 64
+static_assert(kTmemD2 + kSubs * kSub <= kTmemCols, "TMEM budget");
+static_assert(kTmemPb % 8 == 0 && kTmemPi % 8 == 0 && kTmemD2 % 8 == 0, "A operand alignment");
 
-constexpr uint32_t kIdesc1 = idesc_i8_u8u8_s32(128, kBlk);
+constexpr uint32_t kIdesc1 = idesc_i8_u8u8_s32(128, kBox);
 constexpr uint32_t kIdesc2 = idesc_i8_u8u8_s32(128, kSub);
 
 struct Params {
@@ -132,11 +136,10 @@ struct Params {
 // Static schedule: the bands * strips units in band-major order, CTA b takes
 // the contiguous run [b * U / G, (b + 1) * U / G), cut into segments at band
 // boundaries.  A segment [t0, t1) of band `band` streams boxes t0-1 .. t1
-// (its 16-column side halos included).  With U a multiple of G every CTA has
-// the same work (16384^2: 74 x 128 units = 64 per CTA on 148 SMs), and CTAs
-// working on neighbouring bands walk the same strips at the same time, so the
-// 32 rows their boxes share are mostly L2 hits.  Every role of the CTA
-// iterates the same segments in the same order.
+// (its 16-column side halos included).  CTAs on neighbouring bands walk the
+// same strips at about the same time, so the 32 rows their boxes share are
+// mostly L2 hits.  Every role of the CTA iterates the same segments in the
+// same order.
 struct SegIter {
   int64_t u, u_end;
   int32_t S;
@@ -156,12 +159,12 @@ struct SegIter {
   }
 };
 
-// D2 column j holds sub-block row out_row_of_col(j).  With j = [e, m, a0, a1,
-// v] (bit 0 first) the row is [e, a0, a1, m, v]: the stmatrix fragment of
-// column group (m, v) of a 16x256b load then covers the 8 consecutive rows
-// 8*(m + 2v) .. +7.
+// D2 column j holds sub-block row out_row_of_col(j).  Within each 32-column
+// half, with j = [e, m, a0, a1, v] (bit 0 first) the row is [e, a0, a1, m, v]:
+// the stmatrix fragment of column group (m, v) of a 16x256b load then covers
+// the 8 consecutive rows 8*(m + 2v) .. +7 of that half.
 __host__ __device__ constexpr int out_row_of_col(int j) {
-  return (j & 1) | (((j >> 2) & 3) << 1) | (((j >> 1) & 1) << 3) | (j & 16);
+  return (j & 32) | (j & 1) | (((j >> 2) & 3) << 1) | (((j >> 1) & 1) << 3) | (j & 16);
 }
 
 __device__ __forceinline__ uint32_t pack_pairs(uint32_t p0, uint32_t p1) {
@@ -194,12 +197,12 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* x_full = bars;
   uint64_t* x_empty = x_full + kXStages;
   uint64_t* d1_full = x_empty + kXStages;
-  uint64_t* d1_empty = d1_full + kD1Slots;
-  uint64_t* a2_full = d1_empty + kD1Slots;
-  uint64_t* a2_empty = a2_full + kA2Slots;
-  uint64_t* d2_full = a2_empty + kA2Slots;
-  uint64_t* d2_empty = d2_full + kD2Slots;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(d2_empty + kD2Slots);
+  uint64_t* d1_empty = d1_full + 1;
+  uint64_t* a2_full = d1_empty + 1;
+  uint64_t* a2_empty = a2_full + kA2Boxes;
+  uint64_t* d2_full = a2_empty + kA2Boxes;
+  uint64_t* d2_empty = d2_full + kSubs;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(d2_empty + kSubs);
 
   const uint32_t warp = warp_id();
   const uint32_t lane = threadIdx.x & 31;
@@ -226,21 +229,25 @@ __global__ void __launch_bounds__(kThreads, 1)
     *reinterpret_cast<uint32_t*>(smem + kSmemA1 + (k0 / 32) * 4096 + sw32_offset(m, k0 % 32)) =
         word;
   }
-  // pass-2 B tiles [32 n][32 k]: tile t = kind * 2 + c, K chunk c covers
-  // window rows 32c .. 32c+31; output row rho sits at window row 16 + rho
+  // pass-2 B tiles [64 n][32 k]: n = D2 column j (output row rho = out_row_of_col(j)),
+  //   t = 0..2  band, K chunk c = window rows 32c .. 32c+31 (centre at 16 + rho)
+  //   t = 3..4  centre, K chunk c of the shifted plane (centre at rho)
+  //   t = 5..6  16 * centre (state * 2048 for Moore)
   for (uint32_t w = threadIdx.x; w < kNumTiles * kSub * 8u; w += kThreads) {
     const int t = static_cast<int>(w / (kSub * 8)), j = static_cast<int>((w / 8) % kSub),
               k0 = 4 * static_cast<int>(w % 8);
-    const int kind = t / 2, kc = t % 2;
     const int rho = out_row_of_col(j);
     uint32_t word = 0;
 #pragma unroll
     for (int b = 0; b < 4; ++b) {
-      const int d = 32 * kc + k0 + b - 16 - rho;  // window row - centre row
       int v;
-      if (kind == 0) v = (d >= -r && d <= r);  // band
-      else if (kind == 1) v = (d == 0);        // centre
-      else v = 16 * (d == 0);                  // 16 * centre (state * 2048)
+      if (t < 3) {
+        const int d = 32 * t + k0 + b - 16 - rho;
+        v = (d >= -r && d <= r);
+      } else {
+        const int c = (t - 3) % 2;
+        v = (32 * c + k0 + b == rho) ? (t >= 5 ? 16 : 1) : 0;
+      }
       word |= static_cast<uint32_t>(v) << (8 * b);
     }
     *reinterpret_cast<uint32_t*>(smem + kSmemBand + t * kTileBytes + sw32_offset(j, k0)) = word;
@@ -253,15 +260,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&x_full[i], 1);
       mbar_init(&x_empty[i], 1);
     }
-    for (int i = 0; i < kD1Slots; ++i) {
-      mbar_init(&d1_full[i], 1);
-      mbar_init(&d1_empty[i], kConvThreads);
-    }
-    for (int i = 0; i < kA2Slots; ++i) {
+    mbar_init(d1_full, 1);
+    mbar_init(d1_empty, kConvThreads);
+    for (int i = 0; i < kA2Boxes; ++i) {
       mbar_init(&a2_full[i], kConvThreads);
       mbar_init(&a2_empty[i], 1);
     }
-    for (int i = 0; i < kD2Slots; ++i) {
+    for (int i = 0; i < kSubs; ++i) {
       mbar_init(&d2_full[i], 1);
       mbar_init(&d2_empty[i], kGroupThreads);
     }
@@ -296,7 +301,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else if (warp == 1) {
-    // ================= pass-1 MMA issuer =================
+    // ================= pass-1 MMA issuer: one N = 160 block per unit =========
     const uint64_t a1_desc = smem_desc_sw32_kmajor(smem_u32(smem + kSmemA1));
     const uint64_t x_desc = smem_desc_sw128_kmajor(smem_u32(smem + kSmemX));
     auto box = [&](uint32_t idx) { return x_desc + (((idx % kXStages) * kBoxBytes) >> 4); };
@@ -304,37 +309,30 @@ __global__ void __launch_bounds__(kThreads, 1)
     SegIter it(p);
     int band, t0, t1;
     while (it.next(band, t0, t1)) {
-      for (int t = t0; t < t1; ++t) {
+      for (int t = t0; t < t1; ++t, ++h) {
         const uint32_t gl = g + (t - t0), go = gl + 1, gr = gl + 2;
         mbar_wait(&x_full[gl % kXStages], (gl / kXStages) & 1);
         mbar_wait(&x_full[go % kXStages], (go / kXStages) & 1);
         mbar_wait(&x_full[gr % kXStages], (gr / kXStages) & 1);
-        const uint64_t bl = box(gl), bo = box(go), br = box(gr);
-        for (int j = 0; j < kBlocks; ++j, ++h) {
-          const uint32_t d1 = h % kD1Slots;
-          mbar_wait(&d1_empty[d1], ((h / kD1Slots) & 1) ^ 1);
-          LTL_TRACE(1, h);
-          tc_fence_after();
-          if (elect_one()) {
-            const uint32_t dcol = tmem + kTmemD1 + kBlk * d1;
-            const uint32_t rowoff = (j * kBlk * kStrip) >> 4;  // 8 KB per block
-            mma_i8_ss(dcol, a1_desc, bl + rowoff + (96 >> 4), kIdesc1, 0);
+        mbar_wait(d1_empty, (h & 1) ^ 1);
+        LTL_TRACE(1, h);
+        tc_fence_after();
+        if (elect_one()) {
+          const uint32_t dcol = tmem + kTmemD1;
+          mma_i8_ss(dcol, a1_desc, box(gl) + (96 >> 4), kIdesc1, 0);
 #pragma unroll
-            for (int q = 1; q <= 4; ++q)
-              mma_i8_ss(dcol, a1_desc + ((q * 4096) >> 4), bo + rowoff + ((32 * (q - 1)) >> 4),
-                        kIdesc1, 1);
-            mma_i8_ss(dcol, a1_desc + ((5 * 4096) >> 4), br + rowoff, kIdesc1, 1);
-            mma_commit(&d1_full[d1]);
-            if (j == kBlocks - 1) {
-              mma_commit(&x_empty[gl % kXStages]);  // box t-1 is done
-              if (t == t1 - 1) {
-                mma_commit(&x_empty[go % kXStages]);
-                mma_commit(&x_empty[gr % kXStages]);
-              }
-            }
+          for (int q = 1; q <= 4; ++q)
+            mma_i8_ss(dcol, a1_desc + ((q * 4096) >> 4), box(go) + ((32 * (q - 1)) >> 4), kIdesc1,
+                      1);
+          mma_i8_ss(dcol, a1_desc + ((5 * 4096) >> 4), box(gr), kIdesc1, 1);
+          mma_commit(d1_full);
+          mma_commit(&x_empty[gl % kXStages]);  // box t-1 is done
+          if (t == t1 - 1) {
+            mma_commit(&x_empty[go % kXStages]);
+            mma_commit(&x_empty[gr % kXStages]);
           }
-          __syncwarp();
         }
+        __syncwarp();
       }
       g += (t1 - t0) + 2;
     }
@@ -346,55 +344,62 @@ __global__ void __launch_bounds__(kThreads, 1)
     SegIter it(p);
     int band, t0, t1;
     while (it.next(band, t0, t1)) {
-      for (int t = t0; t < t1; ++t) {
-        const bool x_ok = !kChecked || (t * kStrip + 32 * static_cast<int>(q) +
-                                        static_cast<int>(lane)) < p.cols;
-        for (int j = 0; j < kBlocks; ++j, ++h) {
-          const uint32_t d1 = h % kD1Slots;
-          mbar_wait(&d1_full[d1], (h / kD1Slots) & 1);
-          if (warp == 2 && lane == 0) LTL_TRACE(2, h);
-          tc_fence_after();
-          uint32_t v[32];
-          tmem_ld_32x32b_x32_pack16(trow + kTmemD1 + kBlk * d1, v);
-          tmem_ld_wait();
-          tc_fence_before();
-          mbar_arrive(&d1_empty[d1]);
-          uint32_t pb[16], pi[16];
+      for (int t = t0; t < t1; ++t, ++h) {
+        mbar_wait(d1_full, h & 1);
+        if (warp == 2 && lane == 0) LTL_TRACE(2, h);
+        tc_fence_after();
+        // all 160 box rows, two rows (16-bit lanes) per register
+        uint32_t va[32], vb[32], vc[16];
+        tmem_ld_32x32b_x32_pack16(trow + kTmemD1, va);
+        tmem_ld_32x32b_x32_pack16(trow + kTmemD1 + 64, vb);
+        tmem_ld_32x32b_x16_pack16(trow + kTmemD1 + 128, vc);
+        tmem_ld_wait();
+        tc_fence_before();
+        mbar_arrive(d1_empty);
+        auto raw_word = [&](int i) -> uint32_t {  // box rows 4i .. 4i+3 as bytes
+          const int k = 2 * i;
+          const uint32_t lo = k < 32 ? va[k] : k < 64 ? vb[k - 32] : vc[k - 64];
+          const uint32_t hi = k + 1 < 32 ? va[k + 1] : k + 1 < 64 ? vb[k + 1 - 32] : vc[k + 1 - 64];
+          return pack_pairs(lo, hi);
+        };
+        if constexpr (kChecked) {
+          const bool x_ok = t * kStrip + 32 * static_cast<int>(q) + static_cast<int>(lane) < p.cols;
+          const int prow0 = band * kBand;  // padded row of box row 0
 #pragma unroll
-          for (int i = 0; i < 16; ++i) {
-            const uint32_t raw = pack_pairs(v[2 * i], v[2 * i + 1]);  // 4 rows of H + 128*state
-            if (vn) {
-              pb[i] = (raw >> 7) & 0x01010101u;
-              pi[i] = raw;
-            } else {
-              pb[i] = raw & 0x7F7F7F7Fu;
-              pi[i] = raw & 0x80808080u;
+          for (int i = 0; i < kBox / 2; ++i) {
+            const uint32_t pr = i < 32 ? va[i] : i < 64 ? vb[i - 32] : vc[i - 64];
+#pragma unroll
+            for (int hh = 0; hh < 2; ++hh) {
+              const int prow = prow0 + 2 * i + hh;
+              const uint32_t hv = (pr >> (16 * hh)) & 0x7Fu;
+              if (x_ok && prow >= kHalo && prow < p.rows + kHalo) max_h = max(max_h, hv);
             }
           }
-          if constexpr (kChecked) {
-            // rows of this block: padded rows band*224 + 64j + c, interior
-            // iff 16 <= padded < rows + 16 (halo rows hold images anyway)
-            const int prow0 = band * kBand + j * kBlk;
-#pragma unroll
-            for (int i = 0; i < 32; ++i) {
-#pragma unroll
-              for (int hh = 0; hh < 2; ++hh) {
-                const int prow = prow0 + 2 * i + hh;
-                const uint32_t hv = (v[i] >> (16 * hh)) & 0x7Fu;
-                if (x_ok && prow >= kHalo && prow < p.rows + kHalo) max_h = max(max_h, hv);
-              }
-            }
-          }
-          const uint32_t s = h % kA2Slots;
-          mbar_wait(&a2_empty[s], ((h / kA2Slots) & 1) ^ 1);
-          if (warp == 2 && lane == 0) LTL_TRACE(3, h);
-          tc_fence_after();
-          tmem_st_32x32b_x16(trow + kTmemPb + 16 * s, pb);
-          tmem_st_32x32b_x16(trow + kTmemPi + 16 * s, pi);
-          tmem_st_wait();
-          tc_fence_before();
-          mbar_arrive(&a2_full[s]);
         }
+        const uint32_t hb = h % kA2Boxes;
+        mbar_wait(&a2_empty[hb], ((h / kA2Boxes) & 1) ^ 1);
+        if (warp == 2 && lane == 0) LTL_TRACE(3, h);
+        tc_fence_after();
+        const uint32_t pb_col = trow + kTmemPb + kPbCols * hb;
+        const uint32_t pi_col = trow + kTmemPi + kPiCols * hb;
+#pragma unroll
+        for (int c = 0; c < kBox / 32; ++c) {  // 32-row chunk c = words 8c .. 8c+7
+          uint32_t pb[8], pi[8];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const uint32_t raw = raw_word(8 * c + i);
+            pb[i] = vn ? (raw >> 7) & 0x01010101u : raw & 0x7F7F7F7Fu;
+            pi[i] = vn ? raw : raw & 0x80808080u;
+          }
+          tmem_st_32x32b_x8(pb_col + 8 * c, pb);
+          // Pi holds row y at byte y - 16: words 0..3 of chunk c -> Pi words
+          // 8c-4 .. 8c-1, words 4..7 -> 8c .. 8c+3 (rows 0..15, 144..159 unused)
+          if (c > 0) tmem_st_32x32b_x4(pi_col + 8 * c - 4, pi[0], pi[1], pi[2], pi[3]);
+          if (c < kBox / 32 - 1) tmem_st_32x32b_x4(pi_col + 8 * c, pi[4], pi[5], pi[6], pi[7]);
+        }
+        tmem_st_wait();
+        tc_fence_before();
+        mbar_arrive(&a2_full[hb]);
       }
     }
     if constexpr (kChecked) {
@@ -405,37 +410,33 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else if (warp == kWarpP2) {
     // ================= pass-2 MMA issuer =================
-    // sub-block i reads K chunks i and i+1 (box rows 32i .. 32i+63) of both
-    // planes = TMEM columns 8i, 8i+8 of each ring; chunk c was written by the
-    // convert of block c/2.
+    // sub-block s: band over Pb chunks 2s .. 2s+2 (box rows 64s .. 64s+95),
+    // centre over Pi chunks 2s, 2s+1 (centre rows 64s .. 64s+63, shifted)
     const uint64_t band_desc = smem_desc_sw32_kmajor(smem_u32(smem + kSmemBand));
     auto tile = [&](int t) { return band_desc + ((t * kTileBytes) >> 4); };
-    const int ti = vn ? 2 : 4;  // Pi pairs with centre (VN) / 16 * centre (Moore)
-    uint32_t hs = 0, o = 0;
+    const int ti = vn ? 3 : 5;
+    uint32_t h = 0;
     SegIter it(p);
     int band, t0, t1;
     while (it.next(band, t0, t1)) {
-      for (int t = t0; t < t1; ++t, ++hs) {
-        for (int i = 0; i < kSubs; ++i, ++o) {
-          const uint32_t half = hs % kA2Boxes, ph = (hs / kA2Boxes) & 1;
-          const uint32_t ja = kBlocks * half + i / 2, jb = kBlocks * half + (i + 1) / 2;
-          const uint32_t d2 = o % kD2Slots;
-          mbar_wait(&a2_full[ja], ph);
-          mbar_wait(&a2_full[jb], ph);
-          mbar_wait(&d2_empty[d2], ((o / kD2Slots) & 1) ^ 1);
-          LTL_TRACE(4, o);
+      for (int t = t0; t < t1; ++t, ++h) {
+        const uint32_t hb = h % kA2Boxes;
+        mbar_wait(&a2_full[hb], (h / kA2Boxes) & 1);
+        for (int s = 0; s < kSubs; ++s) {
+          mbar_wait(&d2_empty[s], (h & 1) ^ 1);
+          LTL_TRACE(4, 2 * h + s);
           tc_fence_after();
           if (elect_one()) {
-            const uint32_t dcol = tmem + kTmemD2 + kSub * d2;
-            const uint32_t c0 = (kBox / 4) * half + 8 * i, c1 = c0 + 8;
-            mma_i8_ts(dcol, tmem + kTmemPb + c0, tile(0), kIdesc2, 0);
-            mma_i8_ts(dcol, tmem + kTmemPb + c1, tile(1), kIdesc2, 1);
-            mma_i8_ts(dcol, tmem + kTmemPi + c0, tile(ti), kIdesc2, 1);
-            mma_i8_ts(dcol, tmem + kTmemPi + c1, tile(ti + 1), kIdesc2, 1);
-            mma_commit(&d2_full[d2]);
-            // block j is read by sub-blocks 2j-1, 2j, 2j+1
-            if (i & 1) mma_commit(&a2_empty[kBlocks * half + (i - 1) / 2]);
-            if (i == kSubs - 1) mma_commit(&a2_empty[kBlocks * half + kBlocks - 1]);
+            const uint32_t dcol = tmem + kTmemD2 + kSub * s;
+            const uint32_t pb = tmem + kTmemPb + kPbCols * hb + 16 * s;
+            const uint32_t pi = tmem + kTmemPi + kPiCols * hb + 16 * s;
+            mma_i8_ts(dcol, pb, tile(0), kIdesc2, 0);
+            mma_i8_ts(dcol, pb + 8, tile(1), kIdesc2, 1);
+            mma_i8_ts(dcol, pb + 16, tile(2), kIdesc2, 1);
+            mma_i8_ts(dcol, pi, tile(ti), kIdesc2, 1);
+            mma_i8_ts(dcol, pi + 8, tile(ti + 1), kIdesc2, 1);
+            mma_commit(&d2_full[s]);
+            if (s == kSubs - 1) mma_commit(&a2_empty[hb]);
           }
           __syncwarp();
         }
@@ -443,12 +444,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else {
     // ================= output warps (D2 -> rule -> next generation) ==========
-    // Group grp = 0 / 1 takes the even / odd sub-blocks; warp w owns strip
-    // columns 32*(w%4)..+32 of them (its own staging slots and TMA stores: no
-    // CTA-wide barrier on this path).
+    // Group grp takes sub-block grp (64 rows) of every unit; warp w owns strip
+    // columns 32*(w%4)..+32 of it as two 32 x 32 tiles (its own staging slots
+    // and TMA stores: no CTA-wide barrier on this path).
     const uint32_t q = warp & 3;
     const uint32_t grp = (warp - kWarpOut0) >> 2;
-    const uint32_t trow = tmem + ((q * 32) << 16);
+    const uint32_t trow = tmem + ((q * 32) << 16) + kTmemD2 + kSub * grp;
     const RuleConsts rc = p.rule;
     const uint32_t K = vn ? 128u : 2048u;
     SimdRule sr;
@@ -467,29 +468,32 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t stage_u32 = smem_u32(my_stage);
     const uint32_t addr_h0 = lane * 32 + ((0u ^ ((lane >> 2) & 1)) << 4);
     const uint32_t addr_h1 = lane * 32 + ((1u ^ ((lane >> 2) & 1)) << 4);
-    uint32_t o = 0, mine = 0;
+    uint32_t h = 0;
     SegIter it(p);
     int band, t0, t1;
     while (it.next(band, t0, t1)) {
-      for (int t = t0; t < t1; ++t) {
-        for (int i = 0; i < kSubs; ++i, ++o) {
-          if ((o & 1) != grp) continue;  // group g owns D2 slots g, g + 2
-          const uint32_t d2 = o % kD2Slots, slot = mine & 1;
-          ++mine;
-          mbar_wait(&d2_full[d2], (o / kD2Slots) & 1);
-          if (lane == 0 && warp == kWarpOut0) LTL_TRACE(5, mine - 1);
-          if (lane == 0 && warp == kWarpOut0 + 4) LTL_TRACE(7, mine - 1);
-          tc_fence_after();
-          uint32_t z0[8], z1[8];
-          tmem_ld_16x256b_x2_pack16(trow + kTmemD2 + kSub * d2, z0);
-          tmem_ld_16x256b_x2_pack16(trow + (16u << 16) + kTmemD2 + kSub * d2, z1);
-          tmem_ld_wait();
-          if (lane == 0 && warp == kWarpOut0) LTL_TRACE(6, mine - 1);
-          tc_fence_before();
-          mbar_arrive(&d2_empty[d2]);
+      for (int t = t0; t < t1; ++t, ++h) {
+        mbar_wait(&d2_full[grp], h & 1);
+        if (lane == 0 && warp == kWarpOut0) LTL_TRACE(5, h);
+        if (lane == 0 && warp == kWarpOut0 + 4) LTL_TRACE(7, h);
+        tc_fence_after();
+        uint32_t z[2][2][8];  // [tile (rows 32*tt ..)][lane half][register]
+#pragma unroll
+        for (int tt = 0; tt < 2; ++tt) {
+          tmem_ld_16x256b_x2_pack16(trow + 32 * tt, z[tt][0]);
+          tmem_ld_16x256b_x2_pack16(trow + (16u << 16) + 32 * tt, z[tt][1]);
+        }
+        tmem_ld_wait();
+        tc_fence_before();
+        mbar_arrive(&d2_empty[grp]);
+        if (lane == 0 && warp == kWarpOut0) LTL_TRACE(6, h);
+#pragma unroll
+        for (int tt = 0; tt < 2; ++tt) {
           uint32_t w0[4], w1[4];
 #pragma unroll
           for (int v = 0; v < 2; ++v) {
+            const uint32_t* z0 = z[tt][0];
+            const uint32_t* z1 = z[tt][1];
             const uint32_t a0 = rule_pair(z0[4 * v + 0], sr), b0 = rule_pair(z0[4 * v + 1], sr);
             const uint32_t a2 = rule_pair(z0[4 * v + 2], sr), b2 = rule_pair(z0[4 * v + 3], sr);
             w0[2 * v + 0] = prmt(a0, a2, 0xFDB9) & 0x01010101u;
@@ -499,10 +503,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             w1[2 * v + 0] = prmt(c0r, c2r, 0xFDB9) & 0x01010101u;
             w1[2 * v + 1] = prmt(d0r, d2r, 0xFDB9) & 0x01010101u;
           }
+          const int y0 = band * kBand + kSub * static_cast<int>(grp) + 32 * tt;
           if constexpr (kChecked) {
-            // register jj of load hh: strip column 16hh + lane/4 + 8((jj>>1)&1)
+            // register jj of lane half hh: strip column 16hh + lane/4 + 8((jj>>1)&1)
             // of this quarter, D2 columns c, c+1 with c = 4(lane%4) + 2(jj&1) + 16(jj>>2)
-            const int y0 = band * kBand + i * kSub;
 #pragma unroll
             for (int hh = 0; hh < 2; ++hh) {
 #pragma unroll
@@ -513,27 +517,26 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const bool v0 = xv && y0 + out_row_of_col(c) < p.rows;
                 const bool v1 = xv && y0 + out_row_of_col(c + 1) < p.rows;
                 const uint32_t mask = (v0 ? 0xFFFFu : 0u) | (v1 ? 0xFFFF0000u : 0u);
-                const uint32_t z = hh ? z1[jj] : z0[jj];
-                max_r = __vmaxu2(max_r, z & r_mask & mask);
-                bad |= (z + g_live) & ~(z + g_neg) & 0x80008000u & mask;  // live and count < 0
+                const uint32_t zz = z[tt][hh][jj];
+                max_r = __vmaxu2(max_r, zz & r_mask & mask);
+                bad |= (zz + g_live) & ~(zz + g_neg) & 0x80008000u & mask;  // live and count < 0
               }
             }
           }
-          // this warp's staging slot was last read by its TMA store two sub-blocks ago
+          // staging slot tt was last read by this warp's store of the previous unit
           if (lane == 0) tma_store_wait_read<1>();
           __syncwarp();
-          const uint32_t sa = stage_u32 + slot * 1024;
+          const uint32_t sa = stage_u32 + tt * 1024;
           stmatrix_x4_trans_b8(sa + addr_h0, w0[0], w0[1], w0[2], w0[3]);
           stmatrix_x4_trans_b8(sa + addr_h1, w1[0], w1[1], w1[2], w1[3]);
           fence_proxy_async_smem();
           __syncwarp();
           if (lane == 0) {
-            tma_store_3d(&store_map, my_stage + slot * 1024, 32 * q, band * kBand + i * kSub,
-                         t + 1);
+            tma_store_3d(&store_map, my_stage + tt * 1024, 32 * q, y0, t + 1);
             tma_store_commit();
-            if (warp == kWarpOut0) LTL_TRACE(11, o);
           }
         }
+        if (lane == 0 && warp == kWarpOut0) LTL_TRACE(11, h);
       }
     }
     if (lane == 0) tma_store_wait_all<0>();

@@ -52,14 +52,14 @@ cudaError_t encode3(CUtensorMap* map, void* base, uint64_t rows, uint64_t strips
 
 }  // namespace
 
-// Whole padded slab; 128-column x 256-row boxes (one contiguous 32 KB block
+// Whole padded slab; 128-column x 160-row boxes (one contiguous 20 KB block
 // of a strip) in the SWIZZLE_128B K-major layout of the pass-1 B operand
 // (ptx::smem_desc_sw128_kmajor).
 cudaError_t make_load_map(CUtensorMap* map, const SlabView& s) {
   if (s.rows <= 0 || s.cols <= 0) return cudaSuccess;
   return encode3(map, s.buf, static_cast<uint64_t>(s.rows) + 2 * kHalo,
                  static_cast<uint64_t>(s.strips), static_cast<uint64_t>(s.strip_bytes), kStrip,
-                 256, CU_TENSOR_MAP_SWIZZLE_128B);
+                 kTcBox, CU_TENSOR_MAP_SWIZZLE_128B);
 }
 
 // Interior rows of every strip: each epilogue warp stores its own 32 x 32
