@@ -9,7 +9,8 @@
 // single-grid fill, including n < 16 where images wrap repeatedly.
 //
 // All sources are interior cells (never other halo cells), so the parts below
-// run concurrently without ordering:
+// run concurrently without ordering (`parts` selects them; the step kernel
+// fuses them for tile-aligned slabs, ltl_tc.cu):
 //   blockIdx.y == 0  side columns of the interior rows (32 cells per row)
 //   blockIdx.y == 1  the 16 rows above, all logical columns [-16, cols + 16)
 //   blockIdx.y == 2  the 16 rows below
@@ -29,7 +30,7 @@ __device__ __forceinline__ int wrap(int v, int n) {
   return m < 0 ? m + n : m;
 }
 
-__global__ void ltl_halo_kernel(SlabView self, SlabView above, SlabView below) {
+__global__ void ltl_halo_kernel(SlabView self, SlabView above, SlabView below, int parts) {
   // PDL: start early, but read the interiors only once the step is complete
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   asm volatile("griddepcontrol.wait;" ::: "memory");
@@ -37,6 +38,7 @@ __global__ void ltl_halo_kernel(SlabView self, SlabView above, SlabView below) {
   const int tid = blockIdx.x * blockDim.x + threadIdx.x;
   const int nthreads = gridDim.x * blockDim.x;
   if (blockIdx.y == 0) {
+    if (!(parts & kHaloCols)) return;
     for (int i = tid; i < rows * 2 * kHalo; i += nthreads) {
       const int y = i / (2 * kHalo), c = i % (2 * kHalo);
       const int px = c < kHalo ? c - kHalo : cols + (c - kHalo);  // [-16, 0) or [cols, cols+16)
@@ -45,9 +47,9 @@ __global__ void ltl_halo_kernel(SlabView self, SlabView above, SlabView below) {
     }
     return;
   }
+  if (!(parts & kHaloRows)) return;
   const bool top = blockIdx.y == 1;
   const SlabView& src = top ? above : below;
-  if (src.rows < 0) return;  // rows come from an external transport
   // interior columns in 16-byte groups (cols % 16 == 0), edge cells one by one
   const bool vec = (cols % 16) == 0;
   const int groups = vec ? cols / 16 : 0;
@@ -72,8 +74,8 @@ __global__ void ltl_halo_kernel(SlabView self, SlabView above, SlabView below) {
 }  // namespace
 
 cudaError_t launch_halo_fill(const SlabView& self, const SlabView& above, const SlabView& below,
-                             cudaStream_t stream) {
-  if (self.rows <= 0 || self.cols <= 0) return cudaSuccess;
+                             int parts, cudaStream_t stream) {
+  if (self.rows <= 0 || self.cols <= 0 || parts == 0) return cudaSuccess;
   const int64_t side = 2LL * kHalo * self.rows;
   const int64_t band = kHalo * (self.cols / 4 + 2LL * kHalo);
   int64_t work = side > band ? side : band;
@@ -88,7 +90,7 @@ cudaError_t launch_halo_fill(const SlabView& self, const SlabView& above, const 
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, ltl_halo_kernel, self, above, below);
+  return cudaLaunchKernelEx(&cfg, ltl_halo_kernel, self, above, below, parts);
 }
 
 }  // namespace ltl

@@ -74,9 +74,25 @@ struct DeviceStats {
 // ---- tcgen05 banded-MMA step (ltl_tc.cu)
 constexpr int kTcBand = 128;                  // output rows per unit
 constexpr int kTcBox = kTcBand + 2 * kHalo;   // rows per TMA box (160)
+// Periodic wrap done by the LOADS instead of a halo refresh (fill_periodic_halo,
+// src/grid.cpp:75-94): with cols % 128 == 0 the 16 side columns of strip 0 /
+// S-1 are simply the boxes of strip S-1 / 0; with one whole-torus slab and
+// rows % 32 == 0 the 16 rows above band 0 / below the last band are loaded
+// from the other end of the same strip.  The halo cells in HBM are then never
+// read by the step, so it writes none (no halo kernel between generations).
+__host__ __device__ inline bool tc_wrap_cols(int32_t cols) {
+  return cols >= kStrip && cols % kStrip == 0;
+}
+__host__ __device__ inline bool tc_wrap_rows(int32_t rows) {
+  return rows >= 32 && rows % 32 == 0;
+}
+// load maps: [0] whole boxes, [1] 16-row wrap pieces, [2] band-0 bodies
+// (kTcBox - 16 rows), [3] last-band bodies (rows of the last band + 16)
+constexpr int kTcLoadMaps = 4;
 struct TcLaunch {
-  const CUtensorMap* load_map;   // whole source slab, {128, kTcBox, 1} boxes, SWIZZLE_128B
+  const CUtensorMap* load_maps;  // kTcLoadMaps maps over the source slab, SWIZZLE_128B
   const CUtensorMap* store_map;  // destination interior rows, {32, 32, 1} boxes, SWIZZLE_32B
+  int32_t wrap_cols, wrap_rows;
   int32_t rows, cols;
   RuleConsts rule;
   int32_t inject_fault;
@@ -88,7 +104,7 @@ cudaError_t launch_tc_step(const TcLaunch& a, cudaStream_t stream);
 size_t tc_smem_bytes();
 
 // Host-side tensor-map builders (driver entry point fetched at runtime).
-cudaError_t make_load_map(CUtensorMap* map, const SlabView& s);
+cudaError_t make_load_maps(CUtensorMap* maps, const SlabView& s);
 cudaError_t make_store_map(CUtensorMap* map, const SlabView& s);
 
 // ---- CUDA-core shared-memory stencil ablation (ltl_stencil.cu)
@@ -105,10 +121,10 @@ cudaError_t launch_init_random(const SlabView& s, int32_t row0, int32_t fill_row
 // ---- periodic halo refresh (ltl_halo.cu)
 // Fills the halo of `self` from the interiors of `above` (rows over the top
 // edge), `below` (rows under the bottom edge) and `self` (column wrap).  For a
-// single slab all three are the same buffer.  above.rows < 0: refresh only
-// the column wrap (the row halo comes from an external transport).
+// single slab all three are the same buffer.  `parts`: kHaloCols | kHaloRows.
+constexpr int kHaloCols = 1, kHaloRows = 2;
 cudaError_t launch_halo_fill(const SlabView& self, const SlabView& above, const SlabView& below,
-                             cudaStream_t stream);
+                             int parts, cudaStream_t stream);
 
 // ---- layout conversion and edge exchange (ltl_layout.cu)
 // Dense row-major rows x cols interior <-> strip slab interior.

@@ -42,7 +42,7 @@ struct Slab {
   int64_t strip_bytes = 0;
   int32_t strips = 0;
   uint8_t* buf[2] = {nullptr, nullptr};
-  CUtensorMap load_map[2];
+  CUtensorMap load_maps[2][ltl::kTcLoadMaps];
   CUtensorMap store_map[2];
   ltl::DeviceStats* dstats = nullptr;
   cudaStream_t stream = nullptr;
@@ -61,6 +61,7 @@ struct ltl_ctx {
   int32_t rows = 0, cols = 0, f = 16;
   int cur = 0;
   bool external_row_halo = false;
+  bool halo_stale = false;  // halo cells the tcgen05 step does not need were not refreshed
   std::vector<Slab> slabs;
   std::string err;
 };
@@ -113,7 +114,7 @@ void check_run_args(const ltl_ctx* ctx, const ltl_rule_c* rule, int32_t steps) {
 
 void build_maps(Slab& s, int32_t cols) {
   for (int i = 0; i < 2; ++i) {
-    ck(ltl::make_load_map(&s.load_map[i], s.view(i, cols)), "tensor map (load)");
+    ck(ltl::make_load_maps(s.load_maps[i], s.view(i, cols)), "tensor map (load)");
     ck(ltl::make_store_map(&s.store_map[i], s.view(i, cols)), "tensor map (store)");
   }
 }
@@ -185,9 +186,23 @@ void destroy_ctx(ltl_ctx* ctx) {
   ctx->slabs.clear();
 }
 
+// Which periodic wraps the step kernel takes care of by itself, loading the
+// images straight from the interior (ltl_kernels.cuh tc_wrap_*): the column
+// wrap whenever cols % 128 == 0, the row wrap for one whole-torus slab with
+// rows % 32 == 0.  Slabs whose rows come from neighbours keep their row halo.
+bool wrap_cols(const ltl_ctx* ctx) {
+  return ltl::tc_wrap_cols(ctx->cols) && !std::getenv("LTL_NO_WRAP");  // env: diagnostics
+}
+bool wrap_rows(const ltl_ctx* ctx) {
+  return ctx->slabs.size() == 1 && !ctx->external_row_halo &&
+         ltl::tc_wrap_rows(ctx->slabs[0].rows) && !std::getenv("LTL_NO_WRAP");
+}
+
 // Halo refresh of generation buffer `which` on every slab (after all slabs'
-// interiors for that generation are enqueued).
-void enqueue_halo(ltl_ctx* ctx, int which) {
+// interiors for that generation are enqueued).  `for_tc`: only what the next
+// tcgen05 step will read from HBM (the wraps it does not load itself); the
+// halo is then marked stale for consumers that need all of it (the stencil).
+void enqueue_halo(ltl_ctx* ctx, int which, bool for_tc = false) {
   const int32_t G = static_cast<int32_t>(ctx->slabs.size());
   for (int32_t i = 0; i < G; ++i) {
     Slab& s = ctx->slabs[i];
@@ -199,13 +214,17 @@ void enqueue_halo(ltl_ctx* ctx, int which) {
       ck(cudaStreamWaitEvent(s.stream, dn.ev_step, 0), "wait below");
     }
     ltl::SlabView self = s.view(which, ctx->cols);
-    ltl::SlabView above = ctx->external_row_halo ? self : up.view(which, ctx->cols);
-    ltl::SlabView below = ctx->external_row_halo ? self : dn.view(which, ctx->cols);
-    if (ctx->external_row_halo) {
-      // rows come from an external transport; refresh only the column wrap
-      above.rows = below.rows = -1;
+    ltl::SlabView above = up.view(which, ctx->cols);
+    ltl::SlabView below = dn.view(which, ctx->cols);
+    // rows of a part come from an external transport (ltl_unpack_halo)
+    const int all = ctx->external_row_halo ? ltl::kHaloCols : ltl::kHaloCols | ltl::kHaloRows;
+    int parts = all;
+    if (for_tc) {
+      if (wrap_cols(ctx)) parts &= ~ltl::kHaloCols;
+      if (wrap_rows(ctx)) parts &= ~ltl::kHaloRows;
     }
-    ck(ltl::launch_halo_fill(self, above, below, s.stream), "halo kernel");
+    ck(ltl::launch_halo_fill(self, above, below, parts, s.stream), "halo kernel");
+    if (i == 0) ctx->halo_stale = parts != all;
   }
 }
 
@@ -219,49 +238,56 @@ void enqueue_step(ltl_ctx* ctx, const ltl::RuleConsts& rc, uint32_t flags, bool 
     ck(cudaSetDevice(s.dev), "cudaSetDevice");
     if (kt0) ck(cudaEventRecord(kt0[i], s.stream), "event");
     if (flags & LTL_FLAG_STENCIL) {
+      if (ctx->halo_stale) {  // the last tcgen05 steps left wrap-free halos
+        ck(cudaSetDevice(s.dev), "cudaSetDevice");
+        if (i == 0) enqueue_halo(ctx, cur);
+        ck(cudaSetDevice(s.dev), "cudaSetDevice");
+      }
       ck(ltl::launch_stencil_step(s.view(cur, ctx->cols), s.view(nxt, ctx->cols), rc, fault,
                                   want_stats ? s.dstats : nullptr, s.stream),
          "stencil kernel");
     } else {
       ltl::TcLaunch a{};
-      a.load_map = &s.load_map[cur];
+      a.load_maps = s.load_maps[cur];
       a.store_map = &s.store_map[nxt];
+      a.wrap_cols = wrap_cols(ctx);
+      a.wrap_rows = wrap_rows(ctx);
       a.rows = s.rows;
       a.cols = ctx->cols;
       a.rule = rc;
       a.inject_fault = fault;
       a.stats = want_stats ? s.dstats : nullptr;
       // Debug: LTL_TC_TRACE=<file> dumps the pipeline timeline of CTA 0 of
-      // the first traced launch (12 event kinds x 64 chunks of clock64 stamps).
-      static bool traced = false;
+      // the first traced launch (16 event kinds x 256 stamps; 14/15 = per-CTA start/end ns).
+      static int traced_launches = 0;
+      const int trace_skip = std::getenv("LTL_TC_TRACE_SKIP") ? std::atoi(std::getenv("LTL_TC_TRACE_SKIP")) : 0;
       const char* trace_path = std::getenv("LTL_TC_TRACE");
       long long* dtrace = nullptr;
-      if (trace_path && !traced && !want_stats) {
-        ck(cudaMalloc(&dtrace, 12 * 64 * sizeof(long long)), "trace alloc");
-        ck(cudaMemsetAsync(dtrace, 0, 12 * 64 * sizeof(long long), s.stream), "trace memset");
+      if (trace_path && traced_launches++ == trace_skip && !want_stats) {
+        ck(cudaMalloc(&dtrace, 16 * 256 * sizeof(long long)), "trace alloc");
+        ck(cudaMemsetAsync(dtrace, 0, 16 * 256 * sizeof(long long), s.stream), "trace memset");
         a.trace = dtrace;
       }
       ck(ltl::launch_tc_step(a, s.stream), "tcgen05 kernel");
       if (dtrace) {
-        std::vector<long long> h(12 * 64);
+        std::vector<long long> h(16 * 256);
         ck(cudaStreamSynchronize(s.stream), "trace sync");
         ck(cudaMemcpy(h.data(), dtrace, h.size() * sizeof(long long), cudaMemcpyDeviceToHost),
            "trace copy");
         cudaFree(dtrace);
         if (FILE* fh = std::fopen(trace_path, "w")) {
-          for (int e = 0; e < 12; ++e) {
-            for (int k = 0; k < 64; ++k) std::fprintf(fh, "%s%lld", k ? "," : "", h[e * 64 + k]);
+          for (int e = 0; e < 16; ++e) {
+            for (int k = 0; k < 256; ++k) std::fprintf(fh, "%s%lld", k ? "," : "", h[e * 256 + k]);
             std::fprintf(fh, "\n");
           }
           std::fclose(fh);
         }
-        traced = true;
       }
     }
     if (kt1) ck(cudaEventRecord(kt1[i], s.stream), "event");
     if (ctx->slabs.size() > 1) ck(cudaEventRecord(s.ev_step, s.stream), "event");
   }
-  enqueue_halo(ctx, nxt);
+  enqueue_halo(ctx, nxt, !(flags & LTL_FLAG_STENCIL));
   ctx->cur = nxt;
 }
 

@@ -122,15 +122,24 @@ struct Params {
   int32_t bands;
   RuleConsts rule;
   int32_t inject_fault;
+  int32_t wrap_cols, wrap_rows;  // periodic wrap done by the loads (tc_wrap_*)
   DeviceStats* stats;
   long long* trace;  // debug timeline of CTA 0 (only with -DLTL_TC_TRACE_BUILD)
 };
 
 #ifdef LTL_TC_TRACE_BUILD
 #define LTL_TRACE(ev, idx) \
-  do { if (p.trace && blockIdx.x == 0 && (idx) < 64) p.trace[(ev) * 64 + (idx)] = clock64(); } while (0)
+  do { if (p.trace && blockIdx.x == 0 && (idx) < 256) p.trace[(ev) * 256 + (idx)] = clock64(); } while (0)
+__device__ __forceinline__ long long global_ns() {
+  long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define LTL_TRACE_CTA(ev) \
+  do { if (p.trace && threadIdx.x == 0) p.trace[(ev) * 256 + blockIdx.x] = global_ns(); } while (0)
 #else
 #define LTL_TRACE(ev, idx) do { } while (0)
+#define LTL_TRACE_CTA(ev) do { } while (0)
 #endif
 
 // Static schedule: the bands * strips units in band-major order, CTA b takes
@@ -189,6 +198,9 @@ __device__ __forceinline__ uint32_t rule_pair(uint32_t z, const SimdRule& k) {
 template <bool kChecked>
 __global__ void __launch_bounds__(kThreads, 1)
     ltl_tc_step_kernel(const __grid_constant__ CUtensorMap load_map,
+                       const __grid_constant__ CUtensorMap load_piece,
+                       const __grid_constant__ CUtensorMap load_first,
+                       const __grid_constant__ CUtensorMap load_last,
                        const __grid_constant__ CUtensorMap store_map, const Params p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
@@ -256,6 +268,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 0 && lane == 0) {
     prefetch_tmap(&load_map);
     prefetch_tmap(&store_map);
+    if (p.wrap_rows) {
+      prefetch_tmap(&load_piece);
+      prefetch_tmap(&load_first);
+      prefetch_tmap(&load_last);
+    }
     for (int i = 0; i < kXStages; ++i) {
       mbar_init(&x_full[i], 1);
       mbar_init(&x_empty[i], 1);
@@ -281,6 +298,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   // previous kernel's tail (PDL).  The grid is read from here on.
   pdl_launch_dependents();
   pdl_wait_prerequisites();
+  LTL_TRACE_CTA(14);
 
   if (warp == 0) {
     // ================= TMA producer: boxes t0-1 .. t1 of every segment =======
@@ -289,14 +307,41 @@ __global__ void __launch_bounds__(kThreads, 1)
       SegIter it(p);
       int band, t0, t1;
       while (it.next(band, t0, t1)) {
+        const bool first = p.wrap_rows && band == 0;
+        const bool last = p.wrap_rows && band == p.bands - 1;
+        const int last_rows = p.rows - kBand * band;  // interior rows of the last band
         for (int k = 0; k < t1 - t0 + 2; ++k, ++g) {
           const uint32_t s = g % kXStages;
           mbar_wait(&x_empty[s], ((g / kXStages) & 1) ^ 1);
           LTL_TRACE(0, g);
-          mbar_arrive_expect_tx(&x_full[s], kBoxBytes);
-          // logical strip t0-1+k = storage strip t0+k
-          tma_load_3d(smem + kSmemX + s * kBoxBytes, &load_map, &x_full[s], 0, band * kBand,
-                      t0 + k);
+          // logical strip t0-1+k: storage strip t0+k, or its periodic image
+          int strip = t0 + k;
+          if (p.wrap_cols) strip = (t0 - 1 + k + p.strips) % p.strips + 1;
+          uint8_t* dst = smem + kSmemX + s * kBoxBytes;
+          if (!first && !last) {
+            mbar_arrive_expect_tx(&x_full[s], kBoxBytes);
+            tma_load_3d(dst, &load_map, &x_full[s], 0, band * kBand, strip);
+            continue;
+          }
+          // first / last band of a whole torus: the 16 rows beyond the edge
+          // are loaded from the other end of the strip (padded row 16 + y)
+          const int body = last ? last_rows : kBand;  // interior rows in the box body
+          mbar_arrive_expect_tx(&x_full[s], (last ? last_rows + 2 * kHalo : kBox) * kStrip);
+          int row = 0;  // box row being filled
+          if (first) {  // rows -16 .. -1  <-  rows - 16 .. rows - 1
+            tma_load_3d(dst, &load_piece, &x_full[s], 0, p.rows, strip);
+            row = kHalo;
+          }
+          if (first && !last) {  // rows 0 .. 143
+            tma_load_3d(dst + row * kStrip, &load_first, &x_full[s], 0, kHalo, strip);
+          } else {  // last band body: padded rows from 128 * band (its top halo
+                    // included unless it is also the first band)
+            tma_load_3d(dst + row * kStrip, &load_last, &x_full[s], 0,
+                        first ? kHalo : band * kBand, strip);
+            // rows rows .. rows + 15  <-  0 .. 15
+            tma_load_3d(dst + (row + body + (first ? 0 : kHalo)) * kStrip, &load_piece,
+                        &x_full[s], 0, kHalo, strip);
+          }
         }
       }
     }
@@ -461,13 +506,20 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t g_neg = (0x8000u - (K + rc.neg_live)) * 0x10001u;
     const uint32_t r_mask = (K - 1) * 0x10001u;
     uint32_t max_r = 0, bad = 0;
-    // staging: per warp 2 slots of [32 rows][32 B], SWIZZLE_32B (16-byte
-    // chunk ^= (row >> 2) & 1); this thread addresses row `lane`.
+    // staging: per warp 2 tiles of [32 rows][32 B], SWIZZLE_32B (16-byte
+    // chunk ^= (row >> 2) & 1); this thread addresses row `lane`.  Both tiles
+    // of a unit are staged behind one proxy fence.
     const uint32_t wslot = warp - kWarpOut0;
     uint8_t* my_stage = smem + kSmemStage + wslot * 2048;
     const uint32_t stage_u32 = smem_u32(my_stage);
     const uint32_t addr_h0 = lane * 32 + ((0u ^ ((lane >> 2) & 1)) << 4);
     const uint32_t addr_h1 = lane * 32 + ((1u ^ ((lane >> 2) & 1)) << 4);
+    // fill_periodic_halo (src/grid.cpp:75-94) folded into the stores of the
+    // tiles on the torus edge (tile-aligned slabs only, tc_fusable): storage
+    // strip 0 cols 96..127 = logical cols [-32, 0), strip S+1 cols 0..31 =
+    // [cols, cols+32); 16-row halves of a staging tile (the SWIZZLE_32B atom
+    // is 8 rows, so rows 16..31 start at +512 B) go to padded rows
+    // rows+16 .. (images of rows 0..15) and 0 .. 15 (of rows rows-16 ..).
     uint32_t h = 0;
     SegIter it(p);
     int band, t0, t1;
@@ -487,24 +539,25 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc_fence_before();
         mbar_arrive(&d2_empty[grp]);
         if (lane == 0 && warp == kWarpOut0) LTL_TRACE(6, h);
+        uint32_t w[2][2][4];  // [tile][lane half][stmatrix register]
 #pragma unroll
         for (int tt = 0; tt < 2; ++tt) {
-          uint32_t w0[4], w1[4];
 #pragma unroll
-          for (int v = 0; v < 2; ++v) {
-            const uint32_t* z0 = z[tt][0];
-            const uint32_t* z1 = z[tt][1];
-            const uint32_t a0 = rule_pair(z0[4 * v + 0], sr), b0 = rule_pair(z0[4 * v + 1], sr);
-            const uint32_t a2 = rule_pair(z0[4 * v + 2], sr), b2 = rule_pair(z0[4 * v + 3], sr);
-            w0[2 * v + 0] = prmt(a0, a2, 0xFDB9) & 0x01010101u;
-            w0[2 * v + 1] = prmt(b0, b2, 0xFDB9) & 0x01010101u;
-            const uint32_t c0r = rule_pair(z1[4 * v + 0], sr), d0r = rule_pair(z1[4 * v + 1], sr);
-            const uint32_t c2r = rule_pair(z1[4 * v + 2], sr), d2r = rule_pair(z1[4 * v + 3], sr);
-            w1[2 * v + 0] = prmt(c0r, c2r, 0xFDB9) & 0x01010101u;
-            w1[2 * v + 1] = prmt(d0r, d2r, 0xFDB9) & 0x01010101u;
+          for (int hh = 0; hh < 2; ++hh) {
+            const uint32_t* zz = z[tt][hh];
+#pragma unroll
+            for (int v = 0; v < 2; ++v) {
+              const uint32_t a0 = rule_pair(zz[4 * v + 0], sr), b0 = rule_pair(zz[4 * v + 1], sr);
+              const uint32_t a2 = rule_pair(zz[4 * v + 2], sr), b2 = rule_pair(zz[4 * v + 3], sr);
+              w[tt][hh][2 * v + 0] = prmt(a0, a2, 0xFDB9) & 0x01010101u;
+              w[tt][hh][2 * v + 1] = prmt(b0, b2, 0xFDB9) & 0x01010101u;
+            }
           }
-          const int y0 = band * kBand + kSub * static_cast<int>(grp) + 32 * tt;
-          if constexpr (kChecked) {
+        }
+        const int ybase = band * kBand + kSub * static_cast<int>(grp);  // rows of tile 0
+        if constexpr (kChecked) {
+#pragma unroll
+          for (int tt = 0; tt < 2; ++tt) {
             // register jj of lane half hh: strip column 16hh + lane/4 + 8((jj>>1)&1)
             // of this quarter, D2 columns c, c+1 with c = 4(lane%4) + 2(jj&1) + 16(jj>>2)
 #pragma unroll
@@ -513,6 +566,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               for (int jj = 0; jj < 8; ++jj) {
                 const int xl = 16 * hh + static_cast<int>(lane >> 2) + 8 * ((jj >> 1) & 1);
                 const int c = 4 * static_cast<int>(lane & 3) + 2 * (jj & 1) + 16 * (jj >> 2);
+                const int y0 = ybase + 32 * tt;
                 const bool xv = t * kStrip + 32 * static_cast<int>(q) + xl < p.cols;
                 const bool v0 = xv && y0 + out_row_of_col(c) < p.rows;
                 const bool v1 = xv && y0 + out_row_of_col(c + 1) < p.rows;
@@ -523,23 +577,28 @@ __global__ void __launch_bounds__(kThreads, 1)
               }
             }
           }
-          // staging slot tt was last read by this warp's store of the previous unit
-          if (lane == 0) tma_store_wait_read<1>();
-          __syncwarp();
+        }
+        // both staging tiles were last read by this warp's stores of the previous unit
+        tma_store_wait_read<0>();
+        __syncwarp();
+#pragma unroll
+        for (int tt = 0; tt < 2; ++tt) {
           const uint32_t sa = stage_u32 + tt * 1024;
-          stmatrix_x4_trans_b8(sa + addr_h0, w0[0], w0[1], w0[2], w0[3]);
-          stmatrix_x4_trans_b8(sa + addr_h1, w1[0], w1[1], w1[2], w1[3]);
-          fence_proxy_async_smem();
-          __syncwarp();
-          if (lane == 0) {
-            tma_store_3d(&store_map, my_stage + tt * 1024, 32 * q, y0, t + 1);
-            tma_store_commit();
-          }
+          stmatrix_x4_trans_b8(sa + addr_h0, w[tt][0][0], w[tt][0][1], w[tt][0][2], w[tt][0][3]);
+          stmatrix_x4_trans_b8(sa + addr_h1, w[tt][1][0], w[tt][1][1], w[tt][1][2], w[tt][1][3]);
+        }
+        fence_proxy_async_smem();
+        __syncwarp();
+        // the two tiles leave as two TMA stores issued by lanes 0 and 1 (each
+        // lane commits its own bulk group)
+        if (lane < 2) {
+          tma_store_3d(&store_map, my_stage + lane * 1024, 32 * q, ybase + 32 * lane, t + 1);
+          tma_store_commit();
         }
         if (lane == 0 && warp == kWarpOut0) LTL_TRACE(11, h);
       }
     }
-    if (lane == 0) tma_store_wait_all<0>();
+    tma_store_wait_all<0>();
     if constexpr (kChecked) {
       int32_t mr = static_cast<int32_t>(max(max_r & 0xFFFF, max_r >> 16));
 #pragma unroll
@@ -552,6 +611,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncwarp();
   tc_fence_before();
   __syncthreads();
+  LTL_TRACE_CTA(15);
   if (warp == 1) tmem_dealloc(tmem, kTmemCols);
 }
 
@@ -579,6 +639,8 @@ cudaError_t launch_tc_step(const TcLaunch& a, cudaStream_t stream) {
   p.bands = (a.rows + kBand - 1) / kBand;
   p.rule = a.rule;
   p.inject_fault = a.inject_fault;
+  p.wrap_cols = a.wrap_cols && tc_wrap_cols(a.cols);
+  p.wrap_rows = a.wrap_rows && tc_wrap_rows(a.rows);
   p.stats = a.stats;
   p.trace = a.trace;
   // One persistent CTA per SM over the units (fewer for small grids).
@@ -598,10 +660,13 @@ cudaError_t launch_tc_step(const TcLaunch& a, cudaStream_t stream) {
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = std::getenv("LTL_NO_PDL") ? 0 : 1;  // diagnostics
+  const CUtensorMap* lm = a.load_maps;
   if (a.stats)
-    return cudaLaunchKernelEx(&cfg, ltl_tc_step_kernel<true>, *a.load_map, *a.store_map, p);
-  return cudaLaunchKernelEx(&cfg, ltl_tc_step_kernel<false>, *a.load_map, *a.store_map, p);
+    return cudaLaunchKernelEx(&cfg, ltl_tc_step_kernel<true>, lm[0], lm[1], lm[2], lm[3],
+                              *a.store_map, p);
+  return cudaLaunchKernelEx(&cfg, ltl_tc_step_kernel<false>, lm[0], lm[1], lm[2], lm[3],
+                            *a.store_map, p);
 }
 
 }  // namespace ltl

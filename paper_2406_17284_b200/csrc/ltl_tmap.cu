@@ -52,18 +52,28 @@ cudaError_t encode3(CUtensorMap* map, void* base, uint64_t rows, uint64_t strips
 
 }  // namespace
 
-// Whole padded slab; 128-column x 160-row boxes (one contiguous 20 KB block
-// of a strip) in the SWIZZLE_128B K-major layout of the pass-1 B operand
-// (ptx::smem_desc_sw128_kmajor).
-cudaError_t make_load_map(CUtensorMap* map, const SlabView& s) {
+// Whole padded slab in the SWIZZLE_128B K-major layout of the pass-1 B
+// operand (ptx::smem_desc_sw128_kmajor): [0] 160-row boxes (one contiguous
+// 20 KB block of a strip), [1] 16-row pieces, [2] 144-row and [3] (rows of the
+// last band + 16)-row bodies for the row-wrapped first / last band boxes.
+cudaError_t make_load_maps(CUtensorMap* maps, const SlabView& s) {
   if (s.rows <= 0 || s.cols <= 0) return cudaSuccess;
-  return encode3(map, s.buf, static_cast<uint64_t>(s.rows) + 2 * kHalo,
-                 static_cast<uint64_t>(s.strips), static_cast<uint64_t>(s.strip_bytes), kStrip,
-                 kTcBox, CU_TENSOR_MAP_SWIZZLE_128B);
+  const int last = s.rows - kTcBand * ((s.rows - 1) / kTcBand);  // rows of the last band
+  const bool one_band = s.rows <= kTcBand;  // first = last band: body without its top halo
+  const uint32_t box[kTcLoadMaps] = {kTcBox, kHalo, kTcBox - kHalo,
+                                     static_cast<uint32_t>(last + (one_band ? 0 : kHalo))};
+  for (int i = 0; i < kTcLoadMaps; ++i) {
+    const cudaError_t e = encode3(&maps[i], s.buf, static_cast<uint64_t>(s.rows) + 2 * kHalo,
+                                  static_cast<uint64_t>(s.strips),
+                                  static_cast<uint64_t>(s.strip_bytes), kStrip, box[i],
+                                  CU_TENSOR_MAP_SWIZZLE_128B);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
 }
 
 // Interior rows of every strip: each epilogue warp stores its own 32 x 32
-// tile, SWIZZLE_32B so the stmatrix rows land conflict-free.
+// tiles, SWIZZLE_32B so the stmatrix rows land conflict-free.
 cudaError_t make_store_map(CUtensorMap* map, const SlabView& s) {
   if (s.rows <= 0 || s.cols <= 0) return cudaSuccess;
   return encode3(map, s.buf + kHalo * kStrip, static_cast<uint64_t>(s.rows),
