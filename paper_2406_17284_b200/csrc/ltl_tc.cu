@@ -24,7 +24,7 @@
 //            M = 128 (x), N = 160 (all box rows), K = 6 x 32 = columns
 //            [-32, 160) of the strip (box t-1 chunk 3, box t chunks 0..3,
 //            box t+1 chunk 0).  A1[x][k] = [|k-32-x| <= r] + 128*[k == x+32],
-//            resident in SMEM: the row window sums (the reference's H) with
+//            resident in TMEM: the row window sums (the reference's H) with
 //            the cell state in bit 7 (H <= 33 < 128).
 //   convert  D1 (s32 in TMEM) -> two byte planes written back into TMEM as
 //            K-major A operands of pass 2 (no SMEM round trip):
@@ -77,7 +77,7 @@ constexpr int kSubs = kBand / kSub;       // 2
 constexpr int kKChunks = 6;               // pass-1 K = 192 columns [-32, 160)
 constexpr int kXStages = 8;               // 3 boxes in use + 5 prefetched
 constexpr uint32_t kBoxBytes = kBox * kStrip;  // 20 KB
-constexpr int kA2Boxes = 2;               // plane rings hold two units
+constexpr int kSlots = 2;                 // D1 / plane slots (units in flight)
 constexpr int kConvWarps = 4;
 constexpr int kOutWarps = 8;
 constexpr int kThreads = 32 * (3 + kConvWarps + kOutWarps);  // 480
@@ -92,12 +92,11 @@ static_assert(kSubs == 2, "one output group per sub-block");
 
 // Shared-memory carve-up (offsets from a 1024-aligned base).
 constexpr uint32_t kSmemX = 0;                                        // 8 x 20 KB
-constexpr uint32_t kSmemA1 = kSmemX + kXStages * kBoxBytes;           // 6 x [128][32]
-constexpr uint32_t kSmemBand = kSmemA1 + kKChunks * 128 * 32;         // 7 x [64][32]
+constexpr uint32_t kSmemBand = kSmemX + kXStages * kBoxBytes;         // 7 x [64][32]
 constexpr uint32_t kTileBytes = kSub * 32;                            // 2 KB
 constexpr uint32_t kSmemStage = kSmemBand + kNumTiles * kTileBytes;   // 8 warps x 2 x 1 KB
 constexpr uint32_t kSmemBars = kSmemStage + kOutWarps * 2 * 1024;
-constexpr uint32_t kNumBars = 2 * (kXStages + 1 + kA2Boxes + kSubs);
+constexpr uint32_t kNumBars = 2 * kXStages + 3 * kSlots + 2 * kSubs;
 constexpr uint32_t kSmemTotal = kSmemBars + kNumBars * 8 + 16;
 constexpr uint32_t kSmemAlloc = kSmemTotal + 1024;  // alignment slack
 static_assert(kSmemAlloc <= 227 * 1024, "shared memory budget");
@@ -106,12 +105,19 @@ static_assert(kSmemAlloc <= 227 * 1024, "shared memory budget");
 constexpr uint32_t kTmemCols = 512;
 constexpr uint32_t kPbCols = kBox / 4;          // 40: one byte per box row
 constexpr uint32_t kPiCols = kBand / 4;         // 32: one byte per centre row
-constexpr uint32_t kTmemD1 = 0;                 // 160
-constexpr uint32_t kTmemPb = kTmemD1 + kBox;    // 2 x 40
-constexpr uint32_t kTmemPi = kTmemPb + kA2Boxes * kPbCols;  // 2 x 32
-constexpr uint32_t kTmemD2 = kTmemPi + kA2Boxes * kPiCols;  // 2 x 64
-static_assert(kTmemD2 + kSubs * kSub <= kTmemCols, "TMEM budget");
-static_assert(kTmemPb % 8 == 0 && kTmemPi % 8 == 0 && kTmemD2 % 8 == 0, "A operand alignment");
+// A slot first holds D1 (160 s32 columns); once the convert warps have read it
+// into registers they write the two byte planes over its first 72 columns,
+// which pass 2 reads.  Two slots: pass 1 of unit h+1 runs while unit h is
+// converted and reduced.
+constexpr uint32_t kSlotCols = kBox;            // 160
+constexpr uint32_t kTmemSlot = 0;               // 2 x 160
+constexpr uint32_t kPbOff = 0;                  // Pb: 40 columns
+constexpr uint32_t kPiOff = kPbCols;            // Pi: 32 columns
+constexpr uint32_t kTmemD2 = kTmemSlot + kSlots * kSlotCols;  // 2 x 64
+constexpr uint32_t kTmemA1 = kTmemD2 + kSubs * kSub;          // pass-1 A: 192 k / 4 = 48
+static_assert(kPiOff + kPiCols <= kSlotCols, "planes fit in the D1 slot");
+static_assert(kTmemA1 + kKChunks * 8 <= kTmemCols, "TMEM budget");
+static_assert(kSlotCols % 8 == 0 && kPiOff % 8 == 0 && kTmemD2 % 8 == 0, "A operand alignment");
 
 constexpr uint32_t kIdesc1 = idesc_i8_u8u8_s32(128, kBox);
 constexpr uint32_t kIdesc2 = idesc_i8_u8u8_s32(128, kSub);
@@ -137,9 +143,19 @@ __device__ __forceinline__ long long global_ns() {
 }
 #define LTL_TRACE_CTA(ev) \
   do { if (p.trace && threadIdx.x == 0) p.trace[(ev) * 256 + blockIdx.x] = global_ns(); } while (0)
+// cycles spent in each wait site, summed over the launch by CTA 0 (row 13)
+#define LTL_WAIT(site, bar, par)                                                   \
+  do {                                                                             \
+    const long long w0_ = clock64();                                               \
+    mbar_wait(bar, par);                                                           \
+    if (p.trace && blockIdx.x == 0 && (threadIdx.x & 31) == 0)                     \
+      atomicAdd(reinterpret_cast<unsigned long long*>(&p.trace[13 * 256 + (site)]), \
+                static_cast<unsigned long long>(clock64() - w0_));                 \
+  } while (0)
 #else
 #define LTL_TRACE(ev, idx) do { } while (0)
 #define LTL_TRACE_CTA(ev) do { } while (0)
+#define LTL_WAIT(site, bar, par) mbar_wait(bar, par)
 #endif
 
 // Static schedule: the bands * strips units in band-major order, CTA b takes
@@ -149,13 +165,22 @@ __device__ __forceinline__ long long global_ns() {
 // same strips at about the same time, so the 32 rows their boxes share are
 // mostly L2 hits.  Every role of the CTA iterates the same segments in the
 // same order.
+//
+// With the column wrap done by the loads (cols % 128 == 0) band k's strips
+// are walked starting at a rotation rot_k = round(k (S - U/G)) mod S, and a
+// run may cross the torus seam (strip t is t mod S).  CTA b + 1 then reaches
+// band k + 1 at the same strip at which CTA b meets band k: the 32 box rows
+// two vertically adjacent units share are read from HBM once and from L2
+// the second time (without it ~20 % of the reads are the overlap again).
 struct SegIter {
-  int64_t u, u_end;
-  int32_t S;
-  __device__ explicit SegIter(const Params& p) : S(p.strips) {
-    const int64_t U = static_cast<int64_t>(p.bands) * p.strips;
-    u = U * blockIdx.x / gridDim.x;
-    u_end = U * (blockIdx.x + 1) / gridDim.x;
+  int64_t u, u_end, U;
+  int32_t S, G;
+  bool rotate;
+  __device__ explicit SegIter(const Params& p)
+      : U(static_cast<int64_t>(p.bands) * p.strips), S(p.strips), G(gridDim.x),
+        rotate(p.wrap_cols != 0) {
+    u = U * blockIdx.x / G;
+    u_end = U * (blockIdx.x + 1) / G;
   }
   __device__ bool next(int& band, int& t0, int& t1) {
     if (u >= u_end) return false;
@@ -164,6 +189,15 @@ struct SegIter {
     const int64_t e = min(u_end, static_cast<int64_t>(band + 1) * S);
     t1 = t0 + static_cast<int>(e - u);
     u = e;
+    if (rotate) {
+      // rot = round(band * (S - U / G)) mod S, in exact integers (S - U/G may
+      // be negative when a CTA covers more than one band)
+      const int64_t SG = static_cast<int64_t>(S) * G;
+      const int64_t num = (static_cast<int64_t>(band) * (((SG - U) % SG + SG) % SG)) % SG;
+      const int r = static_cast<int>(((num + G / 2) / G) % S);
+      t0 += r;
+      t1 += r;
+    }
     return true;
   }
 };
@@ -208,11 +242,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kSmemBars);
   uint64_t* x_full = bars;
   uint64_t* x_empty = x_full + kXStages;
-  uint64_t* d1_full = x_empty + kXStages;
-  uint64_t* d1_empty = d1_full + 1;
-  uint64_t* a2_full = d1_empty + 1;
-  uint64_t* a2_empty = a2_full + kA2Boxes;
-  uint64_t* d2_full = a2_empty + kA2Boxes;
+  uint64_t* d1_full = x_empty + kXStages;     // pass 1 -> convert
+  uint64_t* a2_full = d1_full + kSlots;       // convert -> pass 2 (planes written)
+  uint64_t* slot_empty = a2_full + kSlots;    // pass 2 -> pass 1 (slot reusable)
+  uint64_t* d2_full = slot_empty + kSlots;
   uint64_t* d2_empty = d2_full + kSubs;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(d2_empty + kSubs);
 
@@ -222,25 +255,6 @@ __global__ void __launch_bounds__(kThreads, 1)
   const bool vn = p.rule.kind != 0;
 
   // ---- one-time setup: resident bands (generic-proxy writes), barriers, TMEM
-  // pass-1 A1 [128 x][192 k], SWIZZLE_32B per 32-column K chunk, built a
-  // 32-bit word (4 consecutive k) at a time; the swizzle moves whole 16-byte
-  // chunks, so a word stays contiguous
-  for (uint32_t w = threadIdx.x; w < 128u * kKChunks * 8; w += kThreads) {
-    const int m = static_cast<int>(w / (kKChunks * 8)), k0 = 4 * static_cast<int>(w % (kKChunks * 8));
-    uint32_t word = 0;
-#pragma unroll
-    for (int b = 0; b < 4; ++b) {
-      const int d = k0 + b - 32 - m;
-      uint32_t v = (d >= -r && d <= r) ? 1u : 0u;
-      if (d == 0) {
-        v += 128u;  // state marker
-        if (p.inject_fault && m == 0) v = 128u;  // test hook: drop one centre entry
-      }
-      word |= v << (8 * b);
-    }
-    *reinterpret_cast<uint32_t*>(smem + kSmemA1 + (k0 / 32) * 4096 + sw32_offset(m, k0 % 32)) =
-        word;
-  }
   // pass-2 B tiles [64 n][32 k]: n = D2 column j (output row rho = out_row_of_col(j)),
   //   t = 0..2  band, K chunk c = window rows 32c .. 32c+31 (centre at 16 + rho)
   //   t = 3..4  centre, K chunk c of the shifted plane (centre at rho)
@@ -277,11 +291,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&x_full[i], 1);
       mbar_init(&x_empty[i], 1);
     }
-    mbar_init(d1_full, 1);
-    mbar_init(d1_empty, kConvThreads);
-    for (int i = 0; i < kA2Boxes; ++i) {
+    for (int i = 0; i < kSlots; ++i) {
+      mbar_init(&d1_full[i], 1);
       mbar_init(&a2_full[i], kConvThreads);
-      mbar_init(&a2_empty[i], 1);
+      mbar_init(&slot_empty[i], 1);
     }
     for (int i = 0; i < kSubs; ++i) {
       mbar_init(&d2_full[i], 1);
@@ -294,6 +307,41 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  // pass-1 A1 [128 x][192 k] resident in TMEM (the A operand of a .ts MMA is
+  // cheaper than an SMEM descriptor one, tools/ubench_mma.cu): lane x holds
+  // A1[x][k] = [|k-32-x| <= r] + 128*[k == x+32], four k per column; warps
+  // 2..5 write their lane quarter.
+  if (warp >= 2 && warp < 2 + kConvWarps) {
+    const int m = 32 * static_cast<int>(warp & 3) + static_cast<int>(lane);
+    uint32_t a1[kKChunks * 8];
+#pragma unroll
+    for (int c = 0; c < kKChunks * 8; ++c) {
+      uint32_t word = 0;
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {
+        const int d = 4 * c + b - 32 - m;
+        uint32_t v = (d >= -r && d <= r) ? 1u : 0u;
+        if (d == 0) {
+          v += 128u;  // state marker
+          if (p.inject_fault && m == 0) v = 128u;  // test hook: drop one centre entry
+        }
+        word |= v << (8 * b);
+      }
+      a1[c] = word;
+    }
+    const uint32_t trow = tmem + ((32u * (warp & 3)) << 16) + kTmemA1;
+#pragma unroll
+    for (int c = 0; c < kKChunks; ++c) {
+      uint32_t v8[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) v8[i] = a1[8 * c + i];
+      tmem_st_32x32b_x8(trow + 8 * c, v8);
+    }
+    tmem_st_wait();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
   // Everything above only touched this CTA's SMEM/TMEM, so it overlapped the
   // previous kernel's tail (PDL).  The grid is read from here on.
   pdl_launch_dependents();
@@ -312,7 +360,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int last_rows = p.rows - kBand * band;  // interior rows of the last band
         for (int k = 0; k < t1 - t0 + 2; ++k, ++g) {
           const uint32_t s = g % kXStages;
-          mbar_wait(&x_empty[s], ((g / kXStages) & 1) ^ 1);
+          LTL_WAIT(0, &x_empty[s], ((g / kXStages) & 1) ^ 1);
           LTL_TRACE(0, g);
           // logical strip t0-1+k: storage strip t0+k, or its periodic image
           int strip = t0 + k;
@@ -347,7 +395,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else if (warp == 1) {
     // ================= pass-1 MMA issuer: one N = 160 block per unit =========
-    const uint64_t a1_desc = smem_desc_sw32_kmajor(smem_u32(smem + kSmemA1));
+    const uint32_t a1 = tmem + kTmemA1;  // K chunk q at column a1 + 8q
     const uint64_t x_desc = smem_desc_sw128_kmajor(smem_u32(smem + kSmemX));
     auto box = [&](uint32_t idx) { return x_desc + (((idx % kXStages) * kBoxBytes) >> 4); };
     uint32_t g = 0, h = 0;
@@ -356,21 +404,21 @@ __global__ void __launch_bounds__(kThreads, 1)
     while (it.next(band, t0, t1)) {
       for (int t = t0; t < t1; ++t, ++h) {
         const uint32_t gl = g + (t - t0), go = gl + 1, gr = gl + 2;
-        mbar_wait(&x_full[gl % kXStages], (gl / kXStages) & 1);
-        mbar_wait(&x_full[go % kXStages], (go / kXStages) & 1);
-        mbar_wait(&x_full[gr % kXStages], (gr / kXStages) & 1);
-        mbar_wait(d1_empty, (h & 1) ^ 1);
+        LTL_WAIT(1, &x_full[gl % kXStages], (gl / kXStages) & 1);
+        LTL_WAIT(1, &x_full[go % kXStages], (go / kXStages) & 1);
+        LTL_WAIT(1, &x_full[gr % kXStages], (gr / kXStages) & 1);
+        const uint32_t sl = h % kSlots;
+        LTL_WAIT(2, &slot_empty[sl], ((h / kSlots) & 1) ^ 1);
         LTL_TRACE(1, h);
         tc_fence_after();
         if (elect_one()) {
-          const uint32_t dcol = tmem + kTmemD1;
-          mma_i8_ss(dcol, a1_desc, box(gl) + (96 >> 4), kIdesc1, 0);
+          const uint32_t dcol = tmem + kTmemSlot + kSlotCols * sl;
+          mma_i8_ts(dcol, a1, box(gl) + (96 >> 4), kIdesc1, 0);
 #pragma unroll
           for (int q = 1; q <= 4; ++q)
-            mma_i8_ss(dcol, a1_desc + ((q * 4096) >> 4), box(go) + ((32 * (q - 1)) >> 4), kIdesc1,
-                      1);
-          mma_i8_ss(dcol, a1_desc + ((5 * 4096) >> 4), box(gr), kIdesc1, 1);
-          mma_commit(d1_full);
+            mma_i8_ts(dcol, a1 + 8 * q, box(go) + ((32 * (q - 1)) >> 4), kIdesc1, 1);
+          mma_i8_ts(dcol, a1 + 40, box(gr), kIdesc1, 1);
+          mma_commit(&d1_full[sl]);
           mma_commit(&x_empty[gl % kXStages]);  // box t-1 is done
           if (t == t1 - 1) {
             mma_commit(&x_empty[go % kXStages]);
@@ -390,17 +438,17 @@ __global__ void __launch_bounds__(kThreads, 1)
     int band, t0, t1;
     while (it.next(band, t0, t1)) {
       for (int t = t0; t < t1; ++t, ++h) {
-        mbar_wait(d1_full, h & 1);
+        const uint32_t sl = h % kSlots;
+        const uint32_t slot_col = trow + kTmemSlot + kSlotCols * sl;
+        LTL_WAIT(3 + (warp & 3), &d1_full[sl], (h / kSlots) & 1);
         if (warp == 2 && lane == 0) LTL_TRACE(2, h);
         tc_fence_after();
         // all 160 box rows, two rows (16-bit lanes) per register
         uint32_t va[32], vb[32], vc[16];
-        tmem_ld_32x32b_x32_pack16(trow + kTmemD1, va);
-        tmem_ld_32x32b_x32_pack16(trow + kTmemD1 + 64, vb);
-        tmem_ld_32x32b_x16_pack16(trow + kTmemD1 + 128, vc);
+        tmem_ld_32x32b_x32_pack16(slot_col, va);
+        tmem_ld_32x32b_x32_pack16(slot_col + 64, vb);
+        tmem_ld_32x32b_x16_pack16(slot_col + 128, vc);
         tmem_ld_wait();
-        tc_fence_before();
-        mbar_arrive(d1_empty);
         auto raw_word = [&](int i) -> uint32_t {  // box rows 4i .. 4i+3 as bytes
           const int k = 2 * i;
           const uint32_t lo = k < 32 ? va[k] : k < 64 ? vb[k - 32] : vc[k - 64];
@@ -408,7 +456,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           return pack_pairs(lo, hi);
         };
         if constexpr (kChecked) {
-          const bool x_ok = t * kStrip + 32 * static_cast<int>(q) + static_cast<int>(lane) < p.cols;
+          const bool x_ok = (t % p.strips) * kStrip + 32 * static_cast<int>(q) +
+                                static_cast<int>(lane) < p.cols;
           const int prow0 = band * kBand;  // padded row of box row 0
 #pragma unroll
           for (int i = 0; i < kBox / 2; ++i) {
@@ -421,12 +470,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
           }
         }
-        const uint32_t hb = h % kA2Boxes;
-        mbar_wait(&a2_empty[hb], ((h / kA2Boxes) & 1) ^ 1);
         if (warp == 2 && lane == 0) LTL_TRACE(3, h);
-        tc_fence_after();
-        const uint32_t pb_col = trow + kTmemPb + kPbCols * hb;
-        const uint32_t pi_col = trow + kTmemPi + kPiCols * hb;
+        // the planes overwrite the D1 columns this thread has just read
+        const uint32_t pb_col = slot_col + kPbOff;
+        const uint32_t pi_col = slot_col + kPiOff;
 #pragma unroll
         for (int c = 0; c < kBox / 32; ++c) {  // 32-row chunk c = words 8c .. 8c+7
           uint32_t pb[8], pi[8];
@@ -444,7 +491,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         tmem_st_wait();
         tc_fence_before();
-        mbar_arrive(&a2_full[hb]);
+        mbar_arrive(&a2_full[sl]);
       }
     }
     if constexpr (kChecked) {
@@ -465,23 +512,23 @@ __global__ void __launch_bounds__(kThreads, 1)
     int band, t0, t1;
     while (it.next(band, t0, t1)) {
       for (int t = t0; t < t1; ++t, ++h) {
-        const uint32_t hb = h % kA2Boxes;
-        mbar_wait(&a2_full[hb], (h / kA2Boxes) & 1);
+        const uint32_t sl = h % kSlots;
+        LTL_WAIT(7, &a2_full[sl], (h / kSlots) & 1);
         for (int s = 0; s < kSubs; ++s) {
-          mbar_wait(&d2_empty[s], (h & 1) ^ 1);
+          LTL_WAIT(8, &d2_empty[s], (h & 1) ^ 1);
           LTL_TRACE(4, 2 * h + s);
           tc_fence_after();
           if (elect_one()) {
             const uint32_t dcol = tmem + kTmemD2 + kSub * s;
-            const uint32_t pb = tmem + kTmemPb + kPbCols * hb + 16 * s;
-            const uint32_t pi = tmem + kTmemPi + kPiCols * hb + 16 * s;
+            const uint32_t pb = tmem + kTmemSlot + kSlotCols * sl + kPbOff + 16 * s;
+            const uint32_t pi = tmem + kTmemSlot + kSlotCols * sl + kPiOff + 16 * s;
             mma_i8_ts(dcol, pb, tile(0), kIdesc2, 0);
             mma_i8_ts(dcol, pb + 8, tile(1), kIdesc2, 1);
             mma_i8_ts(dcol, pb + 16, tile(2), kIdesc2, 1);
             mma_i8_ts(dcol, pi, tile(ti), kIdesc2, 1);
             mma_i8_ts(dcol, pi + 8, tile(ti + 1), kIdesc2, 1);
             mma_commit(&d2_full[s]);
-            if (s == kSubs - 1) mma_commit(&a2_empty[hb]);
+            if (s == kSubs - 1) mma_commit(&slot_empty[sl]);
           }
           __syncwarp();
         }
@@ -525,7 +572,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     int band, t0, t1;
     while (it.next(band, t0, t1)) {
       for (int t = t0; t < t1; ++t, ++h) {
-        mbar_wait(&d2_full[grp], h & 1);
+        LTL_WAIT(9 + (warp - kWarpOut0), &d2_full[grp], h & 1);
         if (lane == 0 && warp == kWarpOut0) LTL_TRACE(5, h);
         if (lane == 0 && warp == kWarpOut0 + 4) LTL_TRACE(7, h);
         tc_fence_after();
@@ -567,7 +614,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const int xl = 16 * hh + static_cast<int>(lane >> 2) + 8 * ((jj >> 1) & 1);
                 const int c = 4 * static_cast<int>(lane & 3) + 2 * (jj & 1) + 16 * (jj >> 2);
                 const int y0 = ybase + 32 * tt;
-                const bool xv = t * kStrip + 32 * static_cast<int>(q) + xl < p.cols;
+                const bool xv = (t % p.strips) * kStrip + 32 * static_cast<int>(q) + xl < p.cols;
                 const bool v0 = xv && y0 + out_row_of_col(c) < p.rows;
                 const bool v1 = xv && y0 + out_row_of_col(c + 1) < p.rows;
                 const uint32_t mask = (v0 ? 0xFFFFu : 0u) | (v1 ? 0xFFFF0000u : 0u);
@@ -592,7 +639,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         // the two tiles leave as two TMA stores issued by lanes 0 and 1 (each
         // lane commits its own bulk group)
         if (lane < 2) {
-          tma_store_3d(&store_map, my_stage + lane * 1024, 32 * q, ybase + 32 * lane, t + 1);
+          tma_store_3d(&store_map, my_stage + lane * 1024, 32 * q, ybase + 32 * lane,
+                       t % p.strips + 1);
           tma_store_commit();
         }
         if (lane == 0 && warp == kWarpOut0) LTL_TRACE(11, h);

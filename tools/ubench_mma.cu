@@ -99,12 +99,50 @@ __global__ void __launch_bounds__(128, 1) kern(Cfg c, long long* out) {
   if (warp == 0) tmem_dealloc(tmem, 512);
 }
 
+__global__ void __launch_bounds__(128, 1) kern_unit(int units, long long* out) {
+  extern __shared__ uint8_t raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(raw) + 1023) & ~uintptr_t(1023));
+  __shared__ uint32_t slot;
+  __shared__ uint64_t bar;
+  const int warp = threadIdx.x / 32;
+  for (int i = threadIdx.x; i < 65536 / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(smem)[i] = 0x01010101u;
+  fence_proxy_async_smem();
+  if (warp == 0) tmem_alloc(&slot, 512);
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    fence_barrier_init();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = slot;
+  if (warp == 1 && elect_one()) {
+    const uint64_t adesc = smem_desc_sw32_kmajor(smem_u32(smem));
+    const uint64_t bdesc = smem_desc_sw128_kmajor(smem_u32(smem + 32768));
+    const long long t0 = clock64();
+    for (int u = 0; u < units; ++u) {
+      for (int q = 0; q < 6; ++q)
+        mma_i8_ss(tmem, adesc + ((4096 * (q % 4)) >> 4), bdesc + ((32 * (q % 4)) >> 4),
+                  idesc_i8_u8u8_s32(128, 160), q > 0);
+      for (int k = 0; k < 10; ++k)
+        mma_i8_ts(tmem + 320 + 64 * (k / 5), tmem + 160 + 8 * (k % 5), bdesc + ((32 * (k % 4)) >> 4),
+                  idesc_i8_u8u8_s32(128, 64), (k % 5) > 0);
+    }
+    mma_commit(&bar);
+    mbar_wait(&bar, 0);
+    out[blockIdx.x] = clock64() - t0;
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc(tmem, 512);
+}
+
 template <int KIND>
 void run_kind(const char* kname, int sms, long long* d) {
   const size_t smem = 96 * 1024;
   cudaFuncSetAttribute(kern<KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   for (int ts : {0, 1})
-    for (int n : {32, 64, 128, 256}) {
+    for (int n : {32, 64, 96, 128, 160, 192, 256}) {
       Cfg c{ts, n, 1, 512};
       kern<KIND><<<sms, 128, smem>>>(c, d);
       cudaError_t e = cudaDeviceSynchronize();
@@ -125,8 +163,17 @@ int main() {
   long long* d;
   cudaMalloc(&d, sms * sizeof(long long));
   run_kind<0>("i8", sms, d);
-  run_kind<1>("f16", sms, d);
-  run_kind<2>("f8f6f4", sms, d);
-  run_kind<3>("tf32", sms, d);
+  {
+    const size_t smem = 96 * 1024;
+    cudaFuncSetAttribute(kern_unit, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const int units = 200;
+    kern_unit<<<sms, 128, smem>>>(units, d);
+    cudaError_t e = cudaDeviceSynchronize();
+    std::vector<long long> h(sms);
+    cudaMemcpy(h.data(), d, sms * sizeof(long long), cudaMemcpyDeviceToHost);
+    std::sort(h.begin(), h.end());
+    std::printf("LTL unit (6 x SS N160 + 10 x TS N64): %.1f cyc/unit  %s\n",
+                static_cast<double>(h[sms / 2]) / units, cudaGetErrorString(e));
+  }
   return 0;
 }
