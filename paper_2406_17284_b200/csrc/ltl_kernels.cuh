@@ -91,7 +91,7 @@ __host__ __device__ inline bool tc_wrap_rows(int32_t rows) {
 constexpr int kTcLoadMaps = 4;
 struct TcLaunch {
   const CUtensorMap* load_maps;  // kTcLoadMaps maps over the source slab, SWIZZLE_128B
-  const CUtensorMap* store_map;  // destination interior rows, {32, 32, 1} boxes, SWIZZLE_32B
+  const CUtensorMap* store_map;  // destination interior rows, {128, 64, 1} boxes, SWIZZLE_128B
   int32_t wrap_cols, wrap_rows;
   int32_t rows, cols;
   RuleConsts rule;

@@ -94,8 +94,10 @@ static_assert(kSubs == 2, "one output group per sub-block");
 constexpr uint32_t kSmemX = 0;                                        // 8 x 20 KB
 constexpr uint32_t kSmemBand = kSmemX + kXStages * kBoxBytes;         // 7 x [64][32]
 constexpr uint32_t kTileBytes = kSub * 32;                            // 2 KB
-constexpr uint32_t kSmemStage = kSmemBand + kNumTiles * kTileBytes;   // 8 warps x 2 x 1 KB
-constexpr uint32_t kSmemBars = kSmemStage + kOutWarps * 2 * 1024;
+constexpr int kStageSlots = 3;                                        // per output group
+constexpr uint32_t kStageBytes = kSub * kStrip;                       // 64 x 128 B = 8 KB
+constexpr uint32_t kSmemStage = kSmemBand + kNumTiles * kTileBytes;   // 2 x 3 x 8 KB
+constexpr uint32_t kSmemBars = kSmemStage + kSubs * kStageSlots * kStageBytes;
 constexpr uint32_t kNumBars = 2 * kXStages + 3 * kSlots + 2 * kSubs;
 constexpr uint32_t kSmemTotal = kSmemBars + kNumBars * 8 + 16;
 constexpr uint32_t kSmemAlloc = kSmemTotal + 1024;  // alignment slack
@@ -553,20 +555,22 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t g_neg = (0x8000u - (K + rc.neg_live)) * 0x10001u;
     const uint32_t r_mask = (K - 1) * 0x10001u;
     uint32_t max_r = 0, bad = 0;
-    // staging: per warp 2 tiles of [32 rows][32 B], SWIZZLE_32B (16-byte
-    // chunk ^= (row >> 2) & 1); this thread addresses row `lane`.  Both tiles
-    // of a unit are staged behind one proxy fence.
-    const uint32_t wslot = warp - kWarpOut0;
-    uint8_t* my_stage = smem + kSmemStage + wslot * 2048;
-    const uint32_t stage_u32 = smem_u32(my_stage);
-    const uint32_t addr_h0 = lane * 32 + ((0u ^ ((lane >> 2) & 1)) << 4);
-    const uint32_t addr_h1 = lane * 32 + ((1u ^ ((lane >> 2) & 1)) << 4);
-    // fill_periodic_halo (src/grid.cpp:75-94) folded into the stores of the
-    // tiles on the torus edge (tile-aligned slabs only, tc_fusable): storage
-    // strip 0 cols 96..127 = logical cols [-32, 0), strip S+1 cols 0..31 =
-    // [cols, cols+32); 16-row halves of a staging tile (the SWIZZLE_32B atom
-    // is 8 rows, so rows 16..31 start at +512 B) go to padded rows
-    // rows+16 .. (images of rows 0..15) and 0 .. 15 (of rows rows-16 ..).
+    // staging: the group's whole 64-row x 128-column sub-block in one
+    // SWIZZLE_128B tile (16-byte chunk c of row y at chunk c ^ (y & 7)), three
+    // slots per group; each warp writes its 32 columns (chunks 2q, 2q+1) with
+    // stmatrix.trans, thread `lane` addressing row 32 tt + lane, and ONE TMA
+    // store per sub-block writes 8 KB of contiguous strip rows.
+    const uint8_t* grp_stage = smem + kSmemStage + grp * kStageSlots * kStageBytes;
+    const uint32_t grp_stage_u32 = smem_u32(grp_stage);
+    const bool issuer = (warp & 3) == 0 && lane == 0;  // one thread per group
+    uint32_t st_off[2][2];  // [tile][16-byte half] byte offset within a slot
+#pragma unroll
+    for (int tt = 0; tt < 2; ++tt)
+#pragma unroll
+      for (int hh = 0; hh < 2; ++hh) {
+        const uint32_t y = 32 * tt + lane, c = 2 * q + hh;
+        st_off[tt][hh] = y * kStrip + ((c ^ (y & 7)) << 4);
+      }
     uint32_t h = 0;
     SegIter it(p);
     int band, t0, t1;
@@ -625,23 +629,22 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
           }
         }
-        // both staging tiles were last read by this warp's stores of the previous unit
-        tma_store_wait_read<0>();
-        __syncwarp();
+        // slot h % 3 was last read by the store of unit h - 3, which the
+        // issuer retired (wait_read<1> after unit h - 2's store) before it
+        // joined the previous unit's group barrier
+        const uint32_t slot = h % kStageSlots;
+        const uint32_t sa = grp_stage_u32 + slot * kStageBytes;
 #pragma unroll
         for (int tt = 0; tt < 2; ++tt) {
-          const uint32_t sa = stage_u32 + tt * 1024;
-          stmatrix_x4_trans_b8(sa + addr_h0, w[tt][0][0], w[tt][0][1], w[tt][0][2], w[tt][0][3]);
-          stmatrix_x4_trans_b8(sa + addr_h1, w[tt][1][0], w[tt][1][1], w[tt][1][2], w[tt][1][3]);
+          stmatrix_x4_trans_b8(sa + st_off[tt][0], w[tt][0][0], w[tt][0][1], w[tt][0][2], w[tt][0][3]);
+          stmatrix_x4_trans_b8(sa + st_off[tt][1], w[tt][1][0], w[tt][1][1], w[tt][1][2], w[tt][1][3]);
         }
         fence_proxy_async_smem();
-        __syncwarp();
-        // the two tiles leave as two TMA stores issued by lanes 0 and 1 (each
-        // lane commits its own bulk group)
-        if (lane < 2) {
-          tma_store_3d(&store_map, my_stage + lane * 1024, 32 * q, ybase + 32 * lane,
-                       t % p.strips + 1);
+        named_barrier(1 + grp, kGroupThreads);
+        if (issuer) {
+          tma_store_3d(&store_map, grp_stage + slot * kStageBytes, 0, ybase, t % p.strips + 1);
           tma_store_commit();
+          tma_store_wait_read<1>();
         }
         if (lane == 0 && warp == kWarpOut0) LTL_TRACE(11, h);
       }

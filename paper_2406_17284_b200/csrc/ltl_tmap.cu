@@ -72,13 +72,14 @@ cudaError_t make_load_maps(CUtensorMap* maps, const SlabView& s) {
   return cudaSuccess;
 }
 
-// Interior rows of every strip: each epilogue warp stores its own 32 x 32
-// tiles, SWIZZLE_32B so the stmatrix rows land conflict-free.
+// Interior rows of every strip: each epilogue group stores one 64-row x
+// 128-column sub-block (8 KB of contiguous strip rows), SWIZZLE_128B so the
+// stmatrix rows land conflict-free.
 cudaError_t make_store_map(CUtensorMap* map, const SlabView& s) {
   if (s.rows <= 0 || s.cols <= 0) return cudaSuccess;
   return encode3(map, s.buf + kHalo * kStrip, static_cast<uint64_t>(s.rows),
-                 static_cast<uint64_t>(s.strips), static_cast<uint64_t>(s.strip_bytes), 32, 32,
-                 CU_TENSOR_MAP_SWIZZLE_32B);
+                 static_cast<uint64_t>(s.strips), static_cast<uint64_t>(s.strip_bytes), kStrip,
+                 64, CU_TENSOR_MAP_SWIZZLE_128B);
 }
 
 }  // namespace ltl

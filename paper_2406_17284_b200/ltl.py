@@ -20,7 +20,8 @@ from dataclasses import dataclass
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libltl_b200.so")
+# LTL_LIB: load another build of the library (A/B timing of kernel variants)
+LIB_PATH = os.environ.get("LTL_LIB", os.path.join(HERE, "libltl_b200.so"))
 
 OK, ERR_INVALID_ARGUMENT, ERR_LOGIC, ERR_RUNTIME, ERR_CUDA = range(5)
 LAYOUT_ROW_MAJOR, LAYOUT_FRAGMENT = 0, 1
