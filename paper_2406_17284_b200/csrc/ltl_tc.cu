@@ -160,42 +160,51 @@ __device__ __forceinline__ long long global_ns() {
 #define LTL_WAIT(site, bar, par) mbar_wait(bar, par)
 #endif
 
-// Static schedule: the bands * strips units in band-major order, CTA b takes
-// the contiguous run [b * U / G, (b + 1) * U / G), cut into segments at band
-// boundaries.  A segment [t0, t1) of band `band` streams boxes t0-1 .. t1
-// (its 16-column side halos included).  CTAs on neighbouring bands walk the
-// same strips at about the same time, so the 32 rows their boxes share are
-// mostly L2 hits.  Every role of the CTA iterates the same segments in the
-// same order.
-//
-// With the column wrap done by the loads (cols % 128 == 0) band k's strips
-// are walked starting at a rotation rot_k = round(k (S - U/G)) mod S, and a
-// run may cross the torus seam (strip t is t mod S).  CTA b + 1 then reaches
-// band k + 1 at the same strip at which CTA b meets band k: the 32 box rows
-// two vertically adjacent units share are read from HBM once and from L2
-// the second time (without it ~20 % of the reads are the overlap again).
+// Static schedule over the bands x strips units.  A CTA walks runs of
+// consecutive strips of one band (a segment [t0, t1) streams boxes t0-1 ..
+// t1, its 16-column side halos included); every role of the CTA iterates the
+// same segments in the same order.  The point of the order is that units of
+// vertically adjacent bands are processed at about the same time by different
+// CTAs, so the 32 box rows they share come from HBM once and from L2 the
+// second time (otherwise ~20 % of all reads are that overlap again):
+//   * full rounds: while at least G bands remain for every CTA, CTA b walks
+//     whole bands b + rG, all CTAs in step (65536^2: three rounds);
+//   * the remaining bands' units are cut into G contiguous runs in band-major
+//     order, and with the column wrap done by the loads (cols % 128 == 0) band
+//     k's strips start at the rotation rot_k = round(k (S - U'/G)) mod S, a run
+//     crossing the torus seam (strip t is t mod S): CTA b + 1 then meets band
+//     k + 1 at the strip where CTA b meets band k.
 struct SegIter {
-  int64_t u, u_end, U;
-  int32_t S, G;
+  int64_t u, u_end, U;  // remainder part: linear unit range of this CTA
+  int32_t S, G, B0, round, rounds;
   bool rotate;
   __device__ explicit SegIter(const Params& p)
-      : U(static_cast<int64_t>(p.bands) * p.strips), S(p.strips), G(gridDim.x),
-        rotate(p.wrap_cols != 0) {
+      : S(p.strips), G(static_cast<int32_t>(gridDim.x)), round(0), rotate(p.wrap_cols != 0) {
+    rounds = p.bands / G;  // whole bands per CTA in step
+    B0 = rounds * G;       // first band of the remainder
+    U = static_cast<int64_t>(p.bands - B0) * S;
     u = U * blockIdx.x / G;
     u_end = U * (blockIdx.x + 1) / G;
   }
   __device__ bool next(int& band, int& t0, int& t1) {
+    if (round < rounds) {
+      band = static_cast<int>(blockIdx.x) + round * G;
+      ++round;
+      t0 = 0;
+      t1 = S;
+      return true;
+    }
     if (u >= u_end) return false;
-    band = static_cast<int>(u / S);
+    const int k = static_cast<int>(u / S);  // band within the remainder
+    band = B0 + k;
     t0 = static_cast<int>(u % S);
-    const int64_t e = min(u_end, static_cast<int64_t>(band + 1) * S);
+    const int64_t e = min(u_end, static_cast<int64_t>(k + 1) * S);
     t1 = t0 + static_cast<int>(e - u);
     u = e;
     if (rotate) {
-      // rot = round(band * (S - U / G)) mod S, in exact integers (S - U/G may
-      // be negative when a CTA covers more than one band)
+      // rot = round(k * (S - U / G)) mod S, in exact integers
       const int64_t SG = static_cast<int64_t>(S) * G;
-      const int64_t num = (static_cast<int64_t>(band) * (((SG - U) % SG + SG) % SG)) % SG;
+      const int64_t num = (static_cast<int64_t>(k) * (((SG - U) % SG + SG) % SG)) % SG;
       const int r = static_cast<int>(((num + G / 2) / G) % S);
       t0 += r;
       t1 += r;
