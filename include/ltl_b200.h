@@ -89,6 +89,9 @@ const char* ltl_last_error(const ltl_ctx* ctx); /* "" after success; never NULL 
 
 /* Geometry queries. */
 int32_t ltl_rows(const ltl_ctx* ctx);
+/* Number of device kernels this context has launched so far (for launch
+ * accounting in benchmarks). */
+int64_t ltl_kernel_launches(const ltl_ctx* ctx);
 int32_t ltl_cols(const ltl_ctx* ctx);
 int32_t ltl_num_slabs(const ltl_ctx* ctx);
 

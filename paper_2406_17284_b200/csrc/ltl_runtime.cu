@@ -62,6 +62,7 @@ struct ltl_ctx {
   int cur = 0;
   bool external_row_halo = false;
   bool halo_stale = false;  // halo cells the tcgen05 step does not need were not refreshed
+  int64_t launches = 0;     // kernels this context has launched (ltl_kernel_launches)
   std::vector<Slab> slabs;
   std::string err;
 };
@@ -224,6 +225,7 @@ void enqueue_halo(ltl_ctx* ctx, int which, bool for_tc = false) {
       if (wrap_rows(ctx)) parts &= ~ltl::kHaloRows;
     }
     ck(ltl::launch_halo_fill(self, above, below, parts, s.stream), "halo kernel");
+    if (parts != 0 && s.rows > 0 && ctx->cols > 0) ++ctx->launches;
     if (i == 0) ctx->halo_stale = parts != all;
   }
 }
@@ -246,6 +248,7 @@ void enqueue_step(ltl_ctx* ctx, const ltl::RuleConsts& rc, uint32_t flags, bool 
       ck(ltl::launch_stencil_step(s.view(cur, ctx->cols), s.view(nxt, ctx->cols), rc, fault,
                                   want_stats ? s.dstats : nullptr, s.stream),
          "stencil kernel");
+      ++ctx->launches;
     } else {
       ltl::TcLaunch a{};
       a.load_maps = s.load_maps[cur];
@@ -269,6 +272,7 @@ void enqueue_step(ltl_ctx* ctx, const ltl::RuleConsts& rc, uint32_t flags, bool 
         a.trace = dtrace;
       }
       ck(ltl::launch_tc_step(a, s.stream), "tcgen05 kernel");
+      if (s.rows > 0 && ctx->cols > 0) ++ctx->launches;
       if (dtrace) {
         std::vector<long long> h(16 * 256);
         ck(cudaStreamSynchronize(s.stream), "trace sync");
@@ -366,6 +370,7 @@ void upload_interior(ltl_ctx* ctx, const uint8_t* interior) {
                        cudaMemcpyHostToDevice, s.stream),
        "upload");
     ck(ltl::launch_to_strips(s.buf[1 - cur], s.view(cur, ctx->cols), s.stream), "to_strips");
+    ++ctx->launches;
     if (ctx->slabs.size() > 1) ck(cudaEventRecord(s.ev_step, s.stream), "event");
   }
   enqueue_halo(ctx, cur);
@@ -379,6 +384,7 @@ void download_interior(ltl_ctx* ctx, uint8_t* interior) {
     if (s.rows == 0 || ctx->cols == 0) continue;
     const size_t n = static_cast<size_t>(s.rows) * ctx->cols;
     ck(ltl::launch_from_strips(s.view(cur, ctx->cols), s.buf[1 - cur], s.stream), "from_strips");
+    ++ctx->launches;
     ck(cudaMemcpyAsync(interior + static_cast<size_t>(s.row0) * ctx->cols, s.buf[1 - cur], n,
                        cudaMemcpyDeviceToHost, s.stream),
        "download");
@@ -446,6 +452,8 @@ void ltl_destroy(ltl_ctx* ctx) {
   destroy_ctx(ctx);
   delete ctx;
 }
+
+int64_t ltl_kernel_launches(const ltl_ctx* ctx) { return ctx ? ctx->launches : -1; }
 
 const char* ltl_last_error(const ltl_ctx* ctx) {
   return ctx ? ctx->err.c_str() : g_last_error.c_str();
@@ -638,6 +646,7 @@ int ltl_init_random(ltl_ctx* ctx, double density, uint64_t seed, int32_t fill_n)
       ck(ltl::launch_init_random(s.view(ctx->cur, ctx->cols), s.row0, fill_rows, fill_cols,
                                  density, seed, s.stream),
          "init kernel");
+      ++ctx->launches;
       if (ctx->slabs.size() > 1) ck(cudaEventRecord(s.ev_step, s.stream), "event");
     }
     enqueue_halo(ctx, ctx->cur);
@@ -676,6 +685,7 @@ int ltl_pack_edges(ltl_ctx* ctx, void* top, void* bot) {
     ck(ltl::launch_pack_edges(s.view(ctx->cur, ctx->cols), static_cast<uint8_t*>(top),
                               static_cast<uint8_t*>(bot), s.stream),
        "pack kernel");
+    ++ctx->launches;
   });
 }
 
@@ -690,6 +700,7 @@ int ltl_unpack_halo(ltl_ctx* ctx, const void* top_halo, const void* bot_halo) {
                                static_cast<const uint8_t*>(top_halo),
                                static_cast<const uint8_t*>(bot_halo), s.stream),
        "unpack kernel");
+    ++ctx->launches;
   });
 }
 

@@ -58,7 +58,7 @@ class ltl_stats_c(ctypes.Structure):
 # Every symbol include/ltl_b200.h declares (tests check the .so exports them all).
 EXPORTS = (
     "ltl_create", "ltl_create_torus", "ltl_destroy", "ltl_last_error", "ltl_rows", "ltl_cols",
-    "ltl_num_slabs", "ltl_upload", "ltl_download", "ltl_upload_interior",
+    "ltl_num_slabs", "ltl_kernel_launches", "ltl_upload", "ltl_download", "ltl_upload_interior",
     "ltl_download_interior", "ltl_run", "ltl_run_async", "ltl_synchronize", "ltl_time",
     "ltl_run_interior", "ltl_create_part", "ltl_set_stream", "ltl_step_part", "ltl_fill_halo",
     "ltl_slab_buffer", "ltl_pack_edges", "ltl_unpack_halo", "ltl_init_random", "ltl_parse_rule", "ltl_format_rule",
@@ -89,6 +89,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
         "ltl_rows": ([vp], ctypes.c_int32),
         "ltl_cols": ([vp], ctypes.c_int32),
         "ltl_num_slabs": ([vp], ctypes.c_int32),
+        "ltl_kernel_launches": ([vp], ctypes.c_int64),
         "ltl_upload": ([vp, u8p, ctypes.c_int32], ctypes.c_int),
         "ltl_download": ([vp, u8p, ctypes.c_int32], ctypes.c_int),
         "ltl_upload_interior": ([vp, u8p], ctypes.c_int),
@@ -339,6 +340,10 @@ class DeviceTorus:
 
     def fill_halo(self) -> None:
         self._check(self.lib.ltl_fill_halo(self._ctx))
+
+    def kernel_launches(self) -> int:
+        """Kernels this context has launched so far (ltl_kernel_launches)."""
+        return int(self.lib.ltl_kernel_launches(self._ctx))
 
     def slab_buffer(self, slab: int = 0, which: int = 0):
         """(device pointer, strip bytes, interior rows) of a generation buffer
