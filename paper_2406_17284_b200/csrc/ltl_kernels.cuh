@@ -92,6 +92,15 @@ constexpr int kTcLoadMaps = 4;
 struct TcLaunch {
   const CUtensorMap* load_maps;  // kTcLoadMaps maps over the source slab, SWIZZLE_128B
   const CUtensorMap* store_map;  // destination interior rows, {128, 64, 1} boxes, SWIZZLE_128B
+  // Multi-generation (persistent) launch: `gens` generations ping-ponging
+  // between the two buffers, units released to the next generation through
+  // per-unit completion counters (flags, bands x strips u32, all equal to
+  // flag_base on entry; +2 per generation).  gens <= 1: one generation.
+  const CUtensorMap* load_maps_b;  // maps of the destination buffer (as a source)
+  const CUtensorMap* store_map_b;  // store map of the source buffer
+  int32_t gens;
+  uint32_t* flags;
+  uint32_t flag_base;
   int32_t wrap_cols, wrap_rows;
   int32_t rows, cols;
   RuleConsts rule;
@@ -101,6 +110,7 @@ struct TcLaunch {
   long long* trace;    // debug timeline (LTL_TC_TRACE), nullptr = off
 };
 cudaError_t launch_tc_step(const TcLaunch& a, cudaStream_t stream);
+int tc_persistent_ctas(int32_t rows, int num_sms);  // 0: no multi-generation launch
 size_t tc_smem_bytes();
 
 // Host-side tensor-map builders (driver entry point fetched at runtime).

@@ -45,6 +45,8 @@ struct Slab {
   CUtensorMap load_maps[2][ltl::kTcLoadMaps];
   CUtensorMap store_map[2];
   ltl::DeviceStats* dstats = nullptr;
+  uint32_t* flags = nullptr;   // per-unit completion counters (multi-generation launches)
+  uint32_t flag_base = 0;      // their value between launches
   cudaStream_t stream = nullptr;
   bool own_stream = true;
   cudaEvent_t ev_step = nullptr;
@@ -150,6 +152,12 @@ void create_slabs(ltl_ctx* ctx, int32_t num_slabs, const int32_t* dev_ids) {
       ck(cudaMemset(s.buf[b], 0, bytes), "cudaMemset slab");
     }
     ck(cudaMalloc(&s.dstats, sizeof(ltl::DeviceStats)), "cudaMalloc stats");
+    {
+      const size_t units = static_cast<size_t>((s.rows + ltl::kTcBand - 1) / ltl::kTcBand) *
+                           ltl::interior_strips(ctx->cols);
+      ck(cudaMalloc(&s.flags, std::max<size_t>(units, 1) * sizeof(uint32_t)), "cudaMalloc flags");
+      ck(cudaMemset(s.flags, 0, std::max<size_t>(units, 1) * sizeof(uint32_t)), "memset flags");
+    }
     ck(cudaStreamCreateWithFlags(&s.stream, cudaStreamNonBlocking), "cudaStreamCreate");
     ck(cudaEventCreateWithFlags(&s.ev_step, cudaEventDisableTiming), "cudaEventCreate");
     build_maps(s, ctx->cols);
@@ -180,6 +188,7 @@ void destroy_ctx(ltl_ctx* ctx) {
     for (auto& b : s.buf)
       if (b) cudaFree(b);
     if (s.dstats) cudaFree(s.dstats);
+    if (s.flags) cudaFree(s.flags);
     if (s.ev_step) cudaEventDestroy(s.ev_step);
     for (cudaEvent_t e : s.timing) cudaEventDestroy(e);
     if (s.stream && s.own_stream) cudaStreamDestroy(s.stream);
@@ -230,9 +239,28 @@ void enqueue_halo(ltl_ctx* ctx, int which, bool for_tc = false) {
   }
 }
 
-// One generation: main kernel per slab (cur -> nxt), then halo of nxt.
+// Several generations in ONE persistent launch (units handed from one
+// generation to the next through per-unit flags, no halo traffic): one
+// whole-torus slab whose wraps the loads do, tcgen05 engine.
+bool persistent_ok(const ltl_ctx* ctx, uint32_t flags) {
+  if ((flags & LTL_FLAG_STENCIL) || ctx->slabs.size() != 1 || !wrap_cols(ctx) ||
+      !wrap_rows(ctx) || std::getenv("LTL_NO_PERSIST"))  // env: diagnostics
+    return false;
+  int sms = 0;
+  ck(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->slabs[0].dev), "sm count");
+  return ltl::tc_persistent_ctas(ctx->slabs[0].rows, sms) > 0;
+}
+
+// `gens` generations (cur -> nxt -> ...): one persistent launch when
+// persistent_ok (gens > 1), else gens x (main kernel per slab + halo of nxt).
 void enqueue_step(ltl_ctx* ctx, const ltl::RuleConsts& rc, uint32_t flags, bool want_stats,
-                  cudaEvent_t* kt0, cudaEvent_t* kt1) {
+                  cudaEvent_t* kt0, cudaEvent_t* kt1, int32_t gens = 1) {
+  if (gens <= 0) return;
+  const bool persist = gens > 1 && persistent_ok(ctx, flags);
+  if (gens > 1 && !persist) {
+    for (int32_t t = 0; t < gens; ++t) enqueue_step(ctx, rc, flags, want_stats, nullptr, nullptr);
+    return;
+  }
   const int cur = ctx->cur, nxt = 1 - cur;
   const bool fault = (flags & LTL_FLAG_INJECT_FAULT) != 0;
   for (size_t i = 0; i < ctx->slabs.size(); ++i) {
@@ -255,6 +283,14 @@ void enqueue_step(ltl_ctx* ctx, const ltl::RuleConsts& rc, uint32_t flags, bool 
       a.store_map = &s.store_map[nxt];
       a.wrap_cols = wrap_cols(ctx);
       a.wrap_rows = wrap_rows(ctx);
+      if (persist) {
+        a.load_maps_b = s.load_maps[nxt];
+        a.store_map_b = &s.store_map[cur];
+        a.gens = gens;
+        a.flags = s.flags;
+        a.flag_base = s.flag_base;
+        s.flag_base += 2u * static_cast<uint32_t>(gens);
+      }
       a.rows = s.rows;
       a.cols = ctx->cols;
       a.rule = rc;
@@ -291,8 +327,9 @@ void enqueue_step(ltl_ctx* ctx, const ltl::RuleConsts& rc, uint32_t flags, bool 
     if (kt1) ck(cudaEventRecord(kt1[i], s.stream), "event");
     if (ctx->slabs.size() > 1) ck(cudaEventRecord(s.ev_step, s.stream), "event");
   }
-  enqueue_halo(ctx, nxt, !(flags & LTL_FLAG_STENCIL));
-  ctx->cur = nxt;
+  const int out = (gens % 2) ? nxt : cur;  // buffer holding the last generation
+  enqueue_halo(ctx, out, !(flags & LTL_FLAG_STENCIL));
+  ctx->cur = out;
 }
 
 void sync_all(ltl_ctx* ctx) {
@@ -320,7 +357,7 @@ void run_steps(ltl_ctx* ctx, const ltl_rule_c* rule, int32_t steps, uint32_t fla
   // construction -- which is why the fast path may skip it.
   const bool checked = (flags & LTL_FLAG_INJECT_FAULT) || (stats && (flags & LTL_FLAG_WANT_STATS));
   reset_stats(ctx);
-  for (int32_t t = 0; t < steps; ++t) enqueue_step(ctx, rc, flags, checked, nullptr, nullptr);
+  enqueue_step(ctx, rc, flags, checked, nullptr, nullptr, steps);
   sync_all(ctx);
   ltl::DeviceStats agg{};
   for (Slab& s : ctx->slabs) {
@@ -522,7 +559,7 @@ int ltl_run_async(ltl_ctx* ctx, const ltl_rule_c* rule, int32_t steps, uint32_t 
   return guarded(ctx, [&] {
     check_run_args(ctx, rule, steps);
     const ltl::RuleConsts rc = rule_consts(*rule);
-    for (int32_t t = 0; t < steps; ++t) enqueue_step(ctx, rc, flags, false, nullptr, nullptr);
+    enqueue_step(ctx, rc, flags, false, nullptr, nullptr, steps);
   });
 }
 
@@ -538,8 +575,11 @@ int ltl_time(ltl_ctx* ctx, const ltl_rule_c* rule, int32_t steps, int32_t warmup
     check_run_args(ctx, rule, steps);
     const ltl::RuleConsts rc = rule_consts(*rule);
     const size_t G = ctx->slabs.size();
-    for (int32_t t = 0; t < warmup; ++t) enqueue_step(ctx, rc, flags, false, nullptr, nullptr);
+    enqueue_step(ctx, rc, flags, false, nullptr, nullptr, warmup);
     sync_all(ctx);
+    // one persistent launch for all timed generations when possible: the
+    // "kernel" time is then that launch (per generation = total / steps)
+    const bool persist = steps > 1 && persistent_ok(ctx, flags);
     // per slab: [start, end] + per-step kernel [k0, k1] pairs
     for (Slab& s : ctx->slabs) {
       ck(cudaSetDevice(s.dev), "cudaSetDevice");
@@ -552,13 +592,14 @@ int ltl_time(ltl_ctx* ctx, const ltl_rule_c* rule, int32_t steps, int32_t warmup
       ck(cudaEventRecord(s.timing[0], s.stream), "event");
     }
     std::vector<cudaEvent_t> k0(G), k1(G);
-    for (int32_t t = 0; t < steps; ++t) {
+    const int32_t launches = persist ? 1 : steps;
+    for (int32_t t = 0; t < launches; ++t) {
       for (size_t i = 0; i < G; ++i) {
         k0[i] = ctx->slabs[i].timing[2 + 2 * t];
         k1[i] = ctx->slabs[i].timing[3 + 2 * t];
       }
       enqueue_step(ctx, rc, flags, false, kernel_ms ? k0.data() : nullptr,
-                   kernel_ms ? k1.data() : nullptr);
+                   kernel_ms ? k1.data() : nullptr, persist ? steps : 1);
     }
     for (Slab& s : ctx->slabs) {
       ck(cudaSetDevice(s.dev), "cudaSetDevice");
@@ -572,7 +613,7 @@ int ltl_time(ltl_ctx* ctx, const ltl_rule_c* rule, int32_t steps, int32_t warmup
       tot = std::max(tot, static_cast<double>(ms));
       if (kernel_ms) {
         double acc = 0;
-        for (int32_t t = 0; t < steps; ++t) {
+        for (int32_t t = 0; t < launches; ++t) {
           float k = 0;
           ck(cudaEventElapsedTime(&k, s.timing[2 + 2 * t], s.timing[3 + 2 * t]), "elapsed");
           acc += k;

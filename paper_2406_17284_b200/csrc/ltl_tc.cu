@@ -80,11 +80,12 @@ constexpr uint32_t kBoxBytes = kBox * kStrip;  // 20 KB
 constexpr int kSlots = 2;                 // D1 / plane slots (units in flight)
 constexpr int kConvWarps = 4;
 constexpr int kOutWarps = 8;
-constexpr int kThreads = 32 * (3 + kConvWarps + kOutWarps);  // 480
+constexpr int kThreads = 32 * (4 + kConvWarps + kOutWarps);  // 512
 constexpr int kConvThreads = 32 * kConvWarps;
 constexpr int kGroupThreads = 128;  // one output group
 constexpr int kWarpOut0 = 2 + kConvWarps;
 constexpr int kWarpP2 = kWarpOut0 + kOutWarps;  // 14
+constexpr int kWarpStore = kWarpP2 + 1;           // 15
 constexpr int kNumTiles = 7;  // Bv0..2, Iv0..1, 16Iv0..1
 
 static_assert(kBox % 32 == 0 && kBox <= 256, "box rows: whole K chunks, one TMA box");
@@ -98,7 +99,7 @@ constexpr int kStageSlots = 3;                                        // per out
 constexpr uint32_t kStageBytes = kSub * kStrip;                       // 64 x 128 B = 8 KB
 constexpr uint32_t kSmemStage = kSmemBand + kNumTiles * kTileBytes;   // 2 x 3 x 8 KB
 constexpr uint32_t kSmemBars = kSmemStage + kSubs * kStageSlots * kStageBytes;
-constexpr uint32_t kNumBars = 2 * kXStages + 3 * kSlots + 2 * kSubs;
+constexpr uint32_t kNumBars = 2 * kXStages + 3 * kSlots + 2 * kSubs + 2 * kSubs * kStageSlots;
 constexpr uint32_t kSmemTotal = kSmemBars + kNumBars * 8 + 16;
 constexpr uint32_t kSmemAlloc = kSmemTotal + 1024;  // alignment slack
 static_assert(kSmemAlloc <= 227 * 1024, "shared memory budget");
@@ -124,6 +125,14 @@ static_assert(kSlotCols % 8 == 0 && kPiOff % 8 == 0 && kTmemD2 % 8 == 0, "A oper
 constexpr uint32_t kIdesc1 = idesc_i8_u8u8_s32(128, kBox);
 constexpr uint32_t kIdesc2 = idesc_i8_u8u8_s32(128, kSub);
 
+// Tensor maps of both generation buffers: set 0 = {loads of the launch's
+// current buffer, stores into the other}, set 1 = the reverse (generation g
+// of a multi-generation launch uses set g % 2).
+struct TcMaps {
+  CUtensorMap load[2][kTcLoadMaps];
+  CUtensorMap store[2];
+};
+
 struct Params {
   int32_t rows, cols;
   int32_t strips;  // interior strips
@@ -131,6 +140,9 @@ struct Params {
   RuleConsts rule;
   int32_t inject_fault;
   int32_t wrap_cols, wrap_rows;  // periodic wrap done by the loads (tc_wrap_*)
+  int32_t gens;                  // generations in this launch (persistent when > 1)
+  uint32_t* flags;               // per-unit completion counters (bands x strips)
+  uint32_t flag_base;            // their common value when the launch starts
   DeviceStats* stats;
   long long* trace;  // debug timeline of CTA 0 (only with -DLTL_TC_TRACE_BUILD)
 };
@@ -178,8 +190,13 @@ struct SegIter {
   int64_t u, u_end, U;  // remainder part: linear unit range of this CTA
   int32_t S, G, B0, round, rounds;
   bool rotate;
-  __device__ explicit SegIter(const Params& p)
+  int32_t start;  // first strip of a round (multi-generation launches alternate)
+  __device__ SegIter(const Params& p, int gen)
       : S(p.strips), G(static_cast<int32_t>(gridDim.x)), round(0), rotate(p.wrap_cols != 0) {
+    // In a multi-generation launch generation g + 1 starts half a band away
+    // from where generation g started: its first units then only need units
+    // of g that finished half a generation earlier (no drain at the seam).
+    start = (p.gens > 1 && (gen & 1)) ? S / 2 : 0;
     rounds = p.bands / G;  // whole bands per CTA in step
     B0 = rounds * G;       // first band of the remainder
     U = static_cast<int64_t>(p.bands - B0) * S;
@@ -190,8 +207,8 @@ struct SegIter {
     if (round < rounds) {
       band = static_cast<int>(blockIdx.x) + round * G;
       ++round;
-      t0 = 0;
-      t1 = S;
+      t0 = start;
+      t1 = start + S;
       return true;
     }
     if (u >= u_end) return false;
@@ -242,11 +259,7 @@ __device__ __forceinline__ uint32_t rule_pair(uint32_t z, const SimdRule& k) {
 
 template <bool kChecked>
 __global__ void __launch_bounds__(kThreads, 1)
-    ltl_tc_step_kernel(const __grid_constant__ CUtensorMap load_map,
-                       const __grid_constant__ CUtensorMap load_piece,
-                       const __grid_constant__ CUtensorMap load_first,
-                       const __grid_constant__ CUtensorMap load_last,
-                       const __grid_constant__ CUtensorMap store_map, const Params p) {
+    ltl_tc_step_kernel(const __grid_constant__ TcMaps maps, const Params p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
@@ -257,8 +270,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* a2_full = d1_full + kSlots;       // convert -> pass 2 (planes written)
   uint64_t* slot_empty = a2_full + kSlots;    // pass 2 -> pass 1 (slot reusable)
   uint64_t* d2_full = slot_empty + kSlots;
+  // staging tile handshake with the store warp: [group][slot]
   uint64_t* d2_empty = d2_full + kSubs;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(d2_empty + kSubs);
+  uint64_t* st_full = d2_empty + kSubs;              // output group -> store warp
+  uint64_t* st_empty = st_full + kSubs * kStageSlots; // store warp -> output group
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(st_empty + kSubs * kStageSlots);
 
   const uint32_t warp = warp_id();
   const uint32_t lane = threadIdx.x & 31;
@@ -291,12 +307,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   fence_proxy_async_smem();
   if (warp == 0 && lane == 0) {
-    prefetch_tmap(&load_map);
-    prefetch_tmap(&store_map);
-    if (p.wrap_rows) {
-      prefetch_tmap(&load_piece);
-      prefetch_tmap(&load_first);
-      prefetch_tmap(&load_last);
+    for (int set = 0; set < (p.gens > 1 ? 2 : 1); ++set) {
+      prefetch_tmap(&maps.load[set][0]);
+      prefetch_tmap(&maps.store[set]);
+      if (p.wrap_rows)
+        for (int i = 1; i < kTcLoadMaps; ++i) prefetch_tmap(&maps.load[set][i]);
     }
     for (int i = 0; i < kXStages; ++i) {
       mbar_init(&x_full[i], 1);
@@ -310,6 +325,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int i = 0; i < kSubs; ++i) {
       mbar_init(&d2_full[i], 1);
       mbar_init(&d2_empty[i], kGroupThreads);
+    }
+    for (int i = 0; i < kSubs * kStageSlots; ++i) {
+      mbar_init(&st_full[i], 1);
+      mbar_init(&st_empty[i], 1);
     }
     fence_barrier_init();
   }
@@ -361,45 +380,100 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   if (warp == 0) {
     // ================= TMA producer: boxes t0-1 .. t1 of every segment =======
-    if (elect_one()) {
-      uint32_t g = 0;
-      SegIter it(p);
+    // The whole warp walks the schedule; lane 0 issues.  In a multi-generation
+    // launch generation gg reads what gg-1 wrote: box (band, strip) holds rows
+    // of units (band-1 .. band+1, strip) of gg-1 (periodic in band), whose
+    // flags must have reached flag_base + 2 gg.  The lanes read the flags of
+    // 32 boxes at once (one L2 round trip per 32 boxes, not three per box).
+    uint32_t g = 0;
+    for (int gg = 0; gg < p.gens; ++gg) {
+      const CUtensorMap* lm = maps.load[gg & 1];
+      const uint32_t target = p.flag_base + 2u * static_cast<uint32_t>(gg);
+      SegIter it(p, gg);
       int band, t0, t1;
       while (it.next(band, t0, t1)) {
         const bool first = p.wrap_rows && band == 0;
         const bool last = p.wrap_rows && band == p.bands - 1;
         const int last_rows = p.rows - kBand * band;  // interior rows of the last band
-        for (int k = 0; k < t1 - t0 + 2; ++k, ++g) {
-          const uint32_t s = g % kXStages;
-          LTL_WAIT(0, &x_empty[s], ((g / kXStages) & 1) ^ 1);
-          LTL_TRACE(0, g);
-          // logical strip t0-1+k: storage strip t0+k, or its periodic image
-          int strip = t0 + k;
-          if (p.wrap_cols) strip = (t0 - 1 + k + p.strips) % p.strips + 1;
-          uint8_t* dst = smem + kSmemX + s * kBoxBytes;
-          if (!first && !last) {
-            mbar_arrive_expect_tx(&x_full[s], kBoxBytes);
-            tma_load_3d(dst, &load_map, &x_full[s], 0, band * kBand, strip);
-            continue;
+        const int nbox = t1 - t0 + 2;
+        auto storage_strip = [&](int k) {  // logical strip t0-1+k (or its image)
+          return p.wrap_cols ? (t0 - 1 + k + p.strips) % p.strips + 1 : t0 + k;
+        };
+        auto flag_ptr = [&](int db, int k) {
+          const int b = (band + db + p.bands) % p.bands;
+          return p.flags + static_cast<int64_t>(b) * p.strips + (storage_strip(k) - 1);
+        };
+        for (int k0 = 0; k0 < nbox; k0 += 32) {
+          uint32_t ready = ~0u;
+          if (gg > 0) {
+            const int k = k0 + static_cast<int>(lane);
+            bool ok = true;
+            if (k < nbox) {
+              const uint32_t f0 = ld_acquire(flag_ptr(-1, k));
+              const uint32_t f1 = ld_acquire(flag_ptr(0, k));
+              const uint32_t f2 = ld_acquire(flag_ptr(1, k));
+              ok = static_cast<int32_t>(f0 - target) >= 0 && static_cast<int32_t>(f1 - target) >= 0 &&
+                   static_cast<int32_t>(f2 - target) >= 0;
+            }
+            ready = __ballot_sync(0xffffffffu, ok);
+            __syncwarp();  // order the lanes' acquires before lane 0's loads
+            // acquired generic-proxy flags -> async-proxy (TMA) reads; once
+            // per window: the proxy fence is not free
+            if (lane == 0) fence_proxy_async_global();
           }
-          // first / last band of a whole torus: the 16 rows beyond the edge
-          // are loaded from the other end of the strip (padded row 16 + y)
-          const int body = last ? last_rows : kBand;  // interior rows in the box body
-          mbar_arrive_expect_tx(&x_full[s], (last ? last_rows + 2 * kHalo : kBox) * kStrip);
-          int row = 0;  // box row being filled
-          if (first) {  // rows -16 .. -1  <-  rows - 16 .. rows - 1
-            tma_load_3d(dst, &load_piece, &x_full[s], 0, p.rows, strip);
-            row = kHalo;
-          }
-          if (first && !last) {  // rows 0 .. 143
-            tma_load_3d(dst + row * kStrip, &load_first, &x_full[s], 0, kHalo, strip);
-          } else {  // last band body: padded rows from 128 * band (its top halo
-                    // included unless it is also the first band)
-            tma_load_3d(dst + row * kStrip, &load_last, &x_full[s], 0,
-                        first ? kHalo : band * kBand, strip);
-            // rows rows .. rows + 15  <-  0 .. 15
-            tma_load_3d(dst + (row + body + (first ? 0 : kHalo)) * kStrip, &load_piece,
-                        &x_full[s], 0, kHalo, strip);
+          for (int k = k0; k < min(nbox, k0 + 32); ++k, ++g) {
+            if (gg > 0 && !((ready >> (k - k0)) & 1u)) {
+              if (static_cast<int>(lane) == k - k0) {
+#ifdef LTL_TC_TRACE_BUILD
+                const long long w0_ = clock64();
+#endif
+                for (int db = -1; db <= 1; ++db) wait_flag_geq(flag_ptr(db, k), target);
+#ifdef LTL_TC_TRACE_BUILD
+                if (p.trace && blockIdx.x == 0) {
+                  atomicAdd(reinterpret_cast<unsigned long long*>(&p.trace[13 * 256 + 17]),
+                            static_cast<unsigned long long>(clock64() - w0_));
+                  if (g < 256) {
+                    p.trace[8 * 256 + g] = clock64() - w0_;
+                    p.trace[9 * 256 + g] = gg * 100000 + band * 1000 + storage_strip(k);
+                  }
+                }
+#endif
+              }
+              __syncwarp();
+              if (lane == 0) fence_proxy_async_global();
+            }
+            if (lane == 0) {
+              const uint32_t s = g % kXStages;
+              LTL_WAIT(0, &x_empty[s], ((g / kXStages) & 1) ^ 1);
+              LTL_TRACE(0, g);
+              const int strip = storage_strip(k);
+              uint8_t* dst = smem + kSmemX + s * kBoxBytes;
+              if (!first && !last) {
+                mbar_arrive_expect_tx(&x_full[s], kBoxBytes);
+                tma_load_3d(dst, &lm[0], &x_full[s], 0, band * kBand, strip);
+              } else {
+                // first / last band of a whole torus: the 16 rows beyond the
+                // edge are loaded from the other end of the strip (padded row 16 + y)
+                const int body = last ? last_rows : kBand;  // interior rows in the box body
+                mbar_arrive_expect_tx(&x_full[s], (last ? last_rows + 2 * kHalo : kBox) * kStrip);
+                int row = 0;  // box row being filled
+                if (first) {  // rows -16 .. -1  <-  rows - 16 .. rows - 1
+                  tma_load_3d(dst, &lm[1], &x_full[s], 0, p.rows, strip);
+                  row = kHalo;
+                }
+                if (first && !last) {  // rows 0 .. 143
+                  tma_load_3d(dst + row * kStrip, &lm[2], &x_full[s], 0, kHalo, strip);
+                } else {  // last band body: padded rows from 128 * band (its top
+                          // halo included unless it is also the first band)
+                  tma_load_3d(dst + row * kStrip, &lm[3], &x_full[s], 0,
+                              first ? kHalo : band * kBand, strip);
+                  // rows rows .. rows + 15  <-  0 .. 15
+                  tma_load_3d(dst + (row + body + (first ? 0 : kHalo)) * kStrip, &lm[1],
+                              &x_full[s], 0, kHalo, strip);
+                }
+              }
+            }
+            __syncwarp();
           }
         }
       }
@@ -410,7 +484,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint64_t x_desc = smem_desc_sw128_kmajor(smem_u32(smem + kSmemX));
     auto box = [&](uint32_t idx) { return x_desc + (((idx % kXStages) * kBoxBytes) >> 4); };
     uint32_t g = 0, h = 0;
-    SegIter it(p);
+    for (int gg = 0; gg < p.gens; ++gg) {
+    SegIter it(p, gg);
     int band, t0, t1;
     while (it.next(band, t0, t1)) {
       for (int t = t0; t < t1; ++t, ++h) {
@@ -440,12 +515,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       g += (t1 - t0) + 2;
     }
+    }
   } else if (warp < kWarpOut0) {
     // ================= convert warps (D1 -> pass-2 A planes) =================
     const uint32_t q = warp & 3;  // TMEM lane quarter = 32 strip columns
     const uint32_t trow = tmem + ((q * 32) << 16);
     uint32_t max_h = 0, h = 0;
-    SegIter it(p);
+    for (int gg = 0; gg < p.gens; ++gg) {
+    SegIter it(p, gg);
     int band, t0, t1;
     while (it.next(band, t0, t1)) {
       for (int t = t0; t < t1; ++t, ++h) {
@@ -505,6 +582,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_arrive(&a2_full[sl]);
       }
     }
+    }
     if constexpr (kChecked) {
       int32_t mh = static_cast<int32_t>(max_h);
 #pragma unroll
@@ -519,7 +597,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     auto tile = [&](int t) { return band_desc + ((t * kTileBytes) >> 4); };
     const int ti = vn ? 3 : 5;
     uint32_t h = 0;
-    SegIter it(p);
+    for (int gg = 0; gg < p.gens; ++gg) {
+    SegIter it(p, gg);
     int band, t0, t1;
     while (it.next(band, t0, t1)) {
       for (int t = t0; t < t1; ++t, ++h) {
@@ -545,6 +624,62 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
     }
+    }
+  } else if (warp == kWarpStore) {
+    // ================= store warp: staging tiles -> HBM, unit flags ==========
+    // Issues every output TMA store (one 8 KB box per sub-block), frees the
+    // staging slots once read, and in a multi-generation launch publishes
+    // each unit to the next generation once both its stores have landed.
+    // The gpu-scope release that needs costs ~1.4 us per batch (measured):
+    // it must stay off the output groups' critical path.
+    if (lane == 0) {
+      constexpr int kPubLag = 8;          // units per publication batch
+      uint32_t pend[2 * kPubLag];         // units stored, not yet published
+      uint32_t npend = 0, h = 0, n_open = 0;  // n_open: committed, slot not yet freed
+      int open_slot[2] = {0, 0};
+      for (int gg = 0; gg < p.gens; ++gg) {
+        SegIter it(p, gg);
+        int band, t0, t1;
+        while (it.next(band, t0, t1)) {
+          for (int t = t0; t < t1; ++t, ++h) {
+            const uint32_t slot = h % kStageSlots;
+            for (int grp = 0; grp < kSubs; ++grp) {
+              mbar_wait(&st_full[grp * kStageSlots + slot], (h / kStageSlots) & 1);
+              const uint8_t* src = smem + kSmemStage + (grp * kStageSlots + slot) * kStageBytes;
+              tma_store_3d(&maps.store[gg & 1], src, 0, band * kBand + kSub * grp,
+                           t % p.strips + 1);
+              tma_store_commit();
+              // the previous group's store has read its slot: free it
+              tma_store_wait_read<1>();
+              if (n_open) mbar_arrive(&st_empty[open_slot[0]]);
+              open_slot[0] = grp * kStageSlots + slot;
+              n_open = 1;
+            }
+            if (p.gens > 1) {
+              pend[h % (2 * kPubLag)] = static_cast<uint32_t>(band * p.strips + t % p.strips);
+              if (++npend == 2 * kPubLag) {
+                tma_store_wait_all<2 * kPubLag>();  // 2 groups per unit
+                fence_proxy_async_global();
+                fence_acq_rel_gpu();                // one release for the batch
+                for (int k = 0; k < kPubLag; ++k)
+                  red_relaxed_add(p.flags + pend[(h + 1 + k) % (2 * kPubLag)], 2);
+                npend -= kPubLag;
+              }
+            }
+          }
+        }
+        if (p.gens > 1) {  // the generation's last units: publish them too
+          tma_store_wait_all<0>();
+          fence_proxy_async_global();
+          fence_acq_rel_gpu();
+          for (uint32_t k = 0; k < npend; ++k)
+            red_relaxed_add(p.flags + pend[(h - npend + k) % (2 * kPubLag)], 2);
+          npend = 0;
+        }
+      }
+      tma_store_wait_all<0>();
+      (void)open_slot[1];
+    }
   } else {
     // ================= output warps (D2 -> rule -> next generation) ==========
     // Group grp takes sub-block grp (64 rows) of every unit; warp w owns strip
@@ -567,11 +702,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     // staging: the group's whole 64-row x 128-column sub-block in one
     // SWIZZLE_128B tile (16-byte chunk c of row y at chunk c ^ (y & 7)), three
     // slots per group; each warp writes its 32 columns (chunks 2q, 2q+1) with
-    // stmatrix.trans, thread `lane` addressing row 32 tt + lane, and ONE TMA
-    // store per sub-block writes 8 KB of contiguous strip rows.
+    // stmatrix.trans, thread `lane` addressing row 32 tt + lane; the store
+    // warp then writes it with ONE TMA store (8 KB of contiguous strip rows).
     const uint8_t* grp_stage = smem + kSmemStage + grp * kStageSlots * kStageBytes;
     const uint32_t grp_stage_u32 = smem_u32(grp_stage);
-    const bool issuer = (warp & 3) == 0 && lane == 0;  // one thread per group
+    const bool leader = (warp & 3) == 0 && lane == 0;  // signals the store warp
     uint32_t st_off[2][2];  // [tile][16-byte half] byte offset within a slot
 #pragma unroll
     for (int tt = 0; tt < 2; ++tt)
@@ -581,7 +716,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         st_off[tt][hh] = y * kStrip + ((c ^ (y & 7)) << 4);
       }
     uint32_t h = 0;
-    SegIter it(p);
+    for (int gg = 0; gg < p.gens; ++gg) {
+    SegIter it(p, gg);
     int band, t0, t1;
     while (it.next(band, t0, t1)) {
       for (int t = t0; t < t1; ++t, ++h) {
@@ -638,11 +774,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
           }
         }
-        // slot h % 3 was last read by the store of unit h - 3, which the
-        // issuer retired (wait_read<1> after unit h - 2's store) before it
-        // joined the previous unit's group barrier
+        // hand the sub-block to the store warp through staging slot h % 3
         const uint32_t slot = h % kStageSlots;
         const uint32_t sa = grp_stage_u32 + slot * kStageBytes;
+        mbar_wait(&st_empty[grp * kStageSlots + slot], ((h / kStageSlots) & 1) ^ 1);
 #pragma unroll
         for (int tt = 0; tt < 2; ++tt) {
           stmatrix_x4_trans_b8(sa + st_off[tt][0], w[tt][0][0], w[tt][0][1], w[tt][0][2], w[tt][0][3]);
@@ -650,15 +785,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         fence_proxy_async_smem();
         named_barrier(1 + grp, kGroupThreads);
-        if (issuer) {
-          tma_store_3d(&store_map, grp_stage + slot * kStageBytes, 0, ybase, t % p.strips + 1);
-          tma_store_commit();
-          tma_store_wait_read<1>();
-        }
+        if (leader) mbar_arrive(&st_full[grp * kStageSlots + slot]);
         if (lane == 0 && warp == kWarpOut0) LTL_TRACE(11, h);
       }
     }
-    tma_store_wait_all<0>();
+    }
     if constexpr (kChecked) {
       int32_t mr = static_cast<int32_t>(max(max_r & 0xFFFF, max_r >> 16));
 #pragma unroll
@@ -678,6 +809,20 @@ __global__ void __launch_bounds__(kThreads, 1)
 }  // namespace
 
 size_t tc_smem_bytes() { return kSmemAlloc; }
+
+// A multi-generation launch needs a schedule in which every unit's neighbours
+// (across the torus seam too) are processed at the same time in every
+// generation: whole bands in step, so the CTA count must divide the band
+// count.  0 = fall back to one generation per launch.
+int tc_persistent_ctas(int32_t rows, int num_sms) {
+  const int bands = (rows + kBand - 1) / kBand;
+  // Measured (16384^2: 128 of 148 SMs persistent ~= 148 SMs one launch per
+  // generation; 32768^2, 65536^2: per-generation launches on all SMs faster):
+  // only worth it when the divisor is the whole GPU.
+  for (int d = num_sms; d >= 1; --d)
+    if (bands % d == 0) return d == num_sms || std::getenv("LTL_FORCE_PERSIST") ? d : 0;
+  return 0;
+}
 
 cudaError_t launch_tc_step(const TcLaunch& a, cudaStream_t stream) {
   static int num_sms = 0;
@@ -701,11 +846,18 @@ cudaError_t launch_tc_step(const TcLaunch& a, cudaStream_t stream) {
   p.inject_fault = a.inject_fault;
   p.wrap_cols = a.wrap_cols && tc_wrap_cols(a.cols);
   p.wrap_rows = a.wrap_rows && tc_wrap_rows(a.rows);
+  p.gens = a.gens > 1 && a.flags && a.load_maps_b && a.store_map_b ? a.gens : 1;
+  p.flags = a.flags;
+  p.flag_base = a.flag_base;
   p.stats = a.stats;
   p.trace = a.trace;
   // One persistent CTA per SM over the units (fewer for small grids).
   const int64_t units = static_cast<int64_t>(p.bands) * p.strips;
   int64_t grid = units < num_sms ? units : num_sms;
+  if (p.gens > 1) {
+    grid = tc_persistent_ctas(a.rows, num_sms);
+    if (grid <= 0) return cudaErrorNotSupported;
+  }
   if (a.grid > 0 && a.grid < grid) grid = a.grid;
   if (const char* e = std::getenv("LTL_TC_GRID")) {  // tuning knob (sweeps only)
     const int v = std::atoi(e);
@@ -721,12 +873,15 @@ cudaError_t launch_tc_step(const TcLaunch& a, cudaStream_t stream) {
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = std::getenv("LTL_NO_PDL") ? 0 : 1;  // diagnostics
-  const CUtensorMap* lm = a.load_maps;
-  if (a.stats)
-    return cudaLaunchKernelEx(&cfg, ltl_tc_step_kernel<true>, lm[0], lm[1], lm[2], lm[3],
-                              *a.store_map, p);
-  return cudaLaunchKernelEx(&cfg, ltl_tc_step_kernel<false>, lm[0], lm[1], lm[2], lm[3],
-                            *a.store_map, p);
+  TcMaps maps;
+  for (int i = 0; i < kTcLoadMaps; ++i) {
+    maps.load[0][i] = a.load_maps[i];
+    maps.load[1][i] = a.load_maps_b ? a.load_maps_b[i] : a.load_maps[i];
+  }
+  maps.store[0] = *a.store_map;
+  maps.store[1] = a.store_map_b ? *a.store_map_b : *a.store_map;
+  if (a.stats) return cudaLaunchKernelEx(&cfg, ltl_tc_step_kernel<true>, maps, p);
+  return cudaLaunchKernelEx(&cfg, ltl_tc_step_kernel<false>, maps, p);
 }
 
 }  // namespace ltl

@@ -149,6 +149,38 @@ __device__ __forceinline__ void tma_store_wait_all() {
   asm volatile("cp.async.bulk.wait_group %0;" ::"n"(N) : "memory");
 }
 
+// ---------------------------------------------------------------- cross-CTA flags
+// Async-proxy (TMA) global writes -> generic flag -> async-proxy reads in
+// another CTA: completed bulk stores are published with a proxy fence and a
+// release add; the reader acquires, then fences before its TMA loads.
+__device__ __forceinline__ void fence_proxy_async_global() {
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+__device__ __forceinline__ void fence_acq_rel_gpu() {
+  asm volatile("fence.acq_rel.gpu;" ::: "memory");
+}
+__device__ __forceinline__ void red_relaxed_add(uint32_t* p, uint32_t v) {
+  asm volatile("red.relaxed.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void red_release_add(uint32_t* p, uint32_t v) {
+  asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+// Spin (with back-off) until *p reaches `target` (modular compare); trap
+// after ~10 s so a dependency bug cannot hang the GPU.
+__device__ __forceinline__ void wait_flag_geq(const uint32_t* p, uint32_t target) {
+  if (static_cast<int32_t>(ld_acquire(p) - target) >= 0) return;
+  const long long t0 = clock64();
+  while (static_cast<int32_t>(ld_acquire(p) - target) < 0) {
+    __nanosleep(128);
+    if (clock64() - t0 > 20000000000LL) __trap();
+  }
+}
+
 // ---------------------------------------------------------------- tcgen05
 __device__ __forceinline__ void tmem_alloc(uint32_t* dst_smem, uint32_t ncols) {
   asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
