@@ -178,3 +178,88 @@ def test_partition_single_rank_matches_torus(ltl, orc):
         t.init_random(0.21, 1)
         init = t.download()
     assert np.array_equal(part.torus.download(), orc.simulate(init, parse_rule_text(text), 5))
+
+
+@pytest.mark.parametrize("rows,cols", [(128, 128), (96, 256), (160, 384), (224, 128),
+                                       (200, 256), (128, 200), (64, 1024)])
+def test_wrap_by_load_geometries(ltl, orc, rows, cols):
+    """The step's own periodic wrap (side boxes of strip 0 / S-1 taken from the
+    other end, first / last band boxes assembled from two pieces) against the
+    oracle, on aligned and unaligned tori (these fall back to the halo kernel
+    for the unaligned direction), several generations, Moore and VN."""
+    rng = np.random.default_rng(rows * 31 + cols)
+    init = (rng.random((rows, cols)) < 0.3).astype(np.uint8)
+    for text in ("R1,C2,M0,S2..3,B3..3,NM", "R16,C2,M0,S170..296,B170..300,NM",
+                 "R9,C2,M0,S5..18,B7..12,NN"):
+        with ltl.DeviceTorus(rows=rows, cols=cols) as t:
+            t.upload(init)
+            t.run(text, 5)
+            got = t.download()
+        assert np.array_equal(got, orc.simulate(init, parse_rule_text(text), 5)), (text, rows, cols)
+
+
+@pytest.mark.parametrize("rows,cols", [(128, 128), (256, 256), (1024, 1024), (512, 384)])
+def test_persistent_multi_generation(ltl, orc, rows, cols, monkeypatch):
+    """Multi-generation launches (units handed between generations through
+    per-unit flags) forced on small tori: odd and even generation counts equal
+    the oracle, Moore and VN, and a second run on the same context continues
+    from the flags' new base."""
+    monkeypatch.setenv("LTL_FORCE_PERSIST", "1")
+    rng = np.random.default_rng(rows + 3 * cols)
+    init = (rng.random((rows, cols)) < 0.3).astype(np.uint8)
+    for text in ("R5,C2,M1,S34..58,B34..45,NM", "R7,C2,M0,S5..15,B4..10,NN"):
+        rule = parse_rule_text(text)
+        with ltl.DeviceTorus(rows=rows, cols=cols) as t:
+            t.upload(init)
+            t.run(text, 7)
+            assert np.array_equal(t.download(), orc.simulate(init, rule, 7)), (text, 7)
+            t.run(text, 6)
+            assert np.array_equal(t.download(), orc.simulate(init, rule, 13)), (text, 13)
+
+
+def test_persistent_full_gpu_equals_per_generation(ltl, monkeypatch):
+    """n = 148 x 128: the band count fills every SM, so ltl_run takes the
+    multi-generation launch by default; bit-identical to one launch per
+    generation (LTL_NO_PERSIST)."""
+    import torch
+    n = 128 * torch.cuda.get_device_properties(0).multi_processor_count
+    text = "R5,C2,M1,S34..58,B34..45,NM"
+    outs = []
+    for env in (None, "1"):
+        if env:
+            monkeypatch.setenv("LTL_NO_PERSIST", env)
+        with ltl.DeviceTorus(rows=n, cols=n) as t:
+            t.init_random(0.21, 1)
+            t.run(text, 5)
+            outs.append(t.download())
+    assert np.array_equal(outs[0], outs[1])
+
+
+def test_stencil_after_tcgen05_refreshes_halo(ltl, orc):
+    """tcgen05 generations leave the halo cells they do not need stale; a
+    stencil generation on the same context must refresh them first."""
+    init = orc.init_random(256, 0.3, 4)
+    text = "R4,C2,M0,S10..20,B8..12,NM"
+    with ltl.DeviceTorus(n=256) as t:
+        t.upload(init)
+        t.run(text, 3)
+        t.run(text, 2, stencil=True)
+        t.run(text, 1)
+        got = t.download()
+    assert np.array_equal(got, orc.simulate(init, parse_rule_text(text), 6))
+
+
+def test_partition_wrap_cols_matches_torus(ltl, orc):
+    """The multi-process slab path on a 128-aligned width (column wrap by the
+    step's loads, rows by pack/exchange/unpack) at world size 1."""
+    from paper_2406_17284_b200.dist import PartitionedTorus
+    part = PartitionedTorus(384, 256, 0, 1, 0)
+    part.init_random(0.3, 2)
+    text = "R16,C2,M0,S170..296,B170..300,NM"
+    for _ in range(4):
+        part.step(text)
+    part.torus.synchronize()
+    with ltl.DeviceTorus(rows=384, cols=256) as t:
+        t.init_random(0.3, 2)
+        init = t.download()
+    assert np.array_equal(part.torus.download(), orc.simulate(init, parse_rule_text(text), 4))
