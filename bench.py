@@ -254,7 +254,7 @@ def ours_multi(args, rank, world, local_rank):
     rule = ltl.parse_ltl_rule(args.rule)
     stencil = args.engine == "stencil"
     torch.cuda.set_device(local_rank)
-    part = PartitionedTorus(world * n, n, rank, world, local_rank)
+    part = PartitionedTorus(world * n, n, rank, world, local_rank, ring=not stencil)
     stream = torch.cuda.current_stream()
     part.use_stream(stream.cuda_stream)
     part.init_random(DENSITY, SEED)
@@ -308,7 +308,10 @@ def ours_multi(args, rank, world, local_rank):
                                    f"({world}*{n})x{n} torus in row slabs",
                        "rule": args.rule, "n": n, "density": DENSITY, "seed": SEED,
                        "l2": "inputs larger than L2",
-                       "parallelism": f"row slabs x{world}, 16-row NCCL halo exchange"},
+                       "parallelism": (f"row slabs x{world}, 16-row halo exchange fused into "
+                                       f"the step (TMA stores into the ring neighbours' "
+                                       f"halo buffers over NVLink, CUDA IPC)" if part.ring else
+                                       f"row slabs x{world}, 16-row NCCL halo exchange")},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": n * n * world,
                     "d2h_bytes_per_step": n * n * world,
                     "step": f"upload + {steps} generations + download per rank"},

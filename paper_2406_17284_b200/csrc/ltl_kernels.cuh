@@ -101,6 +101,18 @@ struct TcLaunch {
   int32_t gens;
   uint32_t* flags;
   uint32_t flag_base;
+  // Ring of slabs (multi-GPU, one generation per launch): halo rows above /
+  // below from halo_in (filled by the neighbours), own boundary rows pushed
+  // into the neighbours' buffers (halo_up / halo_down, peer memory); maps are
+  // {128, 16, 4 * strips} boxes of 16 rows (see ltl_tc.cu Params::ring).
+  int32_t ring;
+  uint32_t ring_gen;
+  const CUtensorMap* halo_in;
+  const CUtensorMap* halo_up;
+  const CUtensorMap* halo_down;
+  uint32_t* in_flags;
+  uint32_t* up_flags;
+  uint32_t* down_flags;
   int32_t wrap_cols, wrap_rows;
   int32_t rows, cols;
   RuleConsts rule;
@@ -116,6 +128,13 @@ size_t tc_smem_bytes();
 // Host-side tensor-map builders (driver entry point fetched at runtime).
 cudaError_t make_load_maps(CUtensorMap* maps, const SlabView& s);
 cudaError_t make_store_map(CUtensorMap* map, const SlabView& s);
+// Ring halo buffer: 2 directions x 2 generation slots x strips x [16][128] B.
+cudaError_t make_ring_halo_map(CUtensorMap* map, uint8_t* halo, int32_t strips);
+inline size_t ring_halo_bytes(int32_t strips) { return 4ull * strips * kHalo * kStrip; }
+// Initial ring halo of generation 0 (slot 0) read from the neighbours' slabs
+// (peer / IPC pointers), in_flags set to 1.
+cudaError_t launch_ring_fill(const SlabView& self, const SlabView& above, const SlabView& below,
+                             uint8_t* halo, uint32_t* in_flags, cudaStream_t stream);
 
 // ---- CUDA-core shared-memory stencil ablation (ltl_stencil.cu)
 cudaError_t launch_stencil_step(const SlabView& in, const SlabView& out, const RuleConsts& rule,

@@ -38,7 +38,8 @@ void ck(cudaError_t e, const char* what) {
 
 struct Slab {
   int dev = 0;
-  int32_t row0 = 0, rows = 0;
+  int32_t row0 = 0, rows = 0;  // global row of the first local row (init_random)
+  int32_t host_row0 = 0;       // its row in the host buffers of upload / download
   int64_t strip_bytes = 0;
   int32_t strips = 0;
   uint8_t* buf[2] = {nullptr, nullptr};
@@ -51,6 +52,19 @@ struct Slab {
   bool own_stream = true;
   cudaEvent_t ev_step = nullptr;
   std::vector<cudaEvent_t> timing;
+  // Ring of row slabs with the halo exchange fused into the step (ltl_tc.cu
+  // Params::ring): own halo rows + delivery counters, and the neighbours'
+  // (peer-accessible in this process: same device, P2P, or CUDA IPC).
+  uint8_t* ring_halo = nullptr;
+  uint32_t* ring_flags = nullptr;
+  CUtensorMap ring_map;                       // own halo rows (loads)
+  CUtensorMap ring_up_map, ring_down_map;     // neighbours' halo rows (stores)
+  uint32_t* up_flags = nullptr;               // neighbours' delivery counters
+  uint32_t* down_flags = nullptr;
+  ltl::SlabView up_slab[2] = {}, down_slab[2] = {};  // neighbours' generation buffers
+  bool ring_ready = false;                    // peers wired
+  uint32_t ring_gen = 0;
+  std::vector<void*> ipc_opened;              // IPC mappings to close
 
   ltl::SlabView view(int which, int32_t cols) const {
     return ltl::SlabView{buf[which], rows, cols, strips, strip_bytes};
@@ -64,6 +78,7 @@ struct ltl_ctx {
   int cur = 0;
   bool external_row_halo = false;
   bool halo_stale = false;  // halo cells the tcgen05 step does not need were not refreshed
+  bool ring_stale = true;   // ring halo buffers do not hold the current generation's rows
   int64_t launches = 0;     // kernels this context has launched (ltl_kernel_launches)
   std::vector<Slab> slabs;
   std::string err;
@@ -122,6 +137,25 @@ void build_maps(Slab& s, int32_t cols) {
   }
 }
 
+void wire_ring(ltl_ctx* ctx, Slab& s, uint8_t* up_halo, uint32_t* up_flags, uint8_t* const* up_buf,
+               int32_t up_rows, uint8_t* dn_halo, uint32_t* dn_flags, uint8_t* const* dn_buf,
+               int32_t dn_rows) {
+  const int32_t S = ltl::interior_strips(ctx->cols);
+  ck(cudaSetDevice(s.dev), "cudaSetDevice");
+  ck(ltl::make_ring_halo_map(&s.ring_up_map, up_halo, S), "tensor map (ring up)");
+  ck(ltl::make_ring_halo_map(&s.ring_down_map, dn_halo, S), "tensor map (ring down)");
+  s.up_flags = up_flags;
+  s.down_flags = dn_flags;
+  const int32_t strips = ltl::storage_strips(ctx->cols);
+  for (int b = 0; b < 2; ++b) {
+    s.up_slab[b] = ltl::SlabView{up_buf[b], up_rows, ctx->cols, strips,
+                                 static_cast<int64_t>(up_rows + 2 * kHalo) * ltl::kStrip};
+    s.down_slab[b] = ltl::SlabView{dn_buf[b], dn_rows, ctx->cols, strips,
+                                   static_cast<int64_t>(dn_rows + 2 * kHalo) * ltl::kStrip};
+  }
+  s.ring_ready = true;
+}
+
 void create_slabs(ltl_ctx* ctx, int32_t num_slabs, const int32_t* dev_ids) {
   int ndev = 0;
   ck(cudaGetDeviceCount(&ndev), "cudaGetDeviceCount");
@@ -141,6 +175,7 @@ void create_slabs(ltl_ctx* ctx, int32_t num_slabs, const int32_t* dev_ids) {
       throw std::invalid_argument("config error: device " + std::to_string(s.dev) +
                                   " not visible");
     s.row0 = row0;
+    s.host_row0 = row0;
     s.rows = base + (i < extra ? 1 : 0);
     row0 += s.rows;
     s.strips = ltl::storage_strips(ctx->cols);
@@ -157,6 +192,14 @@ void create_slabs(ltl_ctx* ctx, int32_t num_slabs, const int32_t* dev_ids) {
                            ltl::interior_strips(ctx->cols);
       ck(cudaMalloc(&s.flags, std::max<size_t>(units, 1) * sizeof(uint32_t)), "cudaMalloc flags");
       ck(cudaMemset(s.flags, 0, std::max<size_t>(units, 1) * sizeof(uint32_t)), "memset flags");
+      const int32_t S = ltl::interior_strips(ctx->cols);
+      if (S > 0) {
+        ck(cudaMalloc(&s.ring_halo, ltl::ring_halo_bytes(S)), "cudaMalloc ring halo");
+        ck(cudaMemset(s.ring_halo, 0, ltl::ring_halo_bytes(S)), "memset ring halo");
+        ck(cudaMalloc(&s.ring_flags, 2 * S * sizeof(uint32_t)), "cudaMalloc ring flags");
+        ck(cudaMemset(s.ring_flags, 0, 2 * S * sizeof(uint32_t)), "memset ring flags");
+        ck(ltl::make_ring_halo_map(&s.ring_map, s.ring_halo, S), "tensor map (ring halo)");
+      }
     }
     ck(cudaStreamCreateWithFlags(&s.stream, cudaStreamNonBlocking), "cudaStreamCreate");
     ck(cudaEventCreateWithFlags(&s.ev_step, cudaEventDisableTiming), "cudaEventCreate");
@@ -179,6 +222,15 @@ void create_slabs(ltl_ctx* ctx, int32_t num_slabs, const int32_t* dev_ids) {
       cudaGetLastError();
     }
   }
+  // in-process ring: every slab's neighbours are peer-accessible already
+  if (num_slabs > 1 && ltl::interior_strips(ctx->cols) > 0)
+    for (int32_t i = 0; i < num_slabs; ++i) {
+      Slab& s = ctx->slabs[i];
+      const Slab& up = ctx->slabs[(i - 1 + num_slabs) % num_slabs];
+      const Slab& dn = ctx->slabs[(i + 1) % num_slabs];
+      wire_ring(ctx, s, up.ring_halo, up.ring_flags, up.buf, up.rows, dn.ring_halo, dn.ring_flags,
+                dn.buf, dn.rows);
+    }
 }
 
 void destroy_ctx(ltl_ctx* ctx) {
@@ -189,6 +241,9 @@ void destroy_ctx(ltl_ctx* ctx) {
       if (b) cudaFree(b);
     if (s.dstats) cudaFree(s.dstats);
     if (s.flags) cudaFree(s.flags);
+    for (void* ptr : s.ipc_opened) cudaIpcCloseMemHandle(ptr);
+    if (s.ring_halo) cudaFree(s.ring_halo);
+    if (s.ring_flags) cudaFree(s.ring_flags);
     if (s.ev_step) cudaEventDestroy(s.ev_step);
     for (cudaEvent_t e : s.timing) cudaEventDestroy(e);
     if (s.stream && s.own_stream) cudaStreamDestroy(s.stream);
@@ -206,6 +261,37 @@ bool wrap_cols(const ltl_ctx* ctx) {
 bool wrap_rows(const ltl_ctx* ctx) {
   return ctx->slabs.size() == 1 && !ctx->external_row_halo &&
          ltl::tc_wrap_rows(ctx->slabs[0].rows) && !std::getenv("LTL_NO_WRAP");
+}
+
+void sync_all(ltl_ctx* ctx) {
+  for (Slab& s : ctx->slabs) {
+    ck(cudaSetDevice(s.dev), "cudaSetDevice");
+    ck(cudaStreamSynchronize(s.stream), "cudaStreamSynchronize");
+  }
+}
+
+// Rows exchanged by the step itself over the ring of slabs (fused halo):
+// 128-aligned widths, 32-aligned slab heights, peers wired (in-process slabs
+// at creation, processes by ltl_ring_connect).
+bool ring_ok(const ltl_ctx* ctx) {
+  if (!wrap_cols(ctx) || std::getenv("LTL_NO_RING")) return false;  // env: diagnostics
+  if (ctx->slabs.size() == 1 && !ctx->external_row_halo) return false;  // torus wrap instead
+  for (const Slab& s : ctx->slabs)
+    if (!s.ring_ready || !ltl::tc_wrap_rows(s.rows)) return false;
+  return true;
+}
+
+// Generation-0 ring halo of every slab from its neighbours' current interiors
+// (after uploads / init; all interiors must be in place: callers sync first).
+void enqueue_ring_fill(ltl_ctx* ctx) {
+  for (Slab& s : ctx->slabs) {
+    ck(cudaSetDevice(s.dev), "cudaSetDevice");
+    ck(ltl::launch_ring_fill(s.view(ctx->cur, ctx->cols), s.up_slab[ctx->cur],
+                             s.down_slab[ctx->cur], s.ring_halo, s.ring_flags, s.stream),
+       "ring fill kernel");
+    ++ctx->launches;
+    s.ring_gen = 0;
+  }
 }
 
 // Halo refresh of generation buffer `which` on every slab (after all slabs'
@@ -231,7 +317,7 @@ void enqueue_halo(ltl_ctx* ctx, int which, bool for_tc = false) {
     int parts = all;
     if (for_tc) {
       if (wrap_cols(ctx)) parts &= ~ltl::kHaloCols;
-      if (wrap_rows(ctx)) parts &= ~ltl::kHaloRows;
+      if (wrap_rows(ctx) || ring_ok(ctx)) parts &= ~ltl::kHaloRows;
     }
     ck(ltl::launch_halo_fill(self, above, below, parts, s.stream), "halo kernel");
     if (parts != 0 && s.rows > 0 && ctx->cols > 0) ++ctx->launches;
@@ -262,6 +348,29 @@ void enqueue_step(ltl_ctx* ctx, const ltl::RuleConsts& rc, uint32_t flags, bool 
     return;
   }
   const int cur = ctx->cur, nxt = 1 - cur;
+  const bool ring = !(flags & LTL_FLAG_STENCIL) && ring_ok(ctx);
+  if (ring && ctx->ring_stale) {
+    if (ctx->external_row_halo)
+      throw std::logic_error(
+          "sequencing error: ring halo not filled (ltl_ring_fill after upload / init)");
+    sync_all(ctx);  // every slab's current interior is in place
+    enqueue_ring_fill(ctx);
+    sync_all(ctx);
+    ctx->ring_stale = false;
+  }
+  if (flags & LTL_FLAG_STENCIL) ctx->ring_stale = true;  // stencil generations bypass the ring
+  if (ring && ctx->slabs.size() > 1) {
+    // a slab's generation G pushes rows into its neighbours' halo slot that
+    // their generation G-1 read, and on one device the neighbours' kernels
+    // must be able to run: order after their previous step (ev_step)
+    const int32_t G = static_cast<int32_t>(ctx->slabs.size());
+    for (int32_t i = 0; i < G; ++i) {
+      Slab& s = ctx->slabs[i];
+      ck(cudaSetDevice(s.dev), "cudaSetDevice");
+      ck(cudaStreamWaitEvent(s.stream, ctx->slabs[(i - 1 + G) % G].ev_step, 0), "wait above");
+      ck(cudaStreamWaitEvent(s.stream, ctx->slabs[(i + 1) % G].ev_step, 0), "wait below");
+    }
+  }
   const bool fault = (flags & LTL_FLAG_INJECT_FAULT) != 0;
   for (size_t i = 0; i < ctx->slabs.size(); ++i) {
     Slab& s = ctx->slabs[i];
@@ -283,6 +392,16 @@ void enqueue_step(ltl_ctx* ctx, const ltl::RuleConsts& rc, uint32_t flags, bool 
       a.store_map = &s.store_map[nxt];
       a.wrap_cols = wrap_cols(ctx);
       a.wrap_rows = wrap_rows(ctx);
+      if (ring) {
+        a.ring = 1;
+        a.ring_gen = s.ring_gen++;
+        a.halo_in = &s.ring_map;
+        a.halo_up = &s.ring_up_map;
+        a.halo_down = &s.ring_down_map;
+        a.in_flags = s.ring_flags;
+        a.up_flags = s.up_flags;
+        a.down_flags = s.down_flags;
+      }
       if (persist) {
         a.load_maps_b = s.load_maps[nxt];
         a.store_map_b = &s.store_map[cur];
@@ -330,13 +449,6 @@ void enqueue_step(ltl_ctx* ctx, const ltl::RuleConsts& rc, uint32_t flags, bool 
   const int out = (gens % 2) ? nxt : cur;  // buffer holding the last generation
   enqueue_halo(ctx, out, !(flags & LTL_FLAG_STENCIL));
   ctx->cur = out;
-}
-
-void sync_all(ltl_ctx* ctx) {
-  for (Slab& s : ctx->slabs) {
-    ck(cudaSetDevice(s.dev), "cudaSetDevice");
-    ck(cudaStreamSynchronize(s.stream), "cudaStreamSynchronize");
-  }
 }
 
 void reset_stats(ltl_ctx* ctx) {
@@ -403,7 +515,7 @@ void upload_interior(ltl_ctx* ctx, const uint8_t* interior) {
     ck(cudaSetDevice(s.dev), "cudaSetDevice");
     if (s.rows == 0 || ctx->cols == 0) continue;
     const size_t n = static_cast<size_t>(s.rows) * ctx->cols;
-    ck(cudaMemcpyAsync(s.buf[1 - cur], interior + static_cast<size_t>(s.row0) * ctx->cols, n,
+    ck(cudaMemcpyAsync(s.buf[1 - cur], interior + static_cast<size_t>(s.host_row0) * ctx->cols, n,
                        cudaMemcpyHostToDevice, s.stream),
        "upload");
     ck(ltl::launch_to_strips(s.buf[1 - cur], s.view(cur, ctx->cols), s.stream), "to_strips");
@@ -412,6 +524,7 @@ void upload_interior(ltl_ctx* ctx, const uint8_t* interior) {
   }
   enqueue_halo(ctx, cur);
   sync_all(ctx);
+  ctx->ring_stale = true;
 }
 
 void download_interior(ltl_ctx* ctx, uint8_t* interior) {
@@ -422,7 +535,7 @@ void download_interior(ltl_ctx* ctx, uint8_t* interior) {
     const size_t n = static_cast<size_t>(s.rows) * ctx->cols;
     ck(ltl::launch_from_strips(s.view(cur, ctx->cols), s.buf[1 - cur], s.stream), "from_strips");
     ++ctx->launches;
-    ck(cudaMemcpyAsync(interior + static_cast<size_t>(s.row0) * ctx->cols, s.buf[1 - cur], n,
+    ck(cudaMemcpyAsync(interior + static_cast<size_t>(s.host_row0) * ctx->cols, s.buf[1 - cur], n,
                        cudaMemcpyDeviceToHost, s.stream),
        "download");
   }
@@ -643,7 +756,8 @@ int ltl_create_part(ltl_ctx** out, int32_t rows_local, int32_t cols, int32_t row
   const int st = ltl_create_torus(out, rows_local, cols, 1, &dev);
   if (st == LTL_OK) {
     (*out)->external_row_halo = true;
-    (*out)->slabs[0].row0 = row0;  // global row of the first local row (init_random)
+    (*out)->slabs[0].row0 = row0;  // global row of the first local row (init_random);
+                                   // host buffers hold this slab only (host_row0 = 0)
   }
   return st;
 }
@@ -692,6 +806,7 @@ int ltl_init_random(ltl_ctx* ctx, double density, uint64_t seed, int32_t fill_n)
     }
     enqueue_halo(ctx, ctx->cur);
     sync_all(ctx);
+    ctx->ring_stale = true;
   });
 }
 
@@ -743,6 +858,80 @@ int ltl_unpack_halo(ltl_ctx* ctx, const void* top_halo, const void* bot_halo) {
        "unpack kernel");
     ++ctx->launches;
   });
+}
+
+// ---- multi-process ring (one process per GPU, CUDA IPC)
+
+int ltl_ring_export(ltl_ctx* ctx, void* handles) {
+  if (!ctx || !handles) return LTL_ERR_INVALID_ARGUMENT;
+  return guarded(ctx, [&] {
+    if (ctx->slabs.size() != 1 || !ctx->external_row_halo)
+      throw std::invalid_argument("config error: ring export needs a part context (ltl_create_part)");
+    Slab& s = ctx->slabs[0];
+    if (!s.ring_halo) throw std::invalid_argument("config error: empty slab");
+    ck(cudaSetDevice(s.dev), "cudaSetDevice");
+    cudaIpcMemHandle_t h[4];
+    ck(cudaIpcGetMemHandle(&h[0], s.ring_halo), "ipc handle (ring halo)");
+    ck(cudaIpcGetMemHandle(&h[1], s.ring_flags), "ipc handle (ring flags)");
+    ck(cudaIpcGetMemHandle(&h[2], s.buf[0]), "ipc handle (buffer 0)");
+    ck(cudaIpcGetMemHandle(&h[3], s.buf[1]), "ipc handle (buffer 1)");
+    std::memcpy(handles, h, sizeof h);
+  });
+}
+
+int ltl_ring_connect(ltl_ctx* ctx, const void* up_handles, int32_t up_rows,
+                     const void* down_handles, int32_t down_rows) {
+  if (!ctx || !up_handles || !down_handles) return LTL_ERR_INVALID_ARGUMENT;
+  return guarded(ctx, [&] {
+    if (ctx->slabs.size() != 1 || !ctx->external_row_halo)
+      throw std::invalid_argument("config error: ring connect needs a part context (ltl_create_part)");
+    Slab& s = ctx->slabs[0];
+    ck(cudaSetDevice(s.dev), "cudaSetDevice");
+    cudaIpcMemHandle_t mine[4];
+    ck(cudaIpcGetMemHandle(&mine[0], s.ring_halo), "ipc handle (ring halo)");
+    // open a neighbour's 4 allocations (its halo, flags, 2 buffers); our own
+    // handles (world size 1) map to our own pointers
+    auto open = [&](const void* hv, void** out) {
+      const cudaIpcMemHandle_t* h = static_cast<const cudaIpcMemHandle_t*>(hv);
+      if (std::memcmp(&h[0], &mine[0], sizeof(cudaIpcMemHandle_t)) == 0) {
+        out[0] = s.ring_halo;
+        out[1] = s.ring_flags;
+        out[2] = s.buf[0];
+        out[3] = s.buf[1];
+        return;
+      }
+      for (int i = 0; i < 4; ++i) {
+        ck(cudaIpcOpenMemHandle(&out[i], h[i], cudaIpcMemLazyEnablePeerAccess), "ipc open");
+        s.ipc_opened.push_back(out[i]);
+      }
+    };
+    void* up[4];
+    void* dn[4];
+    open(up_handles, up);
+    if (std::memcmp(up_handles, down_handles, 4 * sizeof(cudaIpcMemHandle_t)) == 0)
+      std::memcpy(dn, up, sizeof up);  // world size 2: one neighbour on both sides
+    else
+      open(down_handles, dn);
+    uint8_t* upb[2] = {static_cast<uint8_t*>(up[2]), static_cast<uint8_t*>(up[3])};
+    uint8_t* dnb[2] = {static_cast<uint8_t*>(dn[2]), static_cast<uint8_t*>(dn[3])};
+    wire_ring(ctx, s, static_cast<uint8_t*>(up[0]), static_cast<uint32_t*>(up[1]), upb, up_rows,
+              static_cast<uint8_t*>(dn[0]), static_cast<uint32_t*>(dn[1]), dnb, down_rows);
+    ctx->ring_stale = true;
+  });
+}
+
+int ltl_ring_fill(ltl_ctx* ctx) {
+  if (!ctx) return LTL_ERR_INVALID_ARGUMENT;
+  return guarded(ctx, [&] {
+    for (const Slab& s : ctx->slabs)
+      if (!s.ring_ready) throw std::logic_error("sequencing error: ring not connected");
+    enqueue_ring_fill(ctx);
+    ctx->ring_stale = false;
+  });
+}
+
+int32_t ltl_ring_active(const ltl_ctx* ctx) {
+  return ctx && ring_ok(ctx) ? 1 : 0;
 }
 
 }  // extern "C"

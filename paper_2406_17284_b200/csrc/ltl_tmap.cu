@@ -82,4 +82,12 @@ cudaError_t make_store_map(CUtensorMap* map, const SlabView& s) {
                  64, CU_TENSOR_MAP_SWIZZLE_128B);
 }
 
+// Ring halo rows (ltl_tc.cu Params::ring): {128 columns, 16 rows, 4 * strips}
+// boxes of one strip's 16 rows, SWIZZLE_128B like the box they join.
+cudaError_t make_ring_halo_map(CUtensorMap* map, uint8_t* halo, int32_t strips) {
+  if (strips <= 0) return cudaSuccess;
+  return encode3(map, halo, kHalo, 4ull * strips, static_cast<uint64_t>(kHalo) * kStrip, kStrip,
+                 kHalo, CU_TENSOR_MAP_SWIZZLE_128B);
+}
+
 }  // namespace ltl

@@ -170,6 +170,26 @@ __device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
+__device__ __forceinline__ void fence_acq_rel_sys() {
+  asm volatile("fence.acq_rel.sys;" ::: "memory");
+}
+__device__ __forceinline__ void red_relaxed_add_sys(uint32_t* p, uint32_t v) {
+  asm volatile("red.relaxed.sys.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+// Flag written by another GPU (peer store over NVLink): system-scope acquire.
+__device__ __forceinline__ void wait_flag_geq_sys(const uint32_t* p, uint32_t target) {
+  if (static_cast<int32_t>(ld_acquire_sys(p) - target) >= 0) return;
+  const long long t0 = clock64();
+  while (static_cast<int32_t>(ld_acquire_sys(p) - target) < 0) {
+    __nanosleep(256);
+    if (clock64() - t0 > 20000000000LL) __trap();
+  }
+}
 // Spin (with back-off) until *p reaches `target` (modular compare); trap
 // after ~10 s so a dependency bug cannot hang the GPU.
 __device__ __forceinline__ void wait_flag_geq(const uint32_t* p, uint32_t target) {

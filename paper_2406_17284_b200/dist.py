@@ -74,10 +74,24 @@ def exchange_edges(send_top, send_bot, recv_top, recv_bot, plan: HaloPlan, dist_
 
 
 class PartitionedTorus:
-    """One rank's slab of a torus split across processes, driven through the C-ABI."""
+    """One rank's slab of a torus split across processes, driven through the C-ABI.
 
-    def __init__(self, global_rows: int, cols: int, rank: int, world: int, device: int):
+    Two exchange paths for the 16 boundary rows per generation:
+      * ring (cols % 128 == 0, slab rows % 32 == 0): fused into the step --
+        the kernel TMA-stores its first / last rows straight into the ring
+        neighbours' halo buffers (CUDA IPC peer memory over NVLink) and bumps
+        per-strip flags their next step waits on.  No NCCL on the data path,
+        no extra launches, no host synchronisation;
+      * otherwise: ltl_pack_edges -> NCCL send/recv (exchange_edges) ->
+        ltl_unpack_halo on the same stream.
+    """
+
+    def __init__(self, global_rows: int, cols: int, rank: int, world: int, device: int,
+                 ring: bool | None = None, dist_mod=None):
         from .ltl import DeviceTorus
+        if dist_mod is None:
+            import torch.distributed as dist_mod  # noqa: N813
+        self.dist = dist_mod
         self.plan = HaloPlan.ring(rank, world)
         self.row0, self.rows = slab_rows(global_rows, world, rank)
         if world > 1 and self.rows < HALO:
@@ -91,20 +105,58 @@ class PartitionedTorus:
         # packed edge rows: send top / bottom, receive top / bottom halo
         self.edges = [torch.empty(HALO * cols, dtype=torch.uint8, device=f"cuda:{device}")
                       for _ in range(4)]
+        aligned = cols % 128 == 0 and all(
+            slab_rows(global_rows, world, k)[1] % 32 == 0 and slab_rows(global_rows, world, k)[1] >= 32
+            for k in range(world))
+        self.ring = aligned if ring is None else (ring and aligned)
+        if self.ring:
+            handles = self.torus.ring_export()
+            table = [(rank, self.rows, handles)]
+            if world > 1:
+                table = [None] * world
+                self.dist.all_gather_object(table, (rank, self.rows, handles))
+            by_rank = {r: (rows, h) for r, rows, h in table}
+            up_rows, up_h = by_rank[self.plan.up]
+            down_rows, down_h = by_rank[self.plan.down]
+            self.torus.ring_connect(up_h, up_rows, down_h, down_rows)
 
     def use_stream(self, stream_ptr: int) -> None:
         self.torus.set_stream(stream_ptr)
 
+    def _ring_fill(self) -> None:
+        # every rank's interior must be in place before anyone reads it, and
+        # every rank's generation-0 halo / flags before anyone pushes into them
+        self.torus.synchronize()
+        if self.plan.world > 1:
+            self.dist.barrier()
+        self.torus.ring_fill()
+        self.torus.synchronize()
+        if self.plan.world > 1:
+            self.dist.barrier()
+
     def exchange(self) -> None:
+        if self.ring:
+            self._ring_fill()
+            return
         send_top, send_bot, recv_top, recv_bot = self.edges
         self.torus.pack_edges(send_top.data_ptr(), send_bot.data_ptr())
-        exchange_edges(send_top, send_bot, recv_top, recv_bot, self.plan)
+        exchange_edges(send_top, send_bot, recv_top, recv_bot, self.plan, self.dist)
         self.torus.unpack_halo(recv_top.data_ptr(), recv_bot.data_ptr())
+
+    def upload(self, interior) -> None:
+        self.torus.upload(interior)
+        self.exchange()
 
     def init_random(self, density: float, seed: int) -> None:
         self.torus.init_random(density, seed)
         self.exchange()
 
     def step(self, rule, stencil: bool = False) -> None:
+        if self.ring:
+            if stencil:
+                raise ValueError("config error: the stencil engine needs ring=False "
+                                 "(padded halo rows)")
+            self.torus.step_part(rule)  # the exchange happens inside the step
+            return
         self.torus.step_part(rule, stencil=stencil)
         self.exchange()

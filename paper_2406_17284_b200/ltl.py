@@ -61,7 +61,8 @@ EXPORTS = (
     "ltl_num_slabs", "ltl_kernel_launches", "ltl_upload", "ltl_download", "ltl_upload_interior",
     "ltl_download_interior", "ltl_run", "ltl_run_async", "ltl_synchronize", "ltl_time",
     "ltl_run_interior", "ltl_create_part", "ltl_set_stream", "ltl_step_part", "ltl_fill_halo",
-    "ltl_slab_buffer", "ltl_pack_edges", "ltl_unpack_halo", "ltl_init_random", "ltl_parse_rule", "ltl_format_rule",
+    "ltl_slab_buffer", "ltl_pack_edges", "ltl_unpack_halo", "ltl_ring_export",
+    "ltl_ring_connect", "ltl_ring_fill", "ltl_ring_active", "ltl_init_random", "ltl_parse_rule", "ltl_format_rule",
     "ltl_preset_count", "ltl_preset", "ltl_von_neumann_probe_rule", "ltl_build_info",
 )
 
@@ -111,6 +112,10 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
         "ltl_slab_buffer": ([vp, ctypes.c_int32, ctypes.c_int32, P(vp), P(ctypes.c_int64),
                              P(ctypes.c_int32)], ctypes.c_int),
         "ltl_pack_edges": ([vp, vp, vp], ctypes.c_int),
+        "ltl_ring_export": ([vp, vp], ctypes.c_int),
+        "ltl_ring_connect": ([vp, vp, ctypes.c_int32, vp, ctypes.c_int32], ctypes.c_int),
+        "ltl_ring_fill": ([vp], ctypes.c_int),
+        "ltl_ring_active": ([vp], ctypes.c_int32),
         "ltl_unpack_halo": ([vp, vp, vp], ctypes.c_int),
         "ltl_parse_rule": ([ctypes.c_char_p, P(ltl_rule_c), ctypes.c_char_p, ctypes.c_int32],
                            ctypes.c_int),
@@ -352,6 +357,25 @@ class DeviceTorus:
         self._check(self.lib.ltl_slab_buffer(self._ctx, slab, which, ctypes.byref(ptr),
                                              ctypes.byref(strip_bytes), ctypes.byref(rows)))
         return ptr.value, strip_bytes.value, rows.value
+
+    # ---- multi-process ring with the halo exchange fused into the step
+    RING_HANDLE_BYTES = 4 * 64
+
+    def ring_export(self) -> bytes:
+        """4 CUDA IPC handles (halo rows, flags, both generation buffers)."""
+        buf = ctypes.create_string_buffer(self.RING_HANDLE_BYTES)
+        self._check(self.lib.ltl_ring_export(self._ctx, buf))
+        return buf.raw
+
+    def ring_connect(self, up: bytes, up_rows: int, down: bytes, down_rows: int) -> None:
+        self._check(self.lib.ltl_ring_connect(self._ctx, up, up_rows, down, down_rows))
+
+    def ring_fill(self) -> None:
+        """Generation-0 halo rows from the neighbours (after every rank's upload)."""
+        self._check(self.lib.ltl_ring_fill(self._ctx))
+
+    def ring_active(self) -> bool:
+        return bool(self.lib.ltl_ring_active(self._ctx))
 
     def pack_edges(self, top_ptr: int, bot_ptr: int) -> None:
         """Enqueue: device buffers top/bot (16 x cols) <- first / last 16 interior rows."""
