@@ -325,6 +325,11 @@ def ours_multi(args, rank, world, local_rank):
         print(json.dumps(line), flush=True)
 
 
+def torch_device(local_rank):
+    import torch
+    return torch.device("cuda", local_rank)
+
+
 def main():
     ap = argparse.ArgumentParser(description=__doc__.splitlines()[0])
     ap.add_argument("--gpus", type=int, default=1)
@@ -349,7 +354,8 @@ def main():
         return
     if world > 1 or args.dist:
         import torch.distributed as dist
-        dist.init_process_group("nccl")
+        dist.init_process_group(os.environ.get("LTL_DIST_BACKEND", "nccl"),
+                                device_id=torch_device(local_rank))
         try:
             ours_multi(args, rank, world, local_rank)
         finally:

@@ -135,8 +135,11 @@ int ltl_synchronize(ltl_ctx* ctx);
 
 /* Device timing with CUDA events on the slab streams (max over slabs):
  * `warmup` untimed generations then `steps` timed ones.  total_ms covers the
- * whole generation loop; kernel_ms sums only the main step kernel launches
- * (the roofline kernel).  Either output pointer may be NULL. */
+ * whole generation loop (events only around it, so consecutive step kernels
+ * keep their programmatic overlap); kernel_ms = the main step kernel's
+ * average duration over a further sample of up to 100 generations, each
+ * launch bracketed by its own events, times `steps` (the roofline kernel).
+ * Either output pointer may be NULL. */
 int ltl_time(ltl_ctx* ctx, const ltl_rule_c* rule, int32_t steps, int32_t warmup,
              uint32_t flags, double* total_ms, double* kernel_ms);
 

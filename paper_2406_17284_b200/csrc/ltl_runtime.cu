@@ -690,13 +690,16 @@ int ltl_time(ltl_ctx* ctx, const ltl_rule_c* rule, int32_t steps, int32_t warmup
     const size_t G = ctx->slabs.size();
     enqueue_step(ctx, rc, flags, false, nullptr, nullptr, warmup);
     sync_all(ctx);
-    // one persistent launch for all timed generations when possible: the
-    // "kernel" time is then that launch (per generation = total / steps)
+    // one persistent launch for all timed generations when possible
     const bool persist = steps > 1 && persistent_ok(ctx, flags);
-    // per slab: [start, end] + per-step kernel [k0, k1] pairs
+    // pass 1 (total): events only around the whole loop -- an event between
+    // two kernels would cut their programmatic (PDL) overlap
+    // pass 2 (kernel): a sample of up to 100 generations, one event pair
+    // around every launch; the average x steps is the kernel time
+    const int32_t sample = kernel_ms && !persist ? std::min<int32_t>(steps, 100) : 0;
     for (Slab& s : ctx->slabs) {
       ck(cudaSetDevice(s.dev), "cudaSetDevice");
-      const size_t need = 2 + 2 * static_cast<size_t>(steps);
+      const size_t need = 2 + 2 * static_cast<size_t>(std::max<int32_t>(sample, 1));
       while (s.timing.size() < need) {
         cudaEvent_t e;
         ck(cudaEventCreate(&e), "cudaEventCreate");
@@ -704,34 +707,38 @@ int ltl_time(ltl_ctx* ctx, const ltl_rule_c* rule, int32_t steps, int32_t warmup
       }
       ck(cudaEventRecord(s.timing[0], s.stream), "event");
     }
-    std::vector<cudaEvent_t> k0(G), k1(G);
-    const int32_t launches = persist ? 1 : steps;
-    for (int32_t t = 0; t < launches; ++t) {
-      for (size_t i = 0; i < G; ++i) {
-        k0[i] = ctx->slabs[i].timing[2 + 2 * t];
-        k1[i] = ctx->slabs[i].timing[3 + 2 * t];
-      }
-      enqueue_step(ctx, rc, flags, false, kernel_ms ? k0.data() : nullptr,
-                   kernel_ms ? k1.data() : nullptr, persist ? steps : 1);
-    }
+    enqueue_step(ctx, rc, flags, false, nullptr, nullptr, steps);
     for (Slab& s : ctx->slabs) {
       ck(cudaSetDevice(s.dev), "cudaSetDevice");
       ck(cudaEventRecord(s.timing[1], s.stream), "event");
     }
     sync_all(ctx);
-    double tot = 0, ker = 0;
+    double tot = 0;
     for (Slab& s : ctx->slabs) {
       float ms = 0;
       ck(cudaEventElapsedTime(&ms, s.timing[0], s.timing[1]), "elapsed");
       tot = std::max(tot, static_cast<double>(ms));
-      if (kernel_ms) {
+    }
+    double ker = tot;  // persistent: the launch is the kernel
+    if (sample > 0) {
+      std::vector<cudaEvent_t> k0(G), k1(G);
+      for (int32_t t = 0; t < sample; ++t) {
+        for (size_t i = 0; i < G; ++i) {
+          k0[i] = ctx->slabs[i].timing[2 + 2 * t];
+          k1[i] = ctx->slabs[i].timing[3 + 2 * t];
+        }
+        enqueue_step(ctx, rc, flags, false, k0.data(), k1.data(), 1);
+      }
+      sync_all(ctx);
+      ker = 0;
+      for (Slab& s : ctx->slabs) {
         double acc = 0;
-        for (int32_t t = 0; t < launches; ++t) {
+        for (int32_t t = 0; t < sample; ++t) {
           float k = 0;
           ck(cudaEventElapsedTime(&k, s.timing[2 + 2 * t], s.timing[3 + 2 * t]), "elapsed");
           acc += k;
         }
-        ker = std::max(ker, acc);
+        ker = std::max(ker, acc * steps / sample);
       }
     }
     if (total_ms) *total_ms = tot;

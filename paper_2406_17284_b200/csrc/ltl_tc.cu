@@ -478,6 +478,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 mbar_arrive_expect_tx(&x_full[s], (last ? last_rows + 2 * kHalo : kBox) * kStrip);
                 int row = 0;  // box row being filled
                 const uint32_t slot_base = (p.ring_gen & 1u) * p.strips + (strip - 1);
+#ifndef LTL_DBG_RING_NOWAIT
                 if (p.ring) {
                   // the neighbours' rows of generation G for this strip must
                   // have landed in the halo buffer (pushed by their steps)
@@ -485,8 +486,14 @@ __global__ void __launch_bounds__(kThreads, 1)
                   if (last) wait_flag_geq_sys(p.in_flags + p.strips + (strip - 1), p.ring_gen + 1);
                   fence_proxy_async_global();
                 }
+#endif
+#ifdef LTL_DBG_RING_OWNPIECE
+                const bool ring_piece = false;
+#else
+                const bool ring_piece = p.ring;
+#endif
                 if (first) {  // rows -16 .. -1: the torus' other end / the ring halo
-                  if (p.ring)
+                  if (ring_piece)
                     tma_load_3d(dst, &maps.halo_in, &x_full[s], 0, 0, slot_base);
                   else
                     tma_load_3d(dst, &lm[1], &x_full[s], 0, p.rows, strip);
@@ -500,7 +507,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                               first ? kHalo : band * kBand, strip);
                   // rows rows .. rows + 15: the torus' rows 0 .. 15 / the ring halo
                   uint8_t* bot = dst + (row + body + (first ? 0 : kHalo)) * kStrip;
-                  if (p.ring)
+                  if (ring_piece)
                     tma_load_3d(bot, &maps.halo_in, &x_full[s], 0, 0, 2 * p.strips + slot_base);
                   else
                     tma_load_3d(bot, &lm[1], &x_full[s], 0, kHalo, strip);
@@ -683,8 +690,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int i = 0; i < nring; ++i) {
           if (static_cast<int32_t>(done_upto - ring_seq[i]) >= 0) {
             if (!fenced) {
+#ifndef LTL_DBG_RING_NOFENCE
               fence_proxy_async_global();
               fence_acq_rel_sys();
+#endif
               fenced = true;
             }
             red_relaxed_add_sys(ring_flag[i], 1);
@@ -707,7 +716,11 @@ __global__ void __launch_bounds__(kThreads, 1)
               const uint8_t* src = smem + kSmemStage + (grp * kStageSlots + slot) * kStageBytes;
               tma_store_3d(&maps.store[gg & 1], src, 0, band * kBand + kSub * grp,
                            t % p.strips + 1);
+#ifdef LTL_DBG_RING_NOPUSH
+              if (false) {
+#else
               if (p.ring) {
+#endif
                 // push the slab's first / last 16 rows of generation G+1 into
                 // the neighbours' halo buffers (slot (G+1) % 2), then count them
                 const int si = t % p.strips;

@@ -170,15 +170,20 @@ __device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
+#ifdef LTL_DBG_RING_GPU_SCOPE
+#define LTL_RING_SCOPE "gpu"
+#else
+#define LTL_RING_SCOPE "sys"
+#endif
 __device__ __forceinline__ void fence_acq_rel_sys() {
-  asm volatile("fence.acq_rel.sys;" ::: "memory");
+  asm volatile("fence.acq_rel." LTL_RING_SCOPE ";" ::: "memory");
 }
 __device__ __forceinline__ void red_relaxed_add_sys(uint32_t* p, uint32_t v) {
-  asm volatile("red.relaxed.sys.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+  asm volatile("red.relaxed." LTL_RING_SCOPE ".global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 __device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
   uint32_t v;
-  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  asm volatile("ld.acquire." LTL_RING_SCOPE ".global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
 // Flag written by another GPU (peer store over NVLink): system-scope acquire.
