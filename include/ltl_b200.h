@@ -195,6 +195,9 @@ int ltl_ring_connect(ltl_ctx* ctx, const void* up_handles, int32_t up_rows,
                      const void* down_handles, int32_t down_rows);
 int ltl_ring_fill(ltl_ctx* ctx);
 int32_t ltl_ring_active(const ltl_ctx* ctx);
+/* Drop a part context's ring (close the IPC mappings); steps then need the
+ * packed exchange again. */
+int ltl_ring_disconnect(ltl_ctx* ctx);
 
 /* Device pointer of slab `slab`'s current (which = 0) or other (1)
  * generation buffer, its strip size in bytes and interior row count.  The

@@ -927,6 +927,20 @@ int ltl_ring_connect(ltl_ctx* ctx, const void* up_handles, int32_t up_rows,
   });
 }
 
+int ltl_ring_disconnect(ltl_ctx* ctx) {
+  if (!ctx) return LTL_ERR_INVALID_ARGUMENT;
+  return guarded(ctx, [&] {
+    sync_all(ctx);
+    for (Slab& s : ctx->slabs) {
+      if (!ctx->external_row_halo) continue;  // in-process rings stay wired
+      for (void* ptr : s.ipc_opened) cudaIpcCloseMemHandle(ptr);
+      s.ipc_opened.clear();
+      s.ring_ready = false;
+    }
+    ctx->ring_stale = true;
+  });
+}
+
 int ltl_ring_fill(ltl_ctx* ctx) {
   if (!ctx) return LTL_ERR_INVALID_ARGUMENT;
   return guarded(ctx, [&] {

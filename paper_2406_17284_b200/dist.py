@@ -118,7 +118,18 @@ class PartitionedTorus:
             by_rank = {r: (rows, h) for r, rows, h in table}
             up_rows, up_h = by_rank[self.plan.up]
             down_rows, down_h = by_rank[self.plan.down]
-            self.torus.ring_connect(up_h, up_rows, down_h, down_rows)
+            ok = True
+            try:  # needs peer access between the GPUs (NVLink / NVSwitch)
+                self.torus.ring_connect(up_h, up_rows, down_h, down_rows)
+            except Exception:  # noqa: BLE001 -- any failure: everyone falls back
+                ok = False
+            if world > 1:
+                votes = [None] * world
+                self.dist.all_gather_object(votes, ok)
+                ok = all(votes)
+            if not ok:
+                self.torus.ring_disconnect()
+                self.ring = False
 
     def use_stream(self, stream_ptr: int) -> None:
         self.torus.set_stream(stream_ptr)

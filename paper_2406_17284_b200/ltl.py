@@ -62,7 +62,8 @@ EXPORTS = (
     "ltl_download_interior", "ltl_run", "ltl_run_async", "ltl_synchronize", "ltl_time",
     "ltl_run_interior", "ltl_create_part", "ltl_set_stream", "ltl_step_part", "ltl_fill_halo",
     "ltl_slab_buffer", "ltl_pack_edges", "ltl_unpack_halo", "ltl_ring_export",
-    "ltl_ring_connect", "ltl_ring_fill", "ltl_ring_active", "ltl_init_random", "ltl_parse_rule", "ltl_format_rule",
+    "ltl_ring_connect", "ltl_ring_fill", "ltl_ring_active", "ltl_ring_disconnect",
+    "ltl_init_random", "ltl_parse_rule", "ltl_format_rule",
     "ltl_preset_count", "ltl_preset", "ltl_von_neumann_probe_rule", "ltl_build_info",
 )
 
@@ -116,6 +117,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
         "ltl_ring_connect": ([vp, vp, ctypes.c_int32, vp, ctypes.c_int32], ctypes.c_int),
         "ltl_ring_fill": ([vp], ctypes.c_int),
         "ltl_ring_active": ([vp], ctypes.c_int32),
+        "ltl_ring_disconnect": ([vp], ctypes.c_int),
         "ltl_unpack_halo": ([vp, vp, vp], ctypes.c_int),
         "ltl_parse_rule": ([ctypes.c_char_p, P(ltl_rule_c), ctypes.c_char_p, ctypes.c_int32],
                            ctypes.c_int),
@@ -376,6 +378,9 @@ class DeviceTorus:
 
     def ring_active(self) -> bool:
         return bool(self.lib.ltl_ring_active(self._ctx))
+
+    def ring_disconnect(self) -> None:
+        self._check(self.lib.ltl_ring_disconnect(self._ctx))
 
     def pack_edges(self, top_ptr: int, bot_ptr: int) -> None:
         """Enqueue: device buffers top/bot (16 x cols) <- first / last 16 interior rows."""
