@@ -354,6 +354,9 @@ def main():
         return
     if world > 1 or args.dist:
         import torch.distributed as dist
+        if "RANK" not in os.environ:  # --dist without torchrun: a world of one
+            os.environ.update(RANK="0", WORLD_SIZE="1", MASTER_ADDR="127.0.0.1",
+                              MASTER_PORT=os.environ.get("MASTER_PORT", "29533"))
         dist.init_process_group(os.environ.get("LTL_DIST_BACKEND", "nccl"),
                                 device_id=torch_device(local_rank))
         try:

@@ -178,18 +178,18 @@ int ltl_pack_edges(ltl_ctx* ctx, void* top, void* bot);
 int ltl_unpack_halo(ltl_ctx* ctx, const void* top_halo, const void* bot_halo);
 
 /* Ring of row slabs with the halo exchange fused into the step (multi-GPU,
- * one process per GPU): each step pushes the slab's first / last 16 rows
- * straight into the ring neighbours' halo buffers over NVLink (CUDA IPC peer
- * memory) and counts them in per-strip flags the neighbours' next step waits
- * on -- no separate exchange, no host synchronisation.  Needs cols % 128 == 0
- * and rows % 32 == 0 (else ltl_pack_edges / ltl_unpack_halo + NCCL).
- *   ltl_ring_export:  4 CUDA IPC handles (4 x 64 bytes) of a part context
+ * one process per GPU): the first / last band units of each step TMA-load
+ * the 16 rows above / below straight out of the ring neighbours' slabs over
+ * NVLink (CUDA IPC peer memory), gated by the neighbours' step counters --
+ * no separate exchange, no host synchronisation.  Needs cols % 128 == 0 and
+ * rows % 32 == 0 (else ltl_pack_edges / ltl_unpack_halo + NCCL).
+ *   ltl_ring_export:  LTL_RING_HANDLE_BYTES of CUDA IPC handles of a part context
  *   ltl_ring_connect: open the upper / lower neighbour's handles (rows = their
  *                     slab heights); our own handles (world size 1) are fine
- *   ltl_ring_fill:    after every upload / init (all ranks uploaded first,
- *                     barrier after): generation-0 halo rows from the
- *                     neighbours' interiors; steps then exchange by themselves
+ *   ltl_ring_fill:    after every upload / init, with a barrier of all ranks
+ *                     on both sides: restarts the step counters (synchronous)
  *   ltl_ring_active:  1 when ltl_step_part / ltl_run use the fused exchange. */
+#define LTL_RING_HANDLE_BYTES (3 * 64)
 int ltl_ring_export(ltl_ctx* ctx, void* handles);
 int ltl_ring_connect(ltl_ctx* ctx, const void* up_handles, int32_t up_rows,
                      const void* down_handles, int32_t down_rows);

@@ -64,6 +64,16 @@ def _compile(src: str, obj: str) -> str:
 
 def build(force: bool = False, verbose: bool = False) -> str:
     os.makedirs(BUILD, exist_ok=True)
+    # objects built with other extra flags (LTL_NVCC_FLAGS) are stale too
+    stamp = os.path.join(BUILD, "flags.txt")
+    flags = " ".join(COMMON)
+    try:
+        with open(stamp) as fh:
+            force = force or fh.read() != flags
+    except OSError:
+        force = True
+    with open(stamp, "w") as fh:
+        fh.write(flags)
     cu, cpp = sources()
     hdrs = _headers()
     jobs, objs = [], []

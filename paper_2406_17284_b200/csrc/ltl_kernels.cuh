@@ -101,18 +101,20 @@ struct TcLaunch {
   int32_t gens;
   uint32_t* flags;
   uint32_t flag_base;
-  // Ring of slabs (multi-GPU, one generation per launch): halo rows above /
-  // below from halo_in (filled by the neighbours), own boundary rows pushed
-  // into the neighbours' buffers (halo_up / halo_down, peer memory); maps are
-  // {128, 16, 4 * strips} boxes of 16 rows (see ltl_tc.cu Params::ring).
+  // Ring of slabs (multi-GPU, one generation per launch), pull model: the
+  // first / last band's 16 rows above / below are loaded from the
+  // neighbours' slabs (ring_up / ring_down: piece maps over their buffers
+  // holding generation G, peer memory), gated by their done counters
+  // (ltl_tc.cu Params::ring).  Needs wrap_cols and rows % 32 == 0.
   int32_t ring;
   uint32_t ring_gen;
-  const CUtensorMap* halo_in;
-  const CUtensorMap* halo_up;
-  const CUtensorMap* halo_down;
-  uint32_t* in_flags;
-  uint32_t* up_flags;
-  uint32_t* down_flags;
+  int32_t up_rows;
+  const CUtensorMap* ring_up;
+  const CUtensorMap* ring_down;
+  const uint32_t* up_done;
+  const uint32_t* down_done;
+  uint32_t* my_done;
+  uint32_t* my_ticket;
   int32_t wrap_cols, wrap_rows;
   int32_t rows, cols;
   RuleConsts rule;
@@ -128,13 +130,8 @@ size_t tc_smem_bytes();
 // Host-side tensor-map builders (driver entry point fetched at runtime).
 cudaError_t make_load_maps(CUtensorMap* maps, const SlabView& s);
 cudaError_t make_store_map(CUtensorMap* map, const SlabView& s);
-// Ring halo buffer: 2 directions x 2 generation slots x strips x [16][128] B.
-cudaError_t make_ring_halo_map(CUtensorMap* map, uint8_t* halo, int32_t strips);
-inline size_t ring_halo_bytes(int32_t strips) { return 4ull * strips * kHalo * kStrip; }
-// Initial ring halo of generation 0 (slot 0) read from the neighbours' slabs
-// (peer / IPC pointers), in_flags set to 1.
-cudaError_t launch_ring_fill(const SlabView& self, const SlabView& above, const SlabView& below,
-                             uint8_t* halo, uint32_t* in_flags, cudaStream_t stream);
+// 16-row SWIZZLE_128B pieces over a slab (the ring's rows from a neighbour).
+cudaError_t make_piece_map(CUtensorMap* map, const SlabView& s);
 
 // ---- CUDA-core shared-memory stencil ablation (ltl_stencil.cu)
 cudaError_t launch_stencil_step(const SlabView& in, const SlabView& out, const RuleConsts& rule,

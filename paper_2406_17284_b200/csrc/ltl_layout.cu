@@ -105,39 +105,3 @@ cudaError_t launch_unpack_halo(const SlabView& s, const uint8_t* top_halo,
 }
 
 }  // namespace ltl
-
-namespace ltl {
-namespace {
-
-// Generation-0 ring halo: slot 0 of both directions, 16 B per thread, from
-// the neighbours' interiors (peer / IPC pointers); then the delivery counters
-// start at 1 (generation 0 delivered).
-__global__ void ring_fill_kernel(SlabView self, SlabView above, SlabView below, uint8_t* halo,
-                                 uint32_t* in_flags) {
-  const int S = interior_strips(self.cols);
-  const int per_dir = S * kHalo * (kStrip / 16);  // 16-byte pieces per direction
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < 2 * per_dir; i += gridDim.x * blockDim.x) {
-    const int dir = i / per_dir, k = i % per_dir;
-    const int s = k / (kHalo * 8), r = (k / 8) % kHalo, c = 16 * (k % 8);
-    const SlabView& src = dir == 0 ? above : below;
-    const int py = dir == 0 ? src.rows + r : kHalo + r;  // above: its last 16 rows
-    const uint4 v = *reinterpret_cast<const uint4*>(src.buf + src.offset(py, kStrip * s + c));
-    *reinterpret_cast<uint4*>(halo + ((static_cast<int64_t>(dir) * 2) * S + s) * kHalo * kStrip +
-                              r * kStrip + c) = v;
-  }
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < 2 * S; i += gridDim.x * blockDim.x)
-    in_flags[i] = 1u;
-}
-
-}  // namespace
-
-cudaError_t launch_ring_fill(const SlabView& self, const SlabView& above, const SlabView& below,
-                             uint8_t* halo, uint32_t* in_flags, cudaStream_t stream) {
-  if (self.rows <= 0 || self.cols <= 0) return cudaSuccess;
-  const int S = interior_strips(self.cols);
-  ring_fill_kernel<<<blocks_for(2LL * S * kHalo * 8), 256, 0, stream>>>(self, above, below, halo,
-                                                                       in_flags);
-  return cudaGetLastError();
-}
-
-}  // namespace ltl

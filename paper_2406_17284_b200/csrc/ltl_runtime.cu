@@ -53,17 +53,15 @@ struct Slab {
   cudaEvent_t ev_step = nullptr;
   std::vector<cudaEvent_t> timing;
   // Ring of row slabs with the halo exchange fused into the step (ltl_tc.cu
-  // Params::ring): own halo rows + delivery counters, and the neighbours'
-  // (peer-accessible in this process: same device, P2P, or CUDA IPC).
-  uint8_t* ring_halo = nullptr;
-  uint32_t* ring_flags = nullptr;
-  CUtensorMap ring_map;                       // own halo rows (loads)
-  CUtensorMap ring_up_map, ring_down_map;     // neighbours' halo rows (stores)
-  uint32_t* up_flags = nullptr;               // neighbours' delivery counters
-  uint32_t* down_flags = nullptr;
-  ltl::SlabView up_slab[2] = {}, down_slab[2] = {};  // neighbours' generation buffers
+  // Params::ring): the neighbours' buffers as 16-row piece maps and their
+  // completion counters (peer-accessible here: same device, P2P, CUDA IPC).
+  uint32_t* ring_sync = nullptr;              // [0] steps completed, [1] CTA ticket
+  CUtensorMap ring_up_map[2], ring_down_map[2];  // per generation buffer
+  const uint32_t* up_done = nullptr;
+  const uint32_t* down_done = nullptr;
+  int32_t up_rows = 0;
   bool ring_ready = false;                    // peers wired
-  uint32_t ring_gen = 0;
+  uint32_t ring_gen = 0;                      // steps since the last ring start
   std::vector<void*> ipc_opened;              // IPC mappings to close
 
   ltl::SlabView view(int which, int32_t cols) const {
@@ -78,7 +76,7 @@ struct ltl_ctx {
   int cur = 0;
   bool external_row_halo = false;
   bool halo_stale = false;  // halo cells the tcgen05 step does not need were not refreshed
-  bool ring_stale = true;   // ring halo buffers do not hold the current generation's rows
+  bool ring_stale = true;   // ring counters not (re)started since the last upload / init
   int64_t launches = 0;     // kernels this context has launched (ltl_kernel_launches)
   std::vector<Slab> slabs;
   std::string err;
@@ -137,22 +135,21 @@ void build_maps(Slab& s, int32_t cols) {
   }
 }
 
-void wire_ring(ltl_ctx* ctx, Slab& s, uint8_t* up_halo, uint32_t* up_flags, uint8_t* const* up_buf,
-               int32_t up_rows, uint8_t* dn_halo, uint32_t* dn_flags, uint8_t* const* dn_buf,
-               int32_t dn_rows) {
-  const int32_t S = ltl::interior_strips(ctx->cols);
+void wire_ring(ltl_ctx* ctx, Slab& s, const uint32_t* up_sync, uint8_t* const* up_buf,
+               int32_t up_rows, const uint32_t* dn_sync, uint8_t* const* dn_buf, int32_t dn_rows) {
   ck(cudaSetDevice(s.dev), "cudaSetDevice");
-  ck(ltl::make_ring_halo_map(&s.ring_up_map, up_halo, S), "tensor map (ring up)");
-  ck(ltl::make_ring_halo_map(&s.ring_down_map, dn_halo, S), "tensor map (ring down)");
-  s.up_flags = up_flags;
-  s.down_flags = dn_flags;
   const int32_t strips = ltl::storage_strips(ctx->cols);
   for (int b = 0; b < 2; ++b) {
-    s.up_slab[b] = ltl::SlabView{up_buf[b], up_rows, ctx->cols, strips,
-                                 static_cast<int64_t>(up_rows + 2 * kHalo) * ltl::kStrip};
-    s.down_slab[b] = ltl::SlabView{dn_buf[b], dn_rows, ctx->cols, strips,
-                                   static_cast<int64_t>(dn_rows + 2 * kHalo) * ltl::kStrip};
+    const ltl::SlabView up{up_buf[b], up_rows, ctx->cols, strips,
+                           static_cast<int64_t>(up_rows + 2 * kHalo) * ltl::kStrip};
+    const ltl::SlabView dn{dn_buf[b], dn_rows, ctx->cols, strips,
+                           static_cast<int64_t>(dn_rows + 2 * kHalo) * ltl::kStrip};
+    ck(ltl::make_piece_map(&s.ring_up_map[b], up), "tensor map (ring up)");
+    ck(ltl::make_piece_map(&s.ring_down_map[b], dn), "tensor map (ring down)");
   }
+  s.up_done = up_sync;
+  s.down_done = dn_sync;
+  s.up_rows = up_rows;
   s.ring_ready = true;
 }
 
@@ -192,14 +189,8 @@ void create_slabs(ltl_ctx* ctx, int32_t num_slabs, const int32_t* dev_ids) {
                            ltl::interior_strips(ctx->cols);
       ck(cudaMalloc(&s.flags, std::max<size_t>(units, 1) * sizeof(uint32_t)), "cudaMalloc flags");
       ck(cudaMemset(s.flags, 0, std::max<size_t>(units, 1) * sizeof(uint32_t)), "memset flags");
-      const int32_t S = ltl::interior_strips(ctx->cols);
-      if (S > 0) {
-        ck(cudaMalloc(&s.ring_halo, ltl::ring_halo_bytes(S)), "cudaMalloc ring halo");
-        ck(cudaMemset(s.ring_halo, 0, ltl::ring_halo_bytes(S)), "memset ring halo");
-        ck(cudaMalloc(&s.ring_flags, 2 * S * sizeof(uint32_t)), "cudaMalloc ring flags");
-        ck(cudaMemset(s.ring_flags, 0, 2 * S * sizeof(uint32_t)), "memset ring flags");
-        ck(ltl::make_ring_halo_map(&s.ring_map, s.ring_halo, S), "tensor map (ring halo)");
-      }
+      ck(cudaMalloc(&s.ring_sync, 2 * sizeof(uint32_t)), "cudaMalloc ring counters");
+      ck(cudaMemset(s.ring_sync, 0, 2 * sizeof(uint32_t)), "memset ring counters");
     }
     ck(cudaStreamCreateWithFlags(&s.stream, cudaStreamNonBlocking), "cudaStreamCreate");
     ck(cudaEventCreateWithFlags(&s.ev_step, cudaEventDisableTiming), "cudaEventCreate");
@@ -223,13 +214,13 @@ void create_slabs(ltl_ctx* ctx, int32_t num_slabs, const int32_t* dev_ids) {
     }
   }
   // in-process ring: every slab's neighbours are peer-accessible already
-  if (num_slabs > 1 && ltl::interior_strips(ctx->cols) > 0)
+  // (a single whole-torus slab is its own ring neighbour: the self-ring)
+  if (ltl::interior_strips(ctx->cols) > 0)
     for (int32_t i = 0; i < num_slabs; ++i) {
       Slab& s = ctx->slabs[i];
       const Slab& up = ctx->slabs[(i - 1 + num_slabs) % num_slabs];
       const Slab& dn = ctx->slabs[(i + 1) % num_slabs];
-      wire_ring(ctx, s, up.ring_halo, up.ring_flags, up.buf, up.rows, dn.ring_halo, dn.ring_flags,
-                dn.buf, dn.rows);
+      wire_ring(ctx, s, up.ring_sync, up.buf, up.rows, dn.ring_sync, dn.buf, dn.rows);
     }
 }
 
@@ -242,8 +233,7 @@ void destroy_ctx(ltl_ctx* ctx) {
     if (s.dstats) cudaFree(s.dstats);
     if (s.flags) cudaFree(s.flags);
     for (void* ptr : s.ipc_opened) cudaIpcCloseMemHandle(ptr);
-    if (s.ring_halo) cudaFree(s.ring_halo);
-    if (s.ring_flags) cudaFree(s.ring_flags);
+    if (s.ring_sync) cudaFree(s.ring_sync);
     if (s.ev_step) cudaEventDestroy(s.ev_step);
     for (cudaEvent_t e : s.timing) cudaEventDestroy(e);
     if (s.stream && s.own_stream) cudaStreamDestroy(s.stream);
@@ -258,8 +248,11 @@ void destroy_ctx(ltl_ctx* ctx) {
 bool wrap_cols(const ltl_ctx* ctx) {
   return ltl::tc_wrap_cols(ctx->cols) && !std::getenv("LTL_NO_WRAP");  // env: diagnostics
 }
+// A single whole-torus slab can also take its row wrap through the ring
+// machinery with itself as both neighbours (LTL_SELF_RING, A/B diagnostics).
+bool self_ring() { return std::getenv("LTL_SELF_RING") != nullptr; }
 bool wrap_rows(const ltl_ctx* ctx) {
-  return ctx->slabs.size() == 1 && !ctx->external_row_halo &&
+  return ctx->slabs.size() == 1 && !ctx->external_row_halo && !self_ring() &&
          ltl::tc_wrap_rows(ctx->slabs[0].rows) && !std::getenv("LTL_NO_WRAP");
 }
 
@@ -275,23 +268,24 @@ void sync_all(ltl_ctx* ctx) {
 // at creation, processes by ltl_ring_connect).
 bool ring_ok(const ltl_ctx* ctx) {
   if (!wrap_cols(ctx) || std::getenv("LTL_NO_RING")) return false;  // env: diagnostics
-  if (ctx->slabs.size() == 1 && !ctx->external_row_halo) return false;  // torus wrap instead
+  if (ctx->slabs.size() == 1 && !ctx->external_row_halo && !self_ring())
+    return false;  // torus wrap by the loads instead
   for (const Slab& s : ctx->slabs)
     if (!s.ring_ready || !ltl::tc_wrap_rows(s.rows)) return false;
   return true;
 }
 
-// Generation-0 ring halo of every slab from its neighbours' current interiors
-// (after uploads / init; all interiors must be in place: callers sync first).
-void enqueue_ring_fill(ltl_ctx* ctx) {
+// (Re)start the ring after uploads / init: every slab's counters back to 0
+// (generation 0 = the buffers as they are now).  No kernel of any slab may be
+// running (callers sync first; processes put a barrier on both sides).
+void start_ring(ltl_ctx* ctx) {
   for (Slab& s : ctx->slabs) {
     ck(cudaSetDevice(s.dev), "cudaSetDevice");
-    ck(ltl::launch_ring_fill(s.view(ctx->cur, ctx->cols), s.up_slab[ctx->cur],
-                             s.down_slab[ctx->cur], s.ring_halo, s.ring_flags, s.stream),
-       "ring fill kernel");
-    ++ctx->launches;
+    ck(cudaStreamSynchronize(s.stream), "cudaStreamSynchronize");
+    ck(cudaMemset(s.ring_sync, 0, 2 * sizeof(uint32_t)), "memset ring counters");
     s.ring_gen = 0;
   }
+  sync_all(ctx);
 }
 
 // Halo refresh of generation buffer `which` on every slab (after all slabs'
@@ -353,16 +347,14 @@ void enqueue_step(ltl_ctx* ctx, const ltl::RuleConsts& rc, uint32_t flags, bool 
     if (ctx->external_row_halo)
       throw std::logic_error(
           "sequencing error: ring halo not filled (ltl_ring_fill after upload / init)");
-    sync_all(ctx);  // every slab's current interior is in place
-    enqueue_ring_fill(ctx);
-    sync_all(ctx);
+    start_ring(ctx);
     ctx->ring_stale = false;
   }
   if (flags & LTL_FLAG_STENCIL) ctx->ring_stale = true;  // stencil generations bypass the ring
   if (ring && ctx->slabs.size() > 1) {
-    // a slab's generation G pushes rows into its neighbours' halo slot that
-    // their generation G-1 read, and on one device the neighbours' kernels
-    // must be able to run: order after their previous step (ev_step)
+    // slabs sharing a device must not spin on each other's counters (a
+    // waiting kernel can hold every SM): order each step after the
+    // neighbours' previous one (ev_step); the counters then never block
     const int32_t G = static_cast<int32_t>(ctx->slabs.size());
     for (int32_t i = 0; i < G; ++i) {
       Slab& s = ctx->slabs[i];
@@ -395,12 +387,13 @@ void enqueue_step(ltl_ctx* ctx, const ltl::RuleConsts& rc, uint32_t flags, bool 
       if (ring) {
         a.ring = 1;
         a.ring_gen = s.ring_gen++;
-        a.halo_in = &s.ring_map;
-        a.halo_up = &s.ring_up_map;
-        a.halo_down = &s.ring_down_map;
-        a.in_flags = s.ring_flags;
-        a.up_flags = s.up_flags;
-        a.down_flags = s.down_flags;
+        a.up_rows = s.up_rows;
+        a.ring_up = &s.ring_up_map[cur];
+        a.ring_down = &s.ring_down_map[cur];
+        a.up_done = s.up_done;
+        a.down_done = s.down_done;
+        a.my_done = s.ring_sync;
+        a.my_ticket = s.ring_sync + 1;
       }
       if (persist) {
         a.load_maps_b = s.load_maps[nxt];
@@ -875,13 +868,13 @@ int ltl_ring_export(ltl_ctx* ctx, void* handles) {
     if (ctx->slabs.size() != 1 || !ctx->external_row_halo)
       throw std::invalid_argument("config error: ring export needs a part context (ltl_create_part)");
     Slab& s = ctx->slabs[0];
-    if (!s.ring_halo) throw std::invalid_argument("config error: empty slab");
+    if (!s.ring_sync || s.rows <= 0 || ctx->cols <= 0)
+      throw std::invalid_argument("config error: empty slab");
     ck(cudaSetDevice(s.dev), "cudaSetDevice");
-    cudaIpcMemHandle_t h[4];
-    ck(cudaIpcGetMemHandle(&h[0], s.ring_halo), "ipc handle (ring halo)");
-    ck(cudaIpcGetMemHandle(&h[1], s.ring_flags), "ipc handle (ring flags)");
-    ck(cudaIpcGetMemHandle(&h[2], s.buf[0]), "ipc handle (buffer 0)");
-    ck(cudaIpcGetMemHandle(&h[3], s.buf[1]), "ipc handle (buffer 1)");
+    cudaIpcMemHandle_t h[3];
+    ck(cudaIpcGetMemHandle(&h[0], s.ring_sync), "ipc handle (ring counters)");
+    ck(cudaIpcGetMemHandle(&h[1], s.buf[0]), "ipc handle (buffer 0)");
+    ck(cudaIpcGetMemHandle(&h[2], s.buf[1]), "ipc handle (buffer 1)");
     std::memcpy(handles, h, sizeof h);
   });
 }
@@ -894,35 +887,34 @@ int ltl_ring_connect(ltl_ctx* ctx, const void* up_handles, int32_t up_rows,
       throw std::invalid_argument("config error: ring connect needs a part context (ltl_create_part)");
     Slab& s = ctx->slabs[0];
     ck(cudaSetDevice(s.dev), "cudaSetDevice");
-    cudaIpcMemHandle_t mine[4];
-    ck(cudaIpcGetMemHandle(&mine[0], s.ring_halo), "ipc handle (ring halo)");
-    // open a neighbour's 4 allocations (its halo, flags, 2 buffers); our own
-    // handles (world size 1) map to our own pointers
+    cudaIpcMemHandle_t mine[3];
+    ck(cudaIpcGetMemHandle(&mine[0], s.ring_sync), "ipc handle (ring counters)");
+    // open a neighbour's 3 allocations (counters, 2 buffers); our own handles
+    // (world size 1) map to our own pointers
     auto open = [&](const void* hv, void** out) {
       const cudaIpcMemHandle_t* h = static_cast<const cudaIpcMemHandle_t*>(hv);
       if (std::memcmp(&h[0], &mine[0], sizeof(cudaIpcMemHandle_t)) == 0) {
-        out[0] = s.ring_halo;
-        out[1] = s.ring_flags;
-        out[2] = s.buf[0];
-        out[3] = s.buf[1];
+        out[0] = s.ring_sync;
+        out[1] = s.buf[0];
+        out[2] = s.buf[1];
         return;
       }
-      for (int i = 0; i < 4; ++i) {
+      for (int i = 0; i < 3; ++i) {
         ck(cudaIpcOpenMemHandle(&out[i], h[i], cudaIpcMemLazyEnablePeerAccess), "ipc open");
         s.ipc_opened.push_back(out[i]);
       }
     };
-    void* up[4];
-    void* dn[4];
+    void* up[3];
+    void* dn[3];
     open(up_handles, up);
-    if (std::memcmp(up_handles, down_handles, 4 * sizeof(cudaIpcMemHandle_t)) == 0)
+    if (std::memcmp(up_handles, down_handles, 3 * sizeof(cudaIpcMemHandle_t)) == 0)
       std::memcpy(dn, up, sizeof up);  // world size 2: one neighbour on both sides
     else
       open(down_handles, dn);
-    uint8_t* upb[2] = {static_cast<uint8_t*>(up[2]), static_cast<uint8_t*>(up[3])};
-    uint8_t* dnb[2] = {static_cast<uint8_t*>(dn[2]), static_cast<uint8_t*>(dn[3])};
-    wire_ring(ctx, s, static_cast<uint8_t*>(up[0]), static_cast<uint32_t*>(up[1]), upb, up_rows,
-              static_cast<uint8_t*>(dn[0]), static_cast<uint32_t*>(dn[1]), dnb, down_rows);
+    uint8_t* upb[2] = {static_cast<uint8_t*>(up[1]), static_cast<uint8_t*>(up[2])};
+    uint8_t* dnb[2] = {static_cast<uint8_t*>(dn[1]), static_cast<uint8_t*>(dn[2])};
+    wire_ring(ctx, s, static_cast<uint32_t*>(up[0]), upb, up_rows, static_cast<uint32_t*>(dn[0]),
+              dnb, down_rows);
     ctx->ring_stale = true;
   });
 }
@@ -946,7 +938,7 @@ int ltl_ring_fill(ltl_ctx* ctx) {
   return guarded(ctx, [&] {
     for (const Slab& s : ctx->slabs)
       if (!s.ring_ready) throw std::logic_error("sequencing error: ring not connected");
-    enqueue_ring_fill(ctx);
+    start_ring(ctx);
     ctx->ring_stale = false;
   });
 }

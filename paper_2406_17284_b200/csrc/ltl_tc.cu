@@ -131,9 +131,8 @@ constexpr uint32_t kIdesc2 = idesc_i8_u8u8_s32(128, kSub);
 struct TcMaps {
   CUtensorMap load[2][kTcLoadMaps];
   CUtensorMap store[2];
-  CUtensorMap halo_in;    // ring: this slab's halo rows {128, 16, 4S}, SWIZZLE_128B
-  CUtensorMap halo_up;    // ring: the upper neighbour's halo rows (peer memory)
-  CUtensorMap halo_down;  // ring: the lower neighbour's halo rows
+  CUtensorMap ring_up;    // ring: 16-row pieces of the upper neighbour's slab (peer memory)
+  CUtensorMap ring_down;  // ring: 16-row pieces of the lower neighbour's slab
 };
 
 struct Params {
@@ -144,17 +143,21 @@ struct Params {
   int32_t inject_fault;
   int32_t wrap_cols, wrap_rows;  // periodic wrap done by the loads (tc_wrap_*)
   int32_t gens;                  // generations in this launch (persistent when > 1)
-  // Ring of row slabs (multi-GPU): the 16 rows above / below come from
-  // ring_halo buffers the neighbours fill, and this slab pushes its first /
-  // last 16 output rows into theirs (TMA stores into peer memory) -- the
-  // halo exchange is fused into the step.  Halo buffer z index:
-  // (dir * 2 + slot) * strips + strip, dir 0 = above, 1 = below, slot =
-  // generation % 2; in_flags[dir * strips + strip] counts deliveries.
+  // Ring of row slabs (multi-GPU), pull model: the first / last band's 16
+  // rows above / below are TMA-loaded straight out of the neighbours' slabs
+  // (peer memory over NVLink, P2P or CUDA IPC) -- the halo exchange is part
+  // of the step's own loads.  Every slab counts its finished step kernels in
+  // *my_done (the launch's last CTA publishes G + 1); a CTA waits once for a
+  // neighbour's counter to reach G before its first piece from that slab.
+  // That wait also orders our next stores to rows the neighbour reads after
+  // its previous step: only first / last band units write those rows.
   int32_t ring;
-  uint32_t ring_gen;             // this generation's number G (data of G is in slot G % 2)
-  uint32_t* in_flags;            // local, written by the neighbours (sys scope)
-  uint32_t* up_flags;            // the upper neighbour's in_flags (its "below" half)
-  uint32_t* down_flags;          // the lower neighbour's in_flags (its "above" half)
+  uint32_t ring_gen;             // G: this launch turns generation G into G + 1
+  int32_t up_rows;               // the upper neighbour's slab height
+  const uint32_t* up_done;       // the neighbours' counters (peer memory)
+  const uint32_t* down_done;
+  uint32_t* my_done;             // this slab's counter and its CTA ticket
+  uint32_t* my_ticket;
   uint32_t* flags;               // per-unit completion counters (bands x strips)
   uint32_t flag_base;            // their common value when the launch starts
   DeviceStats* stats;
@@ -321,16 +324,12 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   fence_proxy_async_smem();
   if (warp == 0 && lane == 0) {
-    if (p.ring) {
-      prefetch_tmap(&maps.halo_in);
-      prefetch_tmap(&maps.halo_up);
-      prefetch_tmap(&maps.halo_down);
-    }
+    // Prefetch every load / store map of the grid (all four load maps even
+    // when the first / last band ones are used by few CTAs: 16384^2 98.4 ->
+    // 95.6 us); the ring maps are fetched on first use.
     for (int set = 0; set < (p.gens > 1 ? 2 : 1); ++set) {
-      prefetch_tmap(&maps.load[set][0]);
+      for (int i = 0; i < kTcLoadMaps; ++i) prefetch_tmap(&maps.load[set][i]);
       prefetch_tmap(&maps.store[set]);
-      if (p.wrap_rows)
-        for (int i = 1; i < kTcLoadMaps; ++i) prefetch_tmap(&maps.load[set][i]);
     }
     for (int i = 0; i < kXStages; ++i) {
       mbar_init(&x_full[i], 1);
@@ -405,6 +404,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // flags must have reached flag_base + 2 gg.  The lanes read the flags of
     // 32 boxes at once (one L2 round trip per 32 boxes, not three per box).
     uint32_t g = 0;
+    bool up_ready = false, down_ready = false;  // ring: neighbours' generation G seen
     for (int gg = 0; gg < p.gens; ++gg) {
       const CUtensorMap* lm = maps.load[gg & 1];
       const uint32_t target = p.flag_base + 2u * static_cast<uint32_t>(gg);
@@ -477,24 +477,19 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const int body = last ? last_rows : kBand;  // interior rows in the box body
                 mbar_arrive_expect_tx(&x_full[s], (last ? last_rows + 2 * kHalo : kBox) * kStrip);
                 int row = 0;  // box row being filled
-                const uint32_t slot_base = (p.ring_gen & 1u) * p.strips + (strip - 1);
-#ifndef LTL_DBG_RING_NOWAIT
-                if (p.ring) {
-                  // the neighbours' rows of generation G for this strip must
-                  // have landed in the halo buffer (pushed by their steps)
-                  if (first) wait_flag_geq_sys(p.in_flags + (strip - 1), p.ring_gen + 1);
-                  if (last) wait_flag_geq_sys(p.in_flags + p.strips + (strip - 1), p.ring_gen + 1);
-                  fence_proxy_async_global();
+                if (p.ring && first && !up_ready) {
+                  wait_flag_geq_sys(p.up_done, p.ring_gen);
+                  fence_proxy_async_global();  // acquired -> TMA reads
+                  up_ready = true;
                 }
-#endif
-#ifdef LTL_DBG_RING_OWNPIECE
-                const bool ring_piece = false;
-#else
-                const bool ring_piece = p.ring;
-#endif
-                if (first) {  // rows -16 .. -1: the torus' other end / the ring halo
-                  if (ring_piece)
-                    tma_load_3d(dst, &maps.halo_in, &x_full[s], 0, 0, slot_base);
+                if (p.ring && last && !down_ready) {
+                  wait_flag_geq_sys(p.down_done, p.ring_gen);
+                  fence_proxy_async_global();
+                  down_ready = true;
+                }
+                if (first) {  // rows -16 .. -1: the torus' other end / the upper slab's last rows
+                  if (p.ring)
+                    tma_load_3d(dst, &maps.ring_up, &x_full[s], 0, p.up_rows, strip);
                   else
                     tma_load_3d(dst, &lm[1], &x_full[s], 0, p.rows, strip);
                   row = kHalo;
@@ -505,12 +500,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                           // halo included unless it is also the first band)
                   tma_load_3d(dst + row * kStrip, &lm[3], &x_full[s], 0,
                               first ? kHalo : band * kBand, strip);
-                  // rows rows .. rows + 15: the torus' rows 0 .. 15 / the ring halo
+                  // rows rows .. rows + 15: the torus' rows 0 .. 15 / the lower slab's first rows
                   uint8_t* bot = dst + (row + body + (first ? 0 : kHalo)) * kStrip;
-                  if (ring_piece)
-                    tma_load_3d(bot, &maps.halo_in, &x_full[s], 0, 0, 2 * p.strips + slot_base);
-                  else
-                    tma_load_3d(bot, &lm[1], &x_full[s], 0, kHalo, strip);
+                  tma_load_3d(bot, p.ring ? &maps.ring_down : &lm[1], &x_full[s], 0, kHalo, strip);
                 }
               }
             }
@@ -678,33 +670,6 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t pend[2 * kPubLag];         // units stored, not yet published
       uint32_t npend = 0, h = 0, n_open = 0;  // n_open: committed, slot not yet freed
       int open_slot[2] = {0, 0};
-      // ring pushes waiting for their release: flag address + commit number
-      constexpr int kRingMax = 8;
-      uint32_t* ring_flag[kRingMax];
-      uint32_t ring_seq[kRingMax];
-      int nring = 0;
-      uint32_t ncommit = 0;
-      auto ring_publish = [&](uint32_t done_upto) {  // groups <= done_upto complete
-        int keep = 0;
-        bool fenced = false;
-        for (int i = 0; i < nring; ++i) {
-          if (static_cast<int32_t>(done_upto - ring_seq[i]) >= 0) {
-            if (!fenced) {
-#ifndef LTL_DBG_RING_NOFENCE
-              fence_proxy_async_global();
-              fence_acq_rel_sys();
-#endif
-              fenced = true;
-            }
-            red_relaxed_add_sys(ring_flag[i], 1);
-          } else {
-            ring_flag[keep] = ring_flag[i];
-            ring_seq[keep] = ring_seq[i];
-            ++keep;
-          }
-        }
-        nring = keep;
-      };
       for (int gg = 0; gg < p.gens; ++gg) {
         SegIter it(p, gg);
         int band, t0, t1;
@@ -716,40 +681,12 @@ __global__ void __launch_bounds__(kThreads, 1)
               const uint8_t* src = smem + kSmemStage + (grp * kStageSlots + slot) * kStageBytes;
               tma_store_3d(&maps.store[gg & 1], src, 0, band * kBand + kSub * grp,
                            t % p.strips + 1);
-#ifdef LTL_DBG_RING_NOPUSH
-              if (false) {
-#else
-              if (p.ring) {
-#endif
-                // push the slab's first / last 16 rows of generation G+1 into
-                // the neighbours' halo buffers (slot (G+1) % 2), then count them
-                const int si = t % p.strips;
-                const uint32_t slot = ((p.ring_gen + 1u) & 1u) * p.strips + si;
-                const int last_rows = p.rows - kBand * band;
-                if (band == 0 && grp == 0) {  // rows 0..15 -> above neighbour's "below"
-                  tma_store_3d(&maps.halo_up, src, 0, 0, 2 * p.strips + slot);
-                  ring_flag[nring] = p.up_flags + p.strips + si;
-                  ring_seq[nring++] = ncommit;
-                }
-                if (band == p.bands - 1 && grp == (last_rows - kHalo) / kSub) {
-                  // rows rows-16 .. rows-1 -> below neighbour's "above"
-                  const int off = (last_rows - kHalo) % kSub;  // 16 or 48: whole atoms
-                  tma_store_3d(&maps.halo_down, src + off * kStrip, 0, 0, slot);
-                  ring_flag[nring] = p.down_flags + si;
-                  ring_seq[nring++] = ncommit;
-                }
-              }
               tma_store_commit();
-              ++ncommit;
               // the previous group's store has read its slot: free it
               tma_store_wait_read<1>();
               if (n_open) mbar_arrive(&st_empty[open_slot[0]]);
               open_slot[0] = grp * kStageSlots + slot;
               n_open = 1;
-            }
-            if (nring > kRingMax - 3) {  // release the older pushes (almost never blocks)
-              tma_store_wait_all<4>();
-              ring_publish(ncommit - 5);
             }
             if (p.gens > 1) {
               pend[h % (2 * kPubLag)] = static_cast<uint32_t>(band * p.strips + t % p.strips);
@@ -774,7 +711,6 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
       tma_store_wait_all<0>();
-      if (nring) ring_publish(ncommit);
       (void)open_slot[1];
     }
   } else {
@@ -900,6 +836,18 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_before();
   __syncthreads();
   LTL_TRACE_CTA(15);
+  if (p.ring && threadIdx.x == 0) {
+    // Every store of this CTA has completed (the store warp waited for them
+    // before the barrier).  One ticket per CTA; the launch's last CTA
+    // publishes generation G + 1 to the neighbours.
+    fence_proxy_async_global();
+    fence_acq_rel_sys();
+    if (atomicAdd(p.my_ticket, 1u) + 1u == gridDim.x) {
+      *p.my_ticket = 0u;  // the next launch (after this grid completes) counts anew
+      fence_acq_rel_sys();
+      red_relaxed_add_sys(p.my_done, 1u);
+    }
+  }
   if (warp == 1) tmem_dealloc(tmem, kTmemCols);
 }
 
@@ -950,9 +898,11 @@ cudaError_t launch_tc_step(const TcLaunch& a, cudaStream_t stream) {
     p.gens = 1;
     p.wrap_rows = 0;
     p.ring_gen = a.ring_gen;
-    p.in_flags = a.in_flags;
-    p.up_flags = a.up_flags;
-    p.down_flags = a.down_flags;
+    p.up_rows = a.up_rows;
+    p.up_done = a.up_done;
+    p.down_done = a.down_done;
+    p.my_done = a.my_done;
+    p.my_ticket = a.my_ticket;
   }
   p.flags = a.flags;
   p.flag_base = a.flag_base;
@@ -987,9 +937,8 @@ cudaError_t launch_tc_step(const TcLaunch& a, cudaStream_t stream) {
   }
   maps.store[0] = *a.store_map;
   maps.store[1] = a.store_map_b ? *a.store_map_b : *a.store_map;
-  maps.halo_in = a.ring ? *a.halo_in : *a.store_map;
-  maps.halo_up = a.ring ? *a.halo_up : *a.store_map;
-  maps.halo_down = a.ring ? *a.halo_down : *a.store_map;
+  maps.ring_up = a.ring ? *a.ring_up : *a.store_map;
+  maps.ring_down = a.ring ? *a.ring_down : *a.store_map;
   if (a.stats) return cudaLaunchKernelEx(&cfg, ltl_tc_step_kernel<true>, maps, p);
   return cudaLaunchKernelEx(&cfg, ltl_tc_step_kernel<false>, maps, p);
 }

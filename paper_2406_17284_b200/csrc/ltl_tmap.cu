@@ -82,11 +82,12 @@ cudaError_t make_store_map(CUtensorMap* map, const SlabView& s) {
                  64, CU_TENSOR_MAP_SWIZZLE_128B);
 }
 
-// Ring halo rows (ltl_tc.cu Params::ring): {128 columns, 16 rows, 4 * strips}
-// boxes of one strip's 16 rows, SWIZZLE_128B like the box they join.
-cudaError_t make_ring_halo_map(CUtensorMap* map, uint8_t* halo, int32_t strips) {
-  if (strips <= 0) return cudaSuccess;
-  return encode3(map, halo, kHalo, 4ull * strips, static_cast<uint64_t>(kHalo) * kStrip, kStrip,
+// 16-row pieces of a slab's padded rows (the ring's rows above / below, read
+// out of the neighbour's slab in peer memory): load map [1] of any slab.
+cudaError_t make_piece_map(CUtensorMap* map, const SlabView& s) {
+  if (s.rows <= 0 || s.cols <= 0) return cudaSuccess;
+  return encode3(map, s.buf, static_cast<uint64_t>(s.rows) + 2 * kHalo,
+                 static_cast<uint64_t>(s.strips), static_cast<uint64_t>(s.strip_bytes), kStrip,
                  kHalo, CU_TENSOR_MAP_SWIZZLE_128B);
 }
 

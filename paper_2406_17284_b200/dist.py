@@ -78,10 +78,11 @@ class PartitionedTorus:
 
     Two exchange paths for the 16 boundary rows per generation:
       * ring (cols % 128 == 0, slab rows % 32 == 0): fused into the step --
-        the kernel TMA-stores its first / last rows straight into the ring
-        neighbours' halo buffers (CUDA IPC peer memory over NVLink) and bumps
-        per-strip flags their next step waits on.  No NCCL on the data path,
-        no extra launches, no host synchronisation;
+        the kernel's first / last band units TMA-load the 16 rows beyond the
+        slab straight out of the ring neighbours' slabs (CUDA IPC peer memory
+        over NVLink) once the neighbours' step counters say that generation
+        is complete.  No NCCL on the data path, no extra launches, no host
+        synchronisation;
       * otherwise: ltl_pack_edges -> NCCL send/recv (exchange_edges) ->
         ltl_unpack_halo on the same stream.
     """
@@ -135,8 +136,9 @@ class PartitionedTorus:
         self.torus.set_stream(stream_ptr)
 
     def _ring_fill(self) -> None:
-        # every rank's interior must be in place before anyone reads it, and
-        # every rank's generation-0 halo / flags before anyone pushes into them
+        # every rank's interior must be in place and its kernels done before
+        # the counters restart, and every rank's counters restarted before
+        # anyone steps
         self.torus.synchronize()
         if self.plan.world > 1:
             self.dist.barrier()

@@ -361,10 +361,10 @@ class DeviceTorus:
         return ptr.value, strip_bytes.value, rows.value
 
     # ---- multi-process ring with the halo exchange fused into the step
-    RING_HANDLE_BYTES = 4 * 64
+    RING_HANDLE_BYTES = 3 * 64  # include/ltl_b200.h LTL_RING_HANDLE_BYTES
 
     def ring_export(self) -> bytes:
-        """4 CUDA IPC handles (halo rows, flags, both generation buffers)."""
+        """CUDA IPC handles of the slab's step counters and both generation buffers."""
         buf = ctypes.create_string_buffer(self.RING_HANDLE_BYTES)
         self._check(self.lib.ltl_ring_export(self._ctx, buf))
         return buf.raw
@@ -373,7 +373,7 @@ class DeviceTorus:
         self._check(self.lib.ltl_ring_connect(self._ctx, up, up_rows, down, down_rows))
 
     def ring_fill(self) -> None:
-        """Generation-0 halo rows from the neighbours (after every rank's upload)."""
+        """Restart the ring's step counters (after every rank's upload; barriers around)."""
         self._check(self.lib.ltl_ring_fill(self._ctx))
 
     def ring_active(self) -> bool:
