@@ -96,7 +96,7 @@ class Clocks:
         time.sleep(0.15)
         self.proc.terminate()
         self.proc.wait()
-        sm, mx, reasons = [], 0, set()
+        sm, mx, reasons, watts = [], 0, set(), []
         names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
         with open(self.path) as fh:
             for line in fh:
@@ -108,6 +108,10 @@ class Clocks:
                     mx = max(mx, float(parts[2]))
                 except ValueError:
                     continue
+                try:
+                    watts.append(float(parts[3]))
+                except ValueError:
+                    pass
                 for name, val in zip(names, parts[5:9]):
                     if val.lower() == "active":
                         reasons.add(name)
@@ -115,7 +119,7 @@ class Clocks:
         if not sm:
             return None
         return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
-                "samples": len(sm)}
+                "samples": len(sm), "power_w": statistics.median(watts) if watts else None}
 
 
 def cpu_baseline(grid, gens: int):

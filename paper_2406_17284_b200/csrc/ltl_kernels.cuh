@@ -101,6 +101,7 @@ struct TcLaunch {
   int32_t gens;
   uint32_t* flags;
   uint32_t flag_base;
+
   // Ring of slabs (multi-GPU, one generation per launch), pull model: the
   // first / last band's 16 rows above / below are loaded from the
   // neighbours' slabs (ring_up / ring_down: piece maps over their buffers
@@ -124,7 +125,8 @@ struct TcLaunch {
   long long* trace;    // debug timeline (LTL_TC_TRACE), nullptr = off
 };
 cudaError_t launch_tc_step(const TcLaunch& a, cudaStream_t stream);
-int tc_persistent_ctas(int32_t rows, int num_sms);  // 0: no multi-generation launch
+int tc_persistent_ctas(int32_t rows, int32_t cols, int num_sms);  // 0: no multi-generation launch
+int tc_sweep_chunks(int32_t strips);  // chunks per band of a multi-generation launch
 size_t tc_smem_bytes();
 
 // Host-side tensor-map builders (driver entry point fetched at runtime).

@@ -328,7 +328,7 @@ bool persistent_ok(const ltl_ctx* ctx, uint32_t flags) {
     return false;
   int sms = 0;
   ck(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->slabs[0].dev), "sm count");
-  return ltl::tc_persistent_ctas(ctx->slabs[0].rows, sms) > 0;
+  return ltl::tc_persistent_ctas(ctx->slabs[0].rows, ctx->cols, sms) > 0;
 }
 
 // `gens` generations (cur -> nxt -> ...): one persistent launch when

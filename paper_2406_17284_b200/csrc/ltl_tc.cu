@@ -59,6 +59,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 #include <cstdlib>
 
@@ -143,6 +144,7 @@ struct Params {
   int32_t inject_fault;
   int32_t wrap_cols, wrap_rows;  // periodic wrap done by the loads (tc_wrap_*)
   int32_t gens;                  // generations in this launch (persistent when > 1)
+  int32_t sweep_chunks;          // chunks per band of a persistent launch (SegIter)
   // Ring of row slabs (multi-GPU), pull model: the first / last band's 16
   // rows above / below are TMA-loaded straight out of the neighbours' slabs
   // (peer memory over NVLink, P2P or CUDA IPC) -- the halo exchange is part
@@ -203,17 +205,34 @@ __device__ __forceinline__ long long global_ns() {
 //     k's strips start at the rotation rot_k = round(k (S - U'/G)) mod S, a run
 //     crossing the torus seam (strip t is t mod S): CTA b + 1 then meets band
 //     k + 1 at the strip where CTA b meets band k.
+// Multi-generation (persistent) launches sweep instead: generation g is cut
+// into chunks of C per band (band position k, chunk j: strips
+// [jS/C, (j+1)S/C) of band (k + g) mod B), numbered g*B*C + k*C + j and dealt
+// round-robin to the CTAs, so all CTAs advance through the bands together as
+// one wavefront across generation boundaries.  Rotating the band order by one
+// per generation puts every input of a unit (bands k-1 .. k+1 of generation
+// g-1 = its sweep positions k .. k+2) (B - 2) bands behind it in the global
+// order: no unit waits in steady state, whatever the CTA count, and no CTA
+// holds units of a generation before all of its units of the previous one
+// (deadlock-free with all CTAs resident).
 struct SegIter {
   int64_t u, u_end, U;  // remainder part: linear unit range of this CTA
   int32_t S, G, B0, round, rounds;
   bool rotate;
-  int32_t start;  // first strip of a round (multi-generation launches alternate)
-  __device__ SegIter(const Params& p, int gen)
-      : S(p.strips), G(static_cast<int32_t>(gridDim.x)), round(0), rotate(p.wrap_cols != 0) {
-    // In a multi-generation launch generation g + 1 starts half a band away
-    // from where generation g started: its first units then only need units
-    // of g that finished half a generation earlier (no drain at the seam).
-    start = (p.gens > 1 && (gen & 1)) ? S / 2 : 0;
+  // sweep (multi-generation) mode: global chunk index, this generation's end
+  int64_t ci, c_base, c_end;
+  int32_t C, B, gen;
+  __device__ SegIter(const Params& p, int gen_)
+      : S(p.strips), G(static_cast<int32_t>(gridDim.x)), round(0), rotate(p.wrap_cols != 0),
+        C(p.gens > 1 ? p.sweep_chunks : 0), B(p.bands), gen(gen_) {
+    if (C > 0) {
+      c_base = static_cast<int64_t>(gen) * B * C;
+      c_end = c_base + static_cast<int64_t>(B) * C;
+      ci = c_base + ((static_cast<int64_t>(blockIdx.x) - c_base) % G + G) % G;
+      rounds = 0;
+      u = u_end = 0;
+      return;
+    }
     rounds = p.bands / G;  // whole bands per CTA in step
     B0 = rounds * G;       // first band of the remainder
     U = static_cast<int64_t>(p.bands - B0) * S;
@@ -221,11 +240,21 @@ struct SegIter {
     u_end = U * (blockIdx.x + 1) / G;
   }
   __device__ bool next(int& band, int& t0, int& t1) {
+    if (C > 0) {
+      if (ci >= c_end) return false;
+      const int m = static_cast<int>(ci - c_base);
+      const int k = m / C, j = m % C;
+      band = (k + gen) % B;
+      t0 = S * j / C;
+      t1 = S * (j + 1) / C;
+      ci += G;
+      return true;
+    }
     if (round < rounds) {
       band = static_cast<int>(blockIdx.x) + round * G;
       ++round;
-      t0 = start;
-      t1 = start + S;
+      t0 = 0;
+      t1 = S;
       return true;
     }
     if (u >= u_end) return false;
@@ -855,18 +884,26 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 size_t tc_smem_bytes() { return kSmemAlloc; }
 
-// A multi-generation launch needs a schedule in which every unit's neighbours
-// (across the torus seam too) are processed at the same time in every
-// generation: whole bands in step, so the CTA count must divide the band
-// count.  0 = fall back to one generation per launch.
-int tc_persistent_ctas(int32_t rows, int num_sms) {
-  const int bands = (rows + kBand - 1) / kBand;
-  // Measured (16384^2: 128 of 148 SMs persistent ~= 148 SMs one launch per
-  // generation; 32768^2, 65536^2: per-generation launches on all SMs faster):
-  // only worth it when the divisor is the whole GPU.
-  for (int d = num_sms; d >= 1; --d)
-    if (bands % d == 0) return d == num_sms || std::getenv("LTL_FORCE_PERSIST") ? d : 0;
-  return 0;
+// Multi-generation launches (SegIter's sweep): one CTA per SM, all resident.
+// A generation boundary of one-launch-per-generation costs ~12.7 us (grid
+// drain + refill: per-launch time = 12.7 us + 5.09 ns x units at 16384^2 ..
+// 65536^2), the sweep ~5.5 ns per unit (its chunk edges re-read ~20 % more
+// box bytes from L2) and no boundary: it wins below ~190 units per SM and
+// generation (16384^2: 91.5 vs 98.5 us; 32768^2: 360 vs 349 us).  The torus
+// must be tall enough for the sweep's (B - 2)-band dependency distance to
+// clear the wavefront.  0 = one generation per launch.
+int tc_persistent_ctas(int32_t rows, int32_t cols, int num_sms) {
+  const int64_t bands = (rows + kBand - 1) / kBand;
+  const int64_t units = bands * interior_strips(cols);
+  if (std::getenv("LTL_FORCE_PERSIST"))  // tests: small tori, fewer CTAs
+    return static_cast<int>(units < num_sms ? units : num_sms);
+  return bands >= 16 && units >= 8LL * num_sms && units <= 190LL * num_sms ? num_sms : 0;
+}
+
+int tc_sweep_chunks(int32_t strips) {  // <= 16 units per chunk (measured: 8 / 32 / 64 slower)
+  int per = 16;
+  if (const char* e = std::getenv("LTL_SWEEP_UNITS")) per = std::max(1, std::atoi(e));  // tuning
+  return (strips + per - 1) / per;
 }
 
 cudaError_t launch_tc_step(const TcLaunch& a, cudaStream_t stream) {
@@ -912,8 +949,9 @@ cudaError_t launch_tc_step(const TcLaunch& a, cudaStream_t stream) {
   const int64_t units = static_cast<int64_t>(p.bands) * p.strips;
   int64_t grid = units < num_sms ? units : num_sms;
   if (p.gens > 1) {
-    grid = tc_persistent_ctas(a.rows, num_sms);
+    grid = tc_persistent_ctas(a.rows, a.cols, num_sms);
     if (grid <= 0) return cudaErrorNotSupported;
+    p.sweep_chunks = tc_sweep_chunks(p.strips);
   }
   if (a.grid > 0 && a.grid < grid) grid = a.grid;
   if (const char* e = std::getenv("LTL_TC_GRID")) {  // tuning knob (sweeps only)

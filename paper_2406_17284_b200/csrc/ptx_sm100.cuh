@@ -170,11 +170,8 @@ __device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
-#ifdef LTL_DBG_RING_GPU_SCOPE
-#define LTL_RING_SCOPE "gpu"
-#else
+// Ring counters are read / written by peer GPUs: system scope.
 #define LTL_RING_SCOPE "sys"
-#endif
 __device__ __forceinline__ void fence_acq_rel_sys() {
   asm volatile("fence.acq_rel." LTL_RING_SCOPE ";" ::: "memory");
 }

@@ -218,7 +218,7 @@ def test_persistent_multi_generation(ltl, orc, rows, cols, monkeypatch):
 
 
 def test_persistent_full_gpu_equals_per_generation(ltl, monkeypatch):
-    """n = 148 x 128: the band count fills every SM, so ltl_run takes the
+    """n = 148 x 128 (units per SM in the sweep range), so ltl_run takes the
     multi-generation launch by default; bit-identical to one launch per
     generation (LTL_NO_PERSIST)."""
     import torch
