@@ -58,13 +58,13 @@ def measured_peaks():
 
 
 def ncu_traffic():
-    """dram read+write bytes per launch of the step kernel from the committed
-    ncu --set full capture (profiles/), or None."""
+    """dram read+write bytes per generation of the step kernel from the
+    committed ncu --set full capture (profiles/), or None."""
     path = os.path.join(ROOT, "profiles", "ncu_tc_step.json")
     try:
         with open(path) as fh:
             d = json.load(fh)
-        return d.get("dram_bytes_per_launch"), d.get("n")
+        return d.get("dram_bytes_per_generation"), d.get("n")
     except (OSError, ValueError):
         return None, None
 
@@ -195,9 +195,8 @@ def ours_single(args):
 
     clocks = Clocks()
     clocks.start()
-    l0 = torus.kernel_launches()
     total_ms, kernel_ms = torus.time(rule, steps, warmup, stencil=stencil)
-    launches = round((torus.kernel_launches() - l0) * steps / (steps + warmup))
+    launches = torus.time_launches()  # inside the timed loop
     clk = clocks.stop()
 
     cells = n * n
@@ -237,8 +236,11 @@ def ours_single(args):
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"],
                      "unit": "GB/s", "frac": achieved / peaks["hbm_gbs"], "traffic": traffic,
                      "peak_source": f"{peak_kind} hbm_gbs (MEASURED_PEAKS.json)",
-                     "kernel_ms_per_launch": kern_avg_s * 1e3,
-                     "algorithmic_bytes_per_launch": BYTES_PER_CELL * cells},
+                     "kernel_ms_per_generation": kern_avg_s * 1e3,
+                     "algorithmic_bytes_per_generation": BYTES_PER_CELL * cells,
+                     "per": ("generation: one persistent launch runs all timed generations"
+                             if launches == 1 and steps > 1 else
+                             "generation: one step-kernel launch each")},
         "clocks": clk,
     }
     if not args.no_cpu_baseline:

@@ -139,9 +139,12 @@ int ltl_synchronize(ltl_ctx* ctx);
  * keep their programmatic overlap); kernel_ms = the main step kernel's
  * average duration over a further sample of up to 100 generations, each
  * launch bracketed by its own events, times `steps` (the roofline kernel).
+ * A multi-generation (persistent) launch is its own kernel sample.
  * Either output pointer may be NULL. */
 int ltl_time(ltl_ctx* ctx, const ltl_rule_c* rule, int32_t steps, int32_t warmup,
              uint32_t flags, double* total_ms, double* kernel_ms);
+/* Kernels launched inside the last ltl_time's timed loop (total_ms region). */
+int64_t ltl_time_launches(const ltl_ctx* ctx);
 
 /* End-to-end: upload interior from host memory, run `steps` generations,
  * download the interior into `interior_out` -- the whole run_engine(Cat)

@@ -78,6 +78,7 @@ struct ltl_ctx {
   bool halo_stale = false;  // halo cells the tcgen05 step does not need were not refreshed
   bool ring_stale = true;   // ring counters not (re)started since the last upload / init
   int64_t launches = 0;     // kernels this context has launched (ltl_kernel_launches)
+  int64_t timed_launches = 0;  // inside the last ltl_time's timed loop
   std::vector<Slab> slabs;
   std::string err;
 };
@@ -598,6 +599,8 @@ void ltl_destroy(ltl_ctx* ctx) {
 
 int64_t ltl_kernel_launches(const ltl_ctx* ctx) { return ctx ? ctx->launches : -1; }
 
+int64_t ltl_time_launches(const ltl_ctx* ctx) { return ctx ? ctx->timed_launches : 0; }
+
 const char* ltl_last_error(const ltl_ctx* ctx) {
   return ctx ? ctx->err.c_str() : g_last_error.c_str();
 }
@@ -700,7 +703,9 @@ int ltl_time(ltl_ctx* ctx, const ltl_rule_c* rule, int32_t steps, int32_t warmup
       }
       ck(cudaEventRecord(s.timing[0], s.stream), "event");
     }
+    const int64_t l0 = ctx->launches;
     enqueue_step(ctx, rc, flags, false, nullptr, nullptr, steps);
+    ctx->timed_launches = ctx->launches - l0;
     for (Slab& s : ctx->slabs) {
       ck(cudaSetDevice(s.dev), "cudaSetDevice");
       ck(cudaEventRecord(s.timing[1], s.stream), "event");

@@ -58,8 +58,8 @@ class ltl_stats_c(ctypes.Structure):
 # Every symbol include/ltl_b200.h declares (tests check the .so exports them all).
 EXPORTS = (
     "ltl_create", "ltl_create_torus", "ltl_destroy", "ltl_last_error", "ltl_rows", "ltl_cols",
-    "ltl_num_slabs", "ltl_kernel_launches", "ltl_upload", "ltl_download", "ltl_upload_interior",
-    "ltl_download_interior", "ltl_run", "ltl_run_async", "ltl_synchronize", "ltl_time",
+    "ltl_num_slabs", "ltl_kernel_launches", "ltl_time_launches", "ltl_upload", "ltl_download",
+    "ltl_upload_interior", "ltl_download_interior", "ltl_run", "ltl_run_async", "ltl_synchronize", "ltl_time",
     "ltl_run_interior", "ltl_create_part", "ltl_set_stream", "ltl_step_part", "ltl_fill_halo",
     "ltl_slab_buffer", "ltl_pack_edges", "ltl_unpack_halo", "ltl_ring_export",
     "ltl_ring_connect", "ltl_ring_fill", "ltl_ring_active", "ltl_ring_disconnect",
@@ -92,6 +92,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
         "ltl_cols": ([vp], ctypes.c_int32),
         "ltl_num_slabs": ([vp], ctypes.c_int32),
         "ltl_kernel_launches": ([vp], ctypes.c_int64),
+        "ltl_time_launches": ([vp], ctypes.c_int64),
         "ltl_upload": ([vp, u8p, ctypes.c_int32], ctypes.c_int),
         "ltl_download": ([vp, u8p, ctypes.c_int32], ctypes.c_int),
         "ltl_upload_interior": ([vp, u8p], ctypes.c_int),
@@ -351,6 +352,10 @@ class DeviceTorus:
     def kernel_launches(self) -> int:
         """Kernels this context has launched so far (ltl_kernel_launches)."""
         return int(self.lib.ltl_kernel_launches(self._ctx))
+
+    def time_launches(self) -> int:
+        """Kernels launched inside the last time() call's timed loop."""
+        return int(self.lib.ltl_time_launches(self._ctx))
 
     def slab_buffer(self, slab: int = 0, which: int = 0):
         """(device pointer, strip bytes, interior rows) of a generation buffer
