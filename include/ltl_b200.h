@@ -211,6 +211,22 @@ int ltl_ring_disconnect(ltl_ctx* ctx);
 int ltl_slab_buffer(ltl_ctx* ctx, int32_t slab, int32_t which, void** dev_ptr,
                     int64_t* strip_bytes, int32_t* rows);
 
+/* --- CATSNAP v1 snapshots, streamed from / to the device ------------------
+ * snapshot_write / snapshot_read (src/snapshot.cpp:18-91, format in
+ * include/catsim/snapshot.hpp): "CATSNAP 1 <n> <f> <rowmajor|fragment>\n" +
+ * the n x n interior bytes, row-major.  Byte-identical to the reference's
+ * files; the grid never exists on the host (the device gathers / scatters
+ * the strips, 32 MB pinned chunks overlap PCIe with file I/O).  Square
+ * contexts only.  Errors: LTL_ERR_RUNTIME "snapshot format error: ..." with
+ * the reference's text; a file whose n / f differ from the context is
+ * LTL_ERR_INVALID_ARGUMENT "geometry error: ...".  ltl_snapshot_read
+ * returns the declared layout (LTL_LAYOUT_*); the device holds cells only. */
+int ltl_snapshot_write(ltl_ctx* ctx, const char* path, int32_t layout);
+int ltl_snapshot_read(ltl_ctx* ctx, const char* path, int32_t* layout_out);
+/* Header only (no device): the geometry and layout a snapshot declares, with
+ * the reader's header checks. */
+int ltl_snapshot_probe(const char* path, int32_t* n, int32_t* f, int32_t* layout);
+
 /* --- host-side rule helpers (pure C, no device) --------------------------- */
 
 /* parse_ltl_rule (src/rule.cpp:61-87): returns LTL_OK or

@@ -150,6 +150,10 @@ class Reference:
                                        _u8p, _i64p]
         lib.ref_reductions.argtypes = [ctypes.c_int32, ctypes.c_int32, _u8p, ctypes.c_char_p,
                                        _i32p, _i32p]
+        lib.ref_snapshot_write.argtypes = [ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, _u8p,
+                                           ctypes.c_char_p]
+        lib.ref_snapshot_read.argtypes = [ctypes.c_char_p, _i32p, _i32p, _i32p, _u8p,
+                                          ctypes.c_int64]
         self.lib = lib
 
     def _check(self, status: int):
@@ -218,6 +222,22 @@ class Reference:
         self._check(self.lib.ref_reductions(n, f, _ptr(g, _u8p), rule_text.encode(),
                                             _ptr(h, _i32p), _ptr(red, _i32p)))
         return h, red
+
+    def snapshot_write(self, grid: np.ndarray, path: str, f: int = 16, layout: int = 0) -> None:
+        """catsim::snapshot_write of a row-major interior, as layout 0 / 1."""
+        g = np.ascontiguousarray(grid, np.uint8)
+        self._check(self.lib.ref_snapshot_write(g.shape[0], f, layout, _ptr(g, _u8p),
+                                                path.encode()))
+
+    def snapshot_read(self, path: str):
+        """catsim::snapshot_read -> (interior, f, layout)."""
+        n, f, lay = (np.zeros(1, np.int32) for _ in range(3))
+        self._check(self.lib.ref_snapshot_read(path.encode(), _ptr(n, _i32p), _ptr(f, _i32p),
+                                               _ptr(lay, _i32p), None, 0))
+        out = np.zeros((int(n[0]), int(n[0])), np.uint8)
+        self._check(self.lib.ref_snapshot_read(path.encode(), _ptr(n, _i32p), _ptr(f, _i32p),
+                                               _ptr(lay, _i32p), _ptr(out, _u8p), out.size))
+        return out, int(f[0]), int(lay[0])
 
 
 def rule_text(rule) -> str:

@@ -23,6 +23,7 @@
 #include "catsim/grid.hpp"
 #include "catsim/layout.hpp"
 #include "catsim/rule.hpp"
+#include "catsim/snapshot.hpp"
 
 namespace {
 
@@ -175,6 +176,35 @@ int ref_reductions(int32_t n, int32_t f, const uint8_t* interior_in,
         h_out[static_cast<std::size_t>(y) * p + x] = h.at(y, x);
         r_out[static_cast<std::size_t>(y) * p + x] = red.at(y, x);
       }
+  });
+}
+
+// snapshot_write (src/snapshot.cpp:18-37) of an n x n interior in `layout`
+// (0 row-major, 1 fragment-contiguous) to `path`.
+int ref_snapshot_write(int32_t n, int32_t f, int32_t layout, const uint8_t* interior,
+                       const char* path) {
+  return guarded([&] {
+    catsim::Grid g = grid_from_interior(n, f, interior);
+    if (layout == 1) g = catsim::to_fragment_layout(g);
+    catsim::snapshot_write(g, std::string(path));
+  });
+}
+
+// snapshot_read (src/snapshot.cpp:39-91): geometry + layout first (interior
+// may be NULL to probe), then the interior in row-major order.
+int ref_snapshot_read(const char* path, int32_t* n, int32_t* f, int32_t* layout,
+                      uint8_t* interior, int64_t capacity) {
+  return guarded([&] {
+    const catsim::Grid g = catsim::snapshot_read(std::string(path));
+    *n = g.n;
+    *f = g.f;
+    *layout = g.layout == catsim::Layout::RowMajor ? 0 : 1;
+    if (!interior) return;
+    if (static_cast<int64_t>(g.n) * g.n > capacity)
+      throw std::invalid_argument("capacity");
+    for (int y = 0; y < g.n; ++y)
+      for (int x = 0; x < g.n; ++x)
+        interior[static_cast<std::size_t>(y) * g.n + x] = g.interior(y, x);
   });
 }
 

@@ -158,6 +158,9 @@ cudaError_t launch_halo_fill(const SlabView& self, const SlabView& above, const 
 // Dense row-major rows x cols interior <-> strip slab interior.
 cudaError_t launch_to_strips(const uint8_t* dense, const SlabView& s, cudaStream_t stream);
 cudaError_t launch_from_strips(const SlabView& s, uint8_t* dense, cudaStream_t stream);
+// *bad |= 1 if any of dense[0, n) is not 0 / 1 (snapshot payloads).
+cudaError_t launch_check_cells(const uint8_t* dense, int64_t n, int32_t* bad,
+                               cudaStream_t stream);
 // top[16][cols] <- interior rows [0, 16); bot[16][cols] <- rows [rows-16, rows).
 cudaError_t launch_pack_edges(const SlabView& s, uint8_t* top, uint8_t* bot, cudaStream_t stream);
 // halo rows above <- top_halo[16][cols], below <- bot_halo[16][cols] (with the

@@ -68,6 +68,23 @@ __global__ void unpack_halo_kernel(SlabView s, const uint8_t* top, const uint8_t
   }
 }
 
+// Any byte of dense[0, n) above 1 -> *bad = 1 (snapshot payload check,
+// src/snapshot.cpp:79-80), 16 bytes per thread.
+__global__ void check_cells_kernel(const uint8_t* dense, int64_t n, int32_t* bad) {
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  uint32_t acc = 0;
+  const int64_t n16 = (reinterpret_cast<uintptr_t>(dense) % 16 == 0) ? n / 16 : 0;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n16;
+       i += stride) {
+    const uint4 v = reinterpret_cast<const uint4*>(dense)[i];
+    acc |= (v.x | v.y | v.z | v.w) & 0xFEFEFEFEu;
+  }
+  for (int64_t i = 16 * n16 + static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+       i < n; i += stride)
+    acc |= dense[i] & 0xFEu;
+  if (__syncthreads_or(acc != 0) && threadIdx.x == 0) atomicOr(bad, 1);
+}
+
 int blocks_for(int64_t work) {
   int64_t b = (work + 255) / 256;
   if (b > 148 * 8) b = 148 * 8;
@@ -87,6 +104,13 @@ cudaError_t launch_from_strips(const SlabView& s, uint8_t* dense, cudaStream_t s
   if (s.rows <= 0 || s.cols <= 0) return cudaSuccess;
   const int64_t work = static_cast<int64_t>(s.rows) * (s.cols % 16 == 0 ? s.cols / 16 : s.cols);
   relayout_kernel<false><<<blocks_for(work), 256, 0, stream>>>(dense, s);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_check_cells(const uint8_t* dense, int64_t n, int32_t* bad,
+                               cudaStream_t stream) {
+  if (n <= 0) return cudaSuccess;
+  check_cells_kernel<<<blocks_for((n + 15) / 16), 256, 0, stream>>>(dense, n, bad);
   return cudaGetLastError();
 }
 

@@ -13,6 +13,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <exception>
+#include <sstream>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -79,6 +80,8 @@ struct ltl_ctx {
   bool ring_stale = true;   // ring counters not (re)started since the last upload / init
   int64_t launches = 0;     // kernels this context has launched (ltl_kernel_launches)
   int64_t timed_launches = 0;  // inside the last ltl_time's timed loop
+  uint8_t* pinned[2] = {nullptr, nullptr};  // snapshot streaming buffers (lazy)
+  size_t pinned_bytes = 0;
   std::vector<Slab> slabs;
   std::string err;
 };
@@ -594,6 +597,8 @@ int ltl_create(ltl_ctx** out, int32_t n, int32_t f, int32_t num_slabs, const int
 void ltl_destroy(ltl_ctx* ctx) {
   if (!ctx) return;
   destroy_ctx(ctx);
+  for (uint8_t* p : ctx->pinned)
+    if (p) cudaFreeHost(p);
   delete ctx;
 }
 
@@ -950,6 +955,231 @@ int ltl_ring_fill(ltl_ctx* ctx) {
 
 int32_t ltl_ring_active(const ltl_ctx* ctx) {
   return ctx && ring_ok(ctx) ? 1 : 0;
+}
+
+}  // extern "C"
+
+// ---- CATSNAP v1 snapshots streamed from / to the device (src/snapshot.cpp)
+//
+// Format (include/catsim/snapshot.hpp): "CATSNAP 1 <n> <f> <layout>\n" then
+// the n x n interior bytes in row-major order.  Writes gather the strips into
+// the dead generation buffer on the device (one relayout kernel) and stream
+// it out through two pinned chunks, the D2H of chunk k+1 overlapping the
+// fwrite of chunk k; reads mirror that and check the {0,1} bytes on the
+// device.  No host copy of the grid is ever made.
+
+namespace {
+
+[[noreturn]] void snap_fail(const std::string& why) {
+  throw std::runtime_error("snapshot format error: " + why);
+}
+
+constexpr size_t kSnapChunk = 32u << 20;  // bytes per pinned chunk
+
+void ensure_pinned(ltl_ctx* ctx) {
+  if (ctx->pinned_bytes >= kSnapChunk) return;
+  for (uint8_t*& p : ctx->pinned) {
+    if (p) cudaFreeHost(p);
+    p = nullptr;
+    ck(cudaMallocHost(&p, kSnapChunk), "cudaMallocHost (snapshot chunk)");
+  }
+  ctx->pinned_bytes = kSnapChunk;
+}
+
+struct SnapHeader {
+  int32_t n = -1, f = -1, layout = 0;
+};
+
+// snapshot_read's header checks (src/snapshot.cpp:39-66), same order and text.
+SnapHeader parse_snap_header(std::FILE* fh) {
+  std::string header;
+  bool any = false;
+  for (int c; (c = std::fgetc(fh)) != EOF;) {
+    any = true;
+    if (c == '\n') break;
+    header.push_back(static_cast<char>(c));
+  }
+  if (!any) snap_fail("missing header line");
+  std::istringstream hs(header);
+  std::string magic, layout_token;
+  int version = 0, n = -1, f = -1;
+  if (!(hs >> magic >> version >> n >> f >> layout_token))
+    snap_fail("malformed header '" + header + "'");
+  std::string trailing;
+  if (hs >> trailing) snap_fail("trailing tokens in header");
+  if (magic != "CATSNAP") snap_fail("bad magic '" + magic + "'");
+  if (version != 1) snap_fail("unsupported version " + std::to_string(version));
+  SnapHeader h;
+  if (layout_token == "rowmajor")
+    h.layout = LTL_LAYOUT_ROW_MAJOR;
+  else if (layout_token == "fragment")
+    h.layout = LTL_LAYOUT_FRAGMENT;
+  else
+    snap_fail("unknown layout '" + layout_token + "'");
+  if (n < 0 || f <= 0 || n % f != 0)
+    snap_fail("bad geometry n=" + std::to_string(n) + " f=" + std::to_string(f));
+  h.n = n;
+  h.f = f;
+  return h;
+}
+
+struct FileCloser {
+  std::FILE* fh;
+  ~FileCloser() {
+    if (fh) std::fclose(fh);
+  }
+};
+
+void check_square(const ltl_ctx* ctx) {
+  if (ctx->rows != ctx->cols)
+    throw std::invalid_argument("config error: snapshots hold square n x n grids (context is " +
+                                std::to_string(ctx->rows) + " x " + std::to_string(ctx->cols) +
+                                ")");
+}
+
+void snapshot_write_ctx(ltl_ctx* ctx, const char* path, int32_t layout) {
+  check_layout(layout);
+  check_square(ctx);
+  std::FILE* fh = std::fopen(path, "wb");
+  if (!fh) snap_fail(std::string("cannot open '") + path + "' for writing");
+  FileCloser closer{fh};
+  const std::string header = "CATSNAP 1 " + std::to_string(ctx->rows) + " " +
+                             std::to_string(ctx->f) + " " +
+                             (layout == LTL_LAYOUT_ROW_MAJOR ? "rowmajor" : "fragment") + "\n";
+  if (std::fwrite(header.data(), 1, header.size(), fh) != header.size()) snap_fail("write failed");
+  if (ctx->rows > 0) ensure_pinned(ctx);
+  const int cur = ctx->cur;
+  for (Slab& s : ctx->slabs) {
+    ck(cudaSetDevice(s.dev), "cudaSetDevice");
+    if (s.rows == 0 || ctx->cols == 0) continue;
+    uint8_t* dense = s.buf[1 - cur];  // dead between steps (see upload_interior)
+    ck(ltl::launch_from_strips(s.view(cur, ctx->cols), dense, s.stream), "from_strips");
+    ++ctx->launches;
+    const size_t total = static_cast<size_t>(s.rows) * ctx->cols;
+    const size_t nchunks = (total + kSnapChunk - 1) / kSnapChunk;
+    cudaEvent_t ev[2];
+    for (auto& e : ev) ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+    auto issue = [&](size_t k) {
+      const size_t off = k * kSnapChunk, len = std::min(kSnapChunk, total - off);
+      ck(cudaMemcpyAsync(ctx->pinned[k % 2], dense + off, len, cudaMemcpyDeviceToHost, s.stream),
+         "snapshot D2H");
+      ck(cudaEventRecord(ev[k % 2], s.stream), "event");
+    };
+    issue(0);
+    bool ok = true;
+    for (size_t k = 0; k < nchunks; ++k) {
+      if (k + 1 < nchunks) issue(k + 1);  // its buffer's fwrite (chunk k-1) is done
+      ck(cudaEventSynchronize(ev[k % 2]), "snapshot D2H");
+      const size_t len = std::min(kSnapChunk, total - k * kSnapChunk);
+      ok = ok && std::fwrite(ctx->pinned[k % 2], 1, len, fh) == len;
+    }
+    ck(cudaStreamSynchronize(s.stream), "cudaStreamSynchronize");
+    for (auto& e : ev) cudaEventDestroy(e);
+    if (!ok) snap_fail("write failed");
+  }
+  closer.fh = nullptr;
+  if (std::fclose(fh) != 0) snap_fail("write failed");
+}
+
+int32_t snapshot_read_ctx(ltl_ctx* ctx, const char* path) {
+  std::FILE* fh = std::fopen(path, "rb");
+  if (!fh) snap_fail(std::string("cannot open '") + path + "' for reading");
+  FileCloser closer{fh};
+  const SnapHeader h = parse_snap_header(fh);
+  check_square(ctx);
+  if (h.n != ctx->rows || h.f != ctx->f)
+    throw std::invalid_argument("geometry error: snapshot n=" + std::to_string(h.n) +
+                                " f=" + std::to_string(h.f) + " does not match the context (n=" +
+                                std::to_string(ctx->rows) + " f=" + std::to_string(ctx->f) + ")");
+  if (h.n > 0) ensure_pinned(ctx);
+  const int cur = ctx->cur;
+  const std::string truncated = "truncated payload (expected " + std::to_string(h.n) + "x" +
+                                std::to_string(h.n) + " cells)";
+  int32_t* bad = nullptr;
+  for (Slab& s : ctx->slabs) {
+    ck(cudaSetDevice(s.dev), "cudaSetDevice");
+    if (s.rows == 0 || ctx->cols == 0) continue;
+    if (!bad) {
+      ck(cudaMallocHost(&bad, sizeof(int32_t)), "cudaMallocHost");
+    }
+    *bad = 0;
+    uint8_t* dense = s.buf[1 - cur];
+    const size_t total = static_cast<size_t>(s.rows) * ctx->cols;
+    const size_t nchunks = (total + kSnapChunk - 1) / kSnapChunk;
+    cudaEvent_t ev[2];
+    for (auto& e : ev) ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+    bool short_read = false;
+    size_t got_total = 0;
+    for (size_t k = 0; k < nchunks && !short_read; ++k) {
+      if (k >= 2) ck(cudaEventSynchronize(ev[k % 2]), "snapshot H2D");  // buffer free again
+      const size_t off = k * kSnapChunk, len = std::min(kSnapChunk, total - off);
+      const size_t got = std::fread(ctx->pinned[k % 2], 1, len, fh);
+      // the reference reads whole rows: only complete rows reach the {0,1} check
+      const size_t rows_done = (off + got) / ctx->cols;
+      const size_t keep = got == len ? len : rows_done * ctx->cols - std::min(off, rows_done * ctx->cols);
+      if (got != len) short_read = true;
+      if (keep > 0) {
+        ck(cudaMemcpyAsync(dense + off, ctx->pinned[k % 2], keep, cudaMemcpyHostToDevice, s.stream),
+           "snapshot H2D");
+        ck(cudaEventRecord(ev[k % 2], s.stream), "event");
+      }
+      got_total = off + keep;
+    }
+    ck(ltl::launch_check_cells(dense, static_cast<int64_t>(got_total), bad, s.stream), "check");
+    if (!short_read) {
+      ck(ltl::launch_to_strips(dense, s.view(cur, ctx->cols), s.stream), "to_strips");
+      ++ctx->launches;
+    }
+    ck(cudaStreamSynchronize(s.stream), "cudaStreamSynchronize");
+    ++ctx->launches;
+    for (auto& e : ev) cudaEventDestroy(e);
+    const bool any_bad = *bad != 0;
+    if (any_bad || short_read) {
+      cudaFreeHost(bad);
+      if (any_bad) snap_fail("cell byte out of {0,1}");
+      snap_fail(truncated);
+    }
+  }
+  if (bad) cudaFreeHost(bad);
+  if (ctx->slabs.size() > 1)
+    for (Slab& s : ctx->slabs) {
+      ck(cudaSetDevice(s.dev), "cudaSetDevice");
+      ck(cudaEventRecord(s.ev_step, s.stream), "event");
+    }
+  enqueue_halo(ctx, cur);
+  sync_all(ctx);
+  ctx->ring_stale = true;
+  return h.layout;
+}
+
+}  // namespace
+
+extern "C" {
+
+int ltl_snapshot_write(ltl_ctx* ctx, const char* path, int32_t layout) {
+  if (!ctx || !path) return LTL_ERR_INVALID_ARGUMENT;
+  return guarded(ctx, [&] { snapshot_write_ctx(ctx, path, layout); });
+}
+
+int ltl_snapshot_read(ltl_ctx* ctx, const char* path, int32_t* layout_out) {
+  if (!ctx || !path) return LTL_ERR_INVALID_ARGUMENT;
+  return guarded(ctx, [&] {
+    const int32_t layout = snapshot_read_ctx(ctx, path);
+    if (layout_out) *layout_out = layout;
+  });
+}
+
+int ltl_snapshot_probe(const char* path, int32_t* n, int32_t* f, int32_t* layout) {
+  if (!path) return LTL_ERR_INVALID_ARGUMENT;
+  return guarded(nullptr, [&] {
+    std::FILE* fh = std::fopen(path, "rb");
+    if (!fh) snap_fail(std::string("cannot open '") + path + "' for reading");
+    FileCloser closer{fh};
+    const SnapHeader h = parse_snap_header(fh);
+    if (n) *n = h.n;
+    if (f) *f = h.f;
+    if (layout) *layout = h.layout;
+  });
 }
 
 }  // extern "C"

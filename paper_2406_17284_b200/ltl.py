@@ -63,6 +63,7 @@ EXPORTS = (
     "ltl_run_interior", "ltl_create_part", "ltl_set_stream", "ltl_step_part", "ltl_fill_halo",
     "ltl_slab_buffer", "ltl_pack_edges", "ltl_unpack_halo", "ltl_ring_export",
     "ltl_ring_connect", "ltl_ring_fill", "ltl_ring_active", "ltl_ring_disconnect",
+    "ltl_snapshot_write", "ltl_snapshot_read", "ltl_snapshot_probe",
     "ltl_init_random", "ltl_parse_rule", "ltl_format_rule",
     "ltl_preset_count", "ltl_preset", "ltl_von_neumann_probe_rule", "ltl_build_info",
 )
@@ -119,6 +120,10 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
         "ltl_ring_fill": ([vp], ctypes.c_int),
         "ltl_ring_active": ([vp], ctypes.c_int32),
         "ltl_ring_disconnect": ([vp], ctypes.c_int),
+        "ltl_snapshot_write": ([vp, ctypes.c_char_p, ctypes.c_int32], ctypes.c_int),
+        "ltl_snapshot_read": ([vp, ctypes.c_char_p, ctypes.POINTER(ctypes.c_int32)], ctypes.c_int),
+        "ltl_snapshot_probe": ([ctypes.c_char_p, ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int32)],
+                               ctypes.c_int),
         "ltl_unpack_halo": ([vp, vp, vp], ctypes.c_int),
         "ltl_parse_rule": ([ctypes.c_char_p, P(ltl_rule_c), ctypes.c_char_p, ctypes.c_int32],
                            ctypes.c_int),
@@ -278,6 +283,16 @@ class DeviceTorus:
         self._check(self.lib.ltl_download_interior(self._ctx, _u8(out)))
         return out
 
+    def snapshot_write(self, path: str, layout: int = LAYOUT_ROW_MAJOR) -> None:
+        """catsim::snapshot_write of the device grid, streamed (no host grid)."""
+        self._check(self.lib.ltl_snapshot_write(self._ctx, os.fsencode(path), layout))
+
+    def snapshot_read(self, path: str) -> int:
+        """catsim::snapshot_read into the device grid; returns the declared layout."""
+        lay = ctypes.c_int32(-1)
+        self._check(self.lib.ltl_snapshot_read(self._ctx, os.fsencode(path), ctypes.byref(lay)))
+        return lay.value
+
     def init_random(self, density: float, seed: int, fill_n: int = -1) -> None:
         """Device-side init_random (bit-identical to src/grid.cpp:61-73)."""
         self._check(self.lib.ltl_init_random(self._ctx, density, seed, fill_n))
@@ -399,6 +414,18 @@ class DeviceTorus:
 
 
 ENGINES = ("cat", "stencil")
+
+
+def snapshot_probe(path: str):
+    """Header of a CATSNAP v1 file -> (n, f, layout); the reader's header errors
+    (LtlRuntimeError "snapshot format error: ...").  Host only."""
+    lib = load_library()
+    n, f, lay = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32()
+    st = lib.ltl_snapshot_probe(os.fsencode(path), ctypes.byref(n), ctypes.byref(f),
+                                ctypes.byref(lay))
+    if st != OK:
+        raise _EXC.get(st, RuntimeError)(lib.ltl_last_error(None).decode())
+    return n.value, f.value, lay.value
 
 
 def run_engine(engine: str, initial: np.ndarray, rule, steps: int, f: int = 16,
