@@ -900,7 +900,7 @@ int tc_persistent_ctas(int32_t rows, int32_t cols, int num_sms) {
   return bands >= 16 && units >= 8LL * num_sms && units <= 190LL * num_sms ? num_sms : 0;
 }
 
-int tc_sweep_chunks(int32_t strips) {  // <= 12 units per chunk (16384^2: 8 / 12 / 16 / 20 / 32 -> 101 / 93.7 / 94.3 / 97.0 / 93.6+ us)
+int tc_sweep_chunks(int32_t strips) {  // <= 12 units per chunk (16384^2 A/B: 12 -> 93.7 us, 16 -> 94.3, 20 -> 97.0, 8 -> ~101)
   int per = 12;
   if (const char* e = std::getenv("LTL_SWEEP_UNITS")) per = std::max(1, std::atoi(e));  // tuning
   return (strips + per - 1) / per;
