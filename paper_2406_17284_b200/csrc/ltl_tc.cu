@@ -499,7 +499,11 @@ __global__ void __launch_bounds__(kThreads, 1)
               uint8_t* dst = smem + kSmemX + s * kBoxBytes;
               if (!first && !last) {
                 mbar_arrive_expect_tx(&x_full[s], kBoxBytes);
+#ifdef LTL_DIAG_L2_READS  // timing probe only (wrong results): every box from band 1 (L2-resident)
+                tma_load_3d(dst, &lm[0], &x_full[s], 0, kBand, strip);
+#else
                 tma_load_3d(dst, &lm[0], &x_full[s], 0, band * kBand, strip);
+#endif
               } else {
                 // first / last band of a whole torus: the 16 rows beyond the
                 // edge are loaded from the other end of the strip (padded row 16 + y)
