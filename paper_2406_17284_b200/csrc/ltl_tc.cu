@@ -14,8 +14,9 @@
 // MMAs as TMEM allows -- 16 per 128 x 128 output tile:
 //
 //   unit     (band, strip): output rows [128 b, 128 b + 128) x the 128
-//            columns of strip t.  A CTA owns a contiguous run of units in
-//            band-major order and walks its band left to right.
+//            columns of strip t.  A CTA walks runs of consecutive strips of
+//            one band (SegIter: per-launch segments, or the multi-generation
+//            sweep).
 //   box      one TMA load per unit: padded rows [128 b, 128 b + 160) of
 //            strip t = ONE contiguous 20 KB block (SWIZZLE_128B).  The 16 halo
 //            rows above and below come with it; the 16 halo columns on each
@@ -42,20 +43,26 @@
 //            range tests (dead: b1..b2, live: K+s1'..K+s2') are four biased
 //            adds and two LOP3s per register (bit 15 of each lane = result).
 //   store    the D2 columns are permuted (out_row_of_col) so that
-//            stmatrix.trans writes each 16x256b TMEM fragment straight into a
-//            row-major SWIZZLE_32B 32x32 staging tile per warp -> TMA store of
-//            the next generation (no CTA-wide barrier on the output path).
+//            stmatrix.trans writes each 16x256b TMEM fragment straight into
+//            the group's row-major SWIZZLE_128B 64x128 staging tile; the store
+//            warp writes it with one 8 KB TMA store of the next generation
+//            (no CTA-wide barrier on the output path).
 //
 // Every quantity is an exact small integer (H <= 33, R <= 1089, Z < 4096), so
 // the result is bit-identical to the reference's int32 loops.
 //
-// One persistent CTA per SM (all 512 TMEM columns), 15 warps:
-//   warp 0        TMA producer            warp 1   pass-1 MMA issuer, TMEM owner
+// One CTA per SM (all 512 TMEM columns), 16 warps:
+//   warp 0        TMA producer (+ unit flags of multi-generation launches,
+//                 ring counters of slabs)
+//   warp 1        pass-1 MMA issuer, TMEM owner
 //   warps 2..5    convert D1 (warp w: TMEM lane quarter w%4 = 32 strip columns)
-//   warps 6..13   rule + store D2: group g = 0 / 1 takes sub-block g of every unit
+//   warps 6..13   rule + stage D2: group g = 0 / 1 takes sub-block g of every unit
 //   warp 14       pass-2 MMA issuer
+//   warp 15       TMA stores, unit publication (multi-generation launches)
 // Every stage hands over through mbarrier rings, so TMA, both MMA passes and
-// both epilogue groups overlap across sub-blocks and units.
+// both epilogue groups overlap across sub-blocks and units.  Measured limit
+// (DESIGN.md §6): this on-SM pipeline, ~1400 cycles per unit, just above the
+// HBM time of a unit.
 #include <cuda.h>
 #include <cuda_runtime.h>
 
