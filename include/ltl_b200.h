@@ -50,7 +50,8 @@ extern "C" {
 #define LTL_FLAG_INJECT_FAULT 0x1u  /* CatConfig.inject_band_fault, cat_engine.hpp:22-24 */
 #define LTL_FLAG_WANT_STATS 0x2u    /* fill ltl_stats_c (device max-reduction of H / R) */
 #define LTL_FLAG_STENCIL 0x4u       /* run the CUDA-core stencil ablation, not tcgen05 */
-#define LTL_FLAG_NO_GRAPH 0x8u      /* launch step by step instead of a captured CUDA graph */
+#define LTL_FLAG_NO_GRAPH 0x8u      /* accepted, no effect: generations are never graph-captured (a
+                                       captured 2-generation graph measured no faster) */
 
 /* catsim::LtlRule, proj/include/catsim/rule.hpp:17-32 */
 typedef struct ltl_rule_c {
