@@ -187,13 +187,15 @@ int ltl_unpack_halo(ltl_ctx* ctx, const void* top_halo, const void* bot_halo);
  * NVLink (CUDA IPC peer memory), gated by the neighbours' step counters --
  * no separate exchange, no host synchronisation.  Needs cols % 128 == 0 and
  * rows % 32 == 0 (else ltl_pack_edges / ltl_unpack_halo + NCCL).
- *   ltl_ring_export:  LTL_RING_HANDLE_BYTES of CUDA IPC handles of a part context
+ *   ltl_ring_export:  LTL_RING_HANDLE_BYTES: CUDA IPC handles of a part context's
+ *                     step counters, both buffers and unit counters + its GPU's
+ *                     PCI bus id
  *   ltl_ring_connect: open the upper / lower neighbour's handles (rows = their
  *                     slab heights); our own handles (world size 1) are fine
  *   ltl_ring_fill:    after every upload / init, with a barrier of all ranks
  *                     on both sides: restarts the step counters (synchronous)
  *   ltl_ring_active:  1 when ltl_step_part / ltl_run use the fused exchange. */
-#define LTL_RING_HANDLE_BYTES (3 * 64)
+#define LTL_RING_HANDLE_BYTES (4 * 64 + 32)
 int ltl_ring_export(ltl_ctx* ctx, void* handles);
 int ltl_ring_connect(ltl_ctx* ctx, const void* up_handles, int32_t up_rows,
                      const void* down_handles, int32_t down_rows);

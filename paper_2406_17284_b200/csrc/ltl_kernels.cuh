@@ -116,6 +116,11 @@ struct TcLaunch {
   const uint32_t* down_done;
   uint32_t* my_done;
   uint32_t* my_ticket;
+  // multi-generation ring launches (gens > 1): ring_up / ring_down point at
+  // TWO maps each (the neighbour's buffer of generation 0, then of 1), and
+  // the neighbours' per-unit counters (NULL: this slab's own, a self-ring)
+  const uint32_t* up_flags;
+  const uint32_t* down_flags;
   int32_t wrap_cols, wrap_rows;
   int32_t rows, cols;
   RuleConsts rule;

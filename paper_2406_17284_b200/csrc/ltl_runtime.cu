@@ -60,7 +60,13 @@ struct Slab {
   CUtensorMap ring_up_map[2], ring_down_map[2];  // per generation buffer
   const uint32_t* up_done = nullptr;
   const uint32_t* down_done = nullptr;
-  int32_t up_rows = 0;
+  int32_t up_rows = 0, down_rows = 0;
+  // the neighbours' per-unit counters (multi-generation ring launches); a
+  // neighbour that is this slab itself or runs on another GPU can run
+  // concurrently with our persistent kernel, one sharing our GPU cannot
+  const uint32_t* up_unit_flags = nullptr;
+  const uint32_t* down_unit_flags = nullptr;
+  bool up_concurrent = false, down_concurrent = false;
   bool ring_ready = false;                    // peers wired
   uint32_t ring_gen = 0;                      // steps since the last ring start
   std::vector<void*> ipc_opened;              // IPC mappings to close
@@ -87,6 +93,8 @@ struct ltl_ctx {
 };
 
 namespace {
+
+constexpr int kBusIdBytes = LTL_RING_HANDLE_BYTES - 4 * 64;  // PCI bus id after 4 IPC handles
 
 int status_of(const std::exception& e) {
   if (dynamic_cast<const CudaFailure*>(&e)) return LTL_ERR_CUDA;
@@ -139,8 +147,21 @@ void build_maps(Slab& s, int32_t cols) {
   }
 }
 
-void wire_ring(ltl_ctx* ctx, Slab& s, const uint32_t* up_sync, uint8_t* const* up_buf,
-               int32_t up_rows, const uint32_t* dn_sync, uint8_t* const* dn_buf, int32_t dn_rows) {
+struct RingPeer {
+  const uint32_t* sync;
+  uint8_t* const* buf;
+  int32_t rows;
+  const uint32_t* unit_flags;
+  bool concurrent;  // itself, or on another GPU
+};
+
+void wire_ring(ltl_ctx* ctx, Slab& s, const RingPeer& upp, const RingPeer& dnp) {
+  const uint32_t* up_sync = upp.sync;
+  uint8_t* const* up_buf = upp.buf;
+  const int32_t up_rows = upp.rows;
+  const uint32_t* dn_sync = dnp.sync;
+  uint8_t* const* dn_buf = dnp.buf;
+  const int32_t dn_rows = dnp.rows;
   ck(cudaSetDevice(s.dev), "cudaSetDevice");
   const int32_t strips = ltl::storage_strips(ctx->cols);
   for (int b = 0; b < 2; ++b) {
@@ -154,6 +175,11 @@ void wire_ring(ltl_ctx* ctx, Slab& s, const uint32_t* up_sync, uint8_t* const* u
   s.up_done = up_sync;
   s.down_done = dn_sync;
   s.up_rows = up_rows;
+  s.down_rows = dn_rows;
+  s.up_unit_flags = upp.unit_flags;
+  s.down_unit_flags = dnp.unit_flags;
+  s.up_concurrent = upp.concurrent;
+  s.down_concurrent = dnp.concurrent;
   s.ring_ready = true;
 }
 
@@ -224,7 +250,8 @@ void create_slabs(ltl_ctx* ctx, int32_t num_slabs, const int32_t* dev_ids) {
       Slab& s = ctx->slabs[i];
       const Slab& up = ctx->slabs[(i - 1 + num_slabs) % num_slabs];
       const Slab& dn = ctx->slabs[(i + 1) % num_slabs];
-      wire_ring(ctx, s, up.ring_sync, up.buf, up.rows, dn.ring_sync, dn.buf, dn.rows);
+      wire_ring(ctx, s, RingPeer{up.ring_sync, up.buf, up.rows, up.flags, &up == &s || up.dev != s.dev},
+                RingPeer{dn.ring_sync, dn.buf, dn.rows, dn.flags, &dn == &s || dn.dev != s.dev});
     }
 }
 
@@ -288,6 +315,11 @@ void start_ring(ltl_ctx* ctx) {
     ck(cudaStreamSynchronize(s.stream), "cudaStreamSynchronize");
     ck(cudaMemset(s.ring_sync, 0, 2 * sizeof(uint32_t)), "memset ring counters");
     s.ring_gen = 0;
+    // per-unit counters restart too: the neighbours compare them with their own base
+    const size_t units = static_cast<size_t>((s.rows + ltl::kTcBand - 1) / ltl::kTcBand) *
+                         ltl::interior_strips(ctx->cols);
+    ck(cudaMemset(s.flags, 0, std::max<size_t>(units, 1) * sizeof(uint32_t)), "memset flags");
+    s.flag_base = 0;
   }
   sync_all(ctx);
 }
@@ -326,13 +358,24 @@ void enqueue_halo(ltl_ctx* ctx, int which, bool for_tc = false) {
 // Several generations in ONE persistent launch (units handed from one
 // generation to the next through per-unit flags, no halo traffic): one
 // whole-torus slab whose wraps the loads do, tcgen05 engine.
+// For a ring of slabs every slab needs the same geometry (the kernels compare
+// each other's unit counters) and neighbours that run concurrently with it.
 bool persistent_ok(const ltl_ctx* ctx, uint32_t flags) {
-  if ((flags & LTL_FLAG_STENCIL) || ctx->slabs.size() != 1 || !wrap_cols(ctx) ||
-      !wrap_rows(ctx) || std::getenv("LTL_NO_PERSIST"))  // env: diagnostics
-    return false;
-  int sms = 0;
-  ck(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->slabs[0].dev), "sm count");
-  return ltl::tc_persistent_ctas(ctx->slabs[0].rows, ctx->cols, sms) > 0;
+  if ((flags & LTL_FLAG_STENCIL) || !wrap_cols(ctx) || std::getenv("LTL_NO_PERSIST"))
+    return false;  // env: diagnostics
+  const bool single = ctx->slabs.size() == 1 && wrap_rows(ctx);
+  if (!single) {
+    if (!ring_ok(ctx)) return false;
+    for (const Slab& s : ctx->slabs)
+      if (s.up_rows != s.rows || s.down_rows != s.rows || !s.up_concurrent || !s.down_concurrent)
+        return false;
+  }
+  for (const Slab& s : ctx->slabs) {
+    int sms = 0;
+    ck(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, s.dev), "sm count");
+    if (ltl::tc_persistent_ctas(s.rows, ctx->cols, sms) <= 0) return false;
+  }
+  return true;
 }
 
 // `gens` generations (cur -> nxt -> ...): one persistent launch when
@@ -384,16 +427,24 @@ void enqueue_step(ltl_ctx* ctx, const ltl::RuleConsts& rc, uint32_t flags, bool 
       ++ctx->launches;
     } else {
       ltl::TcLaunch a{};
+      CUtensorMap ring_up2[2], ring_down2[2];  // the neighbours' buffers of gen 0, 1
       a.load_maps = s.load_maps[cur];
       a.store_map = &s.store_map[nxt];
       a.wrap_cols = wrap_cols(ctx);
       a.wrap_rows = wrap_rows(ctx);
       if (ring) {
         a.ring = 1;
-        a.ring_gen = s.ring_gen++;
+        a.ring_gen = s.ring_gen;
+        s.ring_gen += persist ? static_cast<uint32_t>(gens) : 1u;
         a.up_rows = s.up_rows;
-        a.ring_up = &s.ring_up_map[cur];
-        a.ring_down = &s.ring_down_map[cur];
+        ring_up2[0] = s.ring_up_map[cur];
+        ring_up2[1] = s.ring_up_map[nxt];
+        ring_down2[0] = s.ring_down_map[cur];
+        ring_down2[1] = s.ring_down_map[nxt];
+        a.ring_up = ring_up2;
+        a.ring_down = ring_down2;
+        a.up_flags = s.up_unit_flags;
+        a.down_flags = s.down_unit_flags;
         a.up_done = s.up_done;
         a.down_done = s.down_done;
         a.my_done = s.ring_sync;
@@ -881,11 +932,15 @@ int ltl_ring_export(ltl_ctx* ctx, void* handles) {
     if (!s.ring_sync || s.rows <= 0 || ctx->cols <= 0)
       throw std::invalid_argument("config error: empty slab");
     ck(cudaSetDevice(s.dev), "cudaSetDevice");
-    cudaIpcMemHandle_t h[3];
+    cudaIpcMemHandle_t h[4];
     ck(cudaIpcGetMemHandle(&h[0], s.ring_sync), "ipc handle (ring counters)");
     ck(cudaIpcGetMemHandle(&h[1], s.buf[0]), "ipc handle (buffer 0)");
     ck(cudaIpcGetMemHandle(&h[2], s.buf[1]), "ipc handle (buffer 1)");
+    ck(cudaIpcGetMemHandle(&h[3], s.flags), "ipc handle (unit counters)");
     std::memcpy(handles, h, sizeof h);
+    char bus[kBusIdBytes] = {};
+    ck(cudaDeviceGetPCIBusId(bus, kBusIdBytes - 1, s.dev), "pci bus id");
+    std::memcpy(static_cast<uint8_t*>(handles) + sizeof h, bus, kBusIdBytes);
   });
 }
 
@@ -897,34 +952,48 @@ int ltl_ring_connect(ltl_ctx* ctx, const void* up_handles, int32_t up_rows,
       throw std::invalid_argument("config error: ring connect needs a part context (ltl_create_part)");
     Slab& s = ctx->slabs[0];
     ck(cudaSetDevice(s.dev), "cudaSetDevice");
-    cudaIpcMemHandle_t mine[3];
+    cudaIpcMemHandle_t mine[1];
     ck(cudaIpcGetMemHandle(&mine[0], s.ring_sync), "ipc handle (ring counters)");
-    // open a neighbour's 3 allocations (counters, 2 buffers); our own handles
-    // (world size 1) map to our own pointers
-    auto open = [&](const void* hv, void** out) {
+    char my_bus[kBusIdBytes] = {};
+    ck(cudaDeviceGetPCIBusId(my_bus, kBusIdBytes - 1, s.dev), "pci bus id");
+    // open a neighbour's 4 allocations (counters, 2 buffers, unit counters);
+    // our own handles (world size 1) map to our own pointers
+    bool self[2] = {false, false};
+    auto open = [&](const void* hv, void** out, bool* is_self) {
       const cudaIpcMemHandle_t* h = static_cast<const cudaIpcMemHandle_t*>(hv);
-      if (std::memcmp(&h[0], &mine[0], sizeof(cudaIpcMemHandle_t)) == 0) {
+      *is_self = std::memcmp(&h[0], &mine[0], sizeof(cudaIpcMemHandle_t)) == 0;
+      if (*is_self) {
         out[0] = s.ring_sync;
         out[1] = s.buf[0];
         out[2] = s.buf[1];
+        out[3] = s.flags;
         return;
       }
-      for (int i = 0; i < 3; ++i) {
+      for (int i = 0; i < 4; ++i) {
         ck(cudaIpcOpenMemHandle(&out[i], h[i], cudaIpcMemLazyEnablePeerAccess), "ipc open");
         s.ipc_opened.push_back(out[i]);
       }
     };
-    void* up[3];
-    void* dn[3];
-    open(up_handles, up);
-    if (std::memcmp(up_handles, down_handles, 3 * sizeof(cudaIpcMemHandle_t)) == 0)
+    auto other_gpu = [&](const void* hv) {
+      return std::memcmp(static_cast<const uint8_t*>(hv) + 4 * sizeof(cudaIpcMemHandle_t),
+                         my_bus, kBusIdBytes) != 0;
+    };
+    void* up[4];
+    void* dn[4];
+    open(up_handles, up, &self[0]);
+    if (std::memcmp(up_handles, down_handles, 4 * sizeof(cudaIpcMemHandle_t)) == 0) {
       std::memcpy(dn, up, sizeof up);  // world size 2: one neighbour on both sides
-    else
-      open(down_handles, dn);
+      self[1] = self[0];
+    } else {
+      open(down_handles, dn, &self[1]);
+    }
     uint8_t* upb[2] = {static_cast<uint8_t*>(up[1]), static_cast<uint8_t*>(up[2])};
     uint8_t* dnb[2] = {static_cast<uint8_t*>(dn[1]), static_cast<uint8_t*>(dn[2])};
-    wire_ring(ctx, s, static_cast<uint32_t*>(up[0]), upb, up_rows, static_cast<uint32_t*>(dn[0]),
-              dnb, down_rows);
+    wire_ring(ctx, s,
+              RingPeer{static_cast<uint32_t*>(up[0]), upb, up_rows, static_cast<uint32_t*>(up[3]),
+                       self[0] || other_gpu(up_handles)},
+              RingPeer{static_cast<uint32_t*>(dn[0]), dnb, down_rows, static_cast<uint32_t*>(dn[3]),
+                       self[1] || other_gpu(down_handles)});
     ctx->ring_stale = true;
   });
 }

@@ -139,8 +139,8 @@ constexpr uint32_t kIdesc2 = idesc_i8_u8u8_s32(128, kSub);
 struct TcMaps {
   CUtensorMap load[2][kTcLoadMaps];
   CUtensorMap store[2];
-  CUtensorMap ring_up;    // ring: 16-row pieces of the upper neighbour's slab (peer memory)
-  CUtensorMap ring_down;  // ring: 16-row pieces of the lower neighbour's slab
+  CUtensorMap ring_up[2];    // ring: 16-row pieces of the upper neighbour's slab (peer
+  CUtensorMap ring_down[2];  // memory), [its buffer of generation gg % 2 of the launch]
 };
 
 struct Params {
@@ -167,6 +167,12 @@ struct Params {
   const uint32_t* down_done;
   uint32_t* my_done;             // this slab's counter and its CTA ticket
   uint32_t* my_ticket;
+  // Multi-generation ring launches: the neighbours' per-unit counters (same
+  // geometry, same flag_base: every slab of the ring runs the same launches)
+  // stand for the bands above band 0 / below the last band, read at system
+  // scope; edge units are published at system scope.
+  const uint32_t* up_flags;
+  const uint32_t* down_flags;
   uint32_t* flags;               // per-unit completion counters (bands x strips)
   uint32_t flag_base;            // their common value when the launch starts
   DeviceStats* stats;
@@ -455,9 +461,18 @@ __global__ void __launch_bounds__(kThreads, 1)
         auto storage_strip = [&](int k) {  // logical strip t0-1+k (or its image)
           return p.wrap_cols ? (t0 - 1 + k + p.strips) % p.strips + 1 : t0 + k;
         };
-        auto flag_ptr = [&](int db, int k) {
-          const int b = (band + db + p.bands) % p.bands;
-          return p.flags + static_cast<int64_t>(b) * p.strips + (storage_strip(k) - 1);
+        const bool peer_up = p.ring && band == 0;  // band -1 is the upper slab's last
+        const bool peer_down = p.ring && band == p.bands - 1;
+        auto flag_ptr = [&](int db, int k) -> const uint32_t* {
+          const int b = band + db;
+          const int64_t col = storage_strip(k) - 1;
+          if (p.ring && b < 0) return p.up_flags + static_cast<int64_t>(p.bands - 1) * p.strips + col;
+          if (p.ring && b >= p.bands) return p.down_flags + col;
+          return p.flags + static_cast<int64_t>((b + p.bands) % p.bands) * p.strips + col;
+        };
+        auto flag_ld = [&](int db, int k) {
+          const bool peer = (db < 0 && peer_up) || (db > 0 && peer_down);
+          return peer ? ld_acquire_sys(flag_ptr(db, k)) : ld_acquire(flag_ptr(db, k));
         };
         for (int k0 = 0; k0 < nbox; k0 += 32) {
           uint32_t ready = ~0u;
@@ -465,9 +480,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int k = k0 + static_cast<int>(lane);
             bool ok = true;
             if (k < nbox) {
-              const uint32_t f0 = ld_acquire(flag_ptr(-1, k));
-              const uint32_t f1 = ld_acquire(flag_ptr(0, k));
-              const uint32_t f2 = ld_acquire(flag_ptr(1, k));
+              const uint32_t f0 = flag_ld(-1, k);
+              const uint32_t f1 = flag_ld(0, k);
+              const uint32_t f2 = flag_ld(1, k);
               ok = static_cast<int32_t>(f0 - target) >= 0 && static_cast<int32_t>(f1 - target) >= 0 &&
                    static_cast<int32_t>(f2 - target) >= 0;
             }
@@ -483,7 +498,12 @@ __global__ void __launch_bounds__(kThreads, 1)
 #ifdef LTL_TC_TRACE_BUILD
                 const long long w0_ = clock64();
 #endif
-                for (int db = -1; db <= 1; ++db) wait_flag_geq(flag_ptr(db, k), target);
+                for (int db = -1; db <= 1; ++db) {
+                  if ((db < 0 && peer_up) || (db > 0 && peer_down))
+                    wait_flag_geq_sys(flag_ptr(db, k), target);
+                  else
+                    wait_flag_geq(flag_ptr(db, k), target);
+                }
 #ifdef LTL_TC_TRACE_BUILD
                 if (p.trace && blockIdx.x == 0) {
                   atomicAdd(reinterpret_cast<unsigned long long*>(&p.trace[13 * 256 + 17]),
@@ -529,7 +549,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
                 if (first) {  // rows -16 .. -1: the torus' other end / the upper slab's last rows
                   if (p.ring)
-                    tma_load_3d(dst, &maps.ring_up, &x_full[s], 0, p.up_rows, strip);
+                    tma_load_3d(dst, &maps.ring_up[gg & 1], &x_full[s], 0, p.up_rows, strip);
                   else
                     tma_load_3d(dst, &lm[1], &x_full[s], 0, p.rows, strip);
                   row = kHalo;
@@ -542,7 +562,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                               first ? kHalo : band * kBand, strip);
                   // rows rows .. rows + 15: the torus' rows 0 .. 15 / the lower slab's first rows
                   uint8_t* bot = dst + (row + body + (first ? 0 : kHalo)) * kStrip;
-                  tma_load_3d(bot, p.ring ? &maps.ring_down : &lm[1], &x_full[s], 0, kHalo, strip);
+                  tma_load_3d(bot, p.ring ? &maps.ring_down[gg & 1] : &lm[1], &x_full[s], 0, kHalo,
+                              strip);
                 }
               }
             }
@@ -733,7 +754,13 @@ __global__ void __launch_bounds__(kThreads, 1)
               if (++npend == 2 * kPubLag) {
                 tma_store_wait_all<2 * kPubLag>();  // 2 groups per unit
                 fence_proxy_async_global();
-                fence_acq_rel_gpu();                // one release for the batch
+                bool edge = false;  // ring: neighbours read edge-band units' counters
+                for (int k = 0; k < kPubLag; ++k) {
+                  const uint32_t b = pend[(h + 1 + k) % (2 * kPubLag)] / p.strips;
+                  edge |= p.ring && (b == 0 || b == static_cast<uint32_t>(p.bands - 1));
+                }
+                if (edge) fence_acq_rel_sys();
+                else fence_acq_rel_gpu();           // one release for the batch
                 for (int k = 0; k < kPubLag; ++k)
                   red_relaxed_add(p.flags + pend[(h + 1 + k) % (2 * kPubLag)], 2);
                 npend -= kPubLag;
@@ -744,7 +771,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (p.gens > 1) {  // the generation's last units: publish them too
           tma_store_wait_all<0>();
           fence_proxy_async_global();
-          fence_acq_rel_gpu();
+          if (p.ring) fence_acq_rel_sys();
+          else fence_acq_rel_gpu();
           for (uint32_t k = 0; k < npend; ++k)
             red_relaxed_add(p.flags + pend[(h - npend + k) % (2 * kPubLag)], 2);
           npend = 0;
@@ -885,7 +913,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (atomicAdd(p.my_ticket, 1u) + 1u == gridDim.x) {
       *p.my_ticket = 0u;  // the next launch (after this grid completes) counts anew
       fence_acq_rel_sys();
-      red_relaxed_add_sys(p.my_done, 1u);
+      red_relaxed_add_sys(p.my_done, static_cast<uint32_t>(p.gens));  // generations completed
     }
   }
   if (warp == 1) tmem_dealloc(tmem, kTmemCols);
@@ -943,8 +971,9 @@ cudaError_t launch_tc_step(const TcLaunch& a, cudaStream_t stream) {
   p.ring = a.ring && p.wrap_cols && tc_wrap_rows(a.rows) ? 1 : 0;
   if (a.ring && !p.ring) return cudaErrorInvalidValue;  // caller must not ask
   if (p.ring) {
-    p.gens = 1;
     p.wrap_rows = 0;
+    p.up_flags = a.up_flags ? a.up_flags : a.flags;
+    p.down_flags = a.down_flags ? a.down_flags : a.flags;
     p.ring_gen = a.ring_gen;
     p.up_rows = a.up_rows;
     p.up_done = a.up_done;
@@ -986,8 +1015,10 @@ cudaError_t launch_tc_step(const TcLaunch& a, cudaStream_t stream) {
   }
   maps.store[0] = *a.store_map;
   maps.store[1] = a.store_map_b ? *a.store_map_b : *a.store_map;
-  maps.ring_up = a.ring ? *a.ring_up : *a.store_map;
-  maps.ring_down = a.ring ? *a.ring_down : *a.store_map;
+  for (int i = 0; i < 2; ++i) {
+    maps.ring_up[i] = a.ring ? a.ring_up[i & (a.gens > 1 ? 1 : 0)] : *a.store_map;
+    maps.ring_down[i] = a.ring ? a.ring_down[i & (a.gens > 1 ? 1 : 0)] : *a.store_map;
+  }
   if (a.stats) return cudaLaunchKernelEx(&cfg, ltl_tc_step_kernel<true>, maps, p);
   return cudaLaunchKernelEx(&cfg, ltl_tc_step_kernel<false>, maps, p);
 }

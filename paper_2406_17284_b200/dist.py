@@ -164,6 +164,18 @@ class PartitionedTorus:
         self.torus.init_random(density, seed)
         self.exchange()
 
+    def run(self, rule, steps: int) -> None:
+        """`steps` generations, enqueued on the slab's stream.  On the ring
+        every rank's kernel reads its neighbours' rows itself, so all steps go
+        in one call (one persistent launch when the geometry allows it, the
+        same decision on every rank: equal slab heights, neighbours on other
+        GPUs); otherwise one step + packed exchange per generation."""
+        if self.ring:
+            self.torus.run_async(rule, steps)
+            return
+        for _ in range(steps):
+            self.step(rule)
+
     def step(self, rule, stencil: bool = False) -> None:
         if self.ring:
             if stencil:

@@ -381,7 +381,7 @@ class DeviceTorus:
         return ptr.value, strip_bytes.value, rows.value
 
     # ---- multi-process ring with the halo exchange fused into the step
-    RING_HANDLE_BYTES = 3 * 64  # include/ltl_b200.h LTL_RING_HANDLE_BYTES
+    RING_HANDLE_BYTES = 4 * 64 + 32  # include/ltl_b200.h LTL_RING_HANDLE_BYTES
 
     def ring_export(self) -> bytes:
         """CUDA IPC handles of the slab's step counters and both generation buffers."""

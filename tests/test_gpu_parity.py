@@ -263,3 +263,23 @@ def test_partition_wrap_cols_matches_torus(ltl, orc):
         t.init_random(0.3, 2)
         init = t.download()
     assert np.array_equal(part.torus.download(), orc.simulate(init, parse_rule_text(text), 4))
+
+
+@pytest.mark.parametrize("rows,cols", [(256, 256), (512, 384)])
+def test_persistent_self_ring(ltl, orc, rows, cols, monkeypatch):
+    """Multi-generation launches of a ring slab (here its own neighbour): the
+    first / last band wait on the neighbours' unit counters (system scope) and
+    read their rows out of the neighbour's buffers; two calls in a row."""
+    monkeypatch.setenv("LTL_SELF_RING", "1")
+    monkeypatch.setenv("LTL_FORCE_PERSIST", "1")
+    rng = np.random.default_rng(rows + cols)
+    init = (rng.random((rows, cols)) < 0.3).astype(np.uint8)
+    for text in ("R5,C2,M1,S34..58,B34..45,NM", "R7,C2,M0,S5..15,B4..10,NN"):
+        rule = parse_rule_text(text)
+        with ltl.DeviceTorus(rows=rows, cols=cols) as t:
+            assert t.ring_active()
+            t.upload(init)
+            t.run(text, 7)
+            assert np.array_equal(t.download(), orc.simulate(init, rule, 7)), (text, 7)
+            t.run(text, 6)
+            assert np.array_equal(t.download(), orc.simulate(init, rule, 13)), (text, 13)

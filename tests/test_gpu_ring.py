@@ -1,7 +1,9 @@
 """The fused ring halo exchange across PROCESSES (one process per GPU in a real
 run), exercised on one B200: 2 and 4 processes share cuda:0, exchange their
-CUDA IPC handles over gloo and step with the halo rows pushed by the kernels
-into each other's buffers.  The assembled torus must equal the oracle."""
+CUDA IPC handles over gloo and step with the halo rows pulled by the kernels
+out of each other's buffers; at world size 1 the slab is its own neighbour
+(and may take the multi-generation ring kernel).  The assembled torus must
+equal the oracle."""
 import os
 import socket
 
@@ -24,8 +26,10 @@ def _free_port():
     return port
 
 
-def _worker(rank, world, port, global_rows, cols, steps, text, q):
+def _worker(rank, world, port, global_rows, cols, steps, text, q, multi=False):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    if multi:  # multi-generation launches even on small slabs (world 1: self-ring)
+        os.environ["LTL_FORCE_PERSIST"] = "1"
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         torch.cuda.set_device(0)
@@ -35,8 +39,12 @@ def _worker(rank, world, port, global_rows, cols, steps, text, q):
         rng = np.random.default_rng(7)
         full = (rng.random((global_rows, cols)) < 0.3).astype(np.uint8)
         part.upload(np.ascontiguousarray(full[part.row0:part.row0 + part.rows]))
-        for _ in range(steps):
-            part.step(text)
+        if multi:
+            part.run(text, steps - 2)  # all generations in one call ...
+            part.run(text, 2)          # ... and a second call continuing the counters
+        else:
+            for _ in range(steps):
+                part.step(text)
         part.torus.synchronize()
         q.put((rank, part.row0, part.torus.download()))
         dist.barrier()
@@ -47,8 +55,12 @@ def _worker(rank, world, port, global_rows, cols, steps, text, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,global_rows,cols", [(2, 256, 256), (4, 512, 128), (1, 96, 384)])
-def test_ring_processes_match_oracle(orc, world, global_rows, cols):
+@pytest.mark.parametrize("world,global_rows,cols,multi", [
+    (2, 256, 256, False), (4, 512, 128, False), (1, 96, 384, False),
+    (2, 256, 256, True),                      # same GPU: one launch per generation
+    (1, 512, 384, True),                      # self-ring: persistent ring kernel
+])
+def test_ring_processes_match_oracle(orc, world, global_rows, cols, multi):
     if not torch.cuda.is_available():
         pytest.skip("no GPU")
     text = "R16,C2,M0,S170..296,B170..300,NM"
@@ -56,7 +68,8 @@ def test_ring_processes_match_oracle(orc, world, global_rows, cols):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, global_rows, cols, steps, text, q))
+    procs = [ctx.Process(target=_worker,
+                         args=(r, world, port, global_rows, cols, steps, text, q, multi))
              for r in range(world)]
     for p in procs:
         p.start()
