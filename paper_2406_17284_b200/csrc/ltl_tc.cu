@@ -674,6 +674,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         tmem_st_wait();
         tc_fence_before();
         mbar_arrive(&a2_full[sl]);
+        if (warp == 2 && lane == 0) LTL_TRACE(8, h);  // convert done (per-launch traces)
       }
     }
     }

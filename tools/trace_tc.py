@@ -30,6 +30,9 @@ if ks:
     print("unit period (p1 issue):", statistics.median(rows[1][k + 1] - rows[1][k] for k in ks))
     print("p1 issue -> cv start  :", statistics.median(d(1, 2, k, k) for k in ks))
     print("cv start -> cv read   :", statistics.median(d(2, 3, k, k) for k in ks))
+    print("cv read  -> cv done   :", statistics.median(d(3, 8, k, k) for k in ks))
+    print("cv done  -> p2 issue s0:", statistics.median(rows[4][2 * k] - rows[8][k] for k in ks))
+    print("p2 s1 issue -> p1 issue(k+2):", statistics.median(rows[1][k + 2] - rows[4][2 * k + 1] for k in ks))
     print("cv read  -> p2 issue s0:", statistics.median(rows[4][2 * k] - rows[3][k] for k in ks))
     print("p2 s0 -> out0 go      :", statistics.median(rows[5][k] - rows[4][2 * k] for k in ks))
     print("out0 go -> out0 read  :", statistics.median(d(5, 6, k, k) for k in ks))
