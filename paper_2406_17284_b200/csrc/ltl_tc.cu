@@ -316,7 +316,7 @@ __device__ __forceinline__ uint32_t rule_pair(uint32_t z, const SimdRule& k) {
   return lop3<0x70>(e, c, d);             // e & ~(c & d)
 }
 
-template <bool kChecked>
+template <bool kChecked, bool kRing>
 __global__ void __launch_bounds__(kThreads, 1)
     ltl_tc_step_kernel(const __grid_constant__ TcMaps maps, const Params p) {
   extern __shared__ uint8_t smem_raw[];
@@ -453,7 +453,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       SegIter it(p, gg);
       int band, t0, t1;
       while (it.next(band, t0, t1)) {
-        const bool edge_rows = p.wrap_rows || p.ring;  // rows beyond the slab by piece loads
+        const bool edge_rows = p.wrap_rows || kRing;  // rows beyond the slab by piece loads
         const bool first = edge_rows && band == 0;
         const bool last = edge_rows && band == p.bands - 1;
         const int last_rows = p.rows - kBand * band;  // interior rows of the last band
@@ -461,13 +461,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         auto storage_strip = [&](int k) {  // logical strip t0-1+k (or its image)
           return p.wrap_cols ? (t0 - 1 + k + p.strips) % p.strips + 1 : t0 + k;
         };
-        const bool peer_up = p.ring && band == 0;  // band -1 is the upper slab's last
-        const bool peer_down = p.ring && band == p.bands - 1;
+        const bool peer_up = kRing && band == 0;  // band -1 is the upper slab's last
+        const bool peer_down = kRing && band == p.bands - 1;
         auto flag_ptr = [&](int db, int k) -> const uint32_t* {
           const int b = band + db;
           const int64_t col = storage_strip(k) - 1;
-          if (p.ring && b < 0) return p.up_flags + static_cast<int64_t>(p.bands - 1) * p.strips + col;
-          if (p.ring && b >= p.bands) return p.down_flags + col;
+          if (kRing && b < 0) return p.up_flags + static_cast<int64_t>(p.bands - 1) * p.strips + col;
+          if (kRing && b >= p.bands) return p.down_flags + col;
           return p.flags + static_cast<int64_t>((b + p.bands) % p.bands) * p.strips + col;
         };
         auto flag_ld = [&](int db, int k) {
@@ -537,18 +537,18 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const int body = last ? last_rows : kBand;  // interior rows in the box body
                 mbar_arrive_expect_tx(&x_full[s], (last ? last_rows + 2 * kHalo : kBox) * kStrip);
                 int row = 0;  // box row being filled
-                if (p.ring && first && !up_ready) {
+                if (kRing && first && !up_ready) {
                   wait_flag_geq_sys(p.up_done, p.ring_gen);
                   fence_proxy_async_global();  // acquired -> TMA reads
                   up_ready = true;
                 }
-                if (p.ring && last && !down_ready) {
+                if (kRing && last && !down_ready) {
                   wait_flag_geq_sys(p.down_done, p.ring_gen);
                   fence_proxy_async_global();
                   down_ready = true;
                 }
                 if (first) {  // rows -16 .. -1: the torus' other end / the upper slab's last rows
-                  if (p.ring)
+                  if (kRing)
                     tma_load_3d(dst, &maps.ring_up[gg & 1], &x_full[s], 0, p.up_rows, strip);
                   else
                     tma_load_3d(dst, &lm[1], &x_full[s], 0, p.rows, strip);
@@ -562,7 +562,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                               first ? kHalo : band * kBand, strip);
                   // rows rows .. rows + 15: the torus' rows 0 .. 15 / the lower slab's first rows
                   uint8_t* bot = dst + (row + body + (first ? 0 : kHalo)) * kStrip;
-                  tma_load_3d(bot, p.ring ? &maps.ring_down[gg & 1] : &lm[1], &x_full[s], 0, kHalo,
+                  tma_load_3d(bot, kRing ? &maps.ring_down[gg & 1] : &lm[1], &x_full[s], 0, kHalo,
                               strip);
                 }
               }
@@ -756,9 +756,13 @@ __global__ void __launch_bounds__(kThreads, 1)
                 tma_store_wait_all<2 * kPubLag>();  // 2 groups per unit
                 fence_proxy_async_global();
                 bool edge = false;  // ring: neighbours read edge-band units' counters
-                for (int k = 0; k < kPubLag; ++k) {
-                  const uint32_t b = pend[(h + 1 + k) % (2 * kPubLag)] / p.strips;
-                  edge |= p.ring && (b == 0 || b == static_cast<uint32_t>(p.bands - 1));
+                if (kRing) {
+                  const uint32_t lo = static_cast<uint32_t>(p.strips);  // band 0: [0, S)
+                  const uint32_t hi = static_cast<uint32_t>(p.bands - 1) * lo;  // last band
+                  for (int k = 0; k < kPubLag; ++k) {
+                    const uint32_t u = pend[(h + 1 + k) % (2 * kPubLag)];
+                    edge |= u < lo || u >= hi;
+                  }
                 }
                 if (edge) fence_acq_rel_sys();
                 else fence_acq_rel_gpu();           // one release for the batch
@@ -772,7 +776,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (p.gens > 1) {  // the generation's last units: publish them too
           tma_store_wait_all<0>();
           fence_proxy_async_global();
-          if (p.ring) fence_acq_rel_sys();
+          if (kRing) fence_acq_rel_sys();
           else fence_acq_rel_gpu();
           for (uint32_t k = 0; k < npend; ++k)
             red_relaxed_add(p.flags + pend[(h - npend + k) % (2 * kPubLag)], 2);
@@ -905,7 +909,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_before();
   __syncthreads();
   LTL_TRACE_CTA(15);
-  if (p.ring && threadIdx.x == 0) {
+  if (kRing && threadIdx.x == 0) {
     // Every store of this CTA has completed (the store warp waited for them
     // before the barrier).  One ticket per CTA; the launch's last CTA
     // publishes generation G + 1 to the neighbours.
@@ -952,7 +956,8 @@ cudaError_t launch_tc_step(const TcLaunch& a, cudaStream_t stream) {
     int dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
-    for (auto fn : {ltl_tc_step_kernel<false>, ltl_tc_step_kernel<true>}) {
+    for (auto fn : {ltl_tc_step_kernel<false, false>, ltl_tc_step_kernel<true, false>,
+                    ltl_tc_step_kernel<false, true>, ltl_tc_step_kernel<true, true>}) {
       cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            static_cast<int>(kSmemAlloc));
       if (e != cudaSuccess) return e;
@@ -1020,8 +1025,13 @@ cudaError_t launch_tc_step(const TcLaunch& a, cudaStream_t stream) {
     maps.ring_up[i] = a.ring ? a.ring_up[i & (a.gens > 1 ? 1 : 0)] : *a.store_map;
     maps.ring_down[i] = a.ring ? a.ring_down[i & (a.gens > 1 ? 1 : 0)] : *a.store_map;
   }
-  if (a.stats) return cudaLaunchKernelEx(&cfg, ltl_tc_step_kernel<true>, maps, p);
-  return cudaLaunchKernelEx(&cfg, ltl_tc_step_kernel<false>, maps, p);
+  // the ring's peer-memory paths are compiled only into the ring kernels
+  if (p.ring) {
+    if (a.stats) return cudaLaunchKernelEx(&cfg, ltl_tc_step_kernel<true, true>, maps, p);
+    return cudaLaunchKernelEx(&cfg, ltl_tc_step_kernel<false, true>, maps, p);
+  }
+  if (a.stats) return cudaLaunchKernelEx(&cfg, ltl_tc_step_kernel<true, false>, maps, p);
+  return cudaLaunchKernelEx(&cfg, ltl_tc_step_kernel<false, false>, maps, p);
 }
 
 }  // namespace ltl
