@@ -283,3 +283,38 @@ def test_persistent_self_ring(ltl, orc, rows, cols, monkeypatch):
             assert np.array_equal(t.download(), orc.simulate(init, rule, 7)), (text, 7)
             t.run(text, 6)
             assert np.array_equal(t.download(), orc.simulate(init, rule, 13)), (text, 13)
+
+
+def test_persistent_sweep_all_radii(ltl, orc, monkeypatch):
+    """The multi-generation sweep (forced onto a 384 x 256 torus: 3 bands x 2
+    strips) for every preset radius 1..16 and von Neumann probes, against the
+    oracle."""
+    monkeypatch.setenv("LTL_FORCE_PERSIST", "1")
+    rng = np.random.default_rng(5)
+    cases = [(text, dens) for _, text, dens in ltl.ltl_presets()]
+    cases += [(ltl.format_ltl_rule(ltl.von_neumann_probe_rule(r)), 0.25) for r in (1, 8, 16)]
+    for text, dens in cases:
+        init = (rng.random((384, 256)) < dens).astype(np.uint8)
+        with ltl.DeviceTorus(rows=384, cols=256) as t:
+            t.upload(init)
+            t.run(text, 6)
+            got = t.download()
+        assert np.array_equal(got, orc.simulate(init, parse_rule_text(text), 6)), text
+
+
+def test_bench_geometry_persistent_vs_stencil(ltl, orc):
+    """The bench workload itself (configs[1]: Bosco r=5 on 16384^2, the
+    persistent sweep by default) against the CUDA-core stencil engine, which
+    is pinned to the oracle above: 4 generations."""
+    n, text = 16384, "R5,C2,M1,S34..58,B34..45,NM"
+    with ltl.DeviceTorus(n=n) as t:
+        t.init_random(0.21, 1)
+        init = t.download()
+        t.run(text, 4)
+        tc = t.download()
+    with ltl.DeviceTorus(n=n) as t:
+        t.upload(init)
+        t.run(text, 4, stencil=True)
+        st = t.download()
+    assert np.array_equal(tc, st)
+    assert 0 < int(tc.sum()) < n * n
