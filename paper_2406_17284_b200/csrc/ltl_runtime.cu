@@ -600,8 +600,8 @@ void check_layout(int32_t layout) {
 extern "C" {
 
 const char* ltl_build_info(void) {
-  return "ltl_b200 abi=2 arch=sm_100a layout=column-strips-128 "
-         "kernels=tcgen05-banded-i8,cuda-core-stencil,halo,relayout";
+  return "ltl_b200 abi=3 arch=sm_100a layout=column-strips-128 "
+         "kernels=tcgen05-banded-i8(sweep,ring),cuda-core-stencil,halo,relayout,snapshot";
 }
 
 int ltl_create_torus(ltl_ctx** out, int32_t rows, int32_t cols, int32_t num_slabs,
