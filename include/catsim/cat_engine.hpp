@@ -3,9 +3,9 @@
 // signatures, validation order and messages (src/cat_engine.cpp:83-90,
 // :260-321).  The generations run on the B200 (ltl_run: one fused tcgen05
 // step kernel per generation); the host Grid is uploaded once per call and
-// the result downloaded once.  The unit-test entry points horizontal_step /
-// vertical_step_* (the materialised H and R fields) are not provided: the
-// device never materialises them.
+// the result downloaded once.  The reference's fragment-level unit-test entry
+// points horizontal_step / vertical_step_* (:123-258) materialise H and R
+// through a debug kernel (ltl_fragment_pass); the step never does.
 #pragma once
 
 #include <algorithm>
@@ -16,6 +16,7 @@
 #include <vector>
 
 #include "catsim/device.hpp"
+#include "catsim/fragment.hpp"
 #include "catsim/grid.hpp"
 #include "catsim/rule.hpp"
 
@@ -115,6 +116,107 @@ inline void run_on_device(const Grid& grid, const LtlRule& rule, const CatConfig
 }
 
 }  // namespace detail
+
+namespace detail {
+
+inline std::vector<int32_t> band_words(const BandFragments& b) {
+  std::vector<int32_t> w;
+  w.reserve(3 * b.pi1.data.size());
+  for (const Fragment* p : {&b.pi1, &b.pi2, &b.pi3}) w.insert(w.end(), p->data.begin(), p->data.end());
+  return w;
+}
+
+// cat_engine.cpp:92-111
+inline void check_engine_grid(const Grid& grid, const BandFragments& bands, const CatConfig& cfg) {
+  check_config(cfg);
+  if (grid.layout != Layout::FragmentContiguous)
+    throw std::invalid_argument("layout error: engine needs a fragment-contiguous grid");
+  check_grid_f(grid, cfg);
+  if (bands.f != grid.f)
+    throw std::invalid_argument("config error: band fragments built for f=" + std::to_string(bands.f));
+  if (!grid.halo_valid) throw std::logic_error("sequencing error: periodic halo not filled");
+}
+
+inline int32_t field_max(const IntField& h) {
+  int32_t m = 0;
+  for (int32_t v : h.values) m = std::max(m, v);
+  return m;
+}
+
+inline void add_pass_stats(CatStats* stats, int fpr, bool all_rows, int32_t max_h,
+                           int32_t max_r) {
+  if (!stats) return;
+  long long mmas = 0;
+  for (int i = all_rows ? 0 : 1; i < (all_rows ? fpr : fpr - 1); ++i)
+    for (int j = 1; j + 1 < fpr; ++j) {
+      stats->mma_per_fragment[static_cast<std::size_t>(i) * fpr + j] += 3;
+      mmas += 3;
+    }
+  stats->mma_count += mmas;
+  stats->max_h = std::max(stats->max_h, max_h);
+  stats->max_r = std::max(stats->max_r, max_r);
+}
+
+}  // namespace detail
+
+// Horizontal window sums of every fragment row, interior fragment columns
+// (horizontal_step, cat_engine.cpp:123-161).
+inline IntField horizontal_step(const Grid& grid, const BandFragments& bands, const CatConfig& cfg,
+                                CatStats* stats = nullptr) {
+  detail::check_engine_grid(grid, bands, cfg);
+  IntField h = make_field(grid.n, grid.f, Layout::FragmentContiguous);
+  const int fpr = grid.fragments_per_row();
+  if (stats) {
+    stats->fragments_per_row = fpr;
+    stats->mma_per_fragment.assign(static_cast<std::size_t>(fpr) * fpr, 0u);
+  }
+  const std::vector<int32_t> bw = detail::band_words(bands);
+  detail::check(ltl_fragment_pass(0, grid.n, grid.f, grid.cells.data(), bw.data(), nullptr,
+                                  h.values.data()),
+                nullptr);
+  detail::add_pass_stats(stats, fpr, true, stats ? detail::field_max(h) : 0, 0);
+  h.valid = true;
+  return h;
+}
+
+// Full box sums, centre once (vertical_step_moore, cat_engine.cpp:163-208).
+inline IntField vertical_step_moore(const IntField& h, const BandFragments& bands,
+                                    const CatConfig& cfg, CatStats* stats = nullptr) {
+  detail::check_config(cfg);
+  if (h.layout != Layout::FragmentContiguous)
+    throw std::invalid_argument("layout error: engine needs a fragment-contiguous field");
+  if (!h.valid) throw std::logic_error("sequencing error: horizontal field not yet computed");
+  if (bands.f != h.f || h.f != cfg.f)
+    throw std::invalid_argument("config error: fragment side mismatch");
+  IntField red = make_field(h.n, h.f, Layout::FragmentContiguous);
+  const std::vector<int32_t> bw = detail::band_words(bands);
+  const std::vector<uint8_t> no_cells(static_cast<std::size_t>(h.padded()) * h.padded(), 0);
+  detail::check(ltl_fragment_pass(1, h.n, h.f, no_cells.data(), bw.data(), h.values.data(),
+                                  red.values.data()),
+                nullptr);
+  detail::add_pass_stats(stats, h.fragments_per_row(), false, 0, stats ? detail::field_max(red) : 0);
+  red.valid = true;
+  return red;
+}
+
+// Cross sums, centre twice (vertical_step_von_neumann, cat_engine.cpp:210-258).
+inline IntField vertical_step_von_neumann(const Grid& grid, const IntField& h,
+                                          const BandFragments& bands, const CatConfig& cfg,
+                                          CatStats* stats = nullptr) {
+  detail::check_engine_grid(grid, bands, cfg);
+  if (h.layout != Layout::FragmentContiguous || h.n != grid.n || h.f != grid.f)
+    throw std::invalid_argument("layout error: horizontal field does not match the grid");
+  if (!h.valid) throw std::logic_error("sequencing error: horizontal field not yet computed");
+  IntField red = make_field(grid.n, grid.f, Layout::FragmentContiguous);
+  const std::vector<int32_t> bw = detail::band_words(bands);
+  detail::check(ltl_fragment_pass(2, grid.n, grid.f, grid.cells.data(), bw.data(),
+                                  h.values.data(), red.values.data()),
+                nullptr);
+  detail::add_pass_stats(stats, grid.fragments_per_row(), false, 0,
+                         stats ? detail::field_max(red) : 0);
+  red.valid = true;
+  return red;
+}
 
 // One generation: grid -> out (simulate_step, cat_engine.cpp:260-306).  Fills
 // grid's periodic halo (as the reference does), writes out's interior and

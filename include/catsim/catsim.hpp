@@ -4,6 +4,7 @@
 
 #include "catsim/cat_engine.hpp"
 #include "catsim/engines.hpp"
+#include "catsim/fragment.hpp"
 #include "catsim/grid.hpp"
 #include "catsim/layout.hpp"
 #include "catsim/rule.hpp"

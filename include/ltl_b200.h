@@ -230,6 +230,17 @@ int ltl_snapshot_read(ltl_ctx* ctx, const char* path, int32_t* layout_out);
  * the reader's header checks. */
 int ltl_snapshot_probe(const char* path, int32_t* n, int32_t* f, int32_t* layout);
 
+/* --- the reference's fragment-level unit-test passes, on the device -------
+ * horizontal_step (stage 0), vertical_step_moore (1), vertical_step_von_neumann
+ * (2), src/cat_engine.cpp:123-258: padded (n + 2f)^2 cells / H / R in
+ * fragment-contiguous order, bands = pi1 | pi2 | pi3 (f x f int32 row-major
+ * each, as gen_band_fragments builds them, faults included).  `cells` needs a
+ * filled periodic halo (the reference checks that).  h_in: stages 1-2.  The
+ * product step never materialises H / R; this is the debug path of the
+ * reference's fragment API.  Synchronous. */
+int ltl_fragment_pass(int32_t stage, int32_t n, int32_t f, const uint8_t* cells,
+                      const int32_t* bands, const int32_t* h_in, int32_t* out);
+
 /* --- host-side rule helpers (pure C, no device) --------------------------- */
 
 /* parse_ltl_rule (src/rule.cpp:61-87): returns LTL_OK or

@@ -144,6 +144,13 @@ cudaError_t make_piece_map(CUtensorMap* map, const SlabView& s);
 cudaError_t launch_stencil_step(const SlabView& in, const SlabView& out, const RuleConsts& rule,
                                 int32_t inject_fault, DeviceStats* stats, cudaStream_t stream);
 
+// ---- the reference's fragment-level passes, materialised (ltl_fragment.cu)
+// stage 0 horizontal, 1 vertical Moore, 2 vertical von Neumann; padded
+// (n + 2f)^2 fragment-contiguous fields, bands = pi1 | pi2 | pi3 (f x f each).
+cudaError_t launch_fragment_pass(int stage, int n, int f, const uint8_t* cells,
+                                 const int32_t* bands, const int32_t* h, int32_t* out,
+                                 cudaStream_t stream);
+
 // ---- device init_random (ltl_init.cu): cell (gy, x) of the global torus gets
 // splitmix64 draw number gy * fill_cols + x when gy < fill_rows and x < fill_cols.
 void density_threshold(double density, int32_t* mode, uint64_t* threshold);

@@ -1252,3 +1252,48 @@ int ltl_snapshot_probe(const char* path, int32_t* n, int32_t* f, int32_t* layout
 }
 
 }  // extern "C"
+
+// ---- the reference's fragment-level unit-test entry points, on the device
+
+extern "C" {
+
+int ltl_fragment_pass(int32_t stage, int32_t n, int32_t f, const uint8_t* cells,
+                      const int32_t* bands, const int32_t* h_in, int32_t* out) {
+  if (!cells || !bands || !out || (stage != 0 && !h_in) || stage < 0 || stage > 2)
+    return LTL_ERR_INVALID_ARGUMENT;
+  return guarded(nullptr, [&] {
+    if (f <= 0 || n < 0 || n % f != 0)
+      throw std::invalid_argument("geometry error: n (" + std::to_string(n) +
+                                  ") must be a non-negative multiple of f (" + std::to_string(f) +
+                                  ")");
+    const size_t p = static_cast<size_t>(n) + 2 * f, cells_n = p * p;
+    uint8_t* d_cells = nullptr;
+    int32_t *d_bands = nullptr, *d_h = nullptr, *d_out = nullptr;
+    auto release = [&] {
+      cudaFree(d_cells);
+      cudaFree(d_bands);
+      cudaFree(d_h);
+      cudaFree(d_out);
+    };
+    try {
+      ck(cudaMalloc(&d_cells, cells_n), "cudaMalloc");
+      ck(cudaMalloc(&d_bands, 3 * sizeof(int32_t) * f * f), "cudaMalloc");
+      ck(cudaMalloc(&d_out, cells_n * sizeof(int32_t)), "cudaMalloc");
+      ck(cudaMemcpy(d_cells, cells, cells_n, cudaMemcpyHostToDevice), "H2D");
+      ck(cudaMemcpy(d_bands, bands, 3 * sizeof(int32_t) * f * f, cudaMemcpyHostToDevice), "H2D");
+      if (stage != 0) {
+        ck(cudaMalloc(&d_h, cells_n * sizeof(int32_t)), "cudaMalloc");
+        ck(cudaMemcpy(d_h, h_in, cells_n * sizeof(int32_t), cudaMemcpyHostToDevice), "H2D");
+      }
+      ck(ltl::launch_fragment_pass(stage, n, f, d_cells, d_bands, d_h, d_out, nullptr),
+         "fragment pass kernel");
+      ck(cudaMemcpy(out, d_out, cells_n * sizeof(int32_t), cudaMemcpyDeviceToHost), "D2H");
+    } catch (...) {
+      release();
+      throw;
+    }
+    release();
+  });
+}
+
+}  // extern "C"

@@ -64,6 +64,7 @@ EXPORTS = (
     "ltl_slab_buffer", "ltl_pack_edges", "ltl_unpack_halo", "ltl_ring_export",
     "ltl_ring_connect", "ltl_ring_fill", "ltl_ring_active", "ltl_ring_disconnect",
     "ltl_snapshot_write", "ltl_snapshot_read", "ltl_snapshot_probe",
+    "ltl_fragment_pass",
     "ltl_init_random", "ltl_parse_rule", "ltl_format_rule",
     "ltl_preset_count", "ltl_preset", "ltl_von_neumann_probe_rule", "ltl_build_info",
 )
@@ -124,6 +125,9 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
         "ltl_snapshot_read": ([vp, ctypes.c_char_p, ctypes.POINTER(ctypes.c_int32)], ctypes.c_int),
         "ltl_snapshot_probe": ([ctypes.c_char_p, ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int32)],
                                ctypes.c_int),
+        "ltl_fragment_pass": ([ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, u8p,
+                               P(ctypes.c_int32), P(ctypes.c_int32), P(ctypes.c_int32)],
+                              ctypes.c_int),
         "ltl_unpack_halo": ([vp, vp, vp], ctypes.c_int),
         "ltl_parse_rule": ([ctypes.c_char_p, P(ltl_rule_c), ctypes.c_char_p, ctypes.c_int32],
                            ctypes.c_int),

@@ -6,6 +6,7 @@
 // of reference runs, tests/golden/anchors.json) arrive on the command line.
 #include <cstdio>
 #include <cstdlib>
+#include <cmath>
 #include <fstream>
 #include <iterator>
 #include <sstream>
@@ -254,6 +255,83 @@ static void snapshots(const std::string& golden_dir, const std::string& tmp) {
   CHECK_THROWS_AS(snapshot_read("/no-such-dir/x.bin"), std::runtime_error, "cannot open");
 }
 
+static int wrapi(int v, int n) { return ((v % n) + n) % n; }
+
+static void fragment_passes() {  // test_cat_engine.cpp:36-151, fragment.cpp
+  const CatConfig moore = config_for(NeighborhoodKind::Moore);
+  const CatConfig vn = config_for(NeighborhoodKind::VonNeumannSimplified);
+  {  // single live cell spreads along its row
+    Grid g = make_grid(16, 16);
+    g.interior(8, 8) = 1;
+    Grid frag = frag_grid(g);
+    fill_periodic_halo(frag);
+    const IntField h = horizontal_step(frag, gen_band_fragments(16, 1), moore);
+    CHECK(h.valid);
+    for (int y = 0; y < 16; ++y)
+      for (int x = 0; x < 16; ++x)
+        CHECK(h.at(y + 16, x + 16) == ((y == 8 && x >= 7 && x <= 9) ? 1 : 0));
+    const BandFragments b1 = gen_band_fragments(16, 1);
+    const IntField box = vertical_step_moore(horizontal_step(frag, b1, moore), b1, moore);
+    for (int y = 0; y < 16; ++y)
+      for (int x = 0; x < 16; ++x)
+        CHECK(box.at(y + 16, x + 16) == ((std::abs(y - 8) <= 1 && std::abs(x - 8) <= 1) ? 1 : 0));
+    const IntField hv = horizontal_step(frag, b1, vn);
+    const IntField cross = vertical_step_von_neumann(frag, hv, b1, vn);
+    for (int y = 0; y < 16; ++y)
+      for (int x = 0; x < 16; ++x) {
+        int expect = 0;
+        if (y == 8 && x == 8) expect = 2;
+        else if ((std::abs(y - 8) == 1 && x == 8) || (std::abs(x - 8) == 1 && y == 8)) expect = 1;
+        CHECK(cross.at(y + 16, x + 16) == expect);
+      }
+  }
+  {  // torus window / box / cross oracles at several radii
+    const Grid base = init_random(48, 0.4, 7);
+    for (const int r : {1, 3, 8, 16}) {
+      Grid frag = frag_grid(base);
+      fill_periodic_halo(frag);
+      const BandFragments bands = gen_band_fragments(16, r);
+      CatStats st;
+      const IntField h = horizontal_step(frag, bands, moore, &st);
+      const IntField box = vertical_step_moore(h, bands, moore, &st);
+      const IntField hv = horizontal_step(frag, bands, vn);
+      const IntField cross = vertical_step_von_neumann(frag, hv, bands, vn);
+      int bad = 0;
+      for (int y = 0; y < 48; ++y)
+        for (int x = 0; x < 48; ++x) {
+          int hs = 0, bs = 0, cs = 0;
+          for (int dx = -r; dx <= r; ++dx) hs += base.interior(y, wrapi(x + dx, 48));
+          for (int dy = -r; dy <= r; ++dy)
+            for (int dx = -r; dx <= r; ++dx) bs += base.interior(wrapi(y + dy, 48), wrapi(x + dx, 48));
+          for (int dy = -r; dy <= r; ++dy) cs += base.interior(wrapi(y + dy, 48), x);
+          cs += hs;
+          bad += h.at(y + 16, x + 16) != hs || box.at(y + 16, x + 16) != bs ||
+                 cross.at(y + 16, x + 16) != cs;
+        }
+      CHECK(bad == 0);
+      CHECK(st.max_h > 0 && st.max_h <= 2 * r + 1);
+      CHECK(st.mma_count == 3 * (5 * 3) + 3 * 9);  // fpr = 5: H 5 rows x 3 cols, R 3 x 3
+    }
+  }
+  {  // sequencing / layout errors (:228-242)
+    const BandFragments bands = gen_band_fragments(16, 1);
+    Grid stale = frag_grid(init_random(16, 0.5, 1));
+    CHECK_THROWS_AS(horizontal_step(stale, bands, moore), std::logic_error, "periodic halo not filled");
+    Grid row_major = init_random(16, 0.5, 1);
+    fill_periodic_halo(row_major);
+    CHECK_THROWS_AS(horizontal_step(row_major, bands, moore), std::invalid_argument, "fragment-contiguous");
+    IntField unready = make_field(16, 16);
+    CHECK_THROWS_AS(vertical_step_moore(unready, bands, moore), std::logic_error, "not yet computed");
+    CHECK_THROWS_AS(gen_band_fragments(16, 17), std::invalid_argument, "unsupported radius r=17");
+    CHECK(fp16_exactness_bound(16, NeighborhoodKind::Moore) == 1089);
+    CHECK(fp16_exactness_bound(16, NeighborhoodKind::VonNeumannSimplified) == 66);
+    const Fragment i4 = identity_fragment(4);
+    Fragment a(4);
+    for (int k = 0; k < 16; ++k) a.data[k] = k;
+    CHECK(mma(a, i4, Fragment(4)).data == a.data);
+  }
+}
+
 static void anchors(int argc, char** argv, int first) {
   // rule n density seed steps alive fnv (reference runs, anchors.json)
   for (int i = first; i + 6 < argc; i += 7) {
@@ -278,6 +356,7 @@ int main(int argc, char** argv) {
     errors_and_config();
     accounting_and_fault();
     grid_kats();
+    fragment_passes();
     snapshots(argv[1], argv[2]);
     anchors(argc, argv, 3);
   } catch (const std::exception& e) {
