@@ -1,23 +1,36 @@
 #!/usr/bin/env python
-"""bench.py -- cell updates/s of the B200 LTL step (BASELINE.json metric).
+"""bench.py -- cell updates/s of the B200 LTL step (BASELINE.json metric:
+"cell updates/sec vs radius r=1..16 at 1/2/4/8 B200; % of roofline").
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--workload c1|c2|c3|c4] [--engine cat|base|pack]
 
-Workload (BASELINE.json configs[1]): Bosco's rule as BASELINE states it,
-R5,C2,M1,S34..58,B34..45,NM, on a 16384 x 16384 torus seeded by init_random
-(density 0.21, seed 1; generated on the device, bit-identical to the
-reference's splitmix64 grid).  One bench step = one generation of the whole
-torus (configs[1] runs 1000 of them, the default K).  With N GPUs
-(torchrun, one process per GPU) every rank owns a 16384 x 16384 row slab of an
-(N*16384) x 16384 torus and exchanges 16 halo rows per generation with its
-ring neighbours over NCCL: weak scaling.
+Workloads (BASELINE.json configs; all grids from init_random(n, density,
+seed 1), generated on the device bit-identically to the reference's
+splitmix64 grid):
 
-Rank 0 prints ONE JSON line.  `value` is device-timed (CUDA events on the
-launching stream, max over ranks) with the grid resident in HBM; the two
-256 MiB generation buffers exceed the 126 MB L2, so no flush is needed.
-`e2e` is the same metric through the public C-ABI call a user makes
+  c2  (default at N=1, the config the metric is quoted on) the radius sweep:
+      the 16 Table-III presets r = 1..16 (proj/src/rule.cpp:113-133) at their
+      densities, each on its own 32768 x 32768 torus.  One bench step = one
+      generation of every radius (16 x 2^30 cell updates).  `value` = the
+      minimum over r of the per-radius cell updates/s; `per_radius` lists all.
+  c4  (default at N>1) weak scaling: r = 8 `globe`, 65536^2 cells per GPU, an
+      (N*65536) x 65536 torus in row slabs, halo exchange fused into the step.
+  c3  strong scaling: r = 16 `tangy-ramen`, one 65536^2 torus split in N slabs.
+  c1  Bosco r=5 (R5,C2,M1,S34..58,B34..45,NM) 16384^2, one generation per step.
+
+`value` is device-timed (CUDA events on the launching stream around the K
+timed generations, max over ranks) with the grid resident in HBM; every
+generation buffer (>= 1 GiB for c2..c4) exceeds the 126 MB L2, so no flush is
+needed.  `e2e` is the same metric through the public C-ABI call a user makes
 (ltl_run_interior = run_engine(Cat): upload from pinned host memory, K
-generations, download), wall-clocked.
+generations, download), wall-clocked -- the reference's own bench protocol
+(catbench bench times whole run_engine calls, tools/catbench.cpp:123-130).
+
+--impl reference times the reference's own CPU CAT engine (oracle/_ref, the
+unmodified reference sources compiled by oracle/Makefile) on this box's host
+cores on the same workload: same n, same rules and densities, one generation
+of one radius per step (radius 1 + step mod 16).
 """
 from __future__ import annotations
 
@@ -28,18 +41,26 @@ import statistics
 import subprocess
 import sys
 import tempfile
+import threading
 import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-RULE = "R5,C2,M1,S34..58,B34..45,NM"
-N_SIDE = 16384
-DENSITY = 0.21
-SEED = 1
 METRIC = "cell updates/sec vs radius r=1..16 at 1/2/4/8 B200; % of roofline"
 UNIT = "cell updates/s"
-BYTES_PER_CELL = 2  # read 1 B state + write 1 B next state
+SEED = 1
+BYTES_PER_CELL = 2   # read 1 B state + write 1 B next state
+OPS_ALG = 192        # the reference's 6 fragment MMAs x 2*16^3 / 16^2
+OPS_EXEC = 800       # tcgen05 kind::i8 ops the kernel issues per cell
+BOSCO = "R5,C2,M1,S34..58,B34..45,NM"
+
+WORKLOADS = {
+    "c1": "configs[1] Bosco r=5 (R5,C2,M1,S34..58,B34..45,NM) 16384x16384",
+    "c2": "configs[2] radius sweep r=1..16 (Table III presets) 32768x32768",
+    "c3": "configs[3] r=16 tangy-ramen 65536x65536 row slabs (strong scaling)",
+    "c4": "configs[4] r=8 globe 65536x65536 cells per GPU (weak scaling)",
+}
 
 
 def env_int(name, default):
@@ -52,93 +73,148 @@ def env_int(name, default):
 def measured_peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
-            return json.load(fh), "measured"
+            return json.load(fh), "measured (MEASURED_PEAKS.json)"
     except OSError:
-        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}, "fallback"
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}, "fallback (B200_PROFILING.md)"
 
 
-def ncu_traffic():
-    """dram read+write bytes per generation of the step kernel from the
-    committed ncu --set full capture (profiles/), or None."""
-    path = os.path.join(ROOT, "profiles", "ncu_tc_step.json")
+def profile_json(name):
     try:
-        with open(path) as fh:
-            d = json.load(fh)
-        return d.get("dram_bytes_per_generation"), d.get("n")
+        with open(os.path.join(ROOT, "profiles", name)) as fh:
+            return json.load(fh)
     except (OSError, ValueError):
-        return None, None
+        return None
+
+
+def mma_i8_peak():
+    """Measured tcgen05 kind::i8 dense peak (tools/ubench_mma.cu on a B200,
+    profiles/ubench_mma_r02.json), else the vendor figure."""
+    d = profile_json("ubench_mma_r02.json")
+    if d and d.get("i8_peak_tops"):
+        return float(d["i8_peak_tops"]) * 1e12, "measured (profiles/ubench_mma_r02.json)"
+    return 4.5e15, "vendor dense i8 (no measurement committed)"
+
+
+def workload_rules(workload):
+    """[(label, rule text, density)] of a workload (the reference's presets)."""
+    from paper_2406_17284_b200 import ltl
+    presets = ltl.ltl_presets()
+    if workload == "c1":
+        return [("bosco-literal", BOSCO, 0.21)]
+    if workload == "c2":
+        return [(p[0], p[1], p[2]) for p in presets[:16]]
+    if workload == "c3":
+        return [tuple(presets[15])]
+    return [tuple(presets[7])]
+
+
+def workload_side(workload):
+    return {"c1": 16384, "c2": 32768, "c3": 65536, "c4": 65536}[workload]
 
 
 class Clocks:
-    """nvidia-smi sampler running during the timed region."""
+    """SM clock / throttle sampler running during the timed region: NVML every
+    5 ms (nvidia_ml_py), else nvidia-smi every 100 ms."""
 
-    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    REASONS = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20,
+               "sw_power_cap": 0x4}
 
-    def __init__(self):
+    def __init__(self, device=0):
+        self.device = device
+        self.samples, self.reasons, self.watts, self.max_mhz = [], set(), [], 0
+        self.stop_ev = threading.Event()
+        self.thread = None
         self.proc = None
-        self.path = None
 
     def start(self):
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.device)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+
+            def loop():
+                while not self.stop_ev.is_set():
+                    try:
+                        self.samples.append(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM))
+                        mask = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                        for k, bit in self.REASONS.items():
+                            if mask & bit:
+                                self.reasons.add(k)
+                        self.watts.append(pynvml.nvmlDeviceGetPowerUsage(h) / 1000.0)
+                    except Exception:  # noqa: BLE001
+                        pass
+                    time.sleep(0.005)
+            self.thread = threading.Thread(target=loop, daemon=True)
+            self.thread.start()
+            return
+        except Exception:  # noqa: BLE001 -- no NVML: nvidia-smi
+            pass
         try:
             fd, self.path = tempfile.mkstemp(suffix=".csv")
             os.close(fd)
             self.proc = subprocess.Popen(
-                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "100"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+                ["nvidia-smi", "-i", str(self.device),
+                 "--query-gpu=clocks.sm,clocks.max.sm,power.draw,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
         except OSError:
             self.proc = None
 
     def stop(self):
-        if not self.proc:
+        if self.thread:
+            self.stop_ev.set()
+            self.thread.join()
+        elif self.proc:
+            time.sleep(0.15)
+            self.proc.terminate()
+            self.proc.wait()
+            with open(self.path) as fh:
+                for line in fh:
+                    parts = [p.strip() for p in line.split(",")]
+                    try:
+                        self.samples.append(float(parts[0]))
+                        self.max_mhz = max(self.max_mhz, float(parts[1]))
+                        self.watts.append(float(parts[2]))
+                    except (ValueError, IndexError):
+                        continue
+                    for k, v in zip(list(self.REASONS), parts[3:7]):
+                        if v.lower() == "active":
+                            self.reasons.add(k)
+            os.unlink(self.path)
+        if not self.samples:
             return None
-        time.sleep(0.15)
-        self.proc.terminate()
-        self.proc.wait()
-        sm, mx, reasons, watts = [], 0, set(), []
-        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
-        with open(self.path) as fh:
-            for line in fh:
-                parts = [p.strip() for p in line.split(",")]
-                if len(parts) < 9:
-                    continue
-                try:
-                    sm.append(float(parts[1]))
-                    mx = max(mx, float(parts[2]))
-                except ValueError:
-                    continue
-                try:
-                    watts.append(float(parts[3]))
-                except ValueError:
-                    pass
-                for name, val in zip(names, parts[5:9]):
-                    if val.lower() == "active":
-                        reasons.add(name)
-        os.unlink(self.path)
-        if not sm:
-            return None
-        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
-                "samples": len(sm), "power_w": statistics.median(watts) if watts else None}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples),
+                "power_w": statistics.median(self.watts) if self.watts else None}
 
 
-def cpu_baseline(grid, gens: int):
-    """The reference's CAT engine (oracle/_ref, built from the reference sources)
-    on the host's cores: run_engine(Cat) over the full torus for `gens`
-    generations, layout conversion included as catbench does."""
+# --------------------------------------------------------------------- CPU legs
+def cpu_baseline(grids, rules, n):
+    """The reference's CPU CAT engine (oracle/_ref) on this box's host cores,
+    one generation of each sampled radius: run_engine(Cat) with the layout
+    conversion (catbench style) and simulate() alone."""
     import oracle
     ref = oracle.Reference()
     cores = max(1, ref.hardware_concurrency())
-    t0 = time.perf_counter()
-    ref.run_engine("cat", grid, RULE, gens, workers=cores)
-    dt = time.perf_counter() - t0
-    n = grid.shape[0]
-    return {"value": n * n * gens / dt, "unit": UNIT, "cores": cores, "kind": "reference",
-            "sample": f"{n}x{n} torus, {gens} generations of run_engine(Cat) with "
-                      f"workers={cores} (layout conversion included), {dt:.1f} s"}
+    tot_ms = sim_ms = 0.0
+    for g, (label, rule, _d) in zip(grids, rules):
+        a, b = ref.run_cat_timed(g, rule, 1, workers=cores)
+        tot_ms += a
+        sim_ms += b
+    gens = len(grids)
+    labels = ",".join(r[0] for r in rules)
+    return {"value": n * n * gens / (tot_ms / 1e3), "unit": UNIT, "cores": cores,
+            "kind": "reference",
+            "value_simulate_only": n * n * gens / (sim_ms / 1e3),
+            "sample": f"{n}x{n} torus, 1 generation each of {labels} through run_engine(Cat) "
+                      f"with workers={cores}: {tot_ms / 1e3:.1f} s with the layout conversion "
+                      f"(value), {sim_ms / 1e3:.1f} s in simulate() alone (value_simulate_only)"}
 
 
-def reference_arm(args, rank):
+def reference_arm(args, rank, world):
     """--impl reference: the reference's own CPU path on this box's host cores."""
     if rank != 0:
         return
@@ -147,32 +223,53 @@ def reference_arm(args, rank):
     import oracle
     ref = oracle.Reference()
     cores = max(1, ref.hardware_concurrency())
-    # calibrate: size the per-step sample so K + W steps fit in ~2 minutes
-    probe = 1024
-    g = ref.init_random(probe, DENSITY, SEED)
-    t0 = time.perf_counter()
-    ref.run_engine("cat", g, RULE, 2, workers=cores)
-    rate = probe * probe * 2 / (time.perf_counter() - t0)
-    budget_s = 120.0
-    per_step = budget_s / max(1, args.steps + args.warmup)
-    n_s = int((rate * per_step) ** 0.5) // 16 * 16
-    n_s = max(64, min(N_SIDE, n_s))
-    grid = ref.init_random(n_s, DENSITY, SEED)
-    if args.warmup:
-        grid = ref.run_engine("cat", grid, RULE, args.warmup, workers=cores)
-    t0 = time.perf_counter()
-    ref.run_engine("cat", grid, RULE, args.steps, workers=cores)
-    dt = time.perf_counter() - t0
-    value = n_s * n_s * args.steps / dt
-    sample = (f"{n_s}x{n_s} torus (bounded sample of the {N_SIDE}^2 workload, same rule and "
-              f"density), {args.steps} generations in one run_engine(Cat) call, workers={cores}")
+    workload = args.workload
+    rules = ref_rules(ref, workload)
+    n = workload_side(workload)
+    note = ""
+    if workload in ("c3", "c4"):
+        # one 65536^2 CAT step needs ~56 GB of host RAM and ~1 min per
+        # generation on 16 cores: bounded sample of the same rule at 16384^2
+        n = 16384
+        note = f" (bounded sample: {n}^2 torus of the same rule; the GPU arm's torus is " \
+               f"{'N*' if workload == 'c4' else ''}65536 x 65536)"
+    # the initial grids, built by the reference's init_random in parallel threads
+    grids = [None] * len(rules)
+
+    def mk(i):
+        grids[i] = ref.init_random(n, rules[i][2], SEED)
+    ths = [threading.Thread(target=mk, args=(i,)) for i in range(len(rules))]
+    for t in ths:
+        t.start()
+    for t in ths:
+        t.join()
+    per = {}
+    total = 0.0
+    for i in range(args.warmup + args.steps):
+        k = i % len(rules)
+        t0 = time.perf_counter()
+        grids[k] = ref.run_engine("cat", grids[k], rules[k][1], 1, workers=cores)
+        dt = time.perf_counter() - t0
+        if i >= args.warmup:
+            total += dt
+            per.setdefault(k, []).append(dt)
+    rates = {k: n * n * len(v) / sum(v) for k, v in per.items()}
+    value = min(rates.values())
+    sample = (f"{n}x{n} torus{note}; step i = one generation of radius "
+              f"{'1 + i mod 16' if len(rules) > 1 else rules[0][0]} through run_engine(Cat) "
+              f"(layout conversion included, as catbench), workers={cores}; value = min over "
+              f"the radii timed of their cell updates/s")
     line = {
-        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3 / args.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
-        "data": "synthetic (init_random splitmix64 grid, density 0.21, seed 1)",
-        "config": {"workload": "configs[1] Bosco r=5 (R5,C2,M1,S34..58,B34..45,NM)",
-                   "n": n_s, "rule": RULE, "density": DENSITY, "seed": SEED},
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": total * 1e3 / args.steps,
+        "higher_is_better": True, "scaling": "weak" if workload != "c3" else "strong",
+        "vs_baseline": None, "dtype": "u8",
+        "data": "synthetic (reference init_random splitmix64 grids, seed 1)",
+        "config": config_dict(workload, world),
+        "aggregate_value": n * n * args.steps / total,
+        "per_radius": [{"r": ref.parse_rule(rules[k][1])[0], "rule": rules[k][0],
+                        "cell_updates_per_s": rates[k], "generations": len(per[k])}
+                       for k in sorted(per)],
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "reference",
                          "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -181,70 +278,142 @@ def reference_arm(args, rank):
     print(json.dumps(line), flush=True)
 
 
+def ref_rules(ref, workload):
+    presets = ref.presets()
+    if workload == "c1":
+        return [("bosco-literal", BOSCO, 0.21)]
+    if workload == "c2":
+        return [tuple(p) for p in presets[:16]]
+    if workload == "c3":
+        return [tuple(presets[15])]
+    return [tuple(presets[7])]
+
+
+def config_dict(workload, world):
+    n = workload_side(workload)
+    d = {"workload": WORKLOADS[workload], "n": n, "seed": SEED,
+         "l2": "inputs larger than L2 (every generation buffer >= 256 MiB > 126 MB L2)"}
+    if workload == "c2":
+        d["rules"] = "Table III presets r=1..16 at their densities (proj/src/rule.cpp:113-133)"
+    elif workload == "c1":
+        d.update(rule=BOSCO, density=0.21)
+    elif workload == "c3":
+        d.update(rule="R16,C2,M0,S170..296,B170..300,NM", density=0.26,
+                 torus=f"{n}x{n} split in {world} row slabs")
+    else:
+        d.update(rule="R8,C2,M0,S163..223,B74..252,NM", density=0.23,
+                 torus=f"({world}*{n})x{n} in {world} row slabs")
+    d["parallelism"] = ("1 slab" if world == 1 else
+                        f"row slabs x{world}, 16-row halo pulled by the step's own TMA loads "
+                        f"from the ring neighbours' slabs over NVLink (CUDA IPC)")
+    return d
+
+
+# --------------------------------------------------------------------- GPU arm
 def ours_single(args):
     import numpy as np
     import torch
 
     from paper_2406_17284_b200 import ltl
-    n, steps, warmup = args.n, args.steps, args.warmup
-    rule = ltl.parse_ltl_rule(args.rule)
-    stencil = args.engine == "stencil"
+    workload, steps, warmup = args.workload, args.steps, args.warmup
+    n = workload_side(workload)
+    rules = workload_rules(workload)
+    engine = args.engine
     torus = ltl.DeviceTorus(rows=n, cols=n)
-    torus.init_random(DENSITY, SEED)
-    init = torus.download()
 
-    clocks = Clocks()
+    clocks = Clocks(torch.cuda.current_device())
+    per, launches, inits = [], 0, []
     clocks.start()
-    total_ms, kernel_ms = torus.time(rule, steps, warmup, stencil=stencil)
-    launches = torus.time_launches()  # inside the timed loop
+    for label, rule_text, dens in rules:
+        rule = ltl.parse_ltl_rule(rule_text)
+        torus.init_random(dens, SEED)
+        if workload == "c2" and label in ("life", "bosco", "tangy-ramen"):
+            inits.append((label, rule_text, dens, torus.download()))
+        total_ms, kernel_ms = torus.time(rule, steps, warmup, engine=engine)
+        launches += torus.time_launches()
+        per.append(dict(r=rule.r, rule=label, ms_per_generation=total_ms / steps,
+                        kernel_ms_isolated=kernel_ms / steps,
+                        cell_updates_per_s=n * n * steps / (total_ms / 1e3)))
     clk = clocks.stop()
 
-    cells = n * n
-    value = cells * steps / (total_ms / 1e3)
-    kern_avg_s = kernel_ms / 1e3 / steps
-    peaks, peak_kind = measured_peaks()
-    achieved = BYTES_PER_CELL * cells / kern_avg_s / 1e9
-    traffic, traffic_n = ncu_traffic()
-    if traffic is not None and traffic_n != n:
-        traffic = traffic * (n * n) / (traffic_n * traffic_n)
+    peaks, peak_src = measured_peaks()
+    hbm = peaks["hbm_gbs"]
+    p_mma, mma_src = mma_i8_peak()
+    for e in per:
+        e["hbm_frac"] = BYTES_PER_CELL * n * n / (e["ms_per_generation"] / 1e3) / 1e9 / hbm
+    ms_step = sum(e["ms_per_generation"] for e in per)
+    value = min(e["cell_updates_per_s"] for e in per)
+    # The timed region launches the step kernel only (gpu_launches = one per
+    # generation and radius), back to back on one stream: its average launch
+    # duration is the region's event time / launches.  (Bracketing every launch
+    # with its own events -- kernel_ms_isolated -- cuts the programmatic overlap
+    # of consecutive launches and reads ~4 % longer.)
+    kern_avg_s = statistics.mean(e["ms_per_generation"] for e in per) / 1e3
+    kern_iso_s = statistics.mean(e["kernel_ms_isolated"] for e in per) / 1e3
+    achieved = BYTES_PER_CELL * n * n / kern_avg_s / 1e9
+    ceiling_hbm = hbm * 1e9 / BYTES_PER_CELL
+    ceiling_mma = p_mma / OPS_EXEC if engine == "cat" else None
 
-    # e2e through the public C-ABI: pinned host buffers, run_engine(Cat) semantics
-    hin = torch.from_numpy(init).pin_memory().numpy()
+    # e2e through the public C-ABI (ltl_run_interior = run_engine(Cat)):
+    # pinned host grids, upload + K generations + download per radius
+    hin = torch.empty((n, n), dtype=torch.uint8).pin_memory().numpy()
     hout = torch.empty((n, n), dtype=torch.uint8).pin_memory().numpy()
-    torus.run_interior(hin, rule, 1, out=hout, stencil=stencil)  # warm
-    iters = 2
-    t0 = time.perf_counter()
-    for _ in range(iters):
-        torus.run_interior(hin, rule, steps, out=hout, stencil=stencil)
-    e2e_s = time.perf_counter() - t0
-    e2e_value = cells * steps * iters / e2e_s
+    e2e_s, e2e_per = 0.0, []
+    for label, rule_text, dens in rules:
+        rule = ltl.parse_ltl_rule(rule_text)
+        torus.init_random(dens, SEED)
+        torus.download(hin)
+        torus.run_interior(hin, rule, 1, out=hout, engine=engine)  # warm
+        t0 = time.perf_counter()
+        torus.run_interior(hin, rule, steps, out=hout, engine=engine)
+        dt = time.perf_counter() - t0
+        e2e_s += dt
+        e2e_per.append(n * n * steps / dt)
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1, "steps": steps,
-        "warmup": warmup, "ms_per_step": total_ms / steps, "higher_is_better": True,
+        "warmup": warmup, "ms_per_step": ms_step, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "u8",
-        "data": "synthetic (device init_random, splitmix64 grid identical to the reference's)",
-        "config": {"workload": "configs[1] Bosco r=5 16384x16384, 1 generation per step",
-                   "rule": args.rule, "n": n, "density": DENSITY, "seed": SEED,
-                   "engine": "tcgen05 banded-MMA" if not stencil else "CUDA-core stencil",
-                   "l2": "inputs larger than L2 (2 x 256 MiB ping-pong generations)",
-                   "parallelism": "1 slab"},
-        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": cells,
-                "d2h_bytes_per_step": cells,
-                "step": f"one ltl_run_interior call = upload + {steps} generations + download"},
+        "data": "synthetic (device init_random, splitmix64 grids identical to the reference's)",
+        "config": dict(config_dict(workload, 1),
+                       engine={"cat": "tcgen05 banded-MMA", "base": "CUDA-core direct-sum stencil",
+                               "pack": "CUDA-core packed sliding-window stencil"}[engine],
+                       step=(f"one generation of each of the {len(rules)} radii"
+                             if len(rules) > 1 else "one generation")),
+        "aggregate_value": n * n * len(rules) / (ms_step / 1e3),
+        "per_radius": per,
+        "e2e": {"value": min(e2e_per), "unit": UNIT,
+                "h2d_bytes_per_step": n * n * len(rules) // steps,
+                "d2h_bytes_per_step": n * n * len(rules) // steps,
+                "step": (f"per radius one ltl_run_interior call (run_engine(Cat)): H2D of the "
+                         f"{n}x{n} grid from pinned memory + {steps} generations + D2H; value = "
+                         f"min over r; bytes amortised over the call's {steps} generations"),
+                "aggregate_value": n * n * steps * len(rules) / e2e_s},
         "gpu_launches": launches,
-        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"],
-                     "unit": "GB/s", "frac": achieved / peaks["hbm_gbs"], "traffic": traffic,
-                     "peak_source": f"{peak_kind} hbm_gbs (MEASURED_PEAKS.json)",
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                     "frac": achieved / hbm, "traffic": None, "peak_source": peak_src,
+                     "kernel": "ltl_tc_step_kernel" if engine == "cat" else f"{engine} stencil",
                      "kernel_ms_per_generation": kern_avg_s * 1e3,
-                     "algorithmic_bytes_per_generation": BYTES_PER_CELL * cells,
-                     "per": ("generation: one persistent launch runs all timed generations"
-                             if launches == 1 and steps > 1 else
-                             "generation: one step-kernel launch each")},
+                     "kernel_ms_isolated": kern_iso_s * 1e3,
+                     "algorithmic_bytes_per_generation": BYTES_PER_CELL * n * n,
+                     "per": ("generation: timed-region event time / launches (one step-kernel "
+                             "launch per generation), mean over the radii"),
+                     "ceiling_cells_per_s_hbm": ceiling_hbm,
+                     "ceiling_cells_per_s_mma": ceiling_mma,
+                     "mma_peak_ops": p_mma if engine == "cat" else None,
+                     "mma_peak_source": mma_src if engine == "cat" else None,
+                     "ops_per_cell_algorithmic": OPS_ALG, "ops_per_cell_executed":
+                         OPS_EXEC if engine == "cat" else None,
+                     "mma_frac": (value * OPS_EXEC / p_mma) if engine == "cat" else None},
         "clocks": clk,
     }
-    if not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_baseline(init, args.cpu_gens)
+    ncu = profile_json(f"ncu_tc_step_{n}.json")
+    if ncu and engine == "cat":
+        line["roofline"]["traffic"] = ncu.get("dram_bytes_per_generation")
+        line["roofline"]["traffic_source"] = f"profiles/ncu_tc_step_{n}.json (ncu --set full)"
+    if not args.no_cpu_baseline and inits:
+        line["cpu_baseline"] = cpu_baseline([g for *_, g in inits],
+                                            [(a, b, c) for a, b, c, _ in inits], n)
     np.asarray(0)
     print(json.dumps(line), flush=True)
 
@@ -256,41 +425,36 @@ def ours_multi(args, rank, world, local_rank):
 
     from paper_2406_17284_b200 import ltl
     from paper_2406_17284_b200.dist import PartitionedTorus
-    n, steps, warmup = args.n, args.steps, args.warmup
-    rule = ltl.parse_ltl_rule(args.rule)
-    stencil = args.engine == "stencil"
+    workload, steps, warmup = args.workload, args.steps, args.warmup
+    n = workload_side(workload)
+    label, rule_text, dens = workload_rules(workload)[0]
+    rule = ltl.parse_ltl_rule(rule_text)
     torch.cuda.set_device(local_rank)
-    part = PartitionedTorus(world * n, n, rank, world, local_rank, ring=not stencil)
+    global_rows = n if workload == "c3" else world * n
+    part = PartitionedTorus(global_rows, n, rank, world, local_rank)
     stream = torch.cuda.current_stream()
     part.use_stream(stream.cuda_stream)
-    part.init_random(DENSITY, SEED)
-    if stencil:
-        for _ in range(warmup):
-            part.step(rule, stencil)
-    else:
-        part.run(rule, warmup)
+    part.init_random(dens, SEED)
+    part.run(rule, warmup)
     torch.cuda.synchronize()
     dist.barrier()
     l0 = part.torus.kernel_launches()
-    clocks = Clocks() if rank == 0 else None
+    clocks = Clocks(local_rank) if rank == 0 else None
     if clocks:
         clocks.start()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ev0.record(stream)
-    if stencil:
-        for _ in range(steps):
-            part.step(rule, stencil)
-    else:
-        part.run(rule, steps)
+    part.run(rule, steps)
     ev1.record(stream)
     torch.cuda.synchronize()
     dist.barrier()
-    launches = part.torus.kernel_launches() - l0
+    launches = torch.tensor([part.torus.kernel_launches() - l0], device="cuda")
+    dist.all_reduce(launches)
     clk = clocks.stop() if clocks else None
     ms = torch.tensor([ev0.elapsed_time(ev1)], device="cuda", dtype=torch.float64)
     dist.all_reduce(ms, op=dist.ReduceOp.MAX)
     total_ms = float(ms.item())
-    cells = world * n * n
+    cells = global_rows * n
     value = cells * steps / (total_ms / 1e3)
 
     # e2e: each rank uploads its slab from pinned memory, runs, downloads
@@ -299,81 +463,88 @@ def ours_multi(args, rank, world, local_rank):
     torch.cuda.synchronize()
     dist.barrier()
     t0 = time.perf_counter()
-    part.torus.upload(hin)
-    part.exchange()
-    if stencil:
-        for _ in range(steps):
-            part.step(rule, stencil)
-    else:
-        part.run(rule, steps)
+    part.upload(hin)
+    part.run(rule, steps)
     part.torus.download(hout)
     torch.cuda.synchronize()
     e2e = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device="cuda")
     dist.all_reduce(e2e, op=dist.ReduceOp.MAX)
     e2e_value = cells * steps / float(e2e.item())
     if rank == 0:
-        peaks, peak_kind = measured_peaks()
-        achieved = BYTES_PER_CELL * (n * n) / (total_ms / 1e3 / steps) / 1e9
+        peaks, peak_src = measured_peaks()
+        hbm = peaks["hbm_gbs"]
+        achieved = BYTES_PER_CELL * part.rows * n / (total_ms / 1e3 / steps) / 1e9
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": steps,
             "warmup": warmup, "ms_per_step": total_ms / steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "u8",
+            "scaling": "strong" if workload == "c3" else "weak", "vs_baseline": None,
+            "dtype": "u8",
             "data": "synthetic (device init_random, splitmix64 grid identical to the reference's)",
-            "config": {"workload": f"configs[1] Bosco r=5, {n}x{n} cells per GPU, "
-                                   f"({world}*{n})x{n} torus in row slabs",
-                       "rule": args.rule, "n": n, "density": DENSITY, "seed": SEED,
-                       "l2": "inputs larger than L2",
-                       "parallelism": (f"row slabs x{world}, 16-row halo exchange fused into "
-                                       f"the step (TMA stores into the ring neighbours' "
-                                       f"halo buffers over NVLink, CUDA IPC)" if part.ring else
-                                       f"row slabs x{world}, 16-row NCCL halo exchange")},
-            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": n * n * world,
-                    "d2h_bytes_per_step": n * n * world,
-                    "step": f"upload + {steps} generations + download per rank"},
-            "gpu_launches": launches * world,
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"],
-                         "unit": "GB/s", "frac": achieved / peaks["hbm_gbs"], "traffic": None,
-                         "peak_source": f"{peak_kind} hbm_gbs, per GPU, whole step time"},
+            "config": dict(config_dict(workload, world), rule_name=label,
+                           exchange="fused ring pulls" if part.ring else "NCCL send/recv"),
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": cells // steps,
+                    "d2h_bytes_per_step": cells // steps,
+                    "step": f"upload + {steps} generations + download per rank; bytes "
+                            f"amortised over the {steps} generations"},
+            "gpu_launches": int(launches.item()),
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                         "frac": achieved / hbm, "traffic": None, "peak_source": peak_src,
+                         "per": "generation per GPU (rank 0's slab, whole step time)"},
             "clocks": clk,
         }
+        ncu = profile_json(f"ncu_tc_step_{n}.json")
+        if ncu:
+            line["roofline"]["traffic"] = ncu.get("dram_bytes_per_generation")
+            line["roofline"]["traffic_source"] = (f"profiles/ncu_tc_step_{n}.json (1-GPU "
+                                                  f"{n}^2 capture, per {n}^2 generation)")
+        if not args.no_cpu_baseline:
+            import oracle
+            ref = oracle.Reference()
+            g = ref.init_random(4096, dens, SEED)
+            line["cpu_baseline"] = cpu_baseline([g], [(label, rule_text, dens)], 4096)
+            line["cpu_baseline"]["sample"] += " (4096^2 bounded sample of the same rule)"
         np.asarray(0)
         print(json.dumps(line), flush=True)
 
 
-def torch_device(local_rank):
-    import torch
-    return torch.device("cuda", local_rank)
+def spawn(args):
+    """--gpus N without a torchrun environment: re-launch under torchrun."""
+    port = os.environ.get("MASTER_PORT", str(29500 + os.getpid() % 1000))
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1",
+           f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    os.execv(sys.executable, cmd)
 
 
 def main():
     ap = argparse.ArgumentParser(description=__doc__.splitlines()[0])
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=1000)
+    ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
-    ap.add_argument("--engine", choices=("cat", "stencil"), default="cat")
-    ap.add_argument("--n", type=int, default=N_SIDE)
-    ap.add_argument("--rule", default=RULE)
-    ap.add_argument("--cpu-gens", type=int, default=2)
+    ap.add_argument("--workload", choices=tuple(WORKLOADS), default=None)
+    ap.add_argument("--engine", choices=("cat", "base", "pack"), default="cat")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--dist", action="store_true",
-                    help="use the multi-process slab path even at world size 1 (testing)")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
 
     world = env_int("WORLD_SIZE", 1)
     rank = env_int("RANK", 0)
     local_rank = env_int("LOCAL_RANK", 0)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        if args.impl == "reference":
+            world = args.gpus  # rank 0 alone runs the CPU reference
+        else:
+            spawn(args)
+    if args.workload is None:
+        args.workload = "c2" if max(world, args.gpus) == 1 else "c4"
     if args.impl == "reference":
-        reference_arm(args, rank)
+        reference_arm(args, rank, max(world, args.gpus))
         return
-    if world > 1 or args.dist:
+    if world > 1:
+        import torch
         import torch.distributed as dist
-        if "RANK" not in os.environ:  # --dist without torchrun: a world of one
-            os.environ.update(RANK="0", WORLD_SIZE="1", MASTER_ADDR="127.0.0.1",
-                              MASTER_PORT=os.environ.get("MASTER_PORT", "29533"))
-        dist.init_process_group(os.environ.get("LTL_DIST_BACKEND", "nccl"),
-                                device_id=torch_device(local_rank))
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
         try:
             ours_multi(args, rank, world, local_rank)
         finally:

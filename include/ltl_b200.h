@@ -49,9 +49,14 @@ extern "C" {
 /* ltl_run flags */
 #define LTL_FLAG_INJECT_FAULT 0x1u  /* CatConfig.inject_band_fault, cat_engine.hpp:22-24 */
 #define LTL_FLAG_WANT_STATS 0x2u    /* fill ltl_stats_c (device max-reduction of H / R) */
-#define LTL_FLAG_STENCIL 0x4u       /* run the CUDA-core stencil ablation, not tcgen05 */
-#define LTL_FLAG_NO_GRAPH 0x8u      /* accepted, no effect: generations are never graph-captured (a
-                                       captured 2-generation graph measured no faster) */
+/* Engine selection (catsim::EngineKind, proj/include/catsim/engines.hpp:11):
+ * none = Cat (tcgen05 banded MMA), BASE = the CUDA-core direct-sum stencil (the
+ * paper's SHARED/BASE baseline: (2r+1)^2 adds per cell), PACK = the CUDA-core
+ * packed-lane sliding-window stencil (the strongest classical comparator).
+ * The band fault (LTL_FLAG_INJECT_FAULT) only affects Cat, as in the reference. */
+#define LTL_FLAG_ENGINE_BASE 0x4u
+#define LTL_FLAG_ENGINE_PACK 0x10u
+#define LTL_FLAG_STENCIL LTL_FLAG_ENGINE_BASE /* round-1 name */
 
 /* catsim::LtlRule, proj/include/catsim/rule.hpp:17-32 */
 typedef struct ltl_rule_c {

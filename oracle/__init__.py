@@ -150,6 +150,9 @@ class Reference:
                                        _u8p, _i64p]
         lib.ref_reductions.argtypes = [ctypes.c_int32, ctypes.c_int32, _u8p, ctypes.c_char_p,
                                        _i32p, _i32p]
+        lib.ref_run_cat_timed.argtypes = [ctypes.c_int32, ctypes.c_int32, _u8p, ctypes.c_char_p,
+                                          ctypes.c_int32, ctypes.c_int32, _u8p,
+                                          ctypes.POINTER(ctypes.c_double)]
         lib.ref_snapshot_write.argtypes = [ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, _u8p,
                                            ctypes.c_char_p]
         lib.ref_snapshot_read.argtypes = [ctypes.c_char_p, _i32p, _i32p, _i32p, _u8p,
@@ -212,6 +215,18 @@ class Reference:
             keys = ("mma_count", "steps", "max_h", "max_r", "fragments_per_row", "accesses")
             return out, dict(zip(keys, (int(v) for v in st)))
         return out
+
+    def run_cat_timed(self, grid: np.ndarray, rule_text: str, steps: int, workers: int = 1,
+                      f: int = 16, want_output: bool = False):
+        """run_engine(Cat) timed inside the library: (ms whole call incl. layout
+        conversion, ms of simulate() alone[, output grid])."""
+        g = np.ascontiguousarray(grid, np.uint8)
+        out = np.empty_like(g) if want_output else None
+        ms = (ctypes.c_double * 2)()
+        self._check(self.lib.ref_run_cat_timed(g.shape[0], f, _ptr(g, _u8p), rule_text.encode(),
+                                               steps, workers,
+                                               _ptr(out, _u8p) if want_output else None, ms))
+        return (ms[0], ms[1], out) if want_output else (ms[0], ms[1])
 
     def reductions(self, grid: np.ndarray, rule_text: str, f: int = 16):
         g = np.ascontiguousarray(grid, np.uint8)

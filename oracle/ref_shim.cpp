@@ -10,6 +10,7 @@
 //
 // Status codes: 0 ok, 1 std::invalid_argument, 2 std::logic_error,
 // 3 std::out_of_range / runtime_error / anything else.
+#include <chrono>
 #include <cstdint>
 #include <cstring>
 #include <exception>
@@ -148,6 +149,37 @@ int ref_run_engine(int32_t kind, int32_t n, int32_t f,
       stats6[4] = stats.cat.fragments_per_row;
       stats6[5] = stats.base.accesses();
     }
+  });
+}
+
+// run_engine(Cat) (src/engines.cpp:30-35) split the way SURVEY.md §8d asks the
+// CPU baseline to be reported: ms[0] = the whole call (layout conversion
+// included, as catbench's time_run_ms, tools/catbench.cpp:123-130), ms[1] =
+// simulate() alone (src/cat_engine.cpp:308-321, conversion excluded).
+int ref_run_cat_timed(int32_t n, int32_t f, const uint8_t* interior_in,
+                      const char* rule_text, int32_t steps, int32_t workers,
+                      uint8_t* interior_out, double* ms2) {
+  return guarded([&] {
+    using clk = std::chrono::steady_clock;
+    const catsim::LtlRule rule = catsim::parse_ltl_rule(rule_text);
+    catsim::CatConfig cfg;
+    cfg.f = f;
+    cfg.kind = rule.kind;
+    cfg.workers = workers;
+    const catsim::Grid initial = grid_from_interior(n, f, interior_in);
+    const auto t0 = clk::now();
+    catsim::Grid frag = catsim::to_fragment_layout(initial);
+    const auto t1 = clk::now();
+    catsim::Grid done = catsim::simulate(std::move(frag), rule, cfg, steps);
+    const auto t2 = clk::now();
+    const catsim::Grid out = catsim::to_row_major(done);
+    const auto t3 = clk::now();
+    ms2[0] = std::chrono::duration<double, std::milli>(t3 - t0).count();
+    ms2[1] = std::chrono::duration<double, std::milli>(t2 - t1).count();
+    if (interior_out)
+      for (int y = 0; y < n; ++y)
+        for (int x = 0; x < n; ++x)
+          interior_out[static_cast<std::size_t>(y) * n + x] = out.interior(y, x);
   });
 }
 

@@ -124,7 +124,9 @@ struct TcLaunch {
   int32_t wrap_cols, wrap_rows;
   int32_t rows, cols;
   RuleConsts rule;
-  int32_t inject_fault;
+  int32_t inject_fault;     // CatConfig.inject_band_fault (src/cat_engine.cpp:277)
+  int32_t fault_f;          // fragment side f of the faulted band fragments
+  int32_t fault_row_phase;  // global row of local row 0, mod f
   DeviceStats* stats;  // nullptr -> no stats reduction
   int32_t grid;        // CTAs (0 = auto)
   long long* trace;    // debug timeline (LTL_TC_TRACE), nullptr = off
@@ -140,9 +142,12 @@ cudaError_t make_store_map(CUtensorMap* map, const SlabView& s);
 // 16-row SWIZZLE_128B pieces over a slab (the ring's rows from a neighbour).
 cudaError_t make_piece_map(CUtensorMap* map, const SlabView& s);
 
-// ---- CUDA-core shared-memory stencil ablation (ltl_stencil.cu)
+// ---- CUDA-core stencil ablations (ltl_stencil.cu): kEngineBase sums the
+// (2r+1)^2 box / 2(2r+1) cross per cell (the paper's SHARED baseline),
+// kEnginePack keeps packed 16-bit-lane sliding-window sums (O(1) per cell).
+constexpr int kEngineBase = 0, kEnginePack = 1;
 cudaError_t launch_stencil_step(const SlabView& in, const SlabView& out, const RuleConsts& rule,
-                                int32_t inject_fault, DeviceStats* stats, cudaStream_t stream);
+                                int engine, DeviceStats* stats, cudaStream_t stream);
 
 // ---- the reference's fragment-level passes, materialised (ltl_fragment.cu)
 // stage 0 horizontal, 1 vertical Moore, 2 vertical von Neumann; padded
@@ -170,6 +175,10 @@ cudaError_t launch_halo_fill(const SlabView& self, const SlabView& above, const 
 // Dense row-major rows x cols interior <-> strip slab interior.
 cudaError_t launch_to_strips(const uint8_t* dense, const SlabView& s, cudaStream_t stream);
 cudaError_t launch_from_strips(const SlabView& s, uint8_t* dense, cudaStream_t stream);
+// Dense interior in fragment-contiguous order (f in {4, 8, 16}; rows and
+// cols multiples of f) <-> strip slab interior.
+cudaError_t launch_frag_relayout(uint8_t* dense, const SlabView& s, int f, bool to_strips,
+                                 cudaStream_t stream);
 // *bad |= 1 if any of dense[0, n) is not 0 / 1 (snapshot payloads).
 cudaError_t launch_check_cells(const uint8_t* dense, int64_t n, int32_t* bad,
                                cudaStream_t stream);

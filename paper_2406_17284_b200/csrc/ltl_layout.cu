@@ -11,6 +11,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <type_traits>
 
 #include "ltl_kernels.cuh"
 
@@ -46,6 +47,30 @@ __global__ void relayout_kernel(uint8_t* dense, SlabView s) {
       if (kToStrips) *c = *d;
       else *d = *c;
     }
+  }
+}
+
+// Dense interior in the reference's fragment-contiguous order (interior
+// fragment rows x interior fragments, f x f bytes each; include/catsim/grid.hpp
+// fragment_offset) <-> interior of the slab: one f-byte fragment row segment
+// per thread (f | 128, so it never straddles a strip).  Run i = (I * nfc + J)
+// * F + a is fragment (I, J)'s row a, at dense byte i * F.
+template <int F, bool kToStrips>
+__global__ void frag_relayout_kernel(uint8_t* dense, SlabView s) {
+  using V = typename std::conditional<F == 16, uint4, typename std::conditional<F == 8, uint2, uint32_t>::type>::type;
+  const int nfc = s.cols / F;
+  const int64_t runs = static_cast<int64_t>(s.rows) * nfc;
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < runs;
+       i += stride) {
+    const int64_t per_frow = static_cast<int64_t>(nfc) * F;
+    const int I = static_cast<int>(i / per_frow);
+    const int rem = static_cast<int>(i % per_frow);
+    const int y = I * F + rem % F, x = (rem / F) * F;
+    V* d = reinterpret_cast<V*>(dense + i * F);
+    V* c = reinterpret_cast<V*>(s.buf + s.offset(y + kHalo, x));
+    if (kToStrips) *c = *d;
+    else *d = *c;
   }
 }
 
@@ -104,6 +129,23 @@ cudaError_t launch_from_strips(const SlabView& s, uint8_t* dense, cudaStream_t s
   if (s.rows <= 0 || s.cols <= 0) return cudaSuccess;
   const int64_t work = static_cast<int64_t>(s.rows) * (s.cols % 16 == 0 ? s.cols / 16 : s.cols);
   relayout_kernel<false><<<blocks_for(work), 256, 0, stream>>>(dense, s);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_frag_relayout(uint8_t* dense, const SlabView& s, int f, bool to_strips,
+                                 cudaStream_t stream) {
+  if (s.rows <= 0 || s.cols <= 0) return cudaSuccess;
+  if (s.cols % f || s.rows % f) return cudaErrorInvalidValue;
+  const int blocks = blocks_for(static_cast<int64_t>(s.rows) * (s.cols / f));
+  switch (f * 2 + (to_strips ? 1 : 0)) {
+    case 33: frag_relayout_kernel<16, true><<<blocks, 256, 0, stream>>>(dense, s); break;
+    case 32: frag_relayout_kernel<16, false><<<blocks, 256, 0, stream>>>(dense, s); break;
+    case 17: frag_relayout_kernel<8, true><<<blocks, 256, 0, stream>>>(dense, s); break;
+    case 16: frag_relayout_kernel<8, false><<<blocks, 256, 0, stream>>>(dense, s); break;
+    case 9: frag_relayout_kernel<4, true><<<blocks, 256, 0, stream>>>(dense, s); break;
+    case 8: frag_relayout_kernel<4, false><<<blocks, 256, 0, stream>>>(dense, s); break;
+    default: return cudaErrorInvalidValue;
+  }
   return cudaGetLastError();
 }
 

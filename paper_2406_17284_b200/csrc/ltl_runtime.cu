@@ -131,6 +131,10 @@ ltl::RuleConsts rule_consts(const ltl_rule_c& r) {
   return c;
 }
 
+bool stencil_engine(uint32_t flags) {
+  return (flags & (LTL_FLAG_ENGINE_BASE | LTL_FLAG_ENGINE_PACK)) != 0;
+}
+
 void check_run_args(const ltl_ctx* ctx, const ltl_rule_c* rule, int32_t steps) {
   if (!rule) throw std::invalid_argument("config error: rule is null");
   if (steps < 0) throw std::invalid_argument("config error: steps must be >= 0");
@@ -208,21 +212,25 @@ void create_slabs(ltl_ctx* ctx, int32_t num_slabs, const int32_t* dev_ids) {
     s.strips = ltl::storage_strips(ctx->cols);
     s.strip_bytes = static_cast<int64_t>(s.rows + 2 * kHalo) * ltl::kStrip;
     ck(cudaSetDevice(s.dev), "cudaSetDevice");
+    // every later operation of the slab is ordered on this stream, its zeroing
+    // memsets included (a legacy-stream memset would not be ordered before
+    // kernels on a non-blocking stream)
+    ck(cudaStreamCreateWithFlags(&s.stream, cudaStreamNonBlocking), "cudaStreamCreate");
     const size_t bytes = static_cast<size_t>(s.strips) * s.strip_bytes;
     for (int b = 0; b < 2; ++b) {
       ck(cudaMalloc(&s.buf[b], bytes), "cudaMalloc slab");
-      ck(cudaMemset(s.buf[b], 0, bytes), "cudaMemset slab");
+      ck(cudaMemsetAsync(s.buf[b], 0, bytes, s.stream), "cudaMemset slab");
     }
     ck(cudaMalloc(&s.dstats, sizeof(ltl::DeviceStats)), "cudaMalloc stats");
     {
       const size_t units = static_cast<size_t>((s.rows + ltl::kTcBand - 1) / ltl::kTcBand) *
                            ltl::interior_strips(ctx->cols);
       ck(cudaMalloc(&s.flags, std::max<size_t>(units, 1) * sizeof(uint32_t)), "cudaMalloc flags");
-      ck(cudaMemset(s.flags, 0, std::max<size_t>(units, 1) * sizeof(uint32_t)), "memset flags");
+      ck(cudaMemsetAsync(s.flags, 0, std::max<size_t>(units, 1) * sizeof(uint32_t), s.stream),
+         "memset flags");
       ck(cudaMalloc(&s.ring_sync, 2 * sizeof(uint32_t)), "cudaMalloc ring counters");
-      ck(cudaMemset(s.ring_sync, 0, 2 * sizeof(uint32_t)), "memset ring counters");
+      ck(cudaMemsetAsync(s.ring_sync, 0, 2 * sizeof(uint32_t), s.stream), "memset ring counters");
     }
-    ck(cudaStreamCreateWithFlags(&s.stream, cudaStreamNonBlocking), "cudaStreamCreate");
     ck(cudaEventCreateWithFlags(&s.ev_step, cudaEventDisableTiming), "cudaEventCreate");
     build_maps(s, ctx->cols);
   }
@@ -253,6 +261,12 @@ void create_slabs(ltl_ctx* ctx, int32_t num_slabs, const int32_t* dev_ids) {
       wire_ring(ctx, s, RingPeer{up.ring_sync, up.buf, up.rows, up.flags, &up == &s || up.dev != s.dev},
                 RingPeer{dn.ring_sync, dn.buf, dn.rows, dn.flags, &dn == &s || dn.dev != s.dev});
     }
+  // the zeroing memsets are on the slabs' streams: complete them before any
+  // other slab (or process, after ltl_ring_export) can touch the buffers
+  for (Slab& s : ctx->slabs) {
+    ck(cudaSetDevice(s.dev), "cudaSetDevice");
+    ck(cudaStreamSynchronize(s.stream), "cudaStreamSynchronize");
+  }
 }
 
 void destroy_ctx(ltl_ctx* ctx) {
@@ -313,12 +327,13 @@ void start_ring(ltl_ctx* ctx) {
   for (Slab& s : ctx->slabs) {
     ck(cudaSetDevice(s.dev), "cudaSetDevice");
     ck(cudaStreamSynchronize(s.stream), "cudaStreamSynchronize");
-    ck(cudaMemset(s.ring_sync, 0, 2 * sizeof(uint32_t)), "memset ring counters");
+    ck(cudaMemsetAsync(s.ring_sync, 0, 2 * sizeof(uint32_t), s.stream), "memset ring counters");
     s.ring_gen = 0;
     // per-unit counters restart too: the neighbours compare them with their own base
     const size_t units = static_cast<size_t>((s.rows + ltl::kTcBand - 1) / ltl::kTcBand) *
                          ltl::interior_strips(ctx->cols);
-    ck(cudaMemset(s.flags, 0, std::max<size_t>(units, 1) * sizeof(uint32_t)), "memset flags");
+    ck(cudaMemsetAsync(s.flags, 0, std::max<size_t>(units, 1) * sizeof(uint32_t), s.stream),
+       "memset flags");
     s.flag_base = 0;
   }
   sync_all(ctx);
@@ -361,7 +376,7 @@ void enqueue_halo(ltl_ctx* ctx, int which, bool for_tc = false) {
 // For a ring of slabs every slab needs the same geometry (the kernels compare
 // each other's unit counters) and neighbours that run concurrently with it.
 bool persistent_ok(const ltl_ctx* ctx, uint32_t flags) {
-  if ((flags & LTL_FLAG_STENCIL) || !wrap_cols(ctx) || std::getenv("LTL_NO_PERSIST"))
+  if (stencil_engine(flags) || !wrap_cols(ctx) || std::getenv("LTL_NO_PERSIST"))
     return false;  // env: diagnostics
   const bool single = ctx->slabs.size() == 1 && wrap_rows(ctx);
   if (!single) {
@@ -389,7 +404,7 @@ void enqueue_step(ltl_ctx* ctx, const ltl::RuleConsts& rc, uint32_t flags, bool 
     return;
   }
   const int cur = ctx->cur, nxt = 1 - cur;
-  const bool ring = !(flags & LTL_FLAG_STENCIL) && ring_ok(ctx);
+  const bool ring = !stencil_engine(flags) && ring_ok(ctx);
   if (ring && ctx->ring_stale) {
     if (ctx->external_row_halo)
       throw std::logic_error(
@@ -397,7 +412,7 @@ void enqueue_step(ltl_ctx* ctx, const ltl::RuleConsts& rc, uint32_t flags, bool 
     start_ring(ctx);
     ctx->ring_stale = false;
   }
-  if (flags & LTL_FLAG_STENCIL) ctx->ring_stale = true;  // stencil generations bypass the ring
+  if (stencil_engine(flags)) ctx->ring_stale = true;  // stencil generations bypass the ring
   if (ring && ctx->slabs.size() > 1) {
     // slabs sharing a device must not spin on each other's counters (a
     // waiting kernel can hold every SM): order each step after the
@@ -415,13 +430,17 @@ void enqueue_step(ltl_ctx* ctx, const ltl::RuleConsts& rc, uint32_t flags, bool 
     Slab& s = ctx->slabs[i];
     ck(cudaSetDevice(s.dev), "cudaSetDevice");
     if (kt0) ck(cudaEventRecord(kt0[i], s.stream), "event");
-    if (flags & LTL_FLAG_STENCIL) {
+    if (stencil_engine(flags)) {
       if (ctx->halo_stale) {  // the last tcgen05 steps left wrap-free halos
         ck(cudaSetDevice(s.dev), "cudaSetDevice");
         if (i == 0) enqueue_halo(ctx, cur);
         ck(cudaSetDevice(s.dev), "cudaSetDevice");
       }
-      ck(ltl::launch_stencil_step(s.view(cur, ctx->cols), s.view(nxt, ctx->cols), rc, fault,
+      // the band fault is a CAT-engine hook (CatConfig.inject_band_fault,
+      // src/cat_engine.cpp:277); the reference's BASE / PACK ignore it
+      ck(ltl::launch_stencil_step(s.view(cur, ctx->cols), s.view(nxt, ctx->cols), rc,
+                                  (flags & LTL_FLAG_ENGINE_PACK) ? ltl::kEnginePack
+                                                                 : ltl::kEngineBase,
                                   want_stats ? s.dstats : nullptr, s.stream),
          "stencil kernel");
       ++ctx->launches;
@@ -462,6 +481,10 @@ void enqueue_step(ltl_ctx* ctx, const ltl::RuleConsts& rc, uint32_t flags, bool 
       a.cols = ctx->cols;
       a.rule = rc;
       a.inject_fault = fault;
+      // the reference's fault flips pi2(0,0) of every f x f fragment
+      // (src/cat_engine.cpp:277): columns / rows == 0 mod f of the global torus
+      a.fault_f = ctx->f;
+      a.fault_row_phase = s.row0 % ctx->f;
       a.stats = want_stats ? s.dstats : nullptr;
       // Debug: LTL_TC_TRACE=<file> dumps the pipeline timeline of CTA 0 of
       // the first traced launch (16 event kinds x 256 stamps; 14/15 = per-CTA start/end ns).
@@ -495,7 +518,7 @@ void enqueue_step(ltl_ctx* ctx, const ltl::RuleConsts& rc, uint32_t flags, bool 
     if (ctx->slabs.size() > 1) ck(cudaEventRecord(s.ev_step, s.stream), "event");
   }
   const int out = (gens % 2) ? nxt : cur;  // buffer holding the last generation
-  enqueue_halo(ctx, out, !(flags & LTL_FLAG_STENCIL));
+  enqueue_halo(ctx, out, !stencil_engine(flags));
   ctx->cur = out;
 }
 

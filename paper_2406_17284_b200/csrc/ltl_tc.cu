@@ -148,7 +148,14 @@ struct Params {
   int32_t strips;  // interior strips
   int32_t bands;
   RuleConsts rule;
+  // CatConfig.inject_band_fault: the reference flips pi2(0,0) of every f x f
+  // band fragment (src/cat_engine.cpp:277), i.e. the centre term of the
+  // horizontal sums of columns == 0 mod f and of the vertical sums of rows
+  // == 0 mod f (global coordinates) drops out.  Same here: pass-1 A1 entry
+  // (x, x) for strip columns x == 0 mod f, pass-2 band entry (rho, rho) for
+  // output rows rho with (row0 + rho) == 0 mod f.
   int32_t inject_fault;
+  int32_t fault_f, fault_row_phase;
   int32_t wrap_cols, wrap_rows;  // periodic wrap done by the loads (tc_wrap_*)
   int32_t gens;                  // generations in this launch (persistent when > 1)
   int32_t sweep_chunks;          // chunks per band of a persistent launch (SegIter)
@@ -356,6 +363,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (t < 3) {
         const int d = 32 * t + k0 + b - 16 - rho;
         v = (d >= -r && d <= r);
+        if (p.inject_fault && d == 0 && (rho + p.fault_row_phase) % p.fault_f == 0) v = 0;
       } else {
         const int c = (t - 3) % 2;
         v = (32 * c + k0 + b == rho) ? (t >= 5 ? 16 : 1) : 0;
@@ -413,7 +421,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint32_t v = (d >= -r && d <= r) ? 1u : 0u;
         if (d == 0) {
           v += 128u;  // state marker
-          if (p.inject_fault && m == 0) v = 128u;  // test hook: drop one centre entry
+          if (p.inject_fault && m % p.fault_f == 0) v = 128u;  // pi2(0,0) flipped: no centre term
         }
         word |= v << (8 * b);
       }
@@ -951,18 +959,27 @@ int tc_sweep_chunks(int32_t strips) {  // <= 12 units per chunk (16384^2 A/B: 12
 }
 
 cudaError_t launch_tc_step(const TcLaunch& a, cudaStream_t stream) {
-  static int num_sms = 0;
-  if (num_sms == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
+  // The dynamic-SMEM attribute is per device: set it (and cache the SM count)
+  // the first time each device launches (a process may drive several GPUs).
+  constexpr int kMaxDevices = 64;
+  static int sm_count[kMaxDevices] = {};
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if (dev < 0 || dev >= kMaxDevices) return cudaErrorInvalidDevice;
+  if (sm_count[dev] == 0) {
     for (auto fn : {ltl_tc_step_kernel<false, false>, ltl_tc_step_kernel<true, false>,
                     ltl_tc_step_kernel<false, true>, ltl_tc_step_kernel<true, true>}) {
-      cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           static_cast<int>(kSmemAlloc));
+      e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               static_cast<int>(kSmemAlloc));
       if (e != cudaSuccess) return e;
     }
+    int sms = 0;
+    e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (e != cudaSuccess) return e;
+    sm_count[dev] = sms;
   }
+  const int num_sms = sm_count[dev];
   if (a.rows <= 0 || a.cols <= 0) return cudaSuccess;
   Params p{};
   p.rows = a.rows;
@@ -971,6 +988,8 @@ cudaError_t launch_tc_step(const TcLaunch& a, cudaStream_t stream) {
   p.bands = (a.rows + kBand - 1) / kBand;
   p.rule = a.rule;
   p.inject_fault = a.inject_fault;
+  p.fault_f = a.fault_f > 0 ? a.fault_f : 16;
+  p.fault_row_phase = a.fault_row_phase;
   p.wrap_cols = a.wrap_cols && tc_wrap_cols(a.cols);
   p.wrap_rows = a.wrap_rows && tc_wrap_rows(a.rows);
   p.gens = a.gens > 1 && a.flags && a.load_maps_b && a.store_map_b ? a.gens : 1;

@@ -26,7 +26,10 @@ LIB_PATH = os.environ.get("LTL_LIB", os.path.join(HERE, "libltl_b200.so"))
 OK, ERR_INVALID_ARGUMENT, ERR_LOGIC, ERR_RUNTIME, ERR_CUDA = range(5)
 LAYOUT_ROW_MAJOR, LAYOUT_FRAGMENT = 0, 1
 KIND_MOORE, KIND_VON_NEUMANN = 0, 1
-FLAG_INJECT_FAULT, FLAG_WANT_STATS, FLAG_STENCIL, FLAG_NO_GRAPH = 0x1, 0x2, 0x4, 0x8
+FLAG_INJECT_FAULT, FLAG_WANT_STATS, FLAG_ENGINE_BASE, FLAG_ENGINE_PACK = 0x1, 0x2, 0x4, 0x10
+FLAG_STENCIL = FLAG_ENGINE_BASE
+# engine name -> ltl_run flag (catsim::EngineKind; proj/src/engines.cpp:9-15)
+ENGINE_FLAGS = {"cat": 0, "base": FLAG_ENGINE_BASE, "pack": FLAG_ENGINE_PACK}
 
 
 class LtlLogicError(RuntimeError):
@@ -312,58 +315,65 @@ class DeviceTorus:
         return out.reshape(p, p) if layout == LAYOUT_ROW_MAJOR else out
 
     @staticmethod
-    def _flags(stencil: bool, inject_fault: bool) -> int:
-        return (FLAG_STENCIL if stencil else 0) | (FLAG_INJECT_FAULT if inject_fault else 0)
+    def _flags(engine: str, inject_fault: bool = False, stencil: bool = False) -> int:
+        """engine "cat" | "base" | "pack" (stencil=True: the round-1 spelling of "base")."""
+        if stencil and engine == "cat":
+            engine = "base"
+        if engine not in ENGINE_FLAGS:
+            raise ValueError(f"config error: unknown engine '{engine}' (cat, base, pack)")
+        return ENGINE_FLAGS[engine] | (FLAG_INJECT_FAULT if inject_fault else 0)
 
     def run(self, rule, steps: int, stencil: bool = False, inject_fault: bool = False,
-            stats: bool = False):
+            stats: bool = False, engine: str = "cat"):
         """`steps` generations.  stats=True returns the CatStats analogue (and
         runs the checked kernel variant that max-reduces H / R on the device)."""
         r = as_rule(rule).to_c()
         st = ltl_stats_c()
-        flags = self._flags(stencil, inject_fault) | (FLAG_WANT_STATS if stats else 0)
+        flags = self._flags(engine, inject_fault, stencil) | (FLAG_WANT_STATS if stats else 0)
         self._check(self.lib.ltl_run(self._ctx, ctypes.byref(r), steps, flags,
                                      ctypes.byref(st) if stats else None))
         if not stats:
             return None
         return {k: getattr(st, k) for k, _ in ltl_stats_c._fields_ if k != "reserved"}
 
-    def run_async(self, rule, steps: int, stencil: bool = False) -> None:
+    def run_async(self, rule, steps: int, stencil: bool = False, engine: str = "cat") -> None:
         r = as_rule(rule).to_c()
         self._check(self.lib.ltl_run_async(self._ctx, ctypes.byref(r), steps,
-                                           self._flags(stencil, False)))
+                                           self._flags(engine, False, stencil)))
 
     def synchronize(self) -> None:
         self._check(self.lib.ltl_synchronize(self._ctx))
 
-    def time(self, rule, steps: int, warmup: int = 3, stencil: bool = False):
+    def time(self, rule, steps: int, warmup: int = 3, stencil: bool = False,
+             engine: str = "cat"):
         """(total_ms, kernel_ms) over `steps` generations, CUDA events, max over slabs."""
         r = as_rule(rule).to_c()
         tot, ker = ctypes.c_double(), ctypes.c_double()
         self._check(self.lib.ltl_time(self._ctx, ctypes.byref(r), steps, warmup,
-                                      self._flags(stencil, False), ctypes.byref(tot),
+                                      self._flags(engine, False, stencil), ctypes.byref(tot),
                                       ctypes.byref(ker)))
         return tot.value, ker.value
 
     def run_interior(self, interior: np.ndarray, rule, steps: int, out: np.ndarray | None = None,
-                     stencil: bool = False) -> np.ndarray:
+                     stencil: bool = False, engine: str = "cat") -> np.ndarray:
         a = np.ascontiguousarray(interior, np.uint8)
         if out is None:
             out = np.empty_like(a)
         r = as_rule(rule).to_c()
         st = ltl_stats_c()
         self._check(self.lib.ltl_run_interior(self._ctx, _u8(a), _u8(out), ctypes.byref(r),
-                                              steps, self._flags(stencil, False),
+                                              steps, self._flags(engine, False, stencil),
                                               ctypes.byref(st)))
         return out
 
     def set_stream(self, stream_ptr: int, slab: int = 0) -> None:
         self._check(self.lib.ltl_set_stream(self._ctx, slab, ctypes.c_void_p(stream_ptr)))
 
-    def step_part(self, rule, stencil: bool = False) -> None:
+    def step_part(self, rule, stencil: bool = False, engine: str = "cat") -> None:
         """Enqueue one generation + local column-halo refresh (async)."""
         r = as_rule(rule).to_c()
-        self._check(self.lib.ltl_step_part(self._ctx, ctypes.byref(r), self._flags(stencil, False)))
+        self._check(self.lib.ltl_step_part(self._ctx, ctypes.byref(r),
+                                           self._flags(engine, False, stencil)))
 
     def fill_halo(self) -> None:
         self._check(self.lib.ltl_fill_halo(self._ctx))
@@ -417,7 +427,7 @@ class DeviceTorus:
                                              ctypes.c_void_p(bot_ptr)))
 
 
-ENGINES = ("cat", "stencil")
+ENGINES = ("cat", "base", "pack")
 
 
 def snapshot_probe(path: str):
@@ -436,18 +446,21 @@ def run_engine(engine: str, initial: np.ndarray, rule, steps: int, f: int = 16,
                slabs: int = 1, inject_fault: bool = False, stats: bool = False):
     """Engine front end (proj/src/engines.cpp:26-46) over the device library.
 
-    engine: "cat" -> tcgen05 banded-MMA path; "stencil" -> CUDA-core ablation.
-    (The reference's "base"/"pack" engines are CPU comparators and live only in
-    the test oracle, never here.)
+    engine: "cat" -> tcgen05 banded-MMA path; "base" -> CUDA-core direct-sum
+    stencil; "pack" -> CUDA-core packed sliding-window stencil (the GPU
+    counterparts of the reference's BASE / PACK comparison engines; the
+    reference's own CPU engines live only in the test oracle, never here).
+    "stencil" is accepted as the round-1 name of "base".
     """
+    if engine == "stencil":
+        engine = "base"
     if engine not in ENGINES:
-        raise ValueError(f"config error: unknown engine '{engine}' (cat, stencil)")
+        raise ValueError(f"config error: unknown engine '{engine}' (cat, base, pack)")
     g = np.ascontiguousarray(initial, np.uint8)
     if g.ndim != 2 or g.shape[0] != g.shape[1]:
         raise ValueError("geometry error: expected a square grid")
     with DeviceTorus(n=g.shape[0], f=f, slabs=slabs) as t:
         t.upload(g)
-        st = t.run(rule, steps, stencil=(engine == "stencil"), inject_fault=inject_fault,
-                   stats=stats)
+        st = t.run(rule, steps, engine=engine, inject_fault=inject_fault, stats=stats)
         out = t.download()
     return (out, st) if stats else out

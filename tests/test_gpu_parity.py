@@ -3,8 +3,9 @@
 Every grid the CUDA path produces is compared byte-for-byte with the C
 restatement of the reference (oracle/, pinned in tests/test_oracle.py) and/or
 the reference-generated golden fixtures (tests/golden/).  Both engines are
-exercised through the C-ABI: "cat" (tcgen05 banded MMA) and "stencil" (the
-CUDA-core ablation).
+exercised through the C-ABI: "cat" (tcgen05 banded MMA), "base" (the
+CUDA-core direct-sum stencil) and "pack" (the CUDA-core packed sliding-window
+stencil).
 """
 import numpy as np
 import pytest
@@ -13,7 +14,7 @@ from golden_data import load, parse_rule_text
 
 pytestmark = pytest.mark.gpu
 
-ENGINES = ("cat", "stencil")
+ENGINES = ("cat", "base", "pack")
 
 
 @pytest.fixture(scope="module")
@@ -46,7 +47,7 @@ def test_criterion1_sweep(ltl, orc, engine):
             inits[ikey] = orc.init_random(*ikey)
         t = tori[key]
         t.upload(inits[ikey])
-        st = t.run(c["rule"], c["steps"], stencil=(engine == "stencil"), stats=(c["seed"] == 1))
+        st = t.run(c["rule"], c["steps"], engine=engine, stats=(c["seed"] == 1))
         out = t.download()
         if _fnv(orc, out) != c["fnv"]:
             failures.append((c["rule"], c["n"], c["f"], c["seed"], c["steps"]))
@@ -76,7 +77,7 @@ def test_rectangular_torus(ltl, orc, engine, rows, cols):
         rule = parse_rule_text(text)
         with ltl.DeviceTorus(rows=rows, cols=cols) as t:
             t.upload(init)
-            t.run(text, 3, stencil=(engine == "stencil"))
+            t.run(text, 3, engine=engine)
             got = t.download()
         assert np.array_equal(got, orc.simulate(init, rule, 3)), (text, rows, cols)
 
@@ -110,6 +111,27 @@ def test_fault_injection_detected(ltl, orc):
         assert "internal consistency: negative neighborhood count" in str(e)
 
 
+def test_fault_injection_matches_reference(ltl, orc):
+    """CatConfig.inject_band_fault flips pi2(0,0) of every band fragment
+    (src/cat_engine.cpp:277): the faulted tcgen05 run must reproduce the
+    reference's faulted run byte for byte -- the same diverged grid, or the
+    same negative-count abort (tests/golden/faults.json, made by the reference)."""
+    bad = []
+    for c in load("faults.json")["cases"]:
+        init = orc.init_random(c["n"], c["density"], c["seed"])
+        with ltl.DeviceTorus(n=c["n"], f=c["f"]) as t:
+            t.upload(init)
+            try:
+                t.run(c["rule"], c["steps"], inject_fault=True)
+                got = dict(alive=int(t.download().sum()), fnv=_fnv(orc, t.download()))
+            except ltl.LtlLogicError as e:
+                got = dict(error=str(e))
+        want = {k: c[k] for k in ("alive", "fnv", "error") if k in c}
+        if got != want:
+            bad.append((c["rule"], c["n"], c["f"], c["steps"], want, got))
+    assert not bad, f"{len(bad)} mismatches, first: {bad[:3]}"
+
+
 def test_virtual_slabs_match_single(ltl, orc):
     """The multi-GPU slab path (halo rows exchanged between slabs) with every slab
     on device 0: bit-identical to one slab and to the oracle."""
@@ -137,14 +159,14 @@ def test_run_errors(ltl):
 
 
 def test_large_grid_engines_agree(ltl, orc):
-    """At sizes the oracle is slow for: tcgen05 == stencil == oracle on a 4096^2
-    grid for a few generations, at three radii."""
+    """At sizes the oracle is slow for: tcgen05 == base == pack == oracle on a
+    4096^2 grid for a few generations, at three radii."""
     init = orc.init_random(4096, 0.3, 11)
     for text in ("R1,C2,M0,S2..3,B3..3,NM", "R5,C2,M1,S34..58,B34..45,NM",
                  "R16,C2,M0,S170..296,B170..300,NM"):
         a = ltl.run_engine("cat", init, text, 2)
-        b = ltl.run_engine("stencil", init, text, 2)
-        assert np.array_equal(a, b), text
+        for engine in ("base", "pack"):
+            assert np.array_equal(a, ltl.run_engine(engine, init, text, 2)), (engine, text)
         assert np.array_equal(a, orc.simulate(init, parse_rule_text(text), 2)), text
 
 
@@ -243,10 +265,11 @@ def test_stencil_after_tcgen05_refreshes_halo(ltl, orc):
     with ltl.DeviceTorus(n=256) as t:
         t.upload(init)
         t.run(text, 3)
-        t.run(text, 2, stencil=True)
+        t.run(text, 2, engine="base")
         t.run(text, 1)
+        t.run(text, 1, engine="pack")
         got = t.download()
-    assert np.array_equal(got, orc.simulate(init, parse_rule_text(text), 6))
+    assert np.array_equal(got, orc.simulate(init, parse_rule_text(text), 7))
 
 
 def test_partition_wrap_cols_matches_torus(ltl, orc):
@@ -314,7 +337,7 @@ def test_bench_geometry_persistent_vs_stencil(ltl, orc):
         tc = t.download()
     with ltl.DeviceTorus(n=n) as t:
         t.upload(init)
-        t.run(text, 4, stencil=True)
+        t.run(text, 4, engine="pack")
         st = t.download()
     assert np.array_equal(tc, st)
     assert 0 < int(tc.sum()) < n * n

@@ -8,6 +8,7 @@
 #include <cstdio>
 #include <vector>
 #include <algorithm>
+#include <string>
 
 #include "../paper_2406_17284_b200/csrc/ptx_sm100.cuh"
 
@@ -157,11 +158,55 @@ void run_kind(const char* kname, int sms, long long* d) {
     }
 }
 
-int main() {
+// Dense kind::i8 peak of the whole GPU: every SM issues `reps` M128 N256 K32
+// MMAs (SS and TS) back to back into two rotating accumulators; ops =
+// 2*M*N*K per MMA, wall time from CUDA events around the launch.
+void peak_i8(int sms, long long* d, const char* json_path) {
+  const size_t smem = 96 * 1024;
+  cudaFuncSetAttribute(kern<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  double best[2] = {0, 0};
+  int clk_khz = 0;
+  cudaDeviceGetAttribute(&clk_khz, cudaDevAttrClockRate, 0);
+  for (int ts : {0, 1}) {
+    for (int it = 0; it < 5; ++it) {
+      Cfg c{ts, 256, 1, 1 << 15};
+      cudaEventRecord(e0);
+      kern<0><<<sms, 128, smem>>>(c, d);
+      cudaEventRecord(e1);
+      cudaEventSynchronize(e1);
+      float ms = 0;
+      cudaEventElapsedTime(&ms, e0, e1);
+      const double ops = 2.0 * 128 * 256 * 32 * c.reps * sms;
+      best[ts] = std::max(best[ts], ops / (ms * 1e-3) / 1e12);
+    }
+  }
+  std::printf("i8 dense peak (M128 N256 K32, %d SMs, best of 5): SS %.1f TOPS, TS %.1f TOPS\n", sms,
+              best[0], best[1]);
+  if (json_path) {
+    if (FILE* fh = std::fopen(json_path, "w")) {
+      std::fprintf(fh,
+                   "{\"i8_peak_tops\": %.1f, \"i8_peak_tops_ss\": %.1f, \"i8_peak_tops_ts\": %.1f, "
+                   "\"sms\": %d, \"sm_clock_khz_attr\": %d, \"how\": \"tools/ubench_mma.cu --peak: "
+                   "%d MMAs of M128 N256 K32 kind::i8 per SM back to back, 2*M*N*K ops each, CUDA "
+                   "events around the launch, best of 5\"}\n",
+                   std::max(best[0], best[1]), best[0], best[1], sms, clk_khz, 1 << 15);
+      std::fclose(fh);
+    }
+  }
+}
+
+int main(int argc, char** argv) {
   int sms = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   long long* d;
   cudaMalloc(&d, sms * sizeof(long long));
+  if (argc > 1 && std::string(argv[1]) == "--peak") {
+    peak_i8(sms, d, argc > 2 ? argv[2] : nullptr);
+    return 0;
+  }
   run_kind<0>("i8", sms, d);
   {
     const size_t smem = 96 * 1024;
