@@ -88,30 +88,32 @@ inline void check_grid_f(const Grid& grid, const CatConfig& cfg) {
                                 " disagrees with config f " + std::to_string(cfg.f));
 }
 
-// `steps` generations of `grid` (its layout) on the device into `out`'s
-// interior (out may be grid); stats as the reference accumulates them.
+// `steps` generations of `grid` (its layout) on the device with the engine
+// `flags` select; the result lands in `out`'s interior only (out's halo is
+// left as it was, as simulate_step leaves it, src/cat_engine.cpp:293-305):
+// one pitched H2D of grid's interior, the generations, one pitched D2H.
+inline void run_device_engine(const Grid& grid, const LtlRule& rule, int steps, uint32_t flags,
+                              Grid& out, ltl_stats_c* s) {
+  if (grid.n == 0) return;
+  DeviceGrid dev(grid.n, grid.f);
+  dev.check(ltl_upload(dev.get(), grid.cells.data(), c_layout(grid.layout)));
+  const ltl_rule_c rc = to_c(rule);
+  dev.check(ltl_run(dev.get(), &rc, steps, flags, s));
+  dev.check(ltl_download_padded(dev.get(), out.cells.data(), c_layout(out.layout), 0));
+}
+
+// The CAT engine: `steps` generations into `out`'s interior (out may be grid);
+// stats as the reference accumulates them.
 inline void run_on_device(const Grid& grid, const LtlRule& rule, const CatConfig& cfg,
                           int steps, Grid& out, CatStats* stats) {
   if (grid.n == 0) {
     if (stats) stats->steps += steps;
     return;
   }
-  DeviceGrid dev(grid.n, grid.f);
-  const int32_t lay = c_layout(grid.layout);
-  dev.check(ltl_upload(dev.get(), grid.cells.data(), lay));
-  const ltl_rule_c rc = to_c(rule);
   uint32_t flags = stats ? LTL_FLAG_WANT_STATS : 0u;
   if (cfg.inject_band_fault) flags |= LTL_FLAG_INJECT_FAULT;
   ltl_stats_c s{};
-  dev.check(ltl_run(dev.get(), &rc, steps, flags, stats ? &s : nullptr));
-  // only the interior of `out` is written, as simulate_step does (:293-305)
-  std::vector<uint8_t> next(grid.cells.size());
-  dev.check(ltl_download(dev.get(), next.data(), c_layout(out.layout)));
-  for (int y = 0; y < grid.n; ++y)
-    for (int x = 0; x < grid.n; ++x) {
-      const std::size_t k = out.index(y + grid.f, x + grid.f);
-      out.cells[k] = next[k];
-    }
+  run_device_engine(grid, rule, steps, flags, out, stats ? &s : nullptr);
   add_stats(stats, s, grid.fragments_per_row());
 }
 
@@ -249,10 +251,9 @@ inline Grid simulate(Grid grid, const LtlRule& rule, const CatConfig& cfg, int s
   if (grid.layout != Layout::FragmentContiguous)
     throw std::invalid_argument("layout error: engine needs fragment-contiguous grids");
   detail::check_grid_f(grid, cfg);
-  Grid out = grid;
-  detail::run_on_device(grid, rule, cfg, steps, out, stats);
-  out.halo_valid = false;
-  return out;
+  detail::run_on_device(grid, rule, cfg, steps, grid, stats);  // in place: upload, run, download
+  grid.halo_valid = false;
+  return grid;
 }
 
 }  // namespace catsim

@@ -28,11 +28,12 @@ inline void check(int status, const ltl_ctx* ctx) {
   if (status != LTL_OK) throw_status(status, ltl_last_error(ctx));
 }
 
-// One device torus (ltl_create): owns the device buffers of a simulation.
+// One device torus: owns the device buffers of a simulation.  One slab:
+// ltl_create_grid (any f > 0 of a host Grid); several: ltl_create.
 class DeviceGrid {
  public:
   DeviceGrid(int n, int f, int slabs = 1) {
-    const int st = ltl_create(&ctx_, n, f, slabs, nullptr);
+    const int st = slabs == 1 ? ltl_create_grid(&ctx_, n, f) : ltl_create(&ctx_, n, f, slabs, nullptr);
     if (st != LTL_OK) throw_status(st, ltl_last_error(nullptr));
   }
   ~DeviceGrid() { ltl_destroy(ctx_); }

@@ -134,36 +134,29 @@ inline IntField make_field(int n, int f = kDefaultFragmentSide,
   return h;
 }
 
-// init_random (grid.cpp:61-73), generated on the device (counter-form
-// splitmix64, bit-identical), downloaded into a row-major grid.
+// init_random (grid.cpp:61-73): generated on the device (counter-form
+// splitmix64, bit-identical, ltl_init_random) and landed in the row-major
+// grid's interior by one pitched copy; the halo stays dead and stale.
 inline Grid init_random(int n, double density, uint64_t seed, int f = kDefaultFragmentSide,
                         int fill_n = -1) {
   if (!(density >= 0.0 && density <= 1.0) || std::isnan(density))
     throw std::invalid_argument("init_random: density must be in [0, 1]");
+  if (fill_n < 0) fill_n = n;
   if (fill_n > n) throw std::invalid_argument("init_random: fill_n exceeds n");
   Grid g = make_grid(n, f, Layout::RowMajor);
-  if (n == 0) return g;
+  if (n == 0 || fill_n == 0) return g;
   detail::DeviceGrid dev(n, f);
   dev.check(ltl_init_random(dev.get(), density, seed, fill_n));
-  dev.check(ltl_download(dev.get(), g.cells.data(), LTL_LAYOUT_ROW_MAJOR));
-  // the reference leaves the halo dead and stale
-  for (int y = 0; y < g.padded(); ++y)
-    for (int x = 0; x < g.padded(); ++x)
-      if (y < f || y >= n + f || x < f || x >= n + f) g.at(y, x) = 0;
-  g.halo_valid = false;
+  dev.check(ltl_download_padded(dev.get(), g.cells.data(), LTL_LAYOUT_ROW_MAJOR, 0));
   return g;
 }
 
-// fill_periodic_halo (grid.cpp:75-94) through the device's halo kernel.
+// fill_periodic_halo (grid.cpp:75-94): the halo cells' periodic images, on the
+// host (ltl_host_fill_halo: 4fn + 4f^2 cells, the interior is not touched).
 inline void fill_periodic_halo(Grid& grid) {
-  if (grid.n > 0) {
-    detail::DeviceGrid dev(grid.n, grid.f);
-    const int32_t lay = detail::c_layout(grid.layout);
-    dev.check(ltl_upload(dev.get(), grid.cells.data(), lay));
-    dev.check(ltl_fill_halo(dev.get()));
-    dev.check(ltl_synchronize(dev.get()));
-    dev.check(ltl_download(dev.get(), grid.cells.data(), lay));
-  }
+  if (grid.n > 0)
+    detail::check(ltl_host_fill_halo(grid.cells.data(), grid.n, grid.f, detail::c_layout(grid.layout)),
+                  nullptr);
   grid.halo_valid = true;
 }
 

@@ -29,7 +29,7 @@
 extern "C" {
 #endif
 
-#define LTL_ABI_VERSION 3
+#define LTL_ABI_VERSION 4
 
 /* status codes <-> reference exception classes */
 #define LTL_OK 0
@@ -90,6 +90,12 @@ int ltl_create(ltl_ctx** out, int32_t n, int32_t f, int32_t num_slabs, const int
 int ltl_create_torus(ltl_ctx** out, int32_t rows, int32_t cols, int32_t num_slabs,
                      const int32_t* dev_ids);
 
+/* Square n x n torus for a host Grid of ANY fragment side f > 0 with n % f
+ * == 0 (make_grid's geometry, src/grid.cpp:11-17, and its messages): the f
+ * used by ltl_upload / ltl_download's padded layouts and by the CAT engine's
+ * r <= f check.  One slab on the current device. */
+int ltl_create_grid(ltl_ctx** out, int32_t n, int32_t f);
+
 void ltl_destroy(ltl_ctx* ctx);
 const char* ltl_last_error(const ltl_ctx* ctx); /* "" after success; never NULL */
 
@@ -105,11 +111,21 @@ int32_t ltl_num_slabs(const ltl_ctx* ctx);
 
 /* Padded (n+2f)^2 host grid in the given layout (catsim::Grid::cells); only
  * the interior is read -- the device refreshes its own periodic halo, which is
- * what simulate_step does first anyway (src/cat_engine.cpp:275). */
+ * what simulate_step does first anyway (src/cat_engine.cpp:275).  One pitched
+ * H2D copy of the interior per slab + a device relayout kernel (no host pass
+ * over the cells; replaces to_fragment_layout's permutation,
+ * src/layout.cpp:23-32, on the run_engine path src/engines.cpp:32). */
 int ltl_upload(ltl_ctx* ctx, const uint8_t* padded, int32_t layout);
 /* Writes the padded grid: interior = current generation, halo = its periodic
  * image (callers may treat it as stale, as the reference does after a step). */
 int ltl_download(ltl_ctx* ctx, uint8_t* padded, int32_t layout);
+/* As ltl_download, but with fill_halo == 0 only the interior bytes of
+ * `padded` are written (what simulate_step writes into `out`,
+ * src/cat_engine.cpp:293-305): a device relayout + ONE pitched D2H per slab. */
+int ltl_download_padded(ltl_ctx* ctx, uint8_t* padded, int32_t layout, int32_t fill_halo);
+/* fill_periodic_halo (src/grid.cpp:75-94) of a padded HOST grid, any f > 0
+ * with n % f == 0 (pure host; halo cells only). */
+int ltl_host_fill_halo(uint8_t* padded, int32_t n, int32_t f, int32_t layout);
 /* Dense rows x cols interior, row-major (no halo). */
 int ltl_upload_interior(ltl_ctx* ctx, const uint8_t* interior);
 int ltl_download_interior(ltl_ctx* ctx, uint8_t* interior);
@@ -234,6 +250,10 @@ int ltl_snapshot_read(ltl_ctx* ctx, const char* path, int32_t* layout_out);
 /* Header only (no device): the geometry and layout a snapshot declares, with
  * the reader's header checks. */
 int ltl_snapshot_probe(const char* path, int32_t* n, int32_t* f, int32_t* layout);
+/* The same checks on a header line already read (without its '\n');
+ * has_line == 0: the stream had no line ("missing header line").  Pure host. */
+int ltl_snapshot_parse_header(const char* line, int32_t has_line, int32_t* n, int32_t* f,
+                              int32_t* layout);
 
 /* --- the reference's fragment-level unit-test passes, on the device -------
  * horizontal_step (stage 0), vertical_step_moore (1), vertical_step_von_neumann

@@ -135,11 +135,15 @@ bool stencil_engine(uint32_t flags) {
   return (flags & (LTL_FLAG_ENGINE_BASE | LTL_FLAG_ENGINE_PACK)) != 0;
 }
 
-void check_run_args(const ltl_ctx* ctx, const ltl_rule_c* rule, int32_t steps) {
+void check_run_args(const ltl_ctx* ctx, const ltl_rule_c* rule, int32_t steps,
+                    uint32_t flags = 0) {
   if (!rule) throw std::invalid_argument("config error: rule is null");
   if (steps < 0) throw std::invalid_argument("config error: steps must be >= 0");
   catsim::validate_rule(catsim::from_c(*rule));
-  if (rule->r < 1 || rule->r > ctx->f)
+  // the CAT engine's band fragments need r <= f (src/fragment.cpp:25-27); the
+  // stencil engines only need the device's 16-cell halo
+  const int32_t limit = stencil_engine(flags) ? kHalo : std::min<int32_t>(ctx->f, kHalo);
+  if (rule->r < 1 || rule->r > limit)
     throw std::invalid_argument("unsupported radius r=" + std::to_string(rule->r) +
                                 " for fragment side f=" + std::to_string(ctx->f));
 }
@@ -531,7 +535,7 @@ void reset_stats(ltl_ctx* ctx) {
 
 void run_steps(ltl_ctx* ctx, const ltl_rule_c* rule, int32_t steps, uint32_t flags,
                ltl_stats_c* stats) {
-  check_run_args(ctx, rule, steps);
+  check_run_args(ctx, rule, steps, flags);
   const ltl::RuleConsts rc = rule_consts(*rule);
   // Checked launches (device max-reduction of H / R plus the negative-count
   // guard of src/rule.cpp:104-107) run when stats are requested or a band
@@ -618,13 +622,141 @@ void check_layout(int32_t layout) {
     throw std::invalid_argument("layout error: unknown layout " + std::to_string(layout));
 }
 
+// Periodic halo of a padded (n + 2f)^2 host grid (fill_periodic_halo,
+// src/grid.cpp:75-94: halo cell (y, x) = interior image ((y-f) mod n, (x-f) mod n)).
+// Row-major: the side columns of every interior row, then whole halo rows,
+// as memcpys.  Fragment-contiguous: per halo cell (4fn + 4f^2 of them).
+void host_fill_halo(uint8_t* padded, int32_t n, int32_t f, int32_t layout) {
+  const size_t p = static_cast<size_t>(n) + 2 * f;
+  if (n == 0) {
+    std::memset(padded, 0, p * p);
+    return;
+  }
+  auto wrapi = [n](int64_t v) { return static_cast<int32_t>(((v % n) + n) % n); };
+  if (layout == LTL_LAYOUT_ROW_MAJOR) {
+    for (int32_t y = f; y < f + n; ++y) {
+      uint8_t* row = padded + y * p;
+      for (int32_t x = 0; x < f; ++x) row[x] = row[f + wrapi(x - f)];
+      for (int32_t x = f + n; x < n + 2 * f; ++x) row[x] = row[f + wrapi(x - f)];
+    }
+    for (int32_t y = 0; y < f; ++y)
+      std::memcpy(padded + y * p, padded + (f + wrapi(y - f)) * p, p);
+    for (int32_t y = f + n; y < n + 2 * f; ++y)
+      std::memcpy(padded + y * p, padded + (f + wrapi(y - f)) * p, p);
+    return;
+  }
+  const int32_t pp = n + 2 * f;
+  for (int32_t y = 0; y < pp; ++y) {
+    const bool halo_row = y < f || y >= f + n;
+    for (int32_t x = 0; x < pp; ++x) {
+      if (!halo_row && x == f) x = f + n;  // skip the interior span of interior rows
+      if (x >= pp) break;
+      padded[host_index(layout, f, pp, y, x)] =
+          padded[host_index(layout, f, pp, f + wrapi(y - f), f + wrapi(x - f))];
+    }
+  }
+}
+
+// Padded host grid (either layout) -> device: the interior goes H2D as ONE
+// pitched copy per slab (row-major: n-byte rows at pitch n + 2f; fragment
+// order: the interior fragments of each fragment row, contiguous, at pitch
+// f (n + 2f)) into the slab's dead generation buffer, and a relayout kernel
+// scatters it into strips.  No host pass over the cells.
+void upload_padded(ltl_ctx* ctx, const uint8_t* padded, int32_t layout) {
+  const int32_t n = ctx->rows, f = ctx->f;
+  const size_t p = static_cast<size_t>(n) + 2 * f;
+  const int cur = ctx->cur;
+  const bool kernel_f = f == 4 || f == 8 || f == 16;
+  for (const Slab& s : ctx->slabs)
+    if (layout == LTL_LAYOUT_FRAGMENT && (!kernel_f || s.host_row0 % f || s.rows % f)) {
+      // fragment rows straddling slabs: gather the interior on the host
+      std::vector<uint8_t> interior(static_cast<size_t>(n) * n);
+      for (int32_t y = 0; y < n; ++y)
+        for (int32_t x0 = 0; x0 < n; x0 += f)
+          std::memcpy(&interior[static_cast<size_t>(y) * n + x0],
+                      padded + host_index(layout, f, static_cast<int32_t>(p), y + f, x0 + f), f);
+      upload_interior(ctx, interior.data());
+      return;
+    }
+  for (Slab& s : ctx->slabs) {
+    ck(cudaSetDevice(s.dev), "cudaSetDevice");
+    if (s.rows == 0 || n == 0) continue;
+    uint8_t* dense = s.buf[1 - cur];
+    if (layout == LTL_LAYOUT_ROW_MAJOR) {
+      ck(cudaMemcpy2DAsync(dense, n, padded + (f + static_cast<size_t>(s.host_row0)) * p + f, p, n,
+                           s.rows, cudaMemcpyHostToDevice, s.stream),
+         "upload (pitched)");
+      ck(ltl::launch_to_strips(dense, s.view(cur, ctx->cols), s.stream), "to_strips");
+    } else {
+      const size_t frow = static_cast<size_t>(f) * p;  // bytes per fragment row
+      ck(cudaMemcpy2DAsync(dense, static_cast<size_t>(n) * f,
+                           padded + (s.host_row0 / f + 1) * frow + static_cast<size_t>(f) * f, frow,
+                           static_cast<size_t>(n) * f, s.rows / f, cudaMemcpyHostToDevice, s.stream),
+         "upload (pitched)");
+      ck(ltl::launch_frag_relayout(dense, s.view(cur, ctx->cols), f, true, s.stream),
+         "fragment to_strips");
+    }
+    ++ctx->launches;
+    if (ctx->slabs.size() > 1) ck(cudaEventRecord(s.ev_step, s.stream), "event");
+  }
+  enqueue_halo(ctx, cur);
+  sync_all(ctx);
+  ctx->ring_stale = true;
+}
+
+// Device -> padded host grid: a relayout kernel gathers the interior into the
+// dead buffer in the host's order and ONE pitched D2H per slab lands it in the
+// interior of `padded`; the halo bytes are untouched unless fill_halo (then
+// the periodic images are written on the host: 4fn + 4f^2 cells).
+void download_padded(ltl_ctx* ctx, uint8_t* padded, int32_t layout, bool fill_halo) {
+  const int32_t n = ctx->rows, f = ctx->f;
+  const size_t p = static_cast<size_t>(n) + 2 * f;
+  const int cur = ctx->cur;
+  bool host_path = false;
+  const bool kernel_f = f == 4 || f == 8 || f == 16;
+  for (const Slab& s : ctx->slabs)
+    host_path |= layout == LTL_LAYOUT_FRAGMENT && (!kernel_f || s.host_row0 % f || s.rows % f);
+  if (host_path) {
+    std::vector<uint8_t> interior(static_cast<size_t>(n) * n);
+    download_interior(ctx, interior.data());
+    for (int32_t y = 0; y < n; ++y)
+      for (int32_t x0 = 0; x0 < n; x0 += f)
+        std::memcpy(padded + host_index(layout, f, static_cast<int32_t>(p), y + f, x0 + f),
+                    &interior[static_cast<size_t>(y) * n + x0], f);
+  } else {
+    for (Slab& s : ctx->slabs) {
+      ck(cudaSetDevice(s.dev), "cudaSetDevice");
+      if (s.rows == 0 || n == 0) continue;
+      uint8_t* dense = s.buf[1 - cur];
+      if (layout == LTL_LAYOUT_ROW_MAJOR) {
+        ck(ltl::launch_from_strips(s.view(cur, ctx->cols), dense, s.stream), "from_strips");
+        ck(cudaMemcpy2DAsync(padded + (f + static_cast<size_t>(s.host_row0)) * p + f, p, dense, n,
+                             n, s.rows, cudaMemcpyDeviceToHost, s.stream),
+           "download (pitched)");
+      } else {
+        ck(ltl::launch_frag_relayout(dense, s.view(cur, ctx->cols), f, false, s.stream),
+           "fragment from_strips");
+        const size_t frow = static_cast<size_t>(f) * p;
+        ck(cudaMemcpy2DAsync(padded + (s.host_row0 / f + 1) * frow + static_cast<size_t>(f) * f,
+                             frow, dense, static_cast<size_t>(n) * f, static_cast<size_t>(n) * f,
+                             s.rows / f, cudaMemcpyDeviceToHost, s.stream),
+           "download (pitched)");
+      }
+      ++ctx->launches;
+    }
+    sync_all(ctx);
+  }
+  if (fill_halo) host_fill_halo(padded, n, f, layout);
+}
+
 }  // namespace
 
 extern "C" {
 
 const char* ltl_build_info(void) {
-  return "ltl_b200 abi=3 arch=sm_100a layout=column-strips-128 "
-         "kernels=tcgen05-banded-i8(sweep,ring),cuda-core-stencil,halo,relayout,snapshot";
+  return "ltl_b200 abi=4 arch=sm_100a layout=column-strips-128 "
+         "engines=cat(tcgen05-banded-i8:sweep,ring),base(cuda-core-direct),pack(cuda-core-sliding) "
+         "kernels=halo,relayout,fragment-relayout,init,snapshot";
 }
 
 int ltl_create_torus(ltl_ctx** out, int32_t rows, int32_t cols, int32_t num_slabs,
@@ -664,6 +796,22 @@ int ltl_create(ltl_ctx** out, int32_t n, int32_t f, int32_t num_slabs, const int
   });
   if (st != LTL_OK) return st;
   const int st2 = ltl_create_torus(out, n, n, num_slabs, dev_ids);
+  if (st2 == LTL_OK) (*out)->f = f;
+  return st2;
+}
+
+int ltl_create_grid(ltl_ctx** out, int32_t n, int32_t f) {
+  if (!out) return LTL_ERR_INVALID_ARGUMENT;
+  *out = nullptr;
+  const int st = guarded(nullptr, [&] {
+    if (f <= 0) throw std::invalid_argument("geometry error: f must be positive");
+    if (n < 0 || n % f != 0)
+      throw std::invalid_argument("geometry error: n (" + std::to_string(n) +
+                                  ") must be a non-negative multiple of f (" +
+                                  std::to_string(f) + ")");
+  });
+  if (st != LTL_OK) return st;
+  const int st2 = ltl_create_torus(out, n, n, 1, nullptr);
   if (st2 == LTL_OK) (*out)->f = f;
   return st2;
 }
@@ -711,28 +859,34 @@ int ltl_upload(ltl_ctx* ctx, const uint8_t* padded, int32_t layout) {
   return guarded(ctx, [&] {
     check_layout(layout);
     if (ctx->rows != ctx->cols) throw std::invalid_argument("layout error: padded grids are square");
-    const int32_t n = ctx->rows, f = ctx->f, p = n + 2 * f;
-    std::vector<uint8_t> interior(static_cast<size_t>(n) * n);
-    for (int32_t y = 0; y < n; ++y)
-      for (int32_t x = 0; x < n; ++x)
-        interior[static_cast<size_t>(y) * n + x] = padded[host_index(layout, f, p, y + f, x + f)];
-    upload_interior(ctx, interior.data());
+    if (!padded && ctx->rows > 0) throw std::invalid_argument("config error: null buffer");
+    upload_padded(ctx, padded, layout);
   });
 }
 
 int ltl_download(ltl_ctx* ctx, uint8_t* padded, int32_t layout) {
+  return ltl_download_padded(ctx, padded, layout, 1);
+}
+
+int ltl_download_padded(ltl_ctx* ctx, uint8_t* padded, int32_t layout, int32_t fill_halo) {
   if (!ctx) return LTL_ERR_INVALID_ARGUMENT;
   return guarded(ctx, [&] {
     check_layout(layout);
     if (ctx->rows != ctx->cols) throw std::invalid_argument("layout error: padded grids are square");
-    const int32_t n = ctx->rows, f = ctx->f, p = n + 2 * f;
-    std::vector<uint8_t> interior(static_cast<size_t>(n) * n);
-    download_interior(ctx, interior.data());
-    for (int32_t y = 0; y < p; ++y)
-      for (int32_t x = 0; x < p; ++x) {
-        const int32_t sy = n ? ((y - f) % n + n) % n : 0, sx = n ? ((x - f) % n + n) % n : 0;
-        padded[host_index(layout, f, p, y, x)] = n ? interior[static_cast<size_t>(sy) * n + sx] : 0;
-      }
+    if (!padded) throw std::invalid_argument("config error: null buffer");
+    download_padded(ctx, padded, layout, fill_halo != 0);
+  });
+}
+
+int ltl_host_fill_halo(uint8_t* padded, int32_t n, int32_t f, int32_t layout) {
+  if (!padded) return LTL_ERR_INVALID_ARGUMENT;
+  return guarded(nullptr, [&] {
+    check_layout(layout);
+    if (f <= 0 || n < 0 || n % f != 0)
+      throw std::invalid_argument("geometry error: n (" + std::to_string(n) +
+                                  ") must be a non-negative multiple of f (" + std::to_string(f) +
+                                  ")");
+    host_fill_halo(padded, n, f, layout);
   });
 }
 
@@ -745,7 +899,7 @@ int ltl_run(ltl_ctx* ctx, const ltl_rule_c* rule, int32_t steps, uint32_t flags,
 int ltl_run_async(ltl_ctx* ctx, const ltl_rule_c* rule, int32_t steps, uint32_t flags) {
   if (!ctx) return LTL_ERR_INVALID_ARGUMENT;
   return guarded(ctx, [&] {
-    check_run_args(ctx, rule, steps);
+    check_run_args(ctx, rule, steps, flags);
     const ltl::RuleConsts rc = rule_consts(*rule);
     enqueue_step(ctx, rc, flags, false, nullptr, nullptr, steps);
   });
@@ -760,7 +914,7 @@ int ltl_time(ltl_ctx* ctx, const ltl_rule_c* rule, int32_t steps, int32_t warmup
              uint32_t flags, double* total_ms, double* kernel_ms) {
   if (!ctx) return LTL_ERR_INVALID_ARGUMENT;
   return guarded(ctx, [&] {
-    check_run_args(ctx, rule, steps);
+    check_run_args(ctx, rule, steps, flags);
     const ltl::RuleConsts rc = rule_consts(*rule);
     const size_t G = ctx->slabs.size();
     enqueue_step(ctx, rc, flags, false, nullptr, nullptr, warmup);
@@ -827,7 +981,7 @@ int ltl_run_interior(ltl_ctx* ctx, const uint8_t* interior_in, uint8_t* interior
                      const ltl_rule_c* rule, int32_t steps, uint32_t flags, ltl_stats_c* stats) {
   if (!ctx) return LTL_ERR_INVALID_ARGUMENT;
   return guarded(ctx, [&] {
-    check_run_args(ctx, rule, steps);
+    check_run_args(ctx, rule, steps, flags);
     upload_interior(ctx, interior_in);
     run_steps(ctx, rule, steps, flags, stats);
     download_interior(ctx, interior_out);
@@ -863,7 +1017,7 @@ int ltl_set_stream(ltl_ctx* ctx, int32_t slab, void* stream) {
 int ltl_step_part(ltl_ctx* ctx, const ltl_rule_c* rule, uint32_t flags) {
   if (!ctx) return LTL_ERR_INVALID_ARGUMENT;
   return guarded(ctx, [&] {
-    check_run_args(ctx, rule, 1);
+    check_run_args(ctx, rule, 1, flags);
     enqueue_step(ctx, rule_consts(*rule), flags, false, nullptr, nullptr);
   });
 }
@@ -1082,15 +1236,9 @@ struct SnapHeader {
   int32_t n = -1, f = -1, layout = 0;
 };
 
-// snapshot_read's header checks (src/snapshot.cpp:39-66), same order and text.
-SnapHeader parse_snap_header(std::FILE* fh) {
-  std::string header;
-  bool any = false;
-  for (int c; (c = std::fgetc(fh)) != EOF;) {
-    any = true;
-    if (c == '\n') break;
-    header.push_back(static_cast<char>(c));
-  }
+// snapshot_read's header checks (src/snapshot.cpp:39-66), same order and text,
+// on the header line (without its newline; `any` = false: no line at all).
+SnapHeader parse_snap_line(const std::string& header, bool any) {
   if (!any) snap_fail("missing header line");
   std::istringstream hs(header);
   std::string magic, layout_token;
@@ -1113,6 +1261,17 @@ SnapHeader parse_snap_header(std::FILE* fh) {
   h.n = n;
   h.f = f;
   return h;
+}
+
+SnapHeader parse_snap_header(std::FILE* fh) {
+  std::string header;
+  bool any = false;
+  for (int c; (c = std::fgetc(fh)) != EOF;) {
+    any = true;
+    if (c == '\n') break;
+    header.push_back(static_cast<char>(c));
+  }
+  return parse_snap_line(header, any);
 }
 
 struct FileCloser {
@@ -1187,13 +1346,18 @@ int32_t snapshot_read_ctx(ltl_ctx* ctx, const char* path) {
   const int cur = ctx->cur;
   const std::string truncated = "truncated payload (expected " + std::to_string(h.n) + "x" +
                                 std::to_string(h.n) + " cells)";
+  // Pass 1: every slab's payload into its dead buffer, checked ({0,1} bytes,
+  // complete).  The live generation is untouched until the whole file is
+  // valid -- the reference's snapshot_read has no side effects when it fails.
   int32_t* bad = nullptr;
+  ck(cudaMallocHost(&bad, sizeof(int32_t)), "cudaMallocHost");
+  struct PinnedFree {
+    int32_t* p;
+    ~PinnedFree() { cudaFreeHost(p); }
+  } free_bad{bad};
   for (Slab& s : ctx->slabs) {
     ck(cudaSetDevice(s.dev), "cudaSetDevice");
     if (s.rows == 0 || ctx->cols == 0) continue;
-    if (!bad) {
-      ck(cudaMallocHost(&bad, sizeof(int32_t)), "cudaMallocHost");
-    }
     *bad = 0;
     uint8_t* dense = s.buf[1 - cur];
     const size_t total = static_cast<size_t>(s.rows) * ctx->cols;
@@ -1218,21 +1382,19 @@ int32_t snapshot_read_ctx(ltl_ctx* ctx, const char* path) {
       got_total = off + keep;
     }
     ck(ltl::launch_check_cells(dense, static_cast<int64_t>(got_total), bad, s.stream), "check");
-    if (!short_read) {
-      ck(ltl::launch_to_strips(dense, s.view(cur, ctx->cols), s.stream), "to_strips");
-      ++ctx->launches;
-    }
-    ck(cudaStreamSynchronize(s.stream), "cudaStreamSynchronize");
     ++ctx->launches;
+    ck(cudaStreamSynchronize(s.stream), "cudaStreamSynchronize");
     for (auto& e : ev) cudaEventDestroy(e);
-    const bool any_bad = *bad != 0;
-    if (any_bad || short_read) {
-      cudaFreeHost(bad);
-      if (any_bad) snap_fail("cell byte out of {0,1}");
-      snap_fail(truncated);
-    }
+    if (*bad) snap_fail("cell byte out of {0,1}");
+    if (short_read) snap_fail(truncated);
   }
-  if (bad) cudaFreeHost(bad);
+  // Pass 2: the whole file is valid -- scatter into the live generation.
+  for (Slab& s : ctx->slabs) {
+    ck(cudaSetDevice(s.dev), "cudaSetDevice");
+    if (s.rows == 0 || ctx->cols == 0) continue;
+    ck(ltl::launch_to_strips(s.buf[1 - cur], s.view(cur, ctx->cols), s.stream), "to_strips");
+    ++ctx->launches;
+  }
   if (ctx->slabs.size() > 1)
     for (Slab& s : ctx->slabs) {
       ck(cudaSetDevice(s.dev), "cudaSetDevice");
@@ -1258,6 +1420,17 @@ int ltl_snapshot_read(ltl_ctx* ctx, const char* path, int32_t* layout_out) {
   return guarded(ctx, [&] {
     const int32_t layout = snapshot_read_ctx(ctx, path);
     if (layout_out) *layout_out = layout;
+  });
+}
+
+int ltl_snapshot_parse_header(const char* line, int32_t has_line, int32_t* n, int32_t* f,
+                              int32_t* layout) {
+  return guarded(nullptr, [&] {
+    const SnapHeader h = parse_snap_line(line && has_line ? std::string(line) : std::string(),
+                                         has_line != 0);
+    if (n) *n = h.n;
+    if (f) *f = h.f;
+    if (layout) *layout = h.layout;
   });
 }
 

@@ -60,13 +60,14 @@ class ltl_stats_c(ctypes.Structure):
 
 # Every symbol include/ltl_b200.h declares (tests check the .so exports them all).
 EXPORTS = (
-    "ltl_create", "ltl_create_torus", "ltl_destroy", "ltl_last_error", "ltl_rows", "ltl_cols",
+    "ltl_create", "ltl_create_torus", "ltl_create_grid", "ltl_destroy", "ltl_last_error", "ltl_rows", "ltl_cols",
     "ltl_num_slabs", "ltl_kernel_launches", "ltl_time_launches", "ltl_upload", "ltl_download",
     "ltl_upload_interior", "ltl_download_interior", "ltl_run", "ltl_run_async", "ltl_synchronize", "ltl_time",
     "ltl_run_interior", "ltl_create_part", "ltl_set_stream", "ltl_step_part", "ltl_fill_halo",
     "ltl_slab_buffer", "ltl_pack_edges", "ltl_unpack_halo", "ltl_ring_export",
     "ltl_ring_connect", "ltl_ring_fill", "ltl_ring_active", "ltl_ring_disconnect",
-    "ltl_snapshot_write", "ltl_snapshot_read", "ltl_snapshot_probe",
+    "ltl_snapshot_write", "ltl_snapshot_read", "ltl_snapshot_probe", "ltl_snapshot_parse_header",
+    "ltl_download_padded", "ltl_host_fill_halo",
     "ltl_fragment_pass",
     "ltl_init_random", "ltl_parse_rule", "ltl_format_rule",
     "ltl_preset_count", "ltl_preset", "ltl_von_neumann_probe_rule", "ltl_build_info",
@@ -91,6 +92,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
                        ctypes.c_int),
         "ltl_create_torus": ([P(vp), ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
                               P(ctypes.c_int32)], ctypes.c_int),
+        "ltl_create_grid": ([P(vp), ctypes.c_int32, ctypes.c_int32], ctypes.c_int),
         "ltl_destroy": ([vp], None),
         "ltl_last_error": ([vp], ctypes.c_char_p),
         "ltl_rows": ([vp], ctypes.c_int32),
@@ -100,6 +102,10 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
         "ltl_time_launches": ([vp], ctypes.c_int64),
         "ltl_upload": ([vp, u8p, ctypes.c_int32], ctypes.c_int),
         "ltl_download": ([vp, u8p, ctypes.c_int32], ctypes.c_int),
+        "ltl_download_padded": ([vp, u8p, ctypes.c_int32, ctypes.c_int32], ctypes.c_int),
+        "ltl_host_fill_halo": ([u8p, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32], ctypes.c_int),
+        "ltl_snapshot_parse_header": ([ctypes.c_char_p, ctypes.c_int32, P(ctypes.c_int32),
+                                       P(ctypes.c_int32), P(ctypes.c_int32)], ctypes.c_int),
         "ltl_upload_interior": ([vp, u8p], ctypes.c_int),
         "ltl_download_interior": ([vp, u8p], ctypes.c_int),
         "ltl_run": ([vp, P(ltl_rule_c), ctypes.c_int32, ctypes.c_uint32, P(ltl_stats_c)],
