@@ -22,7 +22,8 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 BUILD = os.path.join(ROOT, "build", "ltl_b200")
 LIB = os.path.join(PKG, "libltl_b200.so")
-CLI = os.path.join(ROOT, "tools", "catbench")
+CLI_SRC = os.path.join(PKG, "cli", "catbench.cpp")
+CLI = os.path.join(PKG, "bin", "catbench")  # the reference's CLI over include/catsim
 
 NVCC = os.environ.get("NVCC", shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -96,6 +97,14 @@ def build(force: bool = False, verbose: bool = False) -> str:
         res = subprocess.run(cmd, capture_output=True, text=True)
         if res.returncode != 0:
             raise RuntimeError(f"link failed: {' '.join(cmd)}\n{res.stdout}\n{res.stderr}")
+    if force or _newer(CLI, [CLI_SRC, LIB, *hdrs]):
+        os.makedirs(os.path.dirname(CLI), exist_ok=True)
+        cxx = shutil.which("g++") or "g++"
+        cmd = [cxx, "-std=c++20", "-O2", "-Wall", "-Wextra", "-I", os.path.join(ROOT, "include"),
+               CLI_SRC, "-o", CLI, f"-L{PKG}", "-lltl_b200", "-Wl,-rpath,$ORIGIN/.."]
+        res = subprocess.run(cmd, capture_output=True, text=True)
+        if res.returncode != 0:
+            raise RuntimeError(f"catbench build failed: {' '.join(cmd)}\n{res.stderr}")
     if verbose:
         print("\n".join(logs))
     return LIB
