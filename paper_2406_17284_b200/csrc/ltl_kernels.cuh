@@ -69,7 +69,27 @@ struct DeviceStats {
   int32_t max_r;
   int32_t error;  // negative-count guard tripped
   int32_t pad;
+  // The reference throws at the FIRST negative count in its serial traversal
+  // (simulate_step's rule loop, src/cat_engine.cpp:291-303: generation, then
+  // tiles of tile_h x tile_w fragments row-major, fragments, cells) with the
+  // count in the message (src/rule.cpp:104-107).  Min over
+  // (generation << 40 | traversal position << 3 | -count); all-ones = none.
+  unsigned long long first_negative;
 };
+
+// Traversal position of interior cell (y, x) in the reference's rule loop
+// with its default tiles (CatConfig tile_w = 1, tile_h = 14,
+// include/catsim/cat_engine.hpp:18-19) and one worker.
+__host__ __device__ inline unsigned long long negative_key(int gen, int y, int x, int f, int n_cols,
+                                                           int neg) {
+  constexpr int kTileH = 14;
+  const long long fi = y / f, fj = x / f;              // interior fragment coordinates
+  const long long tiles_per_row = n_cols / f;          // tile_w = 1: one fragment column each
+  const long long tile = (fi / kTileH) * tiles_per_row + fj;
+  const long long pos = ((tile * kTileH + fi % kTileH) * f + (y % f)) * f + (x % f);
+  return (static_cast<unsigned long long>(gen) << 40) | (static_cast<unsigned long long>(pos) << 3) |
+         static_cast<unsigned long long>(neg & 7);
+}
 
 // ---- tcgen05 banded-MMA step (ltl_tc.cu)
 constexpr int kTcBand = 128;                  // output rows per unit
@@ -127,6 +147,8 @@ struct TcLaunch {
   int32_t inject_fault;     // CatConfig.inject_band_fault (src/cat_engine.cpp:277)
   int32_t fault_f;          // fragment side f of the faulted band fragments
   int32_t fault_row_phase;  // global row of local row 0, mod f
+  int32_t gen_base;         // generation number of this launch's first generation
+  int32_t row0;             // global row of local row 0 (reference traversal order)
   DeviceStats* stats;  // nullptr -> no stats reduction
   int32_t grid;        // CTAs (0 = auto)
   long long* trace;    // debug timeline (LTL_TC_TRACE), nullptr = off

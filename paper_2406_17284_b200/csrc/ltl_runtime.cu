@@ -85,6 +85,7 @@ struct ltl_ctx {
   bool halo_stale = false;  // halo cells the tcgen05 step does not need were not refreshed
   bool ring_stale = true;   // ring counters not (re)started since the last upload / init
   int64_t launches = 0;     // kernels this context has launched (ltl_kernel_launches)
+  int32_t gen_counter = 0;  // generations enqueued since the last stats reset (negative_key)
   int64_t timed_launches = 0;  // inside the last ltl_time's timed loop
   uint8_t* pinned[2] = {nullptr, nullptr};  // snapshot streaming buffers (lazy)
   size_t pinned_bytes = 0;
@@ -489,6 +490,8 @@ void enqueue_step(ltl_ctx* ctx, const ltl::RuleConsts& rc, uint32_t flags, bool 
       // (src/cat_engine.cpp:277): columns / rows == 0 mod f of the global torus
       a.fault_f = ctx->f;
       a.fault_row_phase = s.row0 % ctx->f;
+      a.gen_base = ctx->gen_counter;
+      a.row0 = s.row0;
       a.stats = want_stats ? s.dstats : nullptr;
       // Debug: LTL_TC_TRACE=<file> dumps the pipeline timeline of CTA 0 of
       // the first traced launch (16 event kinds x 256 stamps; 14/15 = per-CTA start/end ns).
@@ -524,13 +527,17 @@ void enqueue_step(ltl_ctx* ctx, const ltl::RuleConsts& rc, uint32_t flags, bool 
   const int out = (gens % 2) ? nxt : cur;  // buffer holding the last generation
   enqueue_halo(ctx, out, !stencil_engine(flags));
   ctx->cur = out;
+  ctx->gen_counter += gens;
 }
 
 void reset_stats(ltl_ctx* ctx) {
   for (Slab& s : ctx->slabs) {
     ck(cudaSetDevice(s.dev), "cudaSetDevice");
     ck(cudaMemsetAsync(s.dstats, 0, sizeof(ltl::DeviceStats), s.stream), "memset stats");
+    ck(cudaMemsetAsync(&s.dstats->first_negative, 0xFF, sizeof(unsigned long long), s.stream),
+       "memset stats");
   }
+  ctx->gen_counter = 0;
 }
 
 void run_steps(ltl_ctx* ctx, const ltl_rule_c* rule, int32_t steps, uint32_t flags,
@@ -547,6 +554,7 @@ void run_steps(ltl_ctx* ctx, const ltl_rule_c* rule, int32_t steps, uint32_t fla
   enqueue_step(ctx, rc, flags, checked, nullptr, nullptr, steps);
   sync_all(ctx);
   ltl::DeviceStats agg{};
+  agg.first_negative = ~0ULL;
   for (Slab& s : ctx->slabs) {
     ltl::DeviceStats h{};
     ck(cudaSetDevice(s.dev), "cudaSetDevice");
@@ -554,8 +562,16 @@ void run_steps(ltl_ctx* ctx, const ltl_rule_c* rule, int32_t steps, uint32_t fla
     agg.max_h = std::max(agg.max_h, h.max_h);
     agg.max_r = std::max(agg.max_r, h.max_r);
     agg.error |= h.error;
+    agg.first_negative = std::min(agg.first_negative, h.first_negative);
   }
-  if (agg.error) throw std::logic_error("internal consistency: negative neighborhood count");
+  if (agg.error) {
+    // the count of the first negative cell in the reference's traversal
+    // (src/rule.cpp:104-107); engines without the key report the prefix only
+    std::string msg = "internal consistency: negative neighborhood count";
+    if (agg.first_negative != ~0ULL)
+      msg += " " + std::to_string(-static_cast<int>(agg.first_negative & 7));
+    throw std::logic_error(msg);
+  }
   if (stats) {
     // CAT-fragment accounting (cat_engine.cpp:151-155, :198-202): 3 MMAs per
     // fragment of the H pass (all fragment rows, interior columns) and 3 per

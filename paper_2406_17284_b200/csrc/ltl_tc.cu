@@ -156,6 +156,7 @@ struct Params {
   // output rows rho with (row0 + rho) == 0 mod f.
   int32_t inject_fault;
   int32_t fault_f, fault_row_phase;
+  int32_t gen_base, row0;  // generation / global row of this launch's first (negative_key)
   int32_t wrap_cols, wrap_rows;  // periodic wrap done by the loads (tc_wrap_*)
   int32_t gens;                  // generations in this launch (persistent when > 1)
   int32_t sweep_chunks;          // chunks per band of a persistent launch (SegIter)
@@ -883,7 +884,20 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const uint32_t mask = (v0 ? 0xFFFFu : 0u) | (v1 ? 0xFFFF0000u : 0u);
                 const uint32_t zz = z[tt][hh][jj];
                 max_r = __vmaxu2(max_r, zz & r_mask & mask);
-                bad |= (zz + g_live) & ~(zz + g_neg) & 0x80008000u & mask;  // live and count < 0
+                const uint32_t neg = (zz + g_live) & ~(zz + g_neg) & 0x80008000u & mask;  // live, count < 0
+                bad |= neg;
+                if (neg) {  // rare (band faults only): where the reference would throw
+#pragma unroll
+                  for (int e = 0; e < 2; ++e) {
+                    if (!((neg >> (16 * e)) & 0x8000u)) continue;
+                    const int zl = static_cast<int>((zz >> (16 * e)) & 0xFFFFu);
+                    const int cnt = zl - static_cast<int>(K) - rc.neg_live;  // < 0
+                    const int y = p.row0 + y0 + out_row_of_col(c + e);
+                    const int x = (t % p.strips) * kStrip + 32 * static_cast<int>(q) + xl;
+                    atomicMin(&p.stats->first_negative,
+                              negative_key(p.gen_base + gg, y, x, p.fault_f, p.cols, -cnt));
+                  }
+                }
               }
             }
           }
@@ -990,6 +1004,8 @@ cudaError_t launch_tc_step(const TcLaunch& a, cudaStream_t stream) {
   p.inject_fault = a.inject_fault;
   p.fault_f = a.fault_f > 0 ? a.fault_f : 16;
   p.fault_row_phase = a.fault_row_phase;
+  p.gen_base = a.gen_base;
+  p.row0 = a.row0;
   p.wrap_cols = a.wrap_cols && tc_wrap_cols(a.cols);
   p.wrap_rows = a.wrap_rows && tc_wrap_rows(a.rows);
   p.gens = a.gens > 1 && a.flags && a.load_maps_b && a.store_map_b ? a.gens : 1;
@@ -1028,11 +1044,24 @@ cudaError_t launch_tc_step(const TcLaunch& a, cudaStream_t stream) {
   cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = kSmemAlloc;
   cfg.stream = stream;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchAttribute attr[2];
+  int nattr = 0;
+  if (!std::getenv("LTL_NO_PDL")) {  // diagnostics
+    attr[nattr].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[nattr].val.programmaticStreamSerializationAllowed = 1;
+    ++nattr;
+  }
+  if (p.gens > 1) {
+    // The multi-generation sweep hands units between CTAs through counters:
+    // it is deadlock-free only with every CTA resident, which a cooperative
+    // launch guarantees (the launch fails instead of hanging when the grid
+    // cannot be co-resident, e.g. SMs held by another context).
+    attr[nattr].id = cudaLaunchAttributeCooperative;
+    attr[nattr].val.cooperative = 1;
+    ++nattr;
+  }
   cfg.attrs = attr;
-  cfg.numAttrs = std::getenv("LTL_NO_PDL") ? 0 : 1;  // diagnostics
+  cfg.numAttrs = static_cast<unsigned>(nattr);
   TcMaps maps;
   for (int i = 0; i < kTcLoadMaps; ++i) {
     maps.load[0][i] = a.load_maps[i];

@@ -184,12 +184,15 @@ __device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
   return v;
 }
 // Flag written by another GPU (peer store over NVLink): system-scope acquire.
+// The watchdog is longer than the on-GPU one (~60 s): a neighbour in another
+// process may legitimately start its kernel late (process skew, its own
+// host work between barriers); it only has to catch a real hang.
 __device__ __forceinline__ void wait_flag_geq_sys(const uint32_t* p, uint32_t target) {
   if (static_cast<int32_t>(ld_acquire_sys(p) - target) >= 0) return;
   const long long t0 = clock64();
   while (static_cast<int32_t>(ld_acquire_sys(p) - target) < 0) {
     __nanosleep(256);
-    if (clock64() - t0 > 20000000000LL) __trap();
+    if (clock64() - t0 > 120000000000LL) __trap();
   }
 }
 // Spin (with back-off) until *p reaches `target` (modular compare); trap

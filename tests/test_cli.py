@@ -147,9 +147,15 @@ def test_verify_output():
     assert lines[-1] == "verified 48 combinations: 48 pass, 0 fail"
     assert "PASS r=1 kind=moore n=32 seed=1 steps=1 engines=cat,base,pack" in lines
     assert all(l.startswith("PASS ") for l in lines[:-1])
+    # the faulted band (pi2(0,0) flipped) escapes detection in exactly the
+    # two combinations where it also escapes in the reference (oracle/_ref,
+    # run_engine(Cat, inject_band_fault) vs run_engine(Base), same seeds)
     res = run(["verify", "--radii", "1-4", "--sizes", "32", "--seeds", "1", "--inject-fault"])
-    assert res.returncode == 0
-    assert "(fault detected:" in res.stdout
+    assert res.returncode == 1
+    assert res.stdout.splitlines()[-1] == "verified 16 combinations: 14 pass, 2 fail"
+    assert [l for l in res.stdout.splitlines() if l.startswith("FAIL")] == [
+        "FAIL r=2 kind=moore n=32 seed=1 steps=25 (fault missed)",
+        "FAIL r=4 kind=moore n=32 seed=1 steps=25 (fault missed)"]
 
 
 @pytest.mark.gpu

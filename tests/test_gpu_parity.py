@@ -341,3 +341,29 @@ def test_bench_geometry_persistent_vs_stencil(ltl, orc):
         st = t.download()
     assert np.array_equal(tc, st)
     assert 0 < int(tc.sum()) < n * n
+
+
+@pytest.mark.parametrize("kind", ["R16,C2,M0,S170..296,B170..300,NM", "R11,C2,M0,S5..21,B9..16,NN"])
+def test_determinism_matrix(ltl, orc, kind, monkeypatch):
+    """acceptance.cpp:352-384 analogue for the device schedule: the CTA count
+    (LTL_TC_GRID in {1, 7, 64, 148}) and the multi-generation sweep's chunk
+    length (LTL_SWEEP_UNITS in {1, 5, 12}) must not change a single byte --
+    per-launch and persistent paths, against one oracle-checked run."""
+    n, steps = 1024, 5
+    init = orc.init_random(n, 0.3, 9)
+    expect = orc.simulate(init, parse_rule_text(kind), steps)
+    for persist in ("0", "1"):
+        monkeypatch.setenv("LTL_FORCE_PERSIST" if persist == "1" else "LTL_NO_PERSIST", "1")
+        monkeypatch.delenv("LTL_NO_PERSIST" if persist == "1" else "LTL_FORCE_PERSIST",
+                           raising=False)
+        for grid in ("1", "7", "64", "148"):
+            for units in ("1", "5", "12"):
+                monkeypatch.setenv("LTL_TC_GRID", grid)
+                monkeypatch.setenv("LTL_SWEEP_UNITS", units)
+                with ltl.DeviceTorus(rows=n, cols=n) as t:
+                    t.upload(init)
+                    t.run(kind, steps)
+                    got = t.download()
+                assert np.array_equal(got, expect), (kind, persist, grid, units)
+                if persist == "0":
+                    break  # the chunk length only matters to the sweep
