@@ -56,6 +56,7 @@ OPS_EXEC = 800       # tcgen05 kind::i8 ops the kernel issues per cell (DESIGN.m
 BOSCO = "R5,C2,M1,S34..58,B34..45,NM"
 
 WORKLOADS = {
+    "c0": "configs[0] Game of Life (R1,C2,M0,S2..3,B3..3,NM) 1024x1024, density 0.5",
     "c1": "configs[1] Bosco r=5 (R5,C2,M1,S34..58,B34..45,NM) 16384x16384",
     "c2": "configs[2] radius sweep r=1..16 (Table III presets) 32768x32768",
     "c3": "configs[3] r=16 tangy-ramen 65536x65536 row slabs (strong scaling)",
@@ -99,6 +100,8 @@ def workload_rules(workload):
     """[(label, rule text, density)] of a workload (the reference's presets)."""
     from paper_2406_17284_b200 import ltl
     presets = ltl.ltl_presets()
+    if workload == "c0":
+        return [("life", presets[0][1], 0.5)]
     if workload == "c1":
         return [("bosco-literal", BOSCO, 0.21)]
     if workload == "c2":
@@ -109,7 +112,7 @@ def workload_rules(workload):
 
 
 def workload_side(workload):
-    return {"c1": 16384, "c2": 32768, "c3": 65536, "c4": 65536}[workload]
+    return {"c0": 1024, "c1": 16384, "c2": 32768, "c3": 65536, "c4": 65536}[workload]
 
 
 class Clocks:
@@ -280,6 +283,8 @@ def reference_arm(args, rank, world):
 
 def ref_rules(ref, workload):
     presets = ref.presets()
+    if workload == "c0":
+        return [("life", presets[0][1], 0.5)]
     if workload == "c1":
         return [("bosco-literal", BOSCO, 0.21)]
     if workload == "c2":
@@ -297,6 +302,9 @@ def config_dict(workload, world):
         d["rules"] = "Table III presets r=1..16 at their densities (proj/src/rule.cpp:113-133)"
     elif workload == "c1":
         d.update(rule=BOSCO, density=0.21)
+    elif workload == "c0":
+        d.update(rule="R1,C2,M0,S2..3,B3..3,NM", density=0.5,
+                 l2="L2-resident (2 x 1.1 MB): launch / latency bound, no HBM roofline")
     elif workload == "c3":
         d.update(rule="R16,C2,M0,S170..296,B170..300,NM", density=0.26,
                  torus=f"{n}x{n} split in {world} row slabs")

@@ -225,6 +225,12 @@ int32_t ltl_ring_active(const ltl_ctx* ctx);
 /* Drop a part context's ring (close the IPC mappings); steps then need the
  * packed exchange again. */
 int ltl_ring_disconnect(ltl_ctx* ctx);
+/* 1 when ltl_run / ltl_run_async of more than one generation would use ONE
+ * multi-generation (persistent) launch on this context.  Ranks of a ring must
+ * agree (their kernels wait on each other's per-unit counters): a
+ * multi-process caller votes on this and, unless every rank says 1, runs
+ * one generation per call (paper_2406_17284_b200/dist.py). */
+int32_t ltl_persistent_ok(ltl_ctx* ctx, uint32_t flags);
 
 /* Device pointer of slab `slab`'s current (which = 0) or other (1)
  * generation buffer, its strip size in bytes and interior row count.  The

@@ -816,6 +816,13 @@ int ltl_create(ltl_ctx** out, int32_t n, int32_t f, int32_t num_slabs, const int
   return st2;
 }
 
+int32_t ltl_persistent_ok(ltl_ctx* ctx, uint32_t flags) {
+  if (!ctx) return 0;
+  int32_t ok = 0;
+  guarded(ctx, [&] { ok = persistent_ok(ctx, flags) ? 1 : 0; });
+  return ok;
+}
+
 int ltl_create_grid(ltl_ctx** out, int32_t n, int32_t f) {
   if (!out) return LTL_ERR_INVALID_ARGUMENT;
   *out = nullptr;

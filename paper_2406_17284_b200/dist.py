@@ -131,6 +131,14 @@ class PartitionedTorus:
             if not ok:
                 self.torus.ring_disconnect()
                 self.ring = False
+        # Multi-generation (persistent) ring launches wait on the neighbours'
+        # per-unit counters, which only persistent launches publish: every
+        # rank must make the same choice, so it is voted on once here.
+        self.persist = self.ring and self.torus.persistent_ok()
+        if self.ring and world > 1:
+            votes = [None] * world
+            self.dist.all_gather_object(votes, self.persist)
+            self.persist = all(votes)
 
     def use_stream(self, stream_ptr: int) -> None:
         self.torus.set_stream(stream_ptr)
@@ -170,10 +178,10 @@ class PartitionedTorus:
         in one call (one persistent launch when the geometry allows it, the
         same decision on every rank: equal slab heights, neighbours on other
         GPUs); otherwise one step + packed exchange per generation."""
-        if self.ring:
+        if self.ring and self.persist:
             self.torus.run_async(rule, steps)
             return
-        for _ in range(steps):
+        for _ in range(steps):  # one generation per launch on every rank
             self.step(rule)
 
     def step(self, rule, stencil: bool = False) -> None:

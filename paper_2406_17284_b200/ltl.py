@@ -66,6 +66,7 @@ EXPORTS = (
     "ltl_run_interior", "ltl_create_part", "ltl_set_stream", "ltl_step_part", "ltl_fill_halo",
     "ltl_slab_buffer", "ltl_pack_edges", "ltl_unpack_halo", "ltl_ring_export",
     "ltl_ring_connect", "ltl_ring_fill", "ltl_ring_active", "ltl_ring_disconnect",
+    "ltl_persistent_ok",
     "ltl_snapshot_write", "ltl_snapshot_read", "ltl_snapshot_probe", "ltl_snapshot_parse_header",
     "ltl_download_padded", "ltl_host_fill_halo",
     "ltl_fragment_pass",
@@ -130,6 +131,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
         "ltl_ring_fill": ([vp], ctypes.c_int),
         "ltl_ring_active": ([vp], ctypes.c_int32),
         "ltl_ring_disconnect": ([vp], ctypes.c_int),
+        "ltl_persistent_ok": ([vp, ctypes.c_uint32], ctypes.c_int32),
         "ltl_snapshot_write": ([vp, ctypes.c_char_p, ctypes.c_int32], ctypes.c_int),
         "ltl_snapshot_read": ([vp, ctypes.c_char_p, ctypes.POINTER(ctypes.c_int32)], ctypes.c_int),
         "ltl_snapshot_probe": ([ctypes.c_char_p, ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int32)],
@@ -421,6 +423,10 @@ class DeviceTorus:
 
     def ring_disconnect(self) -> None:
         self._check(self.lib.ltl_ring_disconnect(self._ctx))
+
+    def persistent_ok(self, engine: str = "cat") -> bool:
+        """Would a multi-generation run use one persistent launch here?"""
+        return bool(self.lib.ltl_persistent_ok(self._ctx, self._flags(engine)))
 
     def pack_edges(self, top_ptr: int, bot_ptr: int) -> None:
         """Enqueue: device buffers top/bot (16 x cols) <- first / last 16 interior rows."""
