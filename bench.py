@@ -533,6 +533,8 @@ def main():
     ap.add_argument("--workload", choices=tuple(WORKLOADS), default=None)
     ap.add_argument("--engine", choices=("cat", "base", "pack"), default="cat")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--dist", action="store_true",
+                    help="the multi-process slab path even at world size 1 (testing)")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
 
@@ -549,9 +551,12 @@ def main():
     if args.impl == "reference":
         reference_arm(args, rank, max(world, args.gpus))
         return
-    if world > 1:
+    if world > 1 or args.dist:
         import torch
         import torch.distributed as dist
+        if "RANK" not in os.environ:  # --dist without torchrun: a world of one
+            os.environ.update(RANK="0", WORLD_SIZE="1", MASTER_ADDR="127.0.0.1",
+                              MASTER_PORT=os.environ.get("MASTER_PORT", "29533"))
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
         try:
             ours_multi(args, rank, world, local_rank)

@@ -32,7 +32,11 @@ namespace ltl {
 namespace {
 
 constexpr int kThreads = 256;
-constexpr int kTileW = kStrip + 2 * kHalo;  // 160 tile columns: logical [-16, 144) of the strip
+// Tile rows hold logical columns [-16, 144) of the strip (160 bytes) at a
+// 164-byte pitch: 41 words, odd, so the word k of 32 different (row, quarter)
+// pairs a warp reads in the pack engine's row pass fall in 32 different banks.
+constexpr int kTileCols = kStrip + 2 * kHalo;  // 160
+constexpr int kTileW = kTileCols + 4;          // row pitch in bytes
 
 __device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
   uint32_t d;
@@ -84,24 +88,42 @@ __device__ __forceinline__ uint32_t next_word(uint32_t a, uint32_t b) {
 }
 
 // stage padded rows [y0, y0 + TY + 32) x logical columns [x0 - 16, x0 + 144)
-// of the slab into tile[TY + 32][160] (rows past the slab read as 0)
+// of the slab into tile[TY + 32][kTileW] (rows past the slab read as 0).
+// Every thread first issues ALL its 16-byte loads (ncu: with one load in
+// flight per thread the loop stalled ~30 % of the kernel on the store that
+// waits for it), then stores them.
 template <int TY>
 __device__ __forceinline__ void load_tile(const SlabView& in, int strip, int y0, uint8_t* tile) {
-  constexpr int kRows = TY + 2 * kHalo;
+  constexpr int kItems = (TY + 2 * kHalo) * 10;  // 10 chunks of 16 B per row
+  constexpr int kPer = (kItems + kThreads - 1) / kThreads;
   const int rows_pad = in.rows + 2 * kHalo;
   const uint8_t* mid = in.buf + static_cast<int64_t>(strip + 1) * in.strip_bytes;
   const uint8_t* left = mid - in.strip_bytes + (kStrip - kHalo);
   const uint8_t* right = mid + in.strip_bytes;
-  for (int i = threadIdx.x; i < kRows * 10; i += kThreads) {
-    const int row = i / 10, c = i % 10;  // c: 0 left, 1..8 strip, 9 right (16 B each)
+  uint4 v[kPer];
+#pragma unroll
+  for (int u = 0; u < kPer; ++u) {
+    const int i = static_cast<int>(threadIdx.x) + u * kThreads;
+    const int row = i / 10, c = i % 10;  // c: 0 left, 1..8 strip, 9 right
     const int py = y0 + row;
-    uint4 v = make_uint4(0, 0, 0, 0);
-    if (py < rows_pad) {
+    v[u] = make_uint4(0, 0, 0, 0);
+    if (i < kItems && py < rows_pad) {
       const int64_t o = static_cast<int64_t>(py) * kStrip;
       const uint8_t* src = c == 0 ? left + o : c == 9 ? right + o : mid + o + 16 * (c - 1);
-      v = __ldg(reinterpret_cast<const uint4*>(src));
+      v[u] = __ldg(reinterpret_cast<const uint4*>(src));
     }
-    *reinterpret_cast<uint4*>(tile + row * kTileW + 16 * c) = v;
+  }
+#pragma unroll
+  for (int u = 0; u < kPer; ++u) {
+    const int i = static_cast<int>(threadIdx.x) + u * kThreads;
+    if (i < kItems) {
+      const int row = i / 10, c = i % 10;
+      uint32_t* dst = reinterpret_cast<uint32_t*>(tile + row * kTileW + 16 * c);  // 4-byte aligned
+      dst[0] = v[u].x;
+      dst[1] = v[u].y;
+      dst[2] = v[u].z;
+      dst[3] = v[u].w;
+    }
   }
 }
 
@@ -197,7 +219,8 @@ __global__ void __launch_bounds__(kThreads)
 
 // ====================== pack: separable, O(1) per cell ========================
 constexpr int kPackTY = 128;
-constexpr int kHW = kStrip;  // H tile row: the 128 output columns
+constexpr int kHW = kStrip;         // H tile row: the 128 output columns
+constexpr int kHStride = kHW / 4 + 1;  // 33 words: the row pass's stores hit 32 banks
 
 // Horizontal window sums of one 32-column quarter of a tile row (output
 // columns 32q .. 32q+31 = tile columns 16 + 32q ..), written as bytes to
@@ -263,7 +286,7 @@ __global__ void __launch_bounds__(kThreads)
     pack_kernel(const SlabView in, const SlabView out, const RuleConsts rc, DeviceStats* stats) {
   constexpr int kRows = kPackTY + 2 * kHalo;
   __shared__ __align__(16) uint8_t tile[kRows * kTileW];
-  __shared__ __align__(16) uint32_t htile[(kPackTY + 2 * R) * (kHW / 4)];  // H rows y0-r .. y0+TY+r
+  __shared__ __align__(16) uint32_t htile[(kPackTY + 2 * R) * kHStride];  // H rows y0-r .. y0+TY+r
   const int strip = blockIdx.x, y0 = blockIdx.y * kPackTY;
   load_tile<kPackTY>(in, strip, y0, tile);
   __syncthreads();
@@ -280,14 +303,14 @@ __global__ void __launch_bounds__(kThreads)
       vw = vc <= 0 ? 0 : vc >= 32 ? 8 : vc / 4;  // whole words only (cols % 4 tail below)
     }
     const uint32_t mh = row_window_sums<R>(reinterpret_cast<const uint32_t*>(tile + trow * kTileW),
-                                           q, htile + hr * (kHW / 4), static_cast<uint32_t>(vw));
+                                           q, htile + hr * kHStride, static_cast<uint32_t>(vw));
     if (kChecked) max_h = __vmaxu4(max_h, mh);
   }
   __syncthreads();
   if (kChecked) {  // a partial last word of the torus (cols % 4 != 0)
     const int vc = in.cols - x_strip;
     if (vc > 0 && vc < kStrip && (vc & 3) && threadIdx.x < kPackTY && y0 + threadIdx.x < in.rows) {
-      const uint32_t h = htile[(R + threadIdx.x) * (kHW / 4) + (vc >> 2)];
+      const uint32_t h = htile[(R + threadIdx.x) * kHStride + (vc >> 2)];
       max_h = __vmaxu4(max_h, h & ((1u << (8 * (vc & 3))) - 1u));
     }
   }
@@ -301,7 +324,7 @@ __global__ void __launch_bounds__(kThreads)
   const uint32_t rmask_hi = (x + 2 < in.cols ? 0xFFFFu : 0u) | (x + 3 < in.cols ? 0xFFFF0000u : 0u);
   constexpr int kSeg = kPackTY / 8;
   const int ys = seg * kSeg;
-  const uint32_t* hcol = htile + j;  // H word of H row k: hcol[k * 32]
+  const uint32_t* hcol = htile + j;  // H word of H row k: hcol[k * kHStride]
   const uint8_t* ccol = tile + 16 + 4 * j;
   uint32_t lo = 0, hi = 0;  // Moore: R lanes; VN: V (vertical cell sums) bytes in lo
   if (KIND == 0) {
@@ -310,7 +333,7 @@ __global__ void __launch_bounds__(kThreads)
     uint32_t g = 0;
 #pragma unroll
     for (int k = 0; k <= 2 * R; ++k) {
-      g += hcol[(ys + k) * 32];
+      g += hcol[(ys + k) * kHStride];
       if (k % 7 == 6 || k == 2 * R) {
         lo += widen_lo(g);
         hi += widen_hi(g);
@@ -327,7 +350,7 @@ __global__ void __launch_bounds__(kThreads)
     if (yy > 0) {
       if (KIND == 0) {
         // R += H(y + r) - H(y - r - 1): a biased byte difference (31..97), widened
-        const uint32_t d = hcol[(y + 2 * R) * 32] + 0x40404040u - hcol[(y - 1) * 32];
+        const uint32_t d = hcol[(y + 2 * R) * kHStride] + 0x40404040u - hcol[(y - 1) * kHStride];
         lo += widen_lo(d) - 0x00400040u;
         hi += widen_hi(d) - 0x00400040u;
       } else {
@@ -341,7 +364,7 @@ __global__ void __launch_bounds__(kThreads)
       zl = lo + (widen_lo(st) << 11);
       zh = hi + (widen_hi(st) << 11);
     } else {  // R = H + V (centre twice), + 128 * state: all < 256 in byte lanes
-      const uint32_t zb = hcol[(y + R) * 32] + lo + (st << 7);
+      const uint32_t zb = hcol[(y + R) * kHStride] + lo + (st << 7);
       zl = widen_lo(zb);
       zh = widen_hi(zb);
     }

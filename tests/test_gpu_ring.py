@@ -26,15 +26,16 @@ def _free_port():
     return port
 
 
-def _worker(rank, world, port, global_rows, cols, steps, text, q, multi=False):
+def _worker(rank, world, port, global_rows, cols, steps, text, q, multi=False, own_gpu=False):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     if multi:  # multi-generation launches even on small slabs (world 1: self-ring)
         os.environ["LTL_FORCE_PERSIST"] = "1"
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        torch.cuda.set_device(0)
+        dev = rank if own_gpu else 0
+        torch.cuda.set_device(dev)
         from paper_2406_17284_b200.dist import PartitionedTorus
-        part = PartitionedTorus(global_rows, cols, rank, world, 0, ring=True)
+        part = PartitionedTorus(global_rows, cols, rank, world, dev, ring=True)
         assert part.ring and part.torus.ring_active()
         rng = np.random.default_rng(7)
         full = (rng.random((global_rows, cols)) < 0.3).astype(np.uint8)
@@ -55,21 +56,26 @@ def _worker(rank, world, port, global_rows, cols, steps, text, q, multi=False):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,global_rows,cols,multi", [
-    (2, 256, 256, False), (4, 512, 128, False), (1, 96, 384, False),
-    (2, 256, 256, True),                      # same GPU: one launch per generation
-    (1, 512, 384, True),                      # self-ring: persistent ring kernel
+@pytest.mark.parametrize("world,global_rows,cols,multi,own_gpu", [
+    (2, 256, 256, False, False), (4, 512, 128, False, False), (1, 96, 384, False, False),
+    (2, 256, 256, True, False),               # same GPU: one launch per generation
+    (1, 512, 384, True, False),               # self-ring: persistent ring kernel
+    # one process per GPU (needs >= 2 / 4 GPUs): the cross-device persistent
+    # ring kernel, rows pulled over NVLink through CUDA IPC
+    (2, 1024, 512, True, True), (2, 512, 256, False, True), (4, 2048, 256, True, True),
 ])
-def test_ring_processes_match_oracle(orc, world, global_rows, cols, multi):
+def test_ring_processes_match_oracle(orc, world, global_rows, cols, multi, own_gpu):
     if not torch.cuda.is_available():
         pytest.skip("no GPU")
+    if own_gpu and torch.cuda.device_count() < world:
+        pytest.skip(f"needs {world} GPUs")
     text = "R16,C2,M0,S170..296,B170..300,NM"
     steps = 5
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
     procs = [ctx.Process(target=_worker,
-                         args=(r, world, port, global_rows, cols, steps, text, q, multi))
+                         args=(r, world, port, global_rows, cols, steps, text, q, multi, own_gpu))
              for r in range(world)]
     for p in procs:
         p.start()
@@ -84,3 +90,22 @@ def test_ring_processes_match_oracle(orc, world, global_rows, cols, multi):
     rng = np.random.default_rng(7)
     full = (rng.random((global_rows, cols)) < 0.3).astype(np.uint8)
     assert np.array_equal(assembled, orc.simulate(full, parse_rule_text(text), steps))
+
+
+@pytest.mark.parametrize("gpus", [2, 4, 8])
+def test_slabs_on_several_devices_in_one_process(orc, gpus):
+    """One process driving G GPUs (ltl_create with dev_ids 0..G-1): peer access,
+    per-device kernel attributes, the in-process ring -- equal to one slab."""
+    if not torch.cuda.is_available() or torch.cuda.device_count() < gpus:
+        pytest.skip(f"needs {gpus} GPUs")
+    from paper_2406_17284_b200 import ltl
+    n, text = 2048, "R8,C2,M0,S163..223,B74..252,NM"
+    with ltl.DeviceTorus(n=n) as t:
+        t.init_random(0.23, 1)
+        init = t.download()
+        t.run(text, 6)
+        want = t.download()
+    with ltl.DeviceTorus(n=n, slabs=gpus, devices=list(range(gpus))) as t:
+        t.upload(init)
+        t.run(text, 6)
+        assert np.array_equal(t.download(), want)
