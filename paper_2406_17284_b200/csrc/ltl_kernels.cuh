@@ -155,7 +155,7 @@ struct TcLaunch {
 };
 cudaError_t launch_tc_step(const TcLaunch& a, cudaStream_t stream);
 int tc_persistent_ctas(int32_t rows, int32_t cols, int num_sms);  // 0: no multi-generation launch
-int tc_sweep_chunks(int32_t strips);  // chunks per band of a multi-generation launch
+int tc_sweep_chunks(int32_t strips, int32_t bands, int ctas);  // chunks per band of a multi-generation launch
 size_t tc_smem_bytes();
 
 // Host-side tensor-map builders (driver entry point fetched at runtime).

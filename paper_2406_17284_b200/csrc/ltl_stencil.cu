@@ -89,41 +89,53 @@ __device__ __forceinline__ uint32_t next_word(uint32_t a, uint32_t b) {
 
 // stage padded rows [y0, y0 + TY + 32) x logical columns [x0 - 16, x0 + 144)
 // of the slab into tile[TY + 32][kTileW] (rows past the slab read as 0).
-// Every thread first issues ALL its 16-byte loads (ncu: with one load in
-// flight per thread the loop stalled ~30 % of the kernel on the store that
-// waits for it), then stores them.
+// The strip's own 128 columns are ONE contiguous block of the strip layout
+// (16-byte chunk i at byte 16 i); the 16 side columns are one chunk per row
+// of the neighbour strips.  Every thread first issues ALL its loads (ncu:
+// with one load in flight per thread the loop stalled ~30 % of the kernel on
+// the store waiting for it), then stores them.
 template <int TY>
 __device__ __forceinline__ void load_tile(const SlabView& in, int strip, int y0, uint8_t* tile) {
-  constexpr int kItems = (TY + 2 * kHalo) * 10;  // 10 chunks of 16 B per row
-  constexpr int kPer = (kItems + kThreads - 1) / kThreads;
-  const int rows_pad = in.rows + 2 * kHalo;
-  const uint8_t* mid = in.buf + static_cast<int64_t>(strip + 1) * in.strip_bytes;
+  constexpr int kRows = TY + 2 * kHalo;
+  constexpr int kMain = kRows * 8, kSide = kRows * 2;
+  constexpr int kPerMain = (kMain + kThreads - 1) / kThreads;
+  constexpr int kPerSide = (kSide + kThreads - 1) / kThreads;
+  const int valid_rows = min(kRows, in.rows + 2 * kHalo - y0);
+  const uint8_t* mid = in.buf + static_cast<int64_t>(strip + 1) * in.strip_bytes +
+                       static_cast<int64_t>(y0) * kStrip;
   const uint8_t* left = mid - in.strip_bytes + (kStrip - kHalo);
   const uint8_t* right = mid + in.strip_bytes;
-  uint4 v[kPer];
+  uint4 vm[kPerMain], vs[kPerSide];
 #pragma unroll
-  for (int u = 0; u < kPer; ++u) {
+  for (int u = 0; u < kPerMain; ++u) {
     const int i = static_cast<int>(threadIdx.x) + u * kThreads;
-    const int row = i / 10, c = i % 10;  // c: 0 left, 1..8 strip, 9 right
-    const int py = y0 + row;
-    v[u] = make_uint4(0, 0, 0, 0);
-    if (i < kItems && py < rows_pad) {
-      const int64_t o = static_cast<int64_t>(py) * kStrip;
-      const uint8_t* src = c == 0 ? left + o : c == 9 ? right + o : mid + o + 16 * (c - 1);
-      v[u] = __ldg(reinterpret_cast<const uint4*>(src));
-    }
+    vm[u] = (i < kMain && (i >> 3) < valid_rows)
+                ? __ldg(reinterpret_cast<const uint4*>(mid) + i) : make_uint4(0, 0, 0, 0);
   }
 #pragma unroll
-  for (int u = 0; u < kPer; ++u) {
+  for (int u = 0; u < kPerSide; ++u) {
     const int i = static_cast<int>(threadIdx.x) + u * kThreads;
-    if (i < kItems) {
-      const int row = i / 10, c = i % 10;
-      uint32_t* dst = reinterpret_cast<uint32_t*>(tile + row * kTileW + 16 * c);  // 4-byte aligned
-      dst[0] = v[u].x;
-      dst[1] = v[u].y;
-      dst[2] = v[u].z;
-      dst[3] = v[u].w;
-    }
+    const int row = i >> 1;
+    vs[u] = (i < kSide && row < valid_rows)
+                ? __ldg(reinterpret_cast<const uint4*>((i & 1 ? right : left) + row * kStrip))
+                : make_uint4(0, 0, 0, 0);
+  }
+  auto put = [&](int row, int col, const uint4& v) {
+    uint32_t* dst = reinterpret_cast<uint32_t*>(tile + row * kTileW + col);  // 4-byte aligned
+    dst[0] = v.x;
+    dst[1] = v.y;
+    dst[2] = v.z;
+    dst[3] = v.w;
+  };
+#pragma unroll
+  for (int u = 0; u < kPerMain; ++u) {
+    const int i = static_cast<int>(threadIdx.x) + u * kThreads;
+    if (i < kMain) put(i >> 3, kHalo + 16 * (i & 7), vm[u]);
+  }
+#pragma unroll
+  for (int u = 0; u < kPerSide; ++u) {
+    const int i = static_cast<int>(threadIdx.x) + u * kThreads;
+    if (i < kSide) put(i >> 1, (i & 1) ? kHalo + kStrip : 0, vs[u]);
   }
 }
 
@@ -173,9 +185,12 @@ __global__ void __launch_bounds__(kThreads)
   uint32_t max_h = 0, max_r = 0, bad = 0;
   constexpr int kW0 = (16 - R) >> 2;                     // first word a row window touches
   constexpr int kNW = ((16 + 3 + R) >> 2) - kW0 + 1;     // words per row window
-  for (int yy = 0; yy < kBaseTY / 8; ++yy) {
-    const int y = seg * (kBaseTY / 8) + yy;  // output row within the chunk
-    if (y0 + y >= in.rows) break;
+  const int ys = seg * (kBaseTY / 8);
+  const int nrows = max(0, min(kBaseTY / 8, in.rows - (y0 + ys)));
+  const bool full_word = x + 3 < in.cols;
+  uint8_t* optr = out.buf + out.offset(y0 + ys + kHalo, min(x, in.cols - 1));
+  for (int yy = 0; yy < nrows; ++yy, optr += kStrip) {
+    const int y = ys + yy;  // output row within the chunk
     uint32_t acc_lo = 0, acc_hi = 0, h_centre = 0, v_cross = 0;
 #pragma unroll
     for (int dy = -R; dy <= R; ++dy) {
@@ -212,7 +227,8 @@ __global__ void __launch_bounds__(kThreads)
       max_r = __vmaxu2(max_r, acc_hi & sr.r_mask & rmask_hi);
       bad |= (sr.negative(acc_lo) & rmask_lo) | (sr.negative(acc_hi) & rmask_hi);
     }
-    if (x < in.cols) store_word(out, y0 + y, x, nw);
+    if (full_word) *reinterpret_cast<uint32_t*>(optr) = nw;
+    else if (x < in.cols) store_word(out, y0 + y, x, nw);
   }
   if constexpr (kChecked) flush_stats(stats, max_h, max_r, bad);
 }
@@ -344,27 +360,35 @@ __global__ void __launch_bounds__(kThreads)
 #pragma unroll
     for (int k = -R; k <= R; ++k) lo += *reinterpret_cast<const uint32_t*>(ccol + (kHalo + ys + k) * kTileW);
   }
-  for (int yy = 0; yy < kSeg; ++yy) {
+  const int nrows = max(0, min(kSeg, in.rows - (y0 + ys)));
+  const bool full_word = x + 3 < in.cols;
+  uint8_t* optr = out.buf + out.offset(y0 + ys + kHalo, min(x, in.cols - 1));
+  // pointers stepped one row per output row: the H rows entering / leaving
+  // the window (Moore), the cell rows entering / leaving (VN), the centre
+  const uint32_t* h_in = hcol + (ys + 2 * R) * kHStride;
+  const uint32_t* h_mid = hcol + (ys + R) * kHStride;
+  const uint8_t* c_mid = ccol + (kHalo + ys) * kTileW;
+  for (int yy = 0; yy < nrows; ++yy, optr += kStrip, h_in += kHStride, h_mid += kHStride,
+           c_mid += kTileW) {
     const int y = ys + yy;
-    if (y0 + y >= in.rows) break;
     if (yy > 0) {
       if (KIND == 0) {
         // R += H(y + r) - H(y - r - 1): a biased byte difference (31..97), widened
-        const uint32_t d = hcol[(y + 2 * R) * kHStride] + 0x40404040u - hcol[(y - 1) * kHStride];
+        const uint32_t d = h_in[0] + 0x40404040u - h_in[-(2 * R + 1) * kHStride];
         lo += widen_lo(d) - 0x00400040u;
         hi += widen_hi(d) - 0x00400040u;
       } else {
-        lo += *reinterpret_cast<const uint32_t*>(ccol + (kHalo + y + R) * kTileW) -
-              *reinterpret_cast<const uint32_t*>(ccol + (kHalo + y - R - 1) * kTileW);
+        lo += *reinterpret_cast<const uint32_t*>(c_mid + R * kTileW) -
+              *reinterpret_cast<const uint32_t*>(c_mid - (R + 1) * kTileW);
       }
     }
-    const uint32_t st = *reinterpret_cast<const uint32_t*>(ccol + (kHalo + y) * kTileW);
+    const uint32_t st = *reinterpret_cast<const uint32_t*>(c_mid);
     uint32_t zl, zh;
     if (KIND == 0) {
       zl = lo + (widen_lo(st) << 11);
       zh = hi + (widen_hi(st) << 11);
     } else {  // R = H + V (centre twice), + 128 * state: all < 256 in byte lanes
-      const uint32_t zb = hcol[(y + R) * kHStride] + lo + (st << 7);
+      const uint32_t zb = h_mid[0] + lo + (st << 7);
       zl = widen_lo(zb);
       zh = widen_hi(zb);
     }
@@ -374,7 +398,8 @@ __global__ void __launch_bounds__(kThreads)
       max_r = __vmaxu2(max_r, zh & sr.r_mask & rmask_hi);
       bad |= (sr.negative(zl) & rmask_lo) | (sr.negative(zh) & rmask_hi);
     }
-    if (x < in.cols) store_word(out, y0 + y, x, nw);
+    if (full_word) *reinterpret_cast<uint32_t*>(optr) = nw;
+    else if (x < in.cols) store_word(out, y0 + y, x, nw);
   }
   if constexpr (kChecked) flush_stats(stats, max_h, max_r, bad);
 }

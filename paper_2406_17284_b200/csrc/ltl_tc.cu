@@ -963,11 +963,24 @@ int tc_persistent_ctas(int32_t rows, int32_t cols, int num_sms) {
   const int64_t units = bands * interior_strips(cols);
   if (std::getenv("LTL_FORCE_PERSIST"))  // tests: small tori, fewer CTAs
     return static_cast<int>(units < num_sms ? units : num_sms);
+  // A small torus (at most two units per SM: 1024^2 has 64, 2048^2 256): a
+  // generation is one or two latency-bound waves, and a launch per
+  // generation costs more than the sweep's flag hand-over (GoL, us per
+  // generation, launch per generation -> sweep: 1024^2 10.4 -> 8.0, 2048^2
+  // 18.8 -> 12.7; 4096^2 22.2 -> 23.6 stays per launch;
+  // profiles/small_torus_r02.txt).
+  if (units <= 2LL * num_sms && !std::getenv("LTL_NO_SMALL_PERSIST"))
+    return static_cast<int>(units < num_sms ? units : num_sms);
   return bands >= 16 && units >= 8LL * num_sms && units <= 190LL * num_sms ? num_sms : 0;
 }
 
-int tc_sweep_chunks(int32_t strips) {  // <= 12 units per chunk (16384^2 A/B: 12 -> 93.7 us, 16 -> 94.3, 20 -> 97.0, 8 -> ~101)
-  int per = 12;
+// Chunks per band of the multi-generation sweep: <= 12 units per chunk
+// (16384^2 A/B: 12 -> 93.7 us, 16 -> 94.3, 20 -> 97.0, 8 -> ~101), and no
+// more units per chunk than units per CTA (a tiny torus: one unit per chunk,
+// so every CTA gets one).
+int tc_sweep_chunks(int32_t strips, int32_t bands, int ctas) {
+  const int64_t per_cta = ctas > 0 ? static_cast<int64_t>(strips) * bands / ctas : 12;
+  int per = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(12, per_cta)));
   if (const char* e = std::getenv("LTL_SWEEP_UNITS")) per = std::max(1, std::atoi(e));  // tuning
   return (strips + per - 1) / per;
 }
@@ -1032,7 +1045,7 @@ cudaError_t launch_tc_step(const TcLaunch& a, cudaStream_t stream) {
   if (p.gens > 1) {
     grid = tc_persistent_ctas(a.rows, a.cols, num_sms);
     if (grid <= 0) return cudaErrorNotSupported;
-    p.sweep_chunks = tc_sweep_chunks(p.strips);
+    p.sweep_chunks = tc_sweep_chunks(p.strips, p.bands, static_cast<int>(grid));
   }
   if (a.grid > 0 && a.grid < grid) grid = a.grid;
   if (const char* e = std::getenv("LTL_TC_GRID")) {  // tuning knob (sweeps only)
