@@ -478,6 +478,7 @@ def ours_multi(args, rank, world, local_rank):
     e2e = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device="cuda")
     dist.all_reduce(e2e, op=dist.ReduceOp.MAX)
     e2e_value = cells * steps / float(e2e.item())
+    parity = g_vs_1_check(part, hout, rule, dens, warmup + 2 * steps, global_rows, n, rank, world)
     if rank == 0:
         peaks, peak_src = measured_peaks()
         hbm = peaks["hbm_gbs"]
@@ -499,6 +500,7 @@ def ours_multi(args, rank, world, local_rank):
                          "frac": achieved / hbm, "traffic": None, "peak_source": peak_src,
                          "per": "generation per GPU (rank 0's slab, whole step time)"},
             "clocks": clk,
+            "parity": parity,
         }
         ncu = profile_json(f"ncu_tc_step_{n}.json")
         if ncu:
@@ -513,6 +515,36 @@ def ours_multi(args, rank, world, local_rank):
             line["cpu_baseline"]["sample"] += " (4096^2 bounded sample of the same rule)"
         np.asarray(0)
         print(json.dumps(line), flush=True)
+
+
+def g_vs_1_check(part, slab, rule, dens, gens, global_rows, n, rank, world):
+    """Bit-exactness of the G-GPU run: every rank's final slab (CRC-32 +
+    alive count) against the same torus run for the same generations on ONE
+    GPU by rank 0 (after the timed region; device init is bit-identical, so
+    both start from the same grid)."""
+    import zlib
+
+    import numpy as np
+    import torch.distributed as dist
+
+    from paper_2406_17284_b200 import ltl
+    mine = (part.row0, part.rows, zlib.crc32(memoryview(np.ascontiguousarray(slab))),
+            int(np.count_nonzero(slab)))
+    table = [None] * world
+    dist.all_gather_object(table, mine)
+    ok = None
+    if rank == 0:
+        with ltl.DeviceTorus(rows=global_rows, cols=n) as t:
+            t.init_random(dens, SEED)
+            t.run(rule, gens)
+            full = t.download()
+        ok = all(zlib.crc32(memoryview(full[r0:r0 + rows])) == crc and
+                 int(np.count_nonzero(full[r0:r0 + rows])) == alive
+                 for r0, rows, crc, alive in table)
+    dist.barrier()
+    return {"g_vs_1_bit_exact": ok, "generations": gens,
+            "how": f"each rank's slab after {gens} generations (CRC-32 + alive count) vs the "
+                   f"{global_rows}x{n} torus run on one GPU by rank 0"}
 
 
 def spawn(args):

@@ -8,6 +8,7 @@
 #include <cmath>
 #include <cstddef>
 #include <cstdint>
+#include <cstring>
 #include <optional>
 #include <stdexcept>
 #include <string>
@@ -119,9 +120,42 @@ inline Grid make_grid(int n, int f = kDefaultFragmentSide, Layout layout = Layou
   g.n = n;
   g.f = f;
   g.layout = layout;
-  g.cells.assign(static_cast<std::size_t>(g.padded()) * g.padded(), 0);
+  detail::fresh_cells(g.cells, static_cast<std::size_t>(g.padded()) * g.padded());
   return g;
 }
+
+namespace detail {
+
+// A grid of `like`'s geometry and layout whose halo bytes are `like`'s and
+// whose interior is left zero for a device result to land in -- the output
+// of run_engine without copying a whole grid it is about to overwrite.
+inline Grid grid_like(const Grid& like) {
+  Grid g;
+  g.n = like.n;
+  g.f = like.f;
+  g.layout = like.layout;
+  g.halo_valid = like.halo_valid;
+  const std::size_t p = static_cast<std::size_t>(like.padded());
+  fresh_cells(g.cells, p * p);
+  if (like.layout == Layout::RowMajor) {
+    const std::size_t f = static_cast<std::size_t>(like.f), n = static_cast<std::size_t>(like.n);
+    for (std::size_t y = 0; y < p; ++y) {
+      const uint8_t* src = like.cells.data() + y * p;
+      uint8_t* dst = g.cells.data() + y * p;
+      if (y < f || y >= f + n) {
+        std::memcpy(dst, src, p);
+      } else {
+        std::memcpy(dst, src, f);
+        std::memcpy(dst + f + n, src + f + n, f);
+      }
+    }
+  } else {
+    g.cells = like.cells;
+  }
+  return g;
+}
+
+}  // namespace detail
 
 inline IntField make_field(int n, int f = kDefaultFragmentSide,
                            Layout layout = Layout::FragmentContiguous) {

@@ -16,6 +16,7 @@
 #include <sstream>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "host/internal.hpp"
@@ -600,15 +601,126 @@ size_t host_index(int32_t layout, int32_t f, int32_t p, int32_t y, int32_t x) {
 // copy), then the device scatters them into strips; downloads mirror that.
 // The other buffer's contents are dead at these points (the next step
 // rewrites its interior, and its pad bytes only ever meet zero band weights).
+// ---- host <-> device rows, pinned or pageable
+//
+// Pinned host memory (cudaHostAlloc / registered): one pitched DMA.  Pageable
+// memory (a std::vector, the reference's Grid::cells): staged through the
+// context's two 32 MB pinned chunks -- the rows of chunk k are packed by up to
+// 8 host threads while chunk k-1 is in flight -- instead of the driver's
+// single-threaded per-row staging of a pageable cudaMemcpy2D (16384^2
+// row-major upload: 24 ms, profiles/cpp_e2e_r02.txt).
+constexpr size_t kStageChunk = 32u << 20;
+
+void ensure_stage(ltl_ctx* ctx) {
+  if (ctx->pinned_bytes >= kStageChunk) return;
+  for (uint8_t*& p : ctx->pinned) {
+    if (p) cudaFreeHost(p);
+    p = nullptr;
+    ck(cudaMallocHost(&p, kStageChunk), "cudaMallocHost (staging chunk)");
+  }
+  ctx->pinned_bytes = kStageChunk;
+}
+
+bool host_pinned(const void* p) {
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost;
+}
+
+// fn(row) for rows [0, nrows) on up to 8 threads (inline for small copies)
+template <typename Fn>
+void parallel_rows(int64_t nrows, size_t row_bytes, Fn&& fn) {
+  const int64_t bytes = nrows * static_cast<int64_t>(row_bytes);
+  const int hw = static_cast<int>(std::max(1u, std::thread::hardware_concurrency()));
+  const int T = static_cast<int>(std::min<int64_t>({8, hw, std::max<int64_t>(1, bytes >> 22)}));
+  if (T <= 1) {
+    for (int64_t r = 0; r < nrows; ++r) fn(r);
+    return;
+  }
+  std::vector<std::thread> pool;
+  pool.reserve(T);
+  for (int t = 0; t < T; ++t)
+    pool.emplace_back([&, t] {
+      for (int64_t r = nrows * t / T; r < nrows * (t + 1) / T; ++r) fn(r);
+    });
+  for (std::thread& th : pool) th.join();
+}
+
+// `nrows` rows of `row_bytes` at host pitch `pitch` -> dense device rows.
+// Returns with the copies enqueued on `st` (pageable: completed up to the
+// last chunk's DMA, which the caller's stream sync covers).
+void h2d_rows(ltl_ctx* ctx, uint8_t* dev, const uint8_t* host, int64_t nrows, size_t row_bytes,
+              size_t pitch, cudaStream_t st) {
+  if (nrows <= 0 || row_bytes == 0) return;
+  if (host_pinned(host) || row_bytes > kStageChunk) {
+    ck(cudaMemcpy2DAsync(dev, row_bytes, host, pitch, row_bytes, nrows, cudaMemcpyHostToDevice, st),
+       "upload");
+    return;
+  }
+  ensure_stage(ctx);
+  const int64_t per = static_cast<int64_t>(kStageChunk / row_bytes);
+  cudaEvent_t ev[2];
+  for (auto& e : ev) ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+  for (int64_t r0 = 0, k = 0; r0 < nrows; r0 += per, ++k) {
+    const int64_t cnt = std::min(per, nrows - r0);
+    if (k >= 2) ck(cudaEventSynchronize(ev[k % 2]), "staging");  // chunk buffer free again
+    uint8_t* stage = ctx->pinned[k % 2];
+    parallel_rows(cnt, row_bytes, [&](int64_t r) {
+      std::memcpy(stage + r * row_bytes, host + (r0 + r) * pitch, row_bytes);
+    });
+    ck(cudaMemcpyAsync(dev + r0 * row_bytes, stage, cnt * row_bytes, cudaMemcpyHostToDevice, st),
+       "upload");
+    ck(cudaEventRecord(ev[k % 2], st), "event");
+  }
+  ck(cudaStreamSynchronize(st), "staging");
+  for (auto& e : ev) cudaEventDestroy(e);
+}
+
+// dense device rows -> `nrows` rows at host pitch (synchronous on return).
+void d2h_rows(ltl_ctx* ctx, uint8_t* host, const uint8_t* dev, int64_t nrows, size_t row_bytes,
+              size_t pitch, cudaStream_t st) {
+  if (nrows <= 0 || row_bytes == 0) return;
+  if (host_pinned(host) || row_bytes > kStageChunk) {
+    ck(cudaMemcpy2DAsync(host, pitch, dev, row_bytes, row_bytes, nrows, cudaMemcpyDeviceToHost, st),
+       "download");
+    ck(cudaStreamSynchronize(st), "download");
+    return;
+  }
+  ensure_stage(ctx);
+  const int64_t per = static_cast<int64_t>(kStageChunk / row_bytes);
+  const int64_t chunks = (nrows + per - 1) / per;
+  cudaEvent_t ev[2];
+  for (auto& e : ev) ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+  auto issue = [&](int64_t k) {
+    const int64_t r0 = k * per, cnt = std::min(per, nrows - r0);
+    ck(cudaMemcpyAsync(ctx->pinned[k % 2], dev + r0 * row_bytes, cnt * row_bytes,
+                       cudaMemcpyDeviceToHost, st),
+       "download");
+    ck(cudaEventRecord(ev[k % 2], st), "event");
+  };
+  issue(0);
+  for (int64_t k = 0; k < chunks; ++k) {
+    if (k + 1 < chunks) issue(k + 1);  // its buffer's unpack (chunk k-1) is done
+    ck(cudaEventSynchronize(ev[k % 2]), "staging");
+    const int64_t r0 = k * per, cnt = std::min(per, nrows - r0);
+    const uint8_t* stage = ctx->pinned[k % 2];
+    parallel_rows(cnt, row_bytes, [&](int64_t r) {
+      std::memcpy(host + (r0 + r) * pitch, stage + r * row_bytes, row_bytes);
+    });
+  }
+  for (auto& e : ev) cudaEventDestroy(e);
+}
+
 void upload_interior(ltl_ctx* ctx, const uint8_t* interior) {
   const int cur = ctx->cur;
   for (Slab& s : ctx->slabs) {
     ck(cudaSetDevice(s.dev), "cudaSetDevice");
     if (s.rows == 0 || ctx->cols == 0) continue;
-    const size_t n = static_cast<size_t>(s.rows) * ctx->cols;
-    ck(cudaMemcpyAsync(s.buf[1 - cur], interior + static_cast<size_t>(s.host_row0) * ctx->cols, n,
-                       cudaMemcpyHostToDevice, s.stream),
-       "upload");
+    h2d_rows(ctx, s.buf[1 - cur], interior + static_cast<size_t>(s.host_row0) * ctx->cols, s.rows,
+             ctx->cols, ctx->cols, s.stream);
     ck(ltl::launch_to_strips(s.buf[1 - cur], s.view(cur, ctx->cols), s.stream), "to_strips");
     ++ctx->launches;
     if (ctx->slabs.size() > 1) ck(cudaEventRecord(s.ev_step, s.stream), "event");
@@ -626,9 +738,8 @@ void download_interior(ltl_ctx* ctx, uint8_t* interior) {
     const size_t n = static_cast<size_t>(s.rows) * ctx->cols;
     ck(ltl::launch_from_strips(s.view(cur, ctx->cols), s.buf[1 - cur], s.stream), "from_strips");
     ++ctx->launches;
-    ck(cudaMemcpyAsync(interior + static_cast<size_t>(s.host_row0) * ctx->cols, s.buf[1 - cur], n,
-                       cudaMemcpyDeviceToHost, s.stream),
-       "download");
+    d2h_rows(ctx, interior + static_cast<size_t>(s.host_row0) * ctx->cols, s.buf[1 - cur],
+             static_cast<int64_t>(n / ctx->cols), ctx->cols, ctx->cols, s.stream);
   }
   sync_all(ctx);
 }
@@ -699,16 +810,13 @@ void upload_padded(ltl_ctx* ctx, const uint8_t* padded, int32_t layout) {
     if (s.rows == 0 || n == 0) continue;
     uint8_t* dense = s.buf[1 - cur];
     if (layout == LTL_LAYOUT_ROW_MAJOR) {
-      ck(cudaMemcpy2DAsync(dense, n, padded + (f + static_cast<size_t>(s.host_row0)) * p + f, p, n,
-                           s.rows, cudaMemcpyHostToDevice, s.stream),
-         "upload (pitched)");
+      h2d_rows(ctx, dense, padded + (f + static_cast<size_t>(s.host_row0)) * p + f, s.rows, n, p,
+               s.stream);
       ck(ltl::launch_to_strips(dense, s.view(cur, ctx->cols), s.stream), "to_strips");
     } else {
       const size_t frow = static_cast<size_t>(f) * p;  // bytes per fragment row
-      ck(cudaMemcpy2DAsync(dense, static_cast<size_t>(n) * f,
-                           padded + (s.host_row0 / f + 1) * frow + static_cast<size_t>(f) * f, frow,
-                           static_cast<size_t>(n) * f, s.rows / f, cudaMemcpyHostToDevice, s.stream),
-         "upload (pitched)");
+      h2d_rows(ctx, dense, padded + (s.host_row0 / f + 1) * frow + static_cast<size_t>(f) * f,
+               s.rows / f, static_cast<size_t>(n) * f, frow, s.stream);
       ck(ltl::launch_frag_relayout(dense, s.view(cur, ctx->cols), f, true, s.stream),
          "fragment to_strips");
     }
@@ -746,17 +854,14 @@ void download_padded(ltl_ctx* ctx, uint8_t* padded, int32_t layout, bool fill_ha
       uint8_t* dense = s.buf[1 - cur];
       if (layout == LTL_LAYOUT_ROW_MAJOR) {
         ck(ltl::launch_from_strips(s.view(cur, ctx->cols), dense, s.stream), "from_strips");
-        ck(cudaMemcpy2DAsync(padded + (f + static_cast<size_t>(s.host_row0)) * p + f, p, dense, n,
-                             n, s.rows, cudaMemcpyDeviceToHost, s.stream),
-           "download (pitched)");
+        d2h_rows(ctx, padded + (f + static_cast<size_t>(s.host_row0)) * p + f, dense, s.rows, n, p,
+                 s.stream);
       } else {
         ck(ltl::launch_frag_relayout(dense, s.view(cur, ctx->cols), f, false, s.stream),
            "fragment from_strips");
         const size_t frow = static_cast<size_t>(f) * p;
-        ck(cudaMemcpy2DAsync(padded + (s.host_row0 / f + 1) * frow + static_cast<size_t>(f) * f,
-                             frow, dense, static_cast<size_t>(n) * f, static_cast<size_t>(n) * f,
-                             s.rows / f, cudaMemcpyDeviceToHost, s.stream),
-           "download (pitched)");
+        d2h_rows(ctx, padded + (s.host_row0 / f + 1) * frow + static_cast<size_t>(f) * f, dense,
+                 s.rows / f, static_cast<size_t>(n) * f, frow, s.stream);
       }
       ++ctx->launches;
     }
@@ -1245,14 +1350,9 @@ namespace {
 
 constexpr size_t kSnapChunk = 32u << 20;  // bytes per pinned chunk
 
-void ensure_pinned(ltl_ctx* ctx) {
-  if (ctx->pinned_bytes >= kSnapChunk) return;
-  for (uint8_t*& p : ctx->pinned) {
-    if (p) cudaFreeHost(p);
-    p = nullptr;
-    ck(cudaMallocHost(&p, kSnapChunk), "cudaMallocHost (snapshot chunk)");
-  }
-  ctx->pinned_bytes = kSnapChunk;
+void ensure_pinned(ltl_ctx* ctx) {  // snapshot chunks = the staging chunks
+  static_assert(kSnapChunk == kStageChunk, "one pinned chunk size");
+  ensure_stage(ctx);
 }
 
 struct SnapHeader {
