@@ -362,33 +362,32 @@ __global__ void __launch_bounds__(kThreads)
   }
   const int nrows = max(0, min(kSeg, in.rows - (y0 + ys)));
   const bool full_word = x + 3 < in.cols;
-  uint8_t* optr = out.buf + out.offset(y0 + ys + kHalo, min(x, in.cols - 1));
-  // pointers stepped one row per output row: the H rows entering / leaving
-  // the window (Moore), the cell rows entering / leaving (VN), the centre
-  const uint32_t* h_in = hcol + (ys + 2 * R) * kHStride;
-  const uint32_t* h_mid = hcol + (ys + R) * kHStride;
-  const uint8_t* c_mid = ccol + (kHalo + ys) * kTileW;
-  for (int yy = 0; yy < nrows; ++yy, optr += kStrip, h_in += kHStride, h_mid += kHStride,
-           c_mid += kTileW) {
-    const int y = ys + yy;
+  uint8_t* const optr = out.buf + out.offset(y0 + ys + kHalo, min(x, in.cols - 1));
+  // row yy of the segment: the H rows entering / leaving the window (Moore),
+  // the cell rows entering / leaving (VN), the centre -- fixed offsets from
+  // these bases, so the unrolled full-segment loop addresses with immediates
+  const uint32_t* const h_in = hcol + (ys + 2 * R) * kHStride;
+  const uint32_t* const h_mid = hcol + (ys + R) * kHStride;
+  const uint8_t* const c_mid = ccol + (kHalo + ys) * kTileW;
+  auto row = [&](int yy) {
     if (yy > 0) {
       if (KIND == 0) {
         // R += H(y + r) - H(y - r - 1): a biased byte difference (31..97), widened
-        const uint32_t d = h_in[0] + 0x40404040u - h_in[-(2 * R + 1) * kHStride];
+        const uint32_t d = h_in[yy * kHStride] + 0x40404040u - h_in[(yy - 2 * R - 1) * kHStride];
         lo += widen_lo(d) - 0x00400040u;
         hi += widen_hi(d) - 0x00400040u;
       } else {
-        lo += *reinterpret_cast<const uint32_t*>(c_mid + R * kTileW) -
-              *reinterpret_cast<const uint32_t*>(c_mid - (R + 1) * kTileW);
+        lo += *reinterpret_cast<const uint32_t*>(c_mid + (yy + R) * kTileW) -
+              *reinterpret_cast<const uint32_t*>(c_mid + (yy - R - 1) * kTileW);
       }
     }
-    const uint32_t st = *reinterpret_cast<const uint32_t*>(c_mid);
+    const uint32_t st = *reinterpret_cast<const uint32_t*>(c_mid + yy * kTileW);
     uint32_t zl, zh;
     if (KIND == 0) {
       zl = lo + (widen_lo(st) << 11);
       zh = hi + (widen_hi(st) << 11);
     } else {  // R = H + V (centre twice), + 128 * state: all < 256 in byte lanes
-      const uint32_t zb = h_mid[0] + lo + (st << 7);
+      const uint32_t zb = h_mid[yy * kHStride] + lo + (st << 7);
       zl = widen_lo(zb);
       zh = widen_hi(zb);
     }
@@ -398,8 +397,14 @@ __global__ void __launch_bounds__(kThreads)
       max_r = __vmaxu2(max_r, zh & sr.r_mask & rmask_hi);
       bad |= (sr.negative(zl) & rmask_lo) | (sr.negative(zh) & rmask_hi);
     }
-    if (full_word) *reinterpret_cast<uint32_t*>(optr) = nw;
-    else if (x < in.cols) store_word(out, y0 + y, x, nw);
+    if (full_word) *reinterpret_cast<uint32_t*>(optr + yy * kStrip) = nw;
+    else if (x < in.cols) store_word(out, y0 + ys + yy, x, nw);
+  };
+  if (nrows == kSeg && full_word) {  // the common case: a whole segment, whole words
+#pragma unroll
+    for (int yy = 0; yy < kSeg; ++yy) row(yy);
+  } else {
+    for (int yy = 0; yy < nrows; ++yy) row(yy);
   }
   if constexpr (kChecked) flush_stats(stats, max_h, max_r, bad);
 }
