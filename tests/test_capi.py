@@ -112,3 +112,69 @@ def test_geometry_errors_before_device(lib):
         ltl.DeviceTorus(n=10)
     with pytest.raises(ValueError, match="config error: fragment side must be 4, 8, or 16"):
         ltl.DeviceTorus(n=12, f=6)
+
+
+@pytest.mark.parametrize("n,f", [(16, 16), (32, 4), (24, 8), (20, 4), (64, 16), (6, 2), (96, 32)])
+@pytest.mark.parametrize("layout", [0, 1])
+def test_host_fill_halo_matches_reference(lib, ref, orc, n, f, layout):
+    """ltl_host_fill_halo (the drop-in's fill_periodic_halo for host grids, any
+    f > 0) against the reference's own fill_periodic_halo, via the padded
+    grids the reference writes and the oracle's restatement."""
+    import ctypes
+
+    import numpy as np
+    interior = orc.init_random(n, 0.4, n + f)
+    p = n + 2 * f
+    rowmajor = np.zeros((p, p), np.uint8)
+    rowmajor[f:f + n, f:f + n] = interior
+    want = orc.fill_periodic_halo(rowmajor, n, f)
+    if layout == 0:
+        buf = rowmajor.copy()
+    else:  # fragment-contiguous order (grid.hpp:20-25)
+        idx = np.array([[((y // f) * (p // f) + x // f) * f * f + (y % f) * f + x % f
+                         for x in range(p)] for y in range(p)])
+        buf = np.zeros(p * p, np.uint8)
+        buf[idx.ravel()] = rowmajor.ravel()
+    st = lib.ltl_host_fill_halo(buf.ctypes.data_as(ctypes.POINTER(ctypes.c_uint8)), n, f, layout)
+    assert st == 0
+    got = buf if layout == 0 else buf[idx.ravel()].reshape(p, p)
+    assert np.array_equal(got.reshape(p, p), want)
+
+
+def test_host_fill_halo_errors(lib):
+    import ctypes
+
+    import numpy as np
+    buf = np.zeros(64, np.uint8)
+    ptr = buf.ctypes.data_as(ctypes.POINTER(ctypes.c_uint8))
+    assert lib.ltl_host_fill_halo(ptr, 6, 4, 0) == 1
+    assert b"must be a non-negative multiple of f" in lib.ltl_last_error(None)
+    assert lib.ltl_host_fill_halo(ptr, 4, 4, 7) == 1
+    assert b"layout error" in lib.ltl_last_error(None)
+
+
+@pytest.mark.parametrize("line,has,msg", [
+    ("", 0, "snapshot format error: missing header line"),
+    ("CATSNAP", 1, "snapshot format error: malformed header 'CATSNAP'"),
+    ("NOTSNAP 1 16 16 rowmajor", 1, "snapshot format error: bad magic 'NOTSNAP'"),
+    ("CATSNAP 2 16 16 rowmajor", 1, "snapshot format error: unsupported version 2"),
+    ("CATSNAP 1 16 16 diagonal", 1, "snapshot format error: unknown layout 'diagonal'"),
+    ("CATSNAP 1 16 16 rowmajor extra", 1, "snapshot format error: trailing tokens in header"),
+    ("CATSNAP 1 17 16 rowmajor", 1, "snapshot format error: bad geometry n=17 f=16"),
+])
+def test_snapshot_parse_header(lib, line, has, msg):
+    """ltl_snapshot_parse_header (the header checks the C++ stream reader and
+    the device reader share) -- messages of src/snapshot.cpp:39-66."""
+    import ctypes
+    n, f, lay = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32()
+    assert lib.ltl_snapshot_parse_header(line.encode(), has, ctypes.byref(n), ctypes.byref(f),
+                                         ctypes.byref(lay)) == 3
+    assert lib.ltl_last_error(None).decode() == msg
+
+
+def test_snapshot_parse_header_ok(lib):
+    import ctypes
+    n, f, lay = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32()
+    assert lib.ltl_snapshot_parse_header(b"CATSNAP 1 64 8 fragment", 1, ctypes.byref(n),
+                                         ctypes.byref(f), ctypes.byref(lay)) == 0
+    assert (n.value, f.value, lay.value) == (64, 8, 1)
