@@ -9,14 +9,11 @@
 # The binaries are git-ignored build products; they travel to the GPU box with
 # the gpurun snapshot (build/ is not gpurun-ignored), where
 # tests/test_ref_suites.py runs them.  Without $(REF) (the GPU box) nothing is
-# rebuilt.  The analytical cost model (catsim/cost_model.hpp) is out of scope
-# (SURVEY §2 row 8): test_cost_model is not built, and the acceptance gate is
-# compiled with the test-only stub tests/cpp/stub/catsim/cost_model.hpp, which
-# makes its criterion 2 (Table II) FAIL explicitly while criteria 1, 3-7 run.
+# rebuilt.
 REF ?= /root/reference/proj
 OUT ?= build/ref_suites
 CXX ?= g++
-SUITES := grid layout rule fragment cat_engine reference snapshot bench
+SUITES := grid layout rule fragment cat_engine reference snapshot bench cost_model
 EXTRA := $(OUT)/acceptance
 CXXFLAGS := -std=c++20 -O2 -Wall -Wextra -Itests/cpp/shim -Iinclude -I$(REF)/tests -pthread
 LDFLAGS := -Lpaper_2406_17284_b200 -lltl_b200 -Wl,-rpath,'$$ORIGIN/../../paper_2406_17284_b200'
@@ -27,9 +24,9 @@ all: $(SUITES:%=$(OUT)/test_%) $(EXTRA)
 $(OUT)/test_%: $(REF)/tests/test_%.cpp $(HDRS) paper_2406_17284_b200/libltl_b200.so
 	@mkdir -p $(OUT)
 	$(CXX) $(CXXFLAGS) $< -o $@ $(LDFLAGS)
-$(OUT)/acceptance: $(REF)/tests/acceptance.cpp $(HDRS) tests/cpp/stub/catsim/cost_model.hpp paper_2406_17284_b200/libltl_b200.so
+$(OUT)/acceptance: $(REF)/tests/acceptance.cpp $(HDRS) paper_2406_17284_b200/libltl_b200.so
 	@mkdir -p $(OUT)
-	$(CXX) $(CXXFLAGS) -Itests/cpp/stub $< -o $@ $(LDFLAGS)
+	$(CXX) $(CXXFLAGS) $< -o $@ $(LDFLAGS)
 else
 all:
 	@echo "reference tests not found under $(REF); using prebuilt $(OUT)/ if present"

@@ -91,9 +91,6 @@ def test_error_messages_are_the_references():
 @pytest.mark.parametrize("name,args,must_fail", REFERENCE_SMOKE, ids=[t[0] for t in REFERENCE_SMOKE])
 def test_reference_cli_smoke(name, args, must_fail):
     _gpu()
-    if name.startswith("cli_cost_model") and not os.path.exists(
-            os.path.join(ROOT, "include", "catsim", "cost_model.hpp")):
-        pytest.skip("the analytical cost model is out of scope (SURVEY.md §2 row 8)")
     res = run(args)
     if must_fail:
         assert res.returncode != 0, res.stdout
@@ -173,3 +170,31 @@ def test_bench_csv(tmp_path):
         f = r.split(",")
         assert f[1:5] == ["256", "8", "3", "3"]
         assert np.isclose(float(f[7]), 256 * 256 * 1000.0 / float(f[5]), rtol=1e-4)
+
+
+# ---- cost-model (pure host: runs on the CPU) -------------------------------
+def test_cost_model_table_cpu():
+    """catbench cost-model: the paper's Table II from the restated model."""
+    res = run(["cost-model", "--csv"])
+    assert res.returncode == 0, res.stderr
+    rows = [r.split(",") for r in res.stdout.strip().splitlines()]
+    assert rows[0] == ["scenario", "r=1", "r=4", "r=8", "r=16"]
+    published = {"GH100 Chip": [1.20, 8.07, 27.9, 104.0], "More TC Units": [1.59, 10.6, 37.1, 138.0],
+                 "Faster TC Units": [1.55, 10.4, 36.1, 134.0], "More FP Units": [0.60, 4.06, 14.1, 52.5],
+                 "Regular Tiles": [0.17, 1.15, 3.99, 14.8], "Expensive f()": [0.79, 1.17, 2.25, 6.44]}
+    assert [r[0] for r in rows[1:]] == list(published)
+    for r in rows[1:]:
+        for got, want in zip(map(float, r[1:]), published[r[0]]):
+            assert abs(got - want) <= 0.02 * want, (r[0], got, want)
+    text = run(["cost-model"]).stdout
+    assert "speedup limit vs per-cell reference" in text and "GH100 Chip" in text
+
+
+def test_cost_model_derive_cpu():
+    res = run(["cost-model", "--set", "w=16", "--set", "h=16", "--derive-e", "16", "14.8"])
+    assert res.returncode == 0, res.stderr
+    assert res.stdout.startswith("E=9.33700")
+    res = run(["cost-model", "--derive-e", "1", "100"])
+    assert res.returncode == 2 and "infeasible" in res.stderr
+    res = run(["cost-model", "--set", "bogus=1"])
+    assert res.returncode == 2 and "unknown parameter" in res.stderr
