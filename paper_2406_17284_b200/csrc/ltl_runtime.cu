@@ -616,7 +616,8 @@ void ensure_stage(ltl_ctx* ctx) {
   for (uint8_t*& p : ctx->pinned) {
     if (p) cudaFreeHost(p);
     p = nullptr;
-    ck(cudaMallocHost(&p, kStageChunk), "cudaMallocHost (staging chunk)");
+    // portable: slabs on several devices stage through the same chunks
+    ck(cudaHostAlloc(&p, kStageChunk, cudaHostAllocPortable), "cudaHostAlloc (staging chunk)");
   }
   ctx->pinned_bytes = kStageChunk;
 }
