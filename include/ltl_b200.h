@@ -140,13 +140,17 @@ int ltl_init_random(ltl_ctx* ctx, double density, uint64_t seed, int32_t fill_n)
 
 /* --- the hot path --------------------------------------------------------- */
 
-/* `steps` generations (simulate, src/cat_engine.cpp:308-321), each one fused
- * tcgen05 launch per slab + halo exchange.  Validation and messages as the
- * reference: steps < 0 -> "config error: steps must be >= 0"; rule checks of
- * src/rule.cpp:32-57; r > f -> "unsupported radius r=.. for fragment side
- * f=.." (src/fragment.cpp:25-27); negative count (fault injection) ->
- * LTL_ERR_LOGIC "internal consistency: negative neighborhood count".
- * stats may be NULL.  Synchronous. */
+/* `steps` generations (simulate, src/cat_engine.cpp:308-321): per slab one
+ * fused tcgen05 launch per generation, or ONE persistent cooperative launch
+ * for all of them on tori of <= 190 units (128 x 128 cells) per SM; the
+ * CUDA-core engines with LTL_FLAG_ENGINE_BASE / _PACK.  Validation and
+ * messages as the reference: steps < 0 -> "config error: steps must be >= 0";
+ * rule checks of src/rule.cpp:32-57; Cat: r > f -> "unsupported radius r=..
+ * for fragment side f=.." (src/fragment.cpp:25-27; Base / Pack: r <= 16 for
+ * any f); negative count (fault injection) -> LTL_ERR_LOGIC "internal
+ * consistency: negative neighborhood count <c>", c the count of the first
+ * failing cell in the reference's serial traversal.  stats may be NULL.
+ * Synchronous. */
 int ltl_run(ltl_ctx* ctx, const ltl_rule_c* rule, int32_t steps, uint32_t flags,
             ltl_stats_c* stats);
 
