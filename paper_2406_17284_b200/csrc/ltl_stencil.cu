@@ -33,10 +33,12 @@ namespace {
 
 constexpr int kThreads = 256;
 // Tile rows hold logical columns [-16, 144) of the strip (160 bytes) at a
-// 164-byte pitch: 41 words, odd, so the word k of 32 different (row, quarter)
-// pairs a warp reads in the pack engine's row pass fall in 32 different banks.
+// 176-byte pitch: 11 16-byte chunks, odd, so the 16-byte loads of 8
+// consecutive rows (the pack engine's row pass, one row per thread) fall in
+// 8 different bank groups, and every row is 16-byte aligned for 128-bit
+// shared loads / stores.
 constexpr int kTileCols = kStrip + 2 * kHalo;  // 160
-constexpr int kTileW = kTileCols + 4;          // row pitch in bytes
+constexpr int kTileW = kTileCols + 16;         // row pitch in bytes
 
 __device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
   uint32_t d;
@@ -121,11 +123,7 @@ __device__ __forceinline__ void load_tile(const SlabView& in, int strip, int y0,
                 : make_uint4(0, 0, 0, 0);
   }
   auto put = [&](int row, int col, const uint4& v) {
-    uint32_t* dst = reinterpret_cast<uint32_t*>(tile + row * kTileW + col);  // 4-byte aligned
-    dst[0] = v.x;
-    dst[1] = v.y;
-    dst[2] = v.z;
-    dst[3] = v.w;
+    *reinterpret_cast<uint4*>(tile + row * kTileW + col) = v;  // 16-byte aligned
   };
 #pragma unroll
   for (int u = 0; u < kPerMain; ++u) {
@@ -238,6 +236,20 @@ constexpr int kPackTY = 128;
 constexpr int kHW = kStrip;         // H tile row: the 128 output columns
 constexpr int kHStride = kHW / 4 + 1;  // 33 words: the row pass's stores hit 32 banks
 
+// kN words from a 16-byte aligned shared address, as 128-bit loads.
+template <int kN>
+__device__ __forceinline__ void load_words(const uint32_t* src, uint32_t (&w)[kN]) {
+  static_assert(kN % 4 == 0, "whole 16-byte loads");
+#pragma unroll
+  for (int k = 0; k < kN; k += 4) {
+    const uint4 v = reinterpret_cast<const uint4*>(src)[k / 4];
+    w[k] = v.x;
+    w[k + 1] = v.y;
+    w[k + 2] = v.z;
+    w[k + 3] = v.w;
+  }
+}
+
 // Horizontal window sums of one 32-column quarter of a tile row (output
 // columns 32q .. 32q+31 = tile columns 16 + 32q ..), written as bytes to
 // hrow[8q .. 8q+7]; returns their byte-lane max over valid columns.
@@ -247,11 +259,10 @@ __device__ __forceinline__ uint32_t row_window_sums(const uint32_t* trow, int q,
   uint32_t max_h = 0;
   if constexpr (R <= 2) {
     // direct: 2r+1 funnel-shifted words per four columns
-    constexpr int kW0 = (16 - R) >> 2;
-    constexpr int kNW = ((16 + 31 + R) >> 2) - kW0 + 2;
+    constexpr int kW0 = ((16 - R) >> 2) & ~3;             // first word, 16-byte aligned
+    constexpr int kNW = (((16 + 31 + R) >> 2) + 2 - kW0 + 3) & ~3;
     uint32_t w[kNW];
-#pragma unroll
-    for (int k = 0; k < kNW; ++k) w[k] = trow[8 * q + kW0 + k];
+    load_words<kNW>(trow + 8 * q + kW0, w);
 #pragma unroll
     for (int o = 0; o < 8; ++o) {
       uint32_t h = 0;
@@ -265,14 +276,16 @@ __device__ __forceinline__ uint32_t row_window_sums(const uint32_t* trow, int q,
   } else {
     // prefix sums in 16-bit lanes: P(k) = sum of tile columns [32q + kA, k];
     // H(x) = P(16 + x + r) - P(16 + x - r - 1)
-    constexpr int kA = (16 - R - 1) & ~3;             // first column (word aligned)
+    constexpr int kA = (16 - R - 1) & ~15;            // first column (16-byte aligned)
     constexpr int kEnd = 16 + 31 + R;                 // last column needed
-    constexpr int kNW = ((kEnd - kA) >> 2) + 1;       // words of cells
+    constexpr int kNW = ((((kEnd - kA) >> 2) + 1) + 3) & ~3;  // words of cells, whole uint4s
+    uint32_t cw[kNW];
+    load_words<kNW>(trow + 8 * q + (kA >> 2), cw);
     uint32_t pl[2 * kNW];                             // (P(2m), P(2m+1)), relative to kA
     uint32_t c = 0;
 #pragma unroll
     for (int k = 0; k < kNW; ++k) {
-      const uint32_t p = trow[8 * q + (kA >> 2) + k] * 0x01010101u;  // byte-lane prefix (<= 4)
+      const uint32_t p = cw[k] * 0x01010101u;        // byte-lane prefix (<= 4)
       const uint32_t cc = c * 0x10001u;
       pl[2 * k] = widen_lo(p) + cc;
       pl[2 * k + 1] = widen_hi(p) + cc;
@@ -301,16 +314,22 @@ template <int R, int KIND, bool kChecked>
 __global__ void __launch_bounds__(kThreads)
     pack_kernel(const SlabView in, const SlabView out, const RuleConsts rc, DeviceStats* stats) {
   constexpr int kRows = kPackTY + 2 * kHalo;
-  __shared__ __align__(16) uint8_t tile[kRows * kTileW];
-  __shared__ __align__(16) uint32_t htile[(kPackTY + 2 * R) * kHStride];  // H rows y0-r .. y0+TY+r
+  // dynamic: 16 bytes of front padding (at r = 16 the row pass of the first
+  // quarter starts its prefix one 16-byte chunk before column -16 of the row:
+  // garbage that cancels in every prefix difference, but it must be inside
+  // the allocation), the tile, the H rows y0-r .. y0+TY+r
+  extern __shared__ __align__(16) uint8_t pack_smem[];
+  uint8_t* const tile = pack_smem + 16;
+  uint32_t* const htile = reinterpret_cast<uint32_t*>(tile + kRows * kTileW);
   const int strip = blockIdx.x, y0 = blockIdx.y * kPackTY;
   load_tile<kPackTY>(in, strip, y0, tile);
   __syncthreads();
   const int x_strip = strip * kStrip;
   uint32_t max_h = 0, max_r = 0, bad = 0;
   // ---- phase 1: horizontal window sums H of tile rows 16-r .. 16+TY+r-1
-  for (int item = threadIdx.x; item < (kPackTY + 2 * R) * 4; item += kThreads) {
-    const int hr = item >> 2, q = item & 3;
+  constexpr int kHRows = kPackTY + 2 * R;
+  for (int item = threadIdx.x; item < kHRows * 4; item += kThreads) {
+    const int q = item / kHRows, hr = item % kHRows;  // a warp: consecutive rows, one quarter
     const int trow = kHalo - R + hr;  // tile row
     const int y = y0 + trow - kHalo;  // interior row
     int vw = 0;                       // valid words of this quarter (checked stats)
@@ -410,14 +429,39 @@ __global__ void __launch_bounds__(kThreads)
 }
 
 template <int R>
+constexpr size_t pack_smem_bytes() {
+  return 16 + static_cast<size_t>(kPackTY + 2 * kHalo) * kTileW +
+         static_cast<size_t>(kPackTY + 2 * R) * kHStride * sizeof(uint32_t);
+}
+
+template <int R>
 cudaError_t launch_r(const SlabView& in, const SlabView& out, const RuleConsts& rc, int engine,
                      DeviceStats* stats, cudaStream_t stream) {
   const int strips = interior_strips(in.cols);
   const int ty = engine == kEnginePack ? kPackTY : kBaseTY;
   const dim3 grid(strips, (in.rows + ty - 1) / ty);
-#define LTL_STENCIL_LAUNCH(KERNEL, KIND)                                                 \
-  (stats ? KERNEL<R, KIND, true><<<grid, kThreads, 0, stream>>>(in, out, rc, stats)      \
-         : KERNEL<R, KIND, false><<<grid, kThreads, 0, stream>>>(in, out, rc, nullptr))
+  const size_t smem = engine == kEnginePack ? pack_smem_bytes<R>() : 0;
+  if (smem > 48 * 1024) {
+    // the attribute is per device: set once on each (a per-launch call
+    // serialises launches measurably)
+    static bool done[64] = {};
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
+    if (!done[dev]) {
+      for (auto fn : {pack_kernel<R, 0, true>, pack_kernel<R, 0, false>, pack_kernel<R, 1, true>,
+                      pack_kernel<R, 1, false>}) {
+        e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(smem));
+        if (e != cudaSuccess) return e;
+      }
+      done[dev] = true;
+    }
+  }
+#define LTL_STENCIL_LAUNCH(KERNEL, KIND)                                                   \
+  (stats ? KERNEL<R, KIND, true><<<grid, kThreads, smem, stream>>>(in, out, rc, stats)     \
+         : KERNEL<R, KIND, false><<<grid, kThreads, smem, stream>>>(in, out, rc, nullptr))
   if (engine == kEnginePack) {
     if (rc.kind == 0) LTL_STENCIL_LAUNCH(pack_kernel, 0);
     else LTL_STENCIL_LAUNCH(pack_kernel, 1);
