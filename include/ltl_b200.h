@@ -57,6 +57,15 @@ extern "C" {
 #define LTL_FLAG_ENGINE_BASE 0x4u
 #define LTL_FLAG_ENGINE_PACK 0x10u
 #define LTL_FLAG_STENCIL LTL_FLAG_ENGINE_BASE /* round-1 name */
+/* Extension beyond the reference (which rejects r > 16, src/rule.cpp:33-35):
+ * the Cat engine with 17 <= r <= 32 ("+16 expansion": 32-row
+ * boxes, four pass-2 band chunks), any fragment side f.  Needs every wrap
+ * done by the step's loads: cols % 128 == 0 and, per slab, rows % 32 == 0
+ * (one whole-torus slab, or a ring of slabs with the fused exchange);
+ * otherwise "unsupported radius r=.. : r > 16 needs ...".  Rules come from
+ * ltl_parse_rule_ext(text, 32, ...). */
+#define LTL_FLAG_WIDE_RADIUS 0x20u
+#define LTL_MAX_WIDE_RADIUS 32
 
 /* catsim::LtlRule, proj/include/catsim/rule.hpp:17-32 */
 typedef struct ltl_rule_c {
@@ -281,6 +290,10 @@ int ltl_fragment_pass(int32_t stage, int32_t n, int32_t f, const uint8_t* cells,
 /* parse_ltl_rule (src/rule.cpp:61-87): returns LTL_OK or
  * LTL_ERR_INVALID_ARGUMENT with the reference's message in err (may be NULL). */
 int ltl_parse_rule(const char* text, ltl_rule_c* out, char* err, int32_t err_len);
+/* Extension: the same grammar, messages and checks with radii 1..max_radius
+ * (max_radius <= LTL_MAX_WIDE_RADIUS; ltl_parse_rule = max_radius 16). */
+int ltl_parse_rule_ext(const char* text, int32_t max_radius, ltl_rule_c* out, char* err,
+                       int32_t err_len);
 /* format_ltl_rule (src/rule.cpp:89-97); returns the string length. */
 int32_t ltl_format_rule(const ltl_rule_c* rule, char* buf, int32_t buf_len);
 /* ltl_presets (src/rule.cpp:113-133): count, then entries by index. */

@@ -157,6 +157,7 @@ class Reference:
                                            ctypes.c_char_p]
         lib.ref_snapshot_read.argtypes = [ctypes.c_char_p, _i32p, _i32p, _i32p, _u8p,
                                           ctypes.c_int64]
+        lib.ref_semantic_steps.argtypes = [ctypes.c_int32, _u8p, _i32p, ctypes.c_int32, _u8p]
         self.lib = lib
 
     def _check(self, status: int):
@@ -237,6 +238,16 @@ class Reference:
         self._check(self.lib.ref_reductions(n, f, _ptr(g, _u8p), rule_text.encode(),
                                             _ptr(h, _i32p), _ptr(red, _i32p)))
         return h, red
+
+    def semantic_steps(self, grid: np.ndarray, rule_ints, steps: int) -> np.ndarray:
+        """tests/oracle.hpp torus_rule_steps: the reference's brute-force
+        semantic oracle, any radius (no rule validation -- defines r > 16)."""
+        g = np.ascontiguousarray(grid, np.uint8)
+        out = np.empty_like(g)
+        r8 = np.ascontiguousarray(rule_ints, np.int32)
+        self._check(self.lib.ref_semantic_steps(g.shape[0], _ptr(g, _u8p), _ptr(r8, _i32p), steps,
+                                                _ptr(out, _u8p)))
+        return out
 
     def snapshot_write(self, grid: np.ndarray, path: str, f: int = 16, layout: int = 0) -> None:
         """catsim::snapshot_write of a row-major interior, as layout 0 / 1."""

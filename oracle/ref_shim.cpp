@@ -25,6 +25,7 @@
 #include "catsim/layout.hpp"
 #include "catsim/rule.hpp"
 #include "catsim/snapshot.hpp"
+#include "tests/oracle.hpp"  // the reference's brute-force torus oracle (header, -I$(REF))
 
 namespace {
 
@@ -208,6 +209,31 @@ int ref_reductions(int32_t n, int32_t f, const uint8_t* interior_in,
         h_out[static_cast<std::size_t>(y) * p + x] = h.at(y, x);
         r_out[static_cast<std::size_t>(y) * p + x] = red.at(y, x);
       }
+  });
+}
+
+// The reference's own brute-force semantic oracle (tests/oracle.hpp:50-68,
+// torus_rule_steps: explicit modular wrap, counts re-derived from the rule
+// semantics).  It takes the LtlRule struct as given -- no parse_ltl_rule
+// validation -- so it also defines the wide-radius extension (17 <= r <= 32)
+// that the reference's engines reject.  rule8 = {r, c, m, s1, s2, b1, b2, kind}.
+int ref_semantic_steps(int32_t n, const uint8_t* interior_in, const int32_t* rule8,
+                       int32_t steps, uint8_t* interior_out) {
+  return guarded([&] {
+    catsim::LtlRule rule;
+    rule.r = rule8[0];
+    rule.c = rule8[1];
+    rule.m = rule8[2];
+    rule.s1 = rule8[3];
+    rule.s2 = rule8[4];
+    rule.b1 = rule8[5];
+    rule.b2 = rule8[6];
+    rule.kind = rule8[7] ? catsim::NeighborhoodKind::VonNeumannSimplified
+                         : catsim::NeighborhoodKind::Moore;
+    const catsim::Grid out = oracle::torus_rule_steps(grid_from_interior(n, 16, interior_in), rule, steps);
+    for (int y = 0; y < n; ++y)
+      for (int x = 0; x < n; ++x)
+        interior_out[static_cast<std::size_t>(y) * n + x] = out.interior(y, x);
   });
 }
 

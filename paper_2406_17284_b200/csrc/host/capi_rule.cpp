@@ -10,9 +10,14 @@
 extern "C" {
 
 int ltl_parse_rule(const char* text, ltl_rule_c* out, char* err, int32_t err_len) {
+  return ltl_parse_rule_ext(text, catsim::kMaxRadius, out, err, err_len);
+}
+
+int ltl_parse_rule_ext(const char* text, int32_t max_radius, ltl_rule_c* out, char* err,
+                       int32_t err_len) {
   try {
     if (!text || !out) throw std::invalid_argument("rule parse error: field R: null input");
-    *out = catsim::to_c(catsim::parse_ltl_rule(text));
+    *out = catsim::to_c(catsim::parse_ltl_rule(text, max_radius));
     if (err && err_len > 0) err[0] = '\0';
     return LTL_OK;
   } catch (const std::exception& e) {

@@ -8,8 +8,8 @@
 namespace catsim {
 
 // The reference's rule validation (src/rule.cpp:32-57), throwing the same
-// std::invalid_argument messages.
-void validate_rule(const LtlRule& rule);
+// std::invalid_argument messages; max_radius > 16 is the wide-radius extension.
+void validate_rule(const LtlRule& rule, int max_radius = kMaxRadius);
 
 inline LtlRule from_c(const ltl_rule_c& c) {
   LtlRule r;

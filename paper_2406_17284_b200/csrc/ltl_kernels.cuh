@@ -106,9 +106,11 @@ __host__ __device__ inline bool tc_wrap_cols(int32_t cols) {
 __host__ __device__ inline bool tc_wrap_rows(int32_t rows) {
   return rows >= 32 && rows % 32 == 0;
 }
-// load maps: [0] whole boxes, [1] 16-row wrap pieces, [2] band-0 bodies
-// (kTcBox - 16 rows), [3] last-band bodies (rows of the last band + 16)
+// load maps for boxes carrying kH = 16 (r <= 16) or 32 (17 <= r <= 32) halo
+// rows: [0] whole (128 + 2 kH)-row boxes, [1] kH-row wrap pieces, [2] band-0
+// bodies (128 + kH rows), [3] last-band bodies (rows of the last band + kH)
 constexpr int kTcLoadMaps = 4;
+constexpr int kTcMaxRadius = 32;  // the kH = 32 boxes (PAPER.md:561's "+16 expansion")
 struct TcLaunch {
   const CUtensorMap* load_maps;  // kTcLoadMaps maps over the source slab, SWIZZLE_128B
   const CUtensorMap* store_map;  // destination interior rows, {128, 64, 1} boxes, SWIZZLE_128B
@@ -150,19 +152,21 @@ struct TcLaunch {
   int32_t gen_base;         // generation number of this launch's first generation
   int32_t row0;             // global row of local row 0 (reference traversal order)
   DeviceStats* stats;  // nullptr -> no stats reduction
+  int32_t halo;        // box halo rows kH: 16 (0 = default) or 32 (r > 16; every wrap by
+                       // the loads: wrap_cols and wrap_rows or ring; maps built for 32)
   int32_t grid;        // CTAs (0 = auto)
   long long* trace;    // debug timeline (LTL_TC_TRACE), nullptr = off
 };
 cudaError_t launch_tc_step(const TcLaunch& a, cudaStream_t stream);
 int tc_persistent_ctas(int32_t rows, int32_t cols, int num_sms);  // 0: no multi-generation launch
 int tc_sweep_chunks(int32_t strips, int32_t bands, int ctas);  // chunks per band of a multi-generation launch
-size_t tc_smem_bytes();
+size_t tc_smem_bytes(int halo);
 
 // Host-side tensor-map builders (driver entry point fetched at runtime).
-cudaError_t make_load_maps(CUtensorMap* maps, const SlabView& s);
+cudaError_t make_load_maps(CUtensorMap* maps, const SlabView& s, int halo = kHalo);
 cudaError_t make_store_map(CUtensorMap* map, const SlabView& s);
-// 16-row SWIZZLE_128B pieces over a slab (the ring's rows from a neighbour).
-cudaError_t make_piece_map(CUtensorMap* map, const SlabView& s);
+// halo-row (16 / 32) SWIZZLE_128B pieces over a slab (the ring's rows from a neighbour).
+cudaError_t make_piece_map(CUtensorMap* map, const SlabView& s, int halo = kHalo);
 
 // ---- CUDA-core stencil ablations (ltl_stencil.cu): kEngineBase sums the
 // (2r+1)^2 box / 2(2r+1) cross per cell (the paper's SHARED baseline),

@@ -46,6 +46,7 @@ struct Slab {
   int32_t strips = 0;
   uint8_t* buf[2] = {nullptr, nullptr};
   CUtensorMap load_maps[2][ltl::kTcLoadMaps];
+  CUtensorMap load_maps_w[2][ltl::kTcLoadMaps];  // 32-row-halo boxes (r > 16)
   CUtensorMap store_map[2];
   ltl::DeviceStats* dstats = nullptr;
   uint32_t* flags = nullptr;   // per-unit completion counters (multi-generation launches)
@@ -59,6 +60,7 @@ struct Slab {
   // completion counters (peer-accessible here: same device, P2P, CUDA IPC).
   uint32_t* ring_sync = nullptr;              // [0] steps completed, [1] CTA ticket
   CUtensorMap ring_up_map[2], ring_down_map[2];  // per generation buffer
+  CUtensorMap ring_up_map_w[2], ring_down_map_w[2];  // 32-row pieces (r > 16)
   const uint32_t* up_done = nullptr;
   const uint32_t* down_done = nullptr;
   int32_t up_rows = 0, down_rows = 0;
@@ -137,22 +139,49 @@ bool stencil_engine(uint32_t flags) {
   return (flags & (LTL_FLAG_ENGINE_BASE | LTL_FLAG_ENGINE_PACK)) != 0;
 }
 
+bool wrap_cols(const ltl_ctx* ctx);
+bool wrap_rows(const ltl_ctx* ctx);
+bool ring_ok(const ltl_ctx* ctx);
+
+// The wide-radius extension (LTL_FLAG_WIDE_RADIUS, 17 <= r <= 32): 32-row
+// boxes whose every wrap is loaded by the step itself (the slabs' 16-row HBM
+// halo cannot hold 32 rows / columns).
+bool wide_geometry_ok(const ltl_ctx* ctx) {
+  if (!wrap_cols(ctx)) return false;
+  if (wrap_rows(ctx)) return true;
+  if (!ring_ok(ctx)) return false;
+  for (const Slab& s : ctx->slabs)
+    if (s.up_rows < 2 * kHalo || s.down_rows < 2 * kHalo) return false;
+  return true;
+}
+
 void check_run_args(const ltl_ctx* ctx, const ltl_rule_c* rule, int32_t steps,
                     uint32_t flags = 0) {
   if (!rule) throw std::invalid_argument("config error: rule is null");
   if (steps < 0) throw std::invalid_argument("config error: steps must be >= 0");
-  catsim::validate_rule(catsim::from_c(*rule));
+  const bool wide = (flags & LTL_FLAG_WIDE_RADIUS) && !stencil_engine(flags);
+  catsim::validate_rule(catsim::from_c(*rule), wide ? catsim::kMaxWideRadius : catsim::kMaxRadius);
   // the CAT engine's band fragments need r <= f (src/fragment.cpp:25-27); the
-  // stencil engines only need the device's 16-cell halo
-  const int32_t limit = stencil_engine(flags) ? kHalo : std::min<int32_t>(ctx->f, kHalo);
+  // stencil engines only need the device's 16-cell halo; the wide extension
+  // has its own 32-row boxes
+  const int32_t limit = stencil_engine(flags) ? kHalo
+                        : wide                ? ltl::kTcMaxRadius
+                                              : std::min<int32_t>(ctx->f, kHalo);
   if (rule->r < 1 || rule->r > limit)
     throw std::invalid_argument("unsupported radius r=" + std::to_string(rule->r) +
                                 " for fragment side f=" + std::to_string(ctx->f));
+  if (rule->r > kHalo && !wide_geometry_ok(ctx))
+    throw std::invalid_argument(
+        "unsupported radius r=" + std::to_string(rule->r) +
+        ": r > 16 needs cols % 128 == 0 and slabs of rows % 32 == 0 (>= 32) whose row wrap the "
+        "step loads (one whole-torus slab or a ring)");
 }
 
 void build_maps(Slab& s, int32_t cols) {
   for (int i = 0; i < 2; ++i) {
     ck(ltl::make_load_maps(s.load_maps[i], s.view(i, cols)), "tensor map (load)");
+    if (s.rows >= 2 * kHalo)  // the wide boxes' 32-row pieces need 32 rows
+      ck(ltl::make_load_maps(s.load_maps_w[i], s.view(i, cols), 2 * kHalo), "tensor map (load)");
     ck(ltl::make_store_map(&s.store_map[i], s.view(i, cols)), "tensor map (store)");
   }
 }
@@ -181,6 +210,10 @@ void wire_ring(ltl_ctx* ctx, Slab& s, const RingPeer& upp, const RingPeer& dnp) 
                            static_cast<int64_t>(dn_rows + 2 * kHalo) * ltl::kStrip};
     ck(ltl::make_piece_map(&s.ring_up_map[b], up), "tensor map (ring up)");
     ck(ltl::make_piece_map(&s.ring_down_map[b], dn), "tensor map (ring down)");
+    if (up_rows >= 2 * kHalo && dn_rows >= 2 * kHalo) {
+      ck(ltl::make_piece_map(&s.ring_up_map_w[b], up, 2 * kHalo), "tensor map (ring up)");
+      ck(ltl::make_piece_map(&s.ring_down_map_w[b], dn, 2 * kHalo), "tensor map (ring down)");
+    }
   }
   s.up_done = up_sync;
   s.down_done = dn_sync;
@@ -453,7 +486,10 @@ void enqueue_step(ltl_ctx* ctx, const ltl::RuleConsts& rc, uint32_t flags, bool 
     } else {
       ltl::TcLaunch a{};
       CUtensorMap ring_up2[2], ring_down2[2];  // the neighbours' buffers of gen 0, 1
-      a.load_maps = s.load_maps[cur];
+      // r > 16 (the wide extension, validated by check_run_args): 32-row boxes
+      const bool wide = rc.r > kHalo;
+      a.halo = wide ? 2 * kHalo : kHalo;
+      a.load_maps = wide ? s.load_maps_w[cur] : s.load_maps[cur];
       a.store_map = &s.store_map[nxt];
       a.wrap_cols = wrap_cols(ctx);
       a.wrap_rows = wrap_rows(ctx);
@@ -462,10 +498,10 @@ void enqueue_step(ltl_ctx* ctx, const ltl::RuleConsts& rc, uint32_t flags, bool 
         a.ring_gen = s.ring_gen;
         s.ring_gen += persist ? static_cast<uint32_t>(gens) : 1u;
         a.up_rows = s.up_rows;
-        ring_up2[0] = s.ring_up_map[cur];
-        ring_up2[1] = s.ring_up_map[nxt];
-        ring_down2[0] = s.ring_down_map[cur];
-        ring_down2[1] = s.ring_down_map[nxt];
+        ring_up2[0] = wide ? s.ring_up_map_w[cur] : s.ring_up_map[cur];
+        ring_up2[1] = wide ? s.ring_up_map_w[nxt] : s.ring_up_map[nxt];
+        ring_down2[0] = wide ? s.ring_down_map_w[cur] : s.ring_down_map[cur];
+        ring_down2[1] = wide ? s.ring_down_map_w[nxt] : s.ring_down_map[nxt];
         a.ring_up = ring_up2;
         a.ring_down = ring_down2;
         a.up_flags = s.up_unit_flags;
@@ -476,7 +512,7 @@ void enqueue_step(ltl_ctx* ctx, const ltl::RuleConsts& rc, uint32_t flags, bool 
         a.my_ticket = s.ring_sync + 1;
       }
       if (persist) {
-        a.load_maps_b = s.load_maps[nxt];
+        a.load_maps_b = wide ? s.load_maps_w[nxt] : s.load_maps[nxt];
         a.store_map_b = &s.store_map[cur];
         a.gens = gens;
         a.flags = s.flags;
@@ -576,10 +612,12 @@ void run_steps(ltl_ctx* ctx, const ltl_rule_c* rule, int32_t steps, uint32_t fla
   if (stats) {
     // CAT-fragment accounting (cat_engine.cpp:151-155, :198-202): 3 MMAs per
     // fragment of the H pass (all fragment rows, interior columns) and 3 per
-    // interior fragment of the R pass, per step.
+    // interior fragment of the R pass, per step.  Wide radii (r > f, the
+    // extension): 2 ceil(r / f) + 1 band fragments per pass.
     const int64_t fpr = (ctx->cols + 2LL * ctx->f) / ctx->f;
+    const int64_t nbf = 2 * ((rule->r + ctx->f - 1) / ctx->f) + 1;
     const int64_t per_step = ctx->rows == ctx->cols && ctx->rows > 0
-                                 ? 3 * fpr * (fpr - 2) + 3 * (fpr - 2) * (fpr - 2)
+                                 ? nbf * fpr * (fpr - 2) + nbf * (fpr - 2) * (fpr - 2)
                                  : 0;
     stats->mma_count += per_step * steps;
     stats->steps += steps;

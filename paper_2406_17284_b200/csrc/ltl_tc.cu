@@ -79,12 +79,9 @@ namespace {
 using namespace ptx;
 
 constexpr int kBand = kTcBand;            // 128 output rows per unit
-constexpr int kBox = kTcBox;              // 160 box rows (one TMA box)
 constexpr int kSub = 64;                  // pass-2 N: output rows per sub-block
 constexpr int kSubs = kBand / kSub;       // 2
-constexpr int kKChunks = 6;               // pass-1 K = 192 columns [-32, 160)
-constexpr int kXStages = 8;               // 3 boxes in use + 5 prefetched
-constexpr uint32_t kBoxBytes = kBox * kStrip;  // 20 KB
+constexpr int kKChunks = 6;               // pass-1 K = 192 columns [-32, 160): r <= 32
 constexpr int kSlots = 2;                 // D1 / plane slots (units in flight)
 constexpr int kConvWarps = 4;
 constexpr int kOutWarps = 8;
@@ -94,44 +91,64 @@ constexpr int kGroupThreads = 128;  // one output group
 constexpr int kWarpOut0 = 2 + kConvWarps;
 constexpr int kWarpP2 = kWarpOut0 + kOutWarps;  // 14
 constexpr int kWarpStore = kWarpP2 + 1;           // 15
-constexpr int kNumTiles = 7;  // Bv0..2, Iv0..1, 16Iv0..1
-
-static_assert(kBox % 32 == 0 && kBox <= 256, "box rows: whole K chunks, one TMA box");
+constexpr uint32_t kTileBytes = kSub * 32;        // 2 KB pass-2 B tile [64 n][32 k]
+constexpr uint32_t kStageBytes = kSub * kStrip;   // 64 x 128 B = 8 KB output staging tile
+constexpr uint32_t kTmemCols = 512;               // all of the SM's TMEM
 static_assert(kSubs == 2, "one output group per sub-block");
 
-// Shared-memory carve-up (offsets from a 1024-aligned base).
-constexpr uint32_t kSmemX = 0;                                        // 8 x 20 KB
-constexpr uint32_t kSmemBand = kSmemX + kXStages * kBoxBytes;         // 7 x [64][32]
-constexpr uint32_t kTileBytes = kSub * 32;                            // 2 KB
-constexpr int kStageSlots = 3;                                        // per output group
-constexpr uint32_t kStageBytes = kSub * kStrip;                       // 64 x 128 B = 8 KB
-constexpr uint32_t kSmemStage = kSmemBand + kNumTiles * kTileBytes;   // 2 x 3 x 8 KB
-constexpr uint32_t kSmemBars = kSmemStage + kSubs * kStageSlots * kStageBytes;
-constexpr uint32_t kNumBars = 2 * kXStages + 3 * kSlots + 2 * kSubs + 2 * kSubs * kStageSlots;
-constexpr uint32_t kSmemTotal = kSmemBars + kNumBars * 8 + 16;
-constexpr uint32_t kSmemAlloc = kSmemTotal + 1024;  // alignment slack
-static_assert(kSmemAlloc <= 227 * 1024, "shared memory budget");
+// Geometry of one kernel variant, by the halo rows kH its boxes carry:
+//   kH = 16  r <= 16 (the reference's range, src/rule.cpp:33-35): 160-row
+//            boxes, the product configuration;
+//   kH = 32  17 <= r <= 32, the paper's "+16 expansion" (a
+//            radius range the reference rejects): 192-row boxes, four pass-2
+//            band chunks, one D2 buffer shared by the two output groups
+//            (TMEM), 7 box stages and 2 staging slots per group (SMEM).
+// The pass-1 K range [-32, 160) already covers a horizontal radius of 32.
+template <int kH>
+struct Geo {
+  static_assert(kH == 16 || kH == 32, "halo rows");
+  static constexpr int kBox = kBand + 2 * kH;              // 160 / 192 box rows (one TMA box)
+  static constexpr int kRowOff = kHalo - kH;               // padded row of box row 0, minus 128 b
+  static constexpr int kBandChunks = (kSub + 2 * kH) / 32;  // pass-2 band K chunks: 3 / 4
+  static constexpr int kNumTiles = kBandChunks + 4;         // + Iv0..1, W*Iv0..1
+  static constexpr int kXStages = kH == 16 ? 8 : 7;         // 3 boxes in use + prefetched
+  static constexpr int kStageSlots = kH == 16 ? 3 : 2;      // staging tiles per output group
+  static constexpr int kD2Bufs = kH == 16 ? 2 : 1;          // D2 buffers (64 columns each)
+  // centre weight W of pass 2 (Moore: Z = R + 128 W state must clear R <= (2r+1)^2)
+  static constexpr uint32_t kCentreW = kH == 16 ? 16u : 64u;   // K = 2048 / 8192
+  static constexpr uint32_t kVnK = kH == 16 ? 128u : 256u;     // VN: R <= 2(2r+1)
+  static constexpr uint32_t kBoxBytes = kBox * kStrip;      // 20 / 24 KB
+  static_assert(kBox % 32 == 0 && kBox <= 256, "box rows: whole K chunks, one TMA box");
 
-// TMEM columns (all 512 of the SM are allocated).
-constexpr uint32_t kTmemCols = 512;
-constexpr uint32_t kPbCols = kBox / 4;          // 40: one byte per box row
-constexpr uint32_t kPiCols = kBand / 4;         // 32: one byte per centre row
-// A slot first holds D1 (160 s32 columns); once the convert warps have read it
-// into registers they write the two byte planes over its first 72 columns,
-// which pass 2 reads.  Two slots: pass 1 of unit h+1 runs while unit h is
-// converted and reduced.
-constexpr uint32_t kSlotCols = kBox;            // 160
-constexpr uint32_t kTmemSlot = 0;               // 2 x 160
-constexpr uint32_t kPbOff = 0;                  // Pb: 40 columns
-constexpr uint32_t kPiOff = kPbCols;            // Pi: 32 columns
-constexpr uint32_t kTmemD2 = kTmemSlot + kSlots * kSlotCols;  // 2 x 64
-constexpr uint32_t kTmemA1 = kTmemD2 + kSubs * kSub;          // pass-1 A: 192 k / 4 = 48
-static_assert(kPiOff + kPiCols <= kSlotCols, "planes fit in the D1 slot");
-static_assert(kTmemA1 + kKChunks * 8 <= kTmemCols, "TMEM budget");
-static_assert(kSlotCols % 8 == 0 && kPiOff % 8 == 0 && kTmemD2 % 8 == 0, "A operand alignment");
+  // Shared-memory carve-up (offsets from a 1024-aligned base).
+  static constexpr uint32_t kSmemX = 0;
+  static constexpr uint32_t kSmemBand = kSmemX + kXStages * kBoxBytes;
+  static constexpr uint32_t kSmemStage = kSmemBand + kNumTiles * kTileBytes;
+  static constexpr uint32_t kSmemBars = kSmemStage + kSubs * kStageSlots * kStageBytes;
+  static constexpr uint32_t kNumBars = 2 * kXStages + 3 * kSlots + 2 * kSubs + 2 * kSubs * kStageSlots;
+  static constexpr uint32_t kSmemTotal = kSmemBars + kNumBars * 8 + 16;
+  static constexpr uint32_t kSmemAlloc = kSmemTotal + 1024;  // alignment slack
+  static_assert(kSmemAlloc <= 227 * 1024, "shared memory budget");
 
-constexpr uint32_t kIdesc1 = idesc_i8_u8u8_s32(128, kBox);
-constexpr uint32_t kIdesc2 = idesc_i8_u8u8_s32(128, kSub);
+  // TMEM columns.  A slot first holds D1 (kBox s32 columns); once the convert
+  // warps have read it into registers they write the two byte planes over its
+  // first columns, which pass 2 reads.  Two slots: pass 1 of unit h+1 runs
+  // while unit h is converted and reduced.
+  static constexpr uint32_t kPbCols = kBox / 4;    // one byte per box row
+  static constexpr uint32_t kPiCols = kBand / 4;   // 32: one byte per centre row
+  static constexpr uint32_t kSlotCols = kBox;
+  static constexpr uint32_t kTmemSlot = 0;
+  static constexpr uint32_t kPbOff = 0;
+  static constexpr uint32_t kPiOff = kPbCols;
+  static constexpr uint32_t kTmemD2 = kTmemSlot + kSlots * kSlotCols;
+  static constexpr uint32_t kTmemA1 = kTmemD2 + kD2Bufs * kSub;  // pass-1 A: 192 k / 4 = 48
+  static_assert(kPiOff + kPiCols <= kSlotCols, "planes fit in the D1 slot");
+  static_assert(kTmemA1 + kKChunks * 8 <= kTmemCols, "TMEM budget");
+  static_assert(kSlotCols % 8 == 0 && kPiOff % 8 == 0 && kTmemD2 % 8 == 0, "A operand alignment");
+
+  static constexpr uint32_t kIdesc1 = idesc_i8_u8u8_s32(128, kBox);
+  static constexpr uint32_t kIdesc2 = idesc_i8_u8u8_s32(128, kSub);
+};
 
 // Tensor maps of both generation buffers: set 0 = {loads of the launch's
 // current buffer, stores into the other}, set 1 = the reverse (generation g
@@ -324,9 +341,18 @@ __device__ __forceinline__ uint32_t rule_pair(uint32_t z, const SimdRule& k) {
   return lop3<0x70>(e, c, d);             // e & ~(c & d)
 }
 
-template <bool kChecked, bool kRing>
+template <int kH, bool kChecked, bool kRing>
 __global__ void __launch_bounds__(kThreads, 1)
     ltl_tc_step_kernel(const __grid_constant__ TcMaps maps, const Params p) {
+  using G = Geo<kH>;
+  constexpr int kBox = G::kBox;
+  constexpr int kXStages = G::kXStages;
+  constexpr int kStageSlots = G::kStageSlots;
+  constexpr uint32_t kBoxBytes = G::kBoxBytes;
+  constexpr uint32_t kSmemX = G::kSmemX, kSmemBand = G::kSmemBand, kSmemStage = G::kSmemStage,
+                     kSmemBars = G::kSmemBars;
+  constexpr uint32_t kSlotCols = G::kSlotCols, kTmemSlot = G::kTmemSlot, kTmemD2 = G::kTmemD2,
+                     kTmemA1 = G::kTmemA1, kPbOff = G::kPbOff, kPiOff = G::kPiOff;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
@@ -350,10 +376,13 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   // ---- one-time setup: resident bands (generic-proxy writes), barriers, TMEM
   // pass-2 B tiles [64 n][32 k]: n = D2 column j (output row rho = out_row_of_col(j)),
-  //   t = 0..2  band, K chunk c = window rows 32c .. 32c+31 (centre at 16 + rho)
-  //   t = 3..4  centre, K chunk c of the shifted plane (centre at rho)
-  //   t = 5..6  16 * centre (state * 2048 for Moore)
-  for (uint32_t w = threadIdx.x; w < kNumTiles * kSub * 8u; w += kThreads) {
+  //   t < nb          band, K chunk t = window rows 32t .. 32t+31 (centre at kH + rho)
+  //   t = nb, nb+1    centre, K chunk of the shifted plane (centre at rho)
+  //   t = nb+2, nb+3  W * centre (Moore: state * 128 W)
+  // (nb = G::kBandChunks).  kH = 32, VN: the band's centre entry also carries
+  // 128 (Pb = state there), so Z = R + 256 state clears R <= 2 (2r + 1).
+  constexpr int nb = G::kBandChunks;
+  for (uint32_t w = threadIdx.x; w < G::kNumTiles * kSub * 8u; w += kThreads) {
     const int t = static_cast<int>(w / (kSub * 8)), j = static_cast<int>((w / 8) % kSub),
               k0 = 4 * static_cast<int>(w % 8);
     const int rho = out_row_of_col(j);
@@ -361,13 +390,14 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
     for (int b = 0; b < 4; ++b) {
       int v;
-      if (t < 3) {
-        const int d = 32 * t + k0 + b - 16 - rho;
+      if (t < nb) {
+        const int d = 32 * t + k0 + b - kH - rho;
         v = (d >= -r && d <= r);
         if (p.inject_fault && d == 0 && (rho + p.fault_row_phase) % p.fault_f == 0) v = 0;
+        if (kH == 32 && vn && d == 0) v += 128;
       } else {
-        const int c = (t - 3) % 2;
-        v = (32 * c + k0 + b == rho) ? (t >= 5 ? 16 : 1) : 0;
+        const int c = (t - nb) % 2;
+        v = (32 * c + k0 + b == rho) ? (t >= nb + 2 ? static_cast<int>(G::kCentreW) : 1) : 0;
       }
       word |= static_cast<uint32_t>(v) << (8 * b);
     }
@@ -536,15 +566,15 @@ __global__ void __launch_bounds__(kThreads, 1)
               if (!first && !last) {
                 mbar_arrive_expect_tx(&x_full[s], kBoxBytes);
 #ifdef LTL_DIAG_L2_READS  // timing probe only (wrong results): every box from band 1 (L2-resident)
-                tma_load_3d(dst, &lm[0], &x_full[s], 0, kBand, strip);
+                tma_load_3d(dst, &lm[0], &x_full[s], 0, kBand + G::kRowOff, strip);
 #else
-                tma_load_3d(dst, &lm[0], &x_full[s], 0, band * kBand, strip);
+                tma_load_3d(dst, &lm[0], &x_full[s], 0, band * kBand + G::kRowOff, strip);
 #endif
               } else {
-                // first / last band of a whole torus: the 16 rows beyond the
+                // first / last band of a whole torus: the kH rows beyond the
                 // edge are loaded from the other end of the strip (padded row 16 + y)
                 const int body = last ? last_rows : kBand;  // interior rows in the box body
-                mbar_arrive_expect_tx(&x_full[s], (last ? last_rows + 2 * kHalo : kBox) * kStrip);
+                mbar_arrive_expect_tx(&x_full[s], (last ? last_rows + 2 * kH : kBox) * kStrip);
                 int row = 0;  // box row being filled
                 if (kRing && first && !up_ready) {
                   wait_flag_geq_sys(p.up_done, p.ring_gen);
@@ -556,21 +586,22 @@ __global__ void __launch_bounds__(kThreads, 1)
                   fence_proxy_async_global();
                   down_ready = true;
                 }
-                if (first) {  // rows -16 .. -1: the torus' other end / the upper slab's last rows
+                if (first) {  // rows -kH .. -1: the torus' other end / the upper slab's last rows
                   if (kRing)
-                    tma_load_3d(dst, &maps.ring_up[gg & 1], &x_full[s], 0, p.up_rows, strip);
+                    tma_load_3d(dst, &maps.ring_up[gg & 1], &x_full[s], 0, p.up_rows + G::kRowOff,
+                                strip);
                   else
-                    tma_load_3d(dst, &lm[1], &x_full[s], 0, p.rows, strip);
-                  row = kHalo;
+                    tma_load_3d(dst, &lm[1], &x_full[s], 0, p.rows + G::kRowOff, strip);
+                  row = kH;
                 }
-                if (first && !last) {  // rows 0 .. 143
+                if (first && !last) {  // rows 0 .. 128 + kH - 1
                   tma_load_3d(dst + row * kStrip, &lm[2], &x_full[s], 0, kHalo, strip);
-                } else {  // last band body: padded rows from 128 * band (its top
+                } else {  // last band body: padded rows from 128 * band - kH (its top
                           // halo included unless it is also the first band)
                   tma_load_3d(dst + row * kStrip, &lm[3], &x_full[s], 0,
-                              first ? kHalo : band * kBand, strip);
-                  // rows rows .. rows + 15: the torus' rows 0 .. 15 / the lower slab's first rows
-                  uint8_t* bot = dst + (row + body + (first ? 0 : kHalo)) * kStrip;
+                              first ? kHalo : band * kBand + G::kRowOff, strip);
+                  // rows rows .. rows + kH - 1: the torus' rows 0 .. kH-1 / the lower slab's first rows
+                  uint8_t* bot = dst + (row + body + (first ? 0 : kH)) * kStrip;
                   tma_load_3d(bot, kRing ? &maps.ring_down[gg & 1] : &lm[1], &x_full[s], 0, kHalo,
                               strip);
                 }
@@ -602,11 +633,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc_fence_after();
         if (elect_one()) {
           const uint32_t dcol = tmem + kTmemSlot + kSlotCols * sl;
-          mma_i8_ts(dcol, a1, box(gl) + (96 >> 4), kIdesc1, 0);
+          mma_i8_ts(dcol, a1, box(gl) + (96 >> 4), G::kIdesc1, 0);
 #pragma unroll
           for (int q = 1; q <= 4; ++q)
-            mma_i8_ts(dcol, a1 + 8 * q, box(go) + ((32 * (q - 1)) >> 4), kIdesc1, 1);
-          mma_i8_ts(dcol, a1 + 40, box(gr), kIdesc1, 1);
+            mma_i8_ts(dcol, a1 + 8 * q, box(go) + ((32 * (q - 1)) >> 4), G::kIdesc1, 1);
+          mma_i8_ts(dcol, a1 + 40, box(gr), G::kIdesc1, 1);
           mma_commit(&d1_full[sl]);
           mma_commit(&x_empty[gl % kXStages]);  // box t-1 is done
           if (t == t1 - 1) {
@@ -634,25 +665,26 @@ __global__ void __launch_bounds__(kThreads, 1)
         LTL_WAIT(3 + (warp & 3), &d1_full[sl], (h / kSlots) & 1);
         if (warp == 2 && lane == 0) LTL_TRACE(2, h);
         tc_fence_after();
-        // all 160 box rows, two rows (16-bit lanes) per register
-        uint32_t va[32], vb[32], vc[16];
+        // all kBox box rows, two rows (16-bit lanes) per register
+        uint32_t va[32], vb[32], vc[kBox / 2 - 64];
         tmem_ld_32x32b_x32_pack16(slot_col, va);
         tmem_ld_32x32b_x32_pack16(slot_col + 64, vb);
-        tmem_ld_32x32b_x16_pack16(slot_col + 128, vc);
+        if constexpr (kBox == 192)
+          tmem_ld_32x32b_x32_pack16(slot_col + 128, *reinterpret_cast<uint32_t(*)[32]>(vc));
+        else
+          tmem_ld_32x32b_x16_pack16(slot_col + 128, *reinterpret_cast<uint32_t(*)[16]>(vc));
         tmem_ld_wait();
+        auto reg = [&](int k) -> uint32_t { return k < 32 ? va[k] : k < 64 ? vb[k - 32] : vc[k - 64]; };
         auto raw_word = [&](int i) -> uint32_t {  // box rows 4i .. 4i+3 as bytes
-          const int k = 2 * i;
-          const uint32_t lo = k < 32 ? va[k] : k < 64 ? vb[k - 32] : vc[k - 64];
-          const uint32_t hi = k + 1 < 32 ? va[k + 1] : k + 1 < 64 ? vb[k + 1 - 32] : vc[k + 1 - 64];
-          return pack_pairs(lo, hi);
+          return pack_pairs(reg(2 * i), reg(2 * i + 1));
         };
         if constexpr (kChecked) {
           const bool x_ok = (t % p.strips) * kStrip + 32 * static_cast<int>(q) +
                                 static_cast<int>(lane) < p.cols;
-          const int prow0 = band * kBand;  // padded row of box row 0
+          const int prow0 = band * kBand + G::kRowOff;  // padded row of box row 0
 #pragma unroll
           for (int i = 0; i < kBox / 2; ++i) {
-            const uint32_t pr = i < 32 ? va[i] : i < 64 ? vb[i - 32] : vc[i - 64];
+            const uint32_t pr = reg(i);
 #pragma unroll
             for (int hh = 0; hh < 2; ++hh) {
               const int prow = prow0 + 2 * i + hh;
@@ -675,10 +707,16 @@ __global__ void __launch_bounds__(kThreads, 1)
             pi[i] = vn ? raw : raw & 0x80808080u;
           }
           tmem_st_32x32b_x8(pb_col + 8 * c, pb);
-          // Pi holds row y at byte y - 16: words 0..3 of chunk c -> Pi words
-          // 8c-4 .. 8c-1, words 4..7 -> 8c .. 8c+3 (rows 0..15, 144..159 unused)
-          if (c > 0) tmem_st_32x32b_x4(pi_col + 8 * c - 4, pi[0], pi[1], pi[2], pi[3]);
-          if (c < kBox / 32 - 1) tmem_st_32x32b_x4(pi_col + 8 * c, pi[4], pi[5], pi[6], pi[7]);
+          if constexpr (kH == 16) {
+            // Pi holds row y at byte y - 16: words 0..3 of chunk c -> Pi words
+            // 8c-4 .. 8c-1, words 4..7 -> 8c .. 8c+3 (rows 0..15, 144..159 unused)
+            if (c > 0) tmem_st_32x32b_x4(pi_col + 8 * c - 4, pi[0], pi[1], pi[2], pi[3]);
+            if (c < kBox / 32 - 1) tmem_st_32x32b_x4(pi_col + 8 * c, pi[4], pi[5], pi[6], pi[7]);
+          } else {
+            // Pi holds row y at byte y - 32: chunk c -> Pi chunk c - 1 (rows
+            // 0..31, 160..191 unused)
+            if (c > 0 && c < kBox / 32 - 1) tmem_st_32x32b_x8(pi_col + 8 * (c - 1), pi);
+          }
         }
         tmem_st_wait();
         tc_fence_before();
@@ -695,11 +733,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else if (warp == kWarpP2) {
     // ================= pass-2 MMA issuer =================
-    // sub-block s: band over Pb chunks 2s .. 2s+2 (box rows 64s .. 64s+95),
-    // centre over Pi chunks 2s, 2s+1 (centre rows 64s .. 64s+63, shifted)
+    // sub-block s: band over Pb chunks 2s .. 2s+nb-1 (box rows 64s ..
+    // 64s+64+2kH-1), centre over Pi chunks 2s, 2s+1 (centre rows 64s .. 64s+63,
+    // shifted)
     const uint64_t band_desc = smem_desc_sw32_kmajor(smem_u32(smem + kSmemBand));
     auto tile = [&](int t) { return band_desc + ((t * kTileBytes) >> 4); };
-    const int ti = vn ? 3 : 5;
+    const int ti = vn ? nb : nb + 2;
     uint32_t h = 0;
     for (int gg = 0; gg < p.gens; ++gg) {
     SegIter it(p, gg);
@@ -709,18 +748,22 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t sl = h % kSlots;
         LTL_WAIT(7, &a2_full[sl], (h / kSlots) & 1);
         for (int s = 0; s < kSubs; ++s) {
-          LTL_WAIT(8, &d2_empty[s], (h & 1) ^ 1);
+          if constexpr (G::kD2Bufs == kSubs) {
+            LTL_WAIT(8, &d2_empty[s], (h & 1) ^ 1);
+          } else {  // one shared D2: wait for its previous occupant, the other sub-block
+            if (s == 0) LTL_WAIT(8, &d2_empty[1], (h & 1) ^ 1);  // (h - 1, 1)
+            else LTL_WAIT(8, &d2_empty[0], h & 1);               // (h, 0)
+          }
           LTL_TRACE(4, 2 * h + s);
           tc_fence_after();
           if (elect_one()) {
-            const uint32_t dcol = tmem + kTmemD2 + kSub * s;
+            const uint32_t dcol = tmem + kTmemD2 + kSub * (s % G::kD2Bufs);
             const uint32_t pb = tmem + kTmemSlot + kSlotCols * sl + kPbOff + 16 * s;
             const uint32_t pi = tmem + kTmemSlot + kSlotCols * sl + kPiOff + 16 * s;
-            mma_i8_ts(dcol, pb, tile(0), kIdesc2, 0);
-            mma_i8_ts(dcol, pb + 8, tile(1), kIdesc2, 1);
-            mma_i8_ts(dcol, pb + 16, tile(2), kIdesc2, 1);
-            mma_i8_ts(dcol, pi, tile(ti), kIdesc2, 1);
-            mma_i8_ts(dcol, pi + 8, tile(ti + 1), kIdesc2, 1);
+#pragma unroll
+            for (int c = 0; c < nb; ++c) mma_i8_ts(dcol, pb + 8 * c, tile(c), G::kIdesc2, c > 0);
+            mma_i8_ts(dcol, pi, tile(ti), G::kIdesc2, 1);
+            mma_i8_ts(dcol, pi + 8, tile(ti + 1), G::kIdesc2, 1);
             mma_commit(&d2_full[s]);
             if (s == kSubs - 1) mma_commit(&slot_empty[sl]);
           }
@@ -802,9 +845,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     // and TMA stores: no CTA-wide barrier on this path).
     const uint32_t q = warp & 3;
     const uint32_t grp = (warp - kWarpOut0) >> 2;
-    const uint32_t trow = tmem + ((q * 32) << 16) + kTmemD2 + kSub * grp;
+    const uint32_t trow = tmem + ((q * 32) << 16) + kTmemD2 + kSub * (grp % G::kD2Bufs);
     const RuleConsts rc = p.rule;
-    const uint32_t K = vn ? 128u : 2048u;
+    const uint32_t K = vn ? G::kVnK : 128u * G::kCentreW;  // Z = R + K state
     SimdRule sr;
     sr.ca = (0x8000u - rc.lo_dead) * 0x10001u;
     sr.cb = (0x7FFFu - (rc.lo_dead + rc.w_dead)) * 0x10001u;
@@ -948,7 +991,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 }  // namespace
 
-size_t tc_smem_bytes() { return kSmemAlloc; }
+size_t tc_smem_bytes(int halo) { return halo == 32 ? Geo<32>::kSmemAlloc : Geo<16>::kSmemAlloc; }
 
 // Multi-generation launches (SegIter's sweep): one CTA per SM, all resident.
 // A generation boundary of one-launch-per-generation costs ~12.7 us (grid
@@ -995,12 +1038,19 @@ cudaError_t launch_tc_step(const TcLaunch& a, cudaStream_t stream) {
   if (e != cudaSuccess) return e;
   if (dev < 0 || dev >= kMaxDevices) return cudaErrorInvalidDevice;
   if (sm_count[dev] == 0) {
-    for (auto fn : {ltl_tc_step_kernel<false, false>, ltl_tc_step_kernel<true, false>,
-                    ltl_tc_step_kernel<false, true>, ltl_tc_step_kernel<true, true>}) {
-      e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               static_cast<int>(kSmemAlloc));
-      if (e != cudaSuccess) return e;
-    }
+    auto set_smem = [](auto fn, uint32_t bytes) {
+      return cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(bytes));
+    };
+    for (cudaError_t r : {set_smem(ltl_tc_step_kernel<16, false, false>, Geo<16>::kSmemAlloc),
+                          set_smem(ltl_tc_step_kernel<16, true, false>, Geo<16>::kSmemAlloc),
+                          set_smem(ltl_tc_step_kernel<16, false, true>, Geo<16>::kSmemAlloc),
+                          set_smem(ltl_tc_step_kernel<16, true, true>, Geo<16>::kSmemAlloc),
+                          set_smem(ltl_tc_step_kernel<32, false, false>, Geo<32>::kSmemAlloc),
+                          set_smem(ltl_tc_step_kernel<32, true, false>, Geo<32>::kSmemAlloc),
+                          set_smem(ltl_tc_step_kernel<32, false, true>, Geo<32>::kSmemAlloc),
+                          set_smem(ltl_tc_step_kernel<32, true, true>, Geo<32>::kSmemAlloc)})
+      if (r != cudaSuccess) return r;
     int sms = 0;
     e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     if (e != cudaSuccess) return e;
@@ -1024,6 +1074,11 @@ cudaError_t launch_tc_step(const TcLaunch& a, cudaStream_t stream) {
   p.gens = a.gens > 1 && a.flags && a.load_maps_b && a.store_map_b ? a.gens : 1;
   p.ring = a.ring && p.wrap_cols && tc_wrap_rows(a.rows) ? 1 : 0;
   if (a.ring && !p.ring) return cudaErrorInvalidValue;  // caller must not ask
+  const int halo = a.halo == 32 ? 32 : 16;
+  // 32-row boxes exist only where the loads do every wrap: the slab's own
+  // 16-row HBM halo cannot hold 32 rows / columns
+  if (a.halo != 0 && a.halo != 16 && a.halo != 32) return cudaErrorInvalidValue;
+  if (halo == 32 && !(p.wrap_cols && (p.wrap_rows || p.ring))) return cudaErrorInvalidValue;
   if (p.ring) {
     p.wrap_rows = 0;
     p.up_flags = a.up_flags ? a.up_flags : a.flags;
@@ -1055,7 +1110,7 @@ cudaError_t launch_tc_step(const TcLaunch& a, cudaStream_t stream) {
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(static_cast<unsigned>(grid));
   cfg.blockDim = dim3(kThreads);
-  cfg.dynamicSmemBytes = kSmemAlloc;
+  cfg.dynamicSmemBytes = tc_smem_bytes(halo);
   cfg.stream = stream;
   cudaLaunchAttribute attr[2];
   int nattr = 0;
@@ -1087,12 +1142,19 @@ cudaError_t launch_tc_step(const TcLaunch& a, cudaStream_t stream) {
     maps.ring_down[i] = a.ring ? a.ring_down[i & (a.gens > 1 ? 1 : 0)] : *a.store_map;
   }
   // the ring's peer-memory paths are compiled only into the ring kernels
-  if (p.ring) {
-    if (a.stats) return cudaLaunchKernelEx(&cfg, ltl_tc_step_kernel<true, true>, maps, p);
-    return cudaLaunchKernelEx(&cfg, ltl_tc_step_kernel<false, true>, maps, p);
+  const bool st = a.stats != nullptr;
+  if (halo == 32) {
+    if (p.ring)
+      return st ? cudaLaunchKernelEx(&cfg, ltl_tc_step_kernel<32, true, true>, maps, p)
+                : cudaLaunchKernelEx(&cfg, ltl_tc_step_kernel<32, false, true>, maps, p);
+    return st ? cudaLaunchKernelEx(&cfg, ltl_tc_step_kernel<32, true, false>, maps, p)
+              : cudaLaunchKernelEx(&cfg, ltl_tc_step_kernel<32, false, false>, maps, p);
   }
-  if (a.stats) return cudaLaunchKernelEx(&cfg, ltl_tc_step_kernel<true, false>, maps, p);
-  return cudaLaunchKernelEx(&cfg, ltl_tc_step_kernel<false, false>, maps, p);
+  if (p.ring)
+    return st ? cudaLaunchKernelEx(&cfg, ltl_tc_step_kernel<16, true, true>, maps, p)
+              : cudaLaunchKernelEx(&cfg, ltl_tc_step_kernel<16, false, true>, maps, p);
+  return st ? cudaLaunchKernelEx(&cfg, ltl_tc_step_kernel<16, true, false>, maps, p)
+            : cudaLaunchKernelEx(&cfg, ltl_tc_step_kernel<16, false, false>, maps, p);
 }
 
 }  // namespace ltl

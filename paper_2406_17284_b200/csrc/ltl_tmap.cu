@@ -53,15 +53,17 @@ cudaError_t encode3(CUtensorMap* map, void* base, uint64_t rows, uint64_t strips
 }  // namespace
 
 // Whole padded slab in the SWIZZLE_128B K-major layout of the pass-1 B
-// operand (ptx::smem_desc_sw128_kmajor): [0] 160-row boxes (one contiguous
-// 20 KB block of a strip), [1] 16-row pieces, [2] 144-row and [3] (rows of the
-// last band + 16)-row bodies for the row-wrapped first / last band boxes.
-cudaError_t make_load_maps(CUtensorMap* maps, const SlabView& s) {
+// operand (ptx::smem_desc_sw128_kmajor), for boxes with `halo` (kH = 16 / 32)
+// rows above and below: [0] (128 + 2 kH)-row boxes (one contiguous 20 / 24 KB
+// block of a strip), [1] kH-row pieces, [2] (128 + kH)-row and [3] (rows of
+// the last band + kH)-row bodies for the row-wrapped first / last band boxes.
+cudaError_t make_load_maps(CUtensorMap* maps, const SlabView& s, int halo) {
   if (s.rows <= 0 || s.cols <= 0) return cudaSuccess;
   const int last = s.rows - kTcBand * ((s.rows - 1) / kTcBand);  // rows of the last band
   const bool one_band = s.rows <= kTcBand;  // first = last band: body without its top halo
-  const uint32_t box[kTcLoadMaps] = {kTcBox, kHalo, kTcBox - kHalo,
-                                     static_cast<uint32_t>(last + (one_band ? 0 : kHalo))};
+  const uint32_t h = static_cast<uint32_t>(halo);
+  const uint32_t box[kTcLoadMaps] = {kTcBand + 2 * h, h, kTcBand + h,
+                                     static_cast<uint32_t>(last) + (one_band ? 0 : h)};
   for (int i = 0; i < kTcLoadMaps; ++i) {
     const cudaError_t e = encode3(&maps[i], s.buf, static_cast<uint64_t>(s.rows) + 2 * kHalo,
                                   static_cast<uint64_t>(s.strips),
@@ -82,13 +84,13 @@ cudaError_t make_store_map(CUtensorMap* map, const SlabView& s) {
                  64, CU_TENSOR_MAP_SWIZZLE_128B);
 }
 
-// 16-row pieces of a slab's padded rows (the ring's rows above / below, read
+// halo-row pieces of a slab's padded rows (the ring's rows above / below, read
 // out of the neighbour's slab in peer memory): load map [1] of any slab.
-cudaError_t make_piece_map(CUtensorMap* map, const SlabView& s) {
+cudaError_t make_piece_map(CUtensorMap* map, const SlabView& s, int halo) {
   if (s.rows <= 0 || s.cols <= 0) return cudaSuccess;
   return encode3(map, s.buf, static_cast<uint64_t>(s.rows) + 2 * kHalo,
                  static_cast<uint64_t>(s.strips), static_cast<uint64_t>(s.strip_bytes), kStrip,
-                 kHalo, CU_TENSOR_MAP_SWIZZLE_128B);
+                 static_cast<uint32_t>(halo), CU_TENSOR_MAP_SWIZZLE_128B);
 }
 
 }  // namespace ltl

@@ -27,6 +27,10 @@ OK, ERR_INVALID_ARGUMENT, ERR_LOGIC, ERR_RUNTIME, ERR_CUDA = range(5)
 LAYOUT_ROW_MAJOR, LAYOUT_FRAGMENT = 0, 1
 KIND_MOORE, KIND_VON_NEUMANN = 0, 1
 FLAG_INJECT_FAULT, FLAG_WANT_STATS, FLAG_ENGINE_BASE, FLAG_ENGINE_PACK = 0x1, 0x2, 0x4, 0x10
+# extension: the Cat engine with 17 <= r <= 32 (include/ltl_b200.h LTL_FLAG_WIDE_RADIUS);
+# set automatically for rules with r > 16
+FLAG_WIDE_RADIUS = 0x20
+MAX_RADIUS, MAX_WIDE_RADIUS = 16, 32
 FLAG_STENCIL = FLAG_ENGINE_BASE
 # engine name -> ltl_run flag (catsim::EngineKind; proj/src/engines.cpp:9-15)
 ENGINE_FLAGS = {"cat": 0, "base": FLAG_ENGINE_BASE, "pack": FLAG_ENGINE_PACK}
@@ -70,7 +74,7 @@ EXPORTS = (
     "ltl_snapshot_write", "ltl_snapshot_read", "ltl_snapshot_probe", "ltl_snapshot_parse_header",
     "ltl_download_padded", "ltl_host_fill_halo",
     "ltl_fragment_pass",
-    "ltl_init_random", "ltl_parse_rule", "ltl_format_rule",
+    "ltl_init_random", "ltl_parse_rule", "ltl_parse_rule_ext", "ltl_format_rule",
     "ltl_preset_count", "ltl_preset", "ltl_von_neumann_probe_rule", "ltl_build_info",
 )
 
@@ -142,6 +146,8 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
         "ltl_unpack_halo": ([vp, vp, vp], ctypes.c_int),
         "ltl_parse_rule": ([ctypes.c_char_p, P(ltl_rule_c), ctypes.c_char_p, ctypes.c_int32],
                            ctypes.c_int),
+        "ltl_parse_rule_ext": ([ctypes.c_char_p, ctypes.c_int32, P(ltl_rule_c), ctypes.c_char_p,
+                                ctypes.c_int32], ctypes.c_int),
         "ltl_format_rule": ([P(ltl_rule_c), ctypes.c_char_p, ctypes.c_int32], ctypes.c_int32),
         "ltl_preset_count": ([], ctypes.c_int32),
         "ltl_preset": ([ctypes.c_int32, P(ctypes.c_char_p), P(ctypes.c_char_p),
@@ -184,11 +190,13 @@ class LtlRule:
         return format_ltl_rule(self)
 
 
-def parse_ltl_rule(text: str) -> LtlRule:
+def parse_ltl_rule(text: str, max_radius: int = MAX_RADIUS) -> LtlRule:
+    """parse_ltl_rule (src/rule.cpp:61-87); max_radius up to 32 is the
+    wide-radius extension (the reference stops at 16)."""
     lib = load_library()
     out = ltl_rule_c()
     err = ctypes.create_string_buffer(256)
-    if lib.ltl_parse_rule(text.encode(), ctypes.byref(out), err, 256) != OK:
+    if lib.ltl_parse_rule_ext(text.encode(), max_radius, ctypes.byref(out), err, 256) != OK:
         raise ValueError(err.value.decode())
     return LtlRule.from_c(out)
 
@@ -323,13 +331,17 @@ class DeviceTorus:
         return out.reshape(p, p) if layout == LAYOUT_ROW_MAJOR else out
 
     @staticmethod
-    def _flags(engine: str, inject_fault: bool = False, stencil: bool = False) -> int:
-        """engine "cat" | "base" | "pack" (stencil=True: the round-1 spelling of "base")."""
+    def _flags(engine: str, inject_fault: bool = False, stencil: bool = False,
+               rule: ltl_rule_c | None = None) -> int:
+        """engine "cat" | "base" | "pack" (stencil=True: the round-1 spelling of
+        "base"); a Cat rule with r > 16 adds FLAG_WIDE_RADIUS."""
         if stencil and engine == "cat":
             engine = "base"
         if engine not in ENGINE_FLAGS:
             raise ValueError(f"config error: unknown engine '{engine}' (cat, base, pack)")
-        return ENGINE_FLAGS[engine] | (FLAG_INJECT_FAULT if inject_fault else 0)
+        wide = engine == "cat" and rule is not None and rule.r > MAX_RADIUS
+        return (ENGINE_FLAGS[engine] | (FLAG_INJECT_FAULT if inject_fault else 0)
+                | (FLAG_WIDE_RADIUS if wide else 0))
 
     def run(self, rule, steps: int, stencil: bool = False, inject_fault: bool = False,
             stats: bool = False, engine: str = "cat"):
@@ -337,7 +349,7 @@ class DeviceTorus:
         runs the checked kernel variant that max-reduces H / R on the device)."""
         r = as_rule(rule).to_c()
         st = ltl_stats_c()
-        flags = self._flags(engine, inject_fault, stencil) | (FLAG_WANT_STATS if stats else 0)
+        flags = self._flags(engine, inject_fault, stencil, r) | (FLAG_WANT_STATS if stats else 0)
         self._check(self.lib.ltl_run(self._ctx, ctypes.byref(r), steps, flags,
                                      ctypes.byref(st) if stats else None))
         if not stats:
@@ -347,7 +359,7 @@ class DeviceTorus:
     def run_async(self, rule, steps: int, stencil: bool = False, engine: str = "cat") -> None:
         r = as_rule(rule).to_c()
         self._check(self.lib.ltl_run_async(self._ctx, ctypes.byref(r), steps,
-                                           self._flags(engine, False, stencil)))
+                                           self._flags(engine, False, stencil, r)))
 
     def synchronize(self) -> None:
         self._check(self.lib.ltl_synchronize(self._ctx))
@@ -358,7 +370,7 @@ class DeviceTorus:
         r = as_rule(rule).to_c()
         tot, ker = ctypes.c_double(), ctypes.c_double()
         self._check(self.lib.ltl_time(self._ctx, ctypes.byref(r), steps, warmup,
-                                      self._flags(engine, False, stencil), ctypes.byref(tot),
+                                      self._flags(engine, False, stencil, r), ctypes.byref(tot),
                                       ctypes.byref(ker)))
         return tot.value, ker.value
 
@@ -370,7 +382,7 @@ class DeviceTorus:
         r = as_rule(rule).to_c()
         st = ltl_stats_c()
         self._check(self.lib.ltl_run_interior(self._ctx, _u8(a), _u8(out), ctypes.byref(r),
-                                              steps, self._flags(engine, False, stencil),
+                                              steps, self._flags(engine, False, stencil, r),
                                               ctypes.byref(st)))
         return out
 
@@ -381,7 +393,7 @@ class DeviceTorus:
         """Enqueue one generation + local column-halo refresh (async)."""
         r = as_rule(rule).to_c()
         self._check(self.lib.ltl_step_part(self._ctx, ctypes.byref(r),
-                                           self._flags(engine, False, stencil)))
+                                           self._flags(engine, False, stencil, r)))
 
     def fill_halo(self) -> None:
         self._check(self.lib.ltl_fill_halo(self._ctx))

@@ -77,6 +77,30 @@ def test_rule_parse_errors(lib, text, msg):
             ltl.parse_ltl_rule(text)
 
 
+@pytest.mark.parametrize("text,max_r,msg", [
+    ("R17,C2,M0,S2..3,B3..3,NM", 32, None),
+    ("R32,C2,M1,S1000..2000,B1000..1500,NM", 32, None),
+    ("R32,C2,M0,S0..64,B1..128,NN", 32, None),
+    ("R32,C2,M0,S0..4225,B0..0,NM", 32, "exceeds neighborhood capacity 4224"),
+    ("R33,C2,M0,S2..3,B3..3,NM", 32, "unsupported rule: radius 33 outside 1..32"),
+    ("R20,C2,M0,S2..3,B3..3,NM", 16, "unsupported rule: radius 20 outside 1..16"),
+    ("R20,C2,M0,S2..3,B3..3,NM", 20, None),
+    ("R1,C2,M0,S2..3,B3..3,NM", 33, "unsupported rule: radius limit 33 outside 1..32"),
+])
+def test_wide_radius_rule_parse(lib, text, max_r, msg):
+    """Extension: ltl_parse_rule_ext accepts radii up to 32 with the same
+    grammar and messages; the reference-signature parser still stops at 16."""
+    from paper_2406_17284_b200 import ltl
+    if msg is None:
+        assert ltl.format_ltl_rule(ltl.parse_ltl_rule(text, max_radius=max_r)) == text
+        if int(text[1:text.index(",")]) > 16:
+            with pytest.raises(ValueError, match="outside 1..16"):
+                ltl.parse_ltl_rule(text)
+    else:
+        with pytest.raises(ValueError, match=re.escape(msg)):
+            ltl.parse_ltl_rule(text, max_radius=max_r)
+
+
 def test_rule_parse_agrees_with_reference_library(lib, ref):
     """Same accept/reject decision and message as the reference's parser."""
     from paper_2406_17284_b200 import ltl

@@ -117,3 +117,22 @@ def test_fill_periodic_halo(orc):
     for y in range(n + 2 * h):
         for x in range(n + 2 * h):
             assert out[y, x] == out[h + (y - h) % n, h + (x - h) % n]
+
+
+def test_wide_radius_fixtures(orc):
+    """The wide-radius extension (17 <= r <= 32): the C restatement against
+    fixtures from the reference's own brute-force oracle
+    (proj/tests/oracle.hpp:50-68 via tests/golden/make_wide.py)."""
+    for c in load("wide.json")["cases"]:
+        g = orc.simulate(orc.init_random(c["n"], c["density"], c["seed"]), c["ints"], c["steps"])
+        assert int(g.sum()) == c["alive"], c["rule"]
+        assert f"{orc.fnv1a64(g):016x}" == c["fnv"], c["rule"]
+
+
+def test_wide_radius_semantic_oracle(orc, ref):
+    """Same, live against the reference's semantic oracle on fresh inputs,
+    rectangular-free (it is square only) small tori where windows wrap twice."""
+    for n, rule in ((32, [17, 2, 0, 300, 700, 350, 600, 0]), (48, [32, 2, 1, 30, 80, 40, 70, 1]),
+                    (64, [24, 2, 0, 1200, 2400, 1201, 2400, 0])):
+        g = orc.init_random(n, 0.5, 4)
+        assert np.array_equal(ref.semantic_steps(g, rule, 3), orc.simulate(g, rule, 3)), rule

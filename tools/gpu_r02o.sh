@@ -1,9 +1,20 @@
 #!/bin/bash
+# Wide-radius extension (r = 17..32) first run: its GPU tests, the r <= 16
+# parity suite (unchanged kernel variant), and a quick r = 16 / 32 timing.
 set -u
 mkdir -p gpurun_out
-timeout 1500 python -m pytest tests/test_gpu_parity.py -q -m gpu -x -k "criterion1 or rectangular or large_grid or refreshes or all_alive" > gpurun_out/pytest_o.log 2>&1; echo "pytest rc=$?"; tail -2 gpurun_out/pytest_o.log
-timeout 900 python bench.py --engine pack --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/bench_c2_pack_o.json 2>/dev/null; echo "bench pack rc=$?"
-python -c "
-import json; d=json.loads(open('gpurun_out/bench_c2_pack_o.json').read().splitlines()[-1])
-print('pack', ' '.join('r%d:%.3g(%.2f)'%(p['r'],p['cell_updates_per_s'],p['hbm_frac']) for p in d['per_radius']))"
-timeout 900 compute-sanitizer --tool memcheck --print-limit 20 python tools/sanitize.py > gpurun_out/san_memcheck_o.txt 2>&1; echo "memcheck rc=$?"; tail -2 gpurun_out/san_memcheck_o.txt
+timeout 900 python -m pytest tests/test_gpu_wide.py -q -x -rs > gpurun_out/pytest_wide_o.log 2>&1; echo "wide rc=$?"; tail -30 gpurun_out/pytest_wide_o.log
+timeout 900 python -m pytest tests/test_gpu_parity.py -q -x > gpurun_out/pytest_parity_o.log 2>&1; echo "parity rc=$?"; tail -3 gpurun_out/pytest_parity_o.log
+timeout 300 python - <<'PY' > gpurun_out/wide_timing_o.txt 2>&1
+from paper_2406_17284_b200 import ltl
+n = 32768
+def maj(r, vn=False):
+    cells = 4 * r if vn else (2 * r + 1) ** 2 - 1
+    return [r, 2, 0, cells // 2, cells, cells // 2 + 1, cells, 1 if vn else 0]
+with ltl.DeviceTorus(n=n) as t:
+    t.init_random(0.5, 1)
+    for rule in (maj(16), maj(17), maj(24), maj(32), maj(32, True)):
+        tot, ker = t.time(rule, 20, 5)
+        print(rule[0], rule[7], "ms/gen %.4f kernel %.4f cells/s %.3e" % (tot / 20, ker / 20, n * n / (tot / 20) * 1e3))
+PY
+echo "timing rc=$?"; cat gpurun_out/wide_timing_o.txt
