@@ -53,6 +53,7 @@ SEED = 1
 BYTES_PER_CELL = 2   # read 1 B state + write 1 B next state
 OPS_ALG = 192        # the reference's 6 fragment MMAs x 2*16^3 / 16^2
 OPS_EXEC = 800       # tcgen05 kind::i8 ops the kernel issues per cell
+OPS_EXEC_WIDE = 960  # the same for the r = 17..32 boxes (6 x M128.N192.K32 + 12 x M128.N64.K32)
 BOSCO = "R5,C2,M1,S34..58,B34..45,NM"
 
 WORKLOADS = {
@@ -61,7 +62,16 @@ WORKLOADS = {
     "c2": "configs[2] radius sweep r=1..16 (Table III presets) 32768x32768",
     "c3": "configs[3] r=16 tangy-ramen 65536x65536 row slabs (strong scaling)",
     "c4": "configs[4] r=8 globe 65536x65536 cells per GPU (weak scaling)",
+    "wide": "extension: radius sweep r=17..32 (majority rules) 32768x32768 (PAPER.md:561)",
 }
+
+
+def majority_rule(r):
+    """Majority rule at radius r (the shape of the r=4 preset `majority`,
+    S40..80 B41..80): survive with >= half, born with > half of the
+    (2r+1)^2 - 1 neighbours alive; density 0.5."""
+    cells = (2 * r + 1) ** 2 - 1
+    return f"R{r},C2,M0,S{cells // 2}..{cells},B{cells // 2 + 1}..{cells},NM"
 
 
 def env_int(name, default):
@@ -108,11 +118,13 @@ def workload_rules(workload):
         return [(p[0], p[1], p[2]) for p in presets[:16]]
     if workload == "c3":
         return [tuple(presets[15])]
+    if workload == "wide":
+        return [(f"majority-r{r}", majority_rule(r), 0.5) for r in range(17, 33)]
     return [tuple(presets[7])]
 
 
 def workload_side(workload):
-    return {"c0": 1024, "c1": 16384, "c2": 32768, "c3": 65536, "c4": 65536}[workload]
+    return {"c0": 1024, "c1": 16384, "c2": 32768, "c3": 65536, "c4": 65536, "wide": 32768}[workload]
 
 
 class Clocks:
@@ -221,6 +233,10 @@ def reference_arm(args, rank, world):
     """--impl reference: the reference's own CPU path on this box's host cores."""
     if rank != 0:
         return
+    if args.workload == "wide":
+        print(json.dumps({"impl": "reference", "unavailable": "the reference's engines reject "
+                          "r > 16 (proj/src/rule.cpp:33-35)"}), flush=True)
+        return
     import numpy as np
 
     import oracle
@@ -291,6 +307,8 @@ def ref_rules(ref, workload):
         return [tuple(p) for p in presets[:16]]
     if workload == "c3":
         return [tuple(presets[15])]
+    if workload == "wide":
+        return [(f"majority-r{r}", majority_rule(r), 0.5) for r in range(17, 33)]
     return [tuple(presets[7])]
 
 
@@ -300,6 +318,9 @@ def config_dict(workload, world):
          "l2": "inputs larger than L2 (every generation buffer >= 256 MiB > 126 MB L2)"}
     if workload == "c2":
         d["rules"] = "Table III presets r=1..16 at their densities (proj/src/rule.cpp:113-133)"
+    elif workload == "wide":
+        d["rules"] = ("majority rules r=17..32 at density 0.5 (the reference's engines reject "
+                      "r > 16; parity: tests/test_gpu_wide.py)")
     elif workload == "c1":
         d.update(rule=BOSCO, density=0.21)
     elif workload == "c0":
@@ -333,7 +354,7 @@ def ours_single(args):
     per, launches, inits = [], 0, []
     clocks.start()
     for label, rule_text, dens in rules:
-        rule = ltl.parse_ltl_rule(rule_text)
+        rule = ltl.parse_ltl_rule(rule_text, max_radius=ltl.MAX_WIDE_RADIUS)
         torus.init_random(dens, SEED)
         if workload == "c2" and label in ("life", "bosco", "tangy-ramen"):
             inits.append((label, rule_text, dens, torus.download()))
@@ -360,7 +381,8 @@ def ours_single(args):
     kern_iso_s = statistics.mean(e["kernel_ms_isolated"] for e in per) / 1e3
     achieved = BYTES_PER_CELL * n * n / kern_avg_s / 1e9
     ceiling_hbm = hbm * 1e9 / BYTES_PER_CELL
-    ceiling_mma = p_mma / OPS_EXEC if engine == "cat" else None
+    ops_exec = OPS_EXEC_WIDE if workload == "wide" else OPS_EXEC
+    ceiling_mma = p_mma / ops_exec if engine == "cat" else None
 
     # e2e through the public C-ABI (ltl_run_interior = run_engine(Cat)):
     # pinned host grids, upload + K generations + download per radius
@@ -368,7 +390,7 @@ def ours_single(args):
     hout = torch.empty((n, n), dtype=torch.uint8).pin_memory().numpy()
     e2e_s, e2e_per = 0.0, []
     for label, rule_text, dens in rules:
-        rule = ltl.parse_ltl_rule(rule_text)
+        rule = ltl.parse_ltl_rule(rule_text, max_radius=ltl.MAX_WIDE_RADIUS)
         torus.init_random(dens, SEED)
         torus.download(hin)
         torus.run_interior(hin, rule, 1, out=hout, engine=engine)  # warm
@@ -411,14 +433,15 @@ def ours_single(args):
                      "mma_peak_ops": p_mma if engine == "cat" else None,
                      "mma_peak_source": mma_src if engine == "cat" else None,
                      "ops_per_cell_algorithmic": OPS_ALG, "ops_per_cell_executed":
-                         OPS_EXEC if engine == "cat" else None,
-                     "mma_frac": (value * OPS_EXEC / p_mma) if engine == "cat" else None},
+                         ops_exec if engine == "cat" else None,
+                     "mma_frac": (value * ops_exec / p_mma) if engine == "cat" else None},
         "clocks": clk,
     }
-    ncu = profile_json(f"ncu_tc_step_{n}.json")
+    ncu_name = f"ncu_tc_step_{'wide_' if workload == 'wide' else ''}{n}.json"
+    ncu = profile_json(ncu_name)
     if ncu and engine == "cat":
         line["roofline"]["traffic"] = ncu.get("dram_bytes_per_generation")
-        line["roofline"]["traffic_source"] = f"profiles/ncu_tc_step_{n}.json (ncu --set full)"
+        line["roofline"]["traffic_source"] = f"profiles/{ncu_name} (ncu --set full)"
     if not args.no_cpu_baseline and inits:
         line["cpu_baseline"] = cpu_baseline([g for *_, g in inits],
                                             [(a, b, c) for a, b, c, _ in inits], n)

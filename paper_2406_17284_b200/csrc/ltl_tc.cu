@@ -94,7 +94,7 @@ constexpr int kWarpStore = kWarpP2 + 1;           // 15
 constexpr uint32_t kTileBytes = kSub * 32;        // 2 KB pass-2 B tile [64 n][32 k]
 constexpr uint32_t kStageBytes = kSub * kStrip;   // 64 x 128 B = 8 KB output staging tile
 constexpr uint32_t kTmemCols = 512;               // all of the SM's TMEM
-static_assert(kSubs == 2, "one output group per sub-block");
+static_assert(kSubs == 2 && kSlots == kSubs, "one output group per sub-block; barrier arrays sized kSubs");
 
 // Geometry of one kernel variant, by the halo rows kH its boxes carry:
 //   kH = 16  r <= 16 (the reference's range, src/rule.cpp:33-35): 160-row
@@ -113,7 +113,12 @@ struct Geo {
   static constexpr int kNumTiles = kBandChunks + 4;         // + Iv0..1, W*Iv0..1
   static constexpr int kXStages = kH == 16 ? 8 : 7;         // 3 boxes in use + prefetched
   static constexpr int kStageSlots = kH == 16 ? 3 : 2;      // staging tiles per output group
-  static constexpr int kD2Bufs = kH == 16 ? 2 : 1;          // D2 buffers (64 columns each)
+  // D2 buffers (64 columns each).  kH = 32: sub-block 1's only; sub-block 0's
+  // D2 goes into the free columns [kD2InSlot, +64) of the unit's D1 slot
+  // (the planes use [0, 80)), so the slot is free once pass 2 is done AND
+  // output group 0 has read it (slot_empty counts both).
+  static constexpr int kD2Bufs = kH == 16 ? 2 : 1;
+  static constexpr uint32_t kD2InSlot = kBox - kSub;       // 128 (kH = 32)
   // centre weight W of pass 2 (Moore: Z = R + 128 W state must clear R <= (2r+1)^2)
   static constexpr uint32_t kCentreW = kH == 16 ? 16u : 64u;   // K = 2048 / 8192
   static constexpr uint32_t kVnK = kH == 16 ? 128u : 256u;     // VN: R <= 2(2r+1)
@@ -125,7 +130,8 @@ struct Geo {
   static constexpr uint32_t kSmemBand = kSmemX + kXStages * kBoxBytes;
   static constexpr uint32_t kSmemStage = kSmemBand + kNumTiles * kTileBytes;
   static constexpr uint32_t kSmemBars = kSmemStage + kSubs * kStageSlots * kStageBytes;
-  static constexpr uint32_t kNumBars = 2 * kXStages + 3 * kSlots + 2 * kSubs + 2 * kSubs * kStageSlots;
+  static constexpr uint32_t kNumBars =
+      2 * kXStages + 4 * kSlots + 2 * kSubs + 2 * kSubs * kStageSlots;
   static constexpr uint32_t kSmemTotal = kSmemBars + kNumBars * 8 + 16;
   static constexpr uint32_t kSmemAlloc = kSmemTotal + 1024;  // alignment slack
   static_assert(kSmemAlloc <= 227 * 1024, "shared memory budget");
@@ -367,7 +373,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* d2_empty = d2_full + kSubs;
   uint64_t* st_full = d2_empty + kSubs;              // output group -> store warp
   uint64_t* st_empty = st_full + kSubs * kStageSlots; // store warp -> output group
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(st_empty + kSubs * kStageSlots);
+  // kH = 32: sub-block 0's D2 sits in the unit's slot, so pass 2 may run up to
+  // two units ahead of output group 0 -- one "D2 written" barrier per slot
+  uint64_t* d2_slot_full = st_empty + kSubs * kStageSlots;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(d2_slot_full + kSlots);
 
   const uint32_t warp = warp_id();
   const uint32_t lane = threadIdx.x & 31;
@@ -419,10 +428,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int i = 0; i < kSlots; ++i) {
       mbar_init(&d1_full[i], 1);
       mbar_init(&a2_full[i], kConvThreads);
-      mbar_init(&slot_empty[i], 1);
+      mbar_init(&slot_empty[i], kH == 16 ? 1 : 1 + kGroupThreads);
     }
     for (int i = 0; i < kSubs; ++i) {
       mbar_init(&d2_full[i], 1);
+      mbar_init(&d2_slot_full[i], 1);  // (kSlots == kSubs == 2)
       mbar_init(&d2_empty[i], kGroupThreads);
     }
     for (int i = 0; i < kSubs * kStageSlots; ++i) {
@@ -750,21 +760,23 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int s = 0; s < kSubs; ++s) {
           if constexpr (G::kD2Bufs == kSubs) {
             LTL_WAIT(8, &d2_empty[s], (h & 1) ^ 1);
-          } else {  // one shared D2: wait for its previous occupant, the other sub-block
-            if (s == 0) LTL_WAIT(8, &d2_empty[1], (h & 1) ^ 1);  // (h - 1, 1)
-            else LTL_WAIT(8, &d2_empty[0], h & 1);               // (h, 0)
+          } else if (s == 1) {  // sub-block 0's D2 lives in the slot (gated by slot_empty)
+            LTL_WAIT(8, &d2_empty[1], (h & 1) ^ 1);
           }
           LTL_TRACE(4, 2 * h + s);
           tc_fence_after();
           if (elect_one()) {
-            const uint32_t dcol = tmem + kTmemD2 + kSub * (s % G::kD2Bufs);
+            const uint32_t dcol = G::kD2Bufs == kSubs ? tmem + kTmemD2 + kSub * s
+                                  : s == 0 ? tmem + kTmemSlot + kSlotCols * sl + G::kD2InSlot
+                                           : tmem + kTmemD2;
             const uint32_t pb = tmem + kTmemSlot + kSlotCols * sl + kPbOff + 16 * s;
             const uint32_t pi = tmem + kTmemSlot + kSlotCols * sl + kPiOff + 16 * s;
 #pragma unroll
             for (int c = 0; c < nb; ++c) mma_i8_ts(dcol, pb + 8 * c, tile(c), G::kIdesc2, c > 0);
             mma_i8_ts(dcol, pi, tile(ti), G::kIdesc2, 1);
             mma_i8_ts(dcol, pi + 8, tile(ti + 1), G::kIdesc2, 1);
-            mma_commit(&d2_full[s]);
+            if (G::kD2Bufs != kSubs && s == 0) mma_commit(&d2_slot_full[sl]);
+            else mma_commit(&d2_full[s]);
             if (s == kSubs - 1) mma_commit(&slot_empty[sl]);
           }
           __syncwarp();
@@ -845,7 +857,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     // and TMA stores: no CTA-wide barrier on this path).
     const uint32_t q = warp & 3;
     const uint32_t grp = (warp - kWarpOut0) >> 2;
-    const uint32_t trow = tmem + ((q * 32) << 16) + kTmemD2 + kSub * (grp % G::kD2Bufs);
+    // D2 of this group's sub-block: its own buffer, or (kH = 32, group 0) the
+    // free columns of unit h's D1 slot
+    const bool d2_in_slot = G::kD2Bufs != kSubs && grp == 0;
+    const uint32_t trow_base = tmem + ((q * 32) << 16);
+    const uint32_t trow_fixed = trow_base + kTmemD2 + (G::kD2Bufs == kSubs ? kSub * grp : 0);
     const RuleConsts rc = p.rule;
     const uint32_t K = vn ? G::kVnK : 128u * G::kCentreW;  // Z = R + K state
     SimdRule sr;
@@ -879,10 +895,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     int band, t0, t1;
     while (it.next(band, t0, t1)) {
       for (int t = t0; t < t1; ++t, ++h) {
-        LTL_WAIT(9 + (warp - kWarpOut0), &d2_full[grp], h & 1);
+        if (d2_in_slot) LTL_WAIT(9 + (warp - kWarpOut0), &d2_slot_full[h % kSlots], (h / kSlots) & 1);
+        else LTL_WAIT(9 + (warp - kWarpOut0), &d2_full[grp], h & 1);
         if (lane == 0 && warp == kWarpOut0) LTL_TRACE(5, h);
         if (lane == 0 && warp == kWarpOut0 + 4) LTL_TRACE(7, h);
         tc_fence_after();
+        const uint32_t trow =
+            d2_in_slot ? trow_base + kTmemSlot + kSlotCols * (h % kSlots) + G::kD2InSlot : trow_fixed;
         uint32_t z[2][2][8];  // [tile (rows 32*tt ..)][lane half][register]
 #pragma unroll
         for (int tt = 0; tt < 2; ++tt) {
@@ -891,7 +910,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         tmem_ld_wait();
         tc_fence_before();
-        mbar_arrive(&d2_empty[grp]);
+        if (d2_in_slot) mbar_arrive(&slot_empty[h % kSlots]);
+        else mbar_arrive(&d2_empty[grp]);
         if (lane == 0 && warp == kWarpOut0) LTL_TRACE(6, h);
         uint32_t w[2][2][4];  // [tile][lane half][stmatrix register]
 #pragma unroll
