@@ -117,7 +117,11 @@ struct Geo {
   // D2 goes into the free columns [kD2InSlot, +64) of the unit's D1 slot
   // (the planes use [0, 80)), so the slot is free once pass 2 is done AND
   // output group 0 has read it (slot_empty counts both).
+#ifdef LTL_D2_SLOT16  // A/B: the same for the kH = 16 boxes (planes [0, 72), D2 [96, 160))
+  static constexpr int kD2Bufs = 1;
+#else
   static constexpr int kD2Bufs = kH == 16 ? 2 : 1;
+#endif
   static constexpr uint32_t kD2InSlot = kBox - kSub;       // 128 (kH = 32)
   // centre weight W of pass 2 (Moore: Z = R + 128 W state must clear R <= (2r+1)^2)
   static constexpr uint32_t kCentreW = kH == 16 ? 16u : 64u;   // K = 2048 / 8192
@@ -149,6 +153,7 @@ struct Geo {
   static constexpr uint32_t kTmemD2 = kTmemSlot + kSlots * kSlotCols;
   static constexpr uint32_t kTmemA1 = kTmemD2 + kD2Bufs * kSub;  // pass-1 A: 192 k / 4 = 48
   static_assert(kPiOff + kPiCols <= kSlotCols, "planes fit in the D1 slot");
+  static_assert(kD2Bufs == kSubs || kPiOff + kPiCols <= kD2InSlot, "slot D2 clear of the planes");
   static_assert(kTmemA1 + kKChunks * 8 <= kTmemCols, "TMEM budget");
   static_assert(kSlotCols % 8 == 0 && kPiOff % 8 == 0 && kTmemD2 % 8 == 0, "A operand alignment");
 
@@ -428,7 +433,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int i = 0; i < kSlots; ++i) {
       mbar_init(&d1_full[i], 1);
       mbar_init(&a2_full[i], kConvThreads);
-      mbar_init(&slot_empty[i], kH == 16 ? 1 : 1 + kGroupThreads);
+      mbar_init(&slot_empty[i], G::kD2Bufs == kSubs ? 1 : 1 + kGroupThreads);
     }
     for (int i = 0; i < kSubs; ++i) {
       mbar_init(&d2_full[i], 1);
@@ -773,8 +778,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint32_t pi = tmem + kTmemSlot + kSlotCols * sl + kPiOff + 16 * s;
 #pragma unroll
             for (int c = 0; c < nb; ++c) mma_i8_ts(dcol, pb + 8 * c, tile(c), G::kIdesc2, c > 0);
+#ifndef LTL_DIAG_NO_CENTRE  // timing probe only (wrong results): pass 2 without the centre chunks
             mma_i8_ts(dcol, pi, tile(ti), G::kIdesc2, 1);
             mma_i8_ts(dcol, pi + 8, tile(ti + 1), G::kIdesc2, 1);
+#endif
             if (G::kD2Bufs != kSubs && s == 0) mma_commit(&d2_slot_full[sl]);
             else mma_commit(&d2_full[s]);
             if (s == kSubs - 1) mma_commit(&slot_empty[sl]);
