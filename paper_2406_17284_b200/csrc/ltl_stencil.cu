@@ -23,7 +23,9 @@
 // Templated on the radius so every window offset is a compile-time constant.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 #include <utility>
 
 #include "ltl_kernels.cuh"
@@ -81,6 +83,34 @@ struct SimdRule {
   // live cell whose count R - (mult - m) is negative (the reference's guard)
   __device__ __forceinline__ uint32_t negative(uint32_t z) const {
     return (z + g_live) & ~(z + g_neg) & 0x80008000u;
+  }
+};
+
+// The same rule on FOUR cells per register (8-bit lanes hold Z = R + 64 state,
+// < 128): usable while R < 64 -- Moore r <= 3 (R <= 49), VN r <= 15
+// (R <= 62).  Bit 7 of each byte of the result = next state.  Half the
+// instructions of two 16-bit pairs, and no widening of the sums.
+constexpr uint32_t kByteK = 64;
+template <int R, int KIND>
+__host__ __device__ constexpr bool byte_rule() { return KIND == 0 ? R <= 3 : R <= 15; }
+
+struct ByteRule {
+  uint32_t ca, cb, cc, cd, g_live, g_neg;
+  __device__ ByteRule(const RuleConsts& rc) {
+    ca = (0x80u - rc.lo_dead) * 0x01010101u;
+    cb = (0x7Fu - (rc.lo_dead + rc.w_dead)) * 0x01010101u;
+    cc = (0x80u - (kByteK + rc.lo_live)) * 0x01010101u;
+    cd = (0x7Fu - (kByteK + rc.lo_live + rc.w_live)) * 0x01010101u;
+    g_live = (0x80u - kByteK) * 0x01010101u;
+    g_neg = (0x80u - (kByteK + rc.neg_live)) * 0x01010101u;
+  }
+  // four next states as 0/1 bytes
+  __device__ __forceinline__ uint32_t next4(uint32_t z) const {
+    const uint32_t a = z + ca, b = z + cb, c = z + cc, d = z + cd;
+    return (lop3<0x70>(lop3<0xBA>(a, b, c), c, d) >> 7) & 0x01010101u;
+  }
+  __device__ __forceinline__ uint32_t negative(uint32_t z) const {
+    return (z + g_live) & ~(z + g_neg) & 0x80808080u;
   }
 };
 
@@ -187,9 +217,11 @@ __global__ void __launch_bounds__(kThreads)
   const int nrows = max(0, min(kBaseTY / 8, in.rows - (y0 + ys)));
   const bool full_word = x + 3 < in.cols;
   uint8_t* optr = out.buf + out.offset(y0 + ys + kHalo, min(x, in.cols - 1));
+  constexpr bool kByte = byte_rule<R, KIND>();  // R < 64: sums and rule in byte lanes
+  const ByteRule br(rc);
   for (int yy = 0; yy < nrows; ++yy, optr += kStrip) {
     const int y = ys + yy;  // output row within the chunk
-    uint32_t acc_lo = 0, acc_hi = 0, h_centre = 0, v_cross = 0;
+    uint32_t acc_lo = 0, acc_hi = 0, acc_b = 0, h_centre = 0, v_cross = 0;
 #pragma unroll
     for (int dy = -R; dy <= R; ++dy) {
       const uint32_t* trow =
@@ -202,7 +234,9 @@ __global__ void __launch_bounds__(kThreads)
 #pragma unroll
         for (int dx = -R; dx <= R; ++dx) h += bytes_at(w, 16 + dx - 4 * kW0);
         if (dy == 0) h_centre = h;
-        if (KIND == 0) {
+        if (KIND == 0 && kByte) {
+          acc_b += h;  // <= 49
+        } else if (KIND == 0) {
           acc_lo += widen_lo(h);
           acc_hi += widen_hi(h);
         }
@@ -210,24 +244,37 @@ __global__ void __launch_bounds__(kThreads)
       if (KIND == 1) v_cross += bytes_at(w, 16 - 4 * kW0);  // column sum, byte lanes
     }
     const uint32_t st = *reinterpret_cast<const uint32_t*>(tile + (kHalo + y) * kTileW + 16 + 4 * j);
-    if (KIND == 1) {  // R = H + V (centre twice), plus 128 * state: all < 256
-      const uint32_t zb = h_centre + v_cross + (st << 7);
-      acc_lo = widen_lo(zb);
-      acc_hi = widen_hi(zb);
+    uint32_t nw;
+    if constexpr (kByte) {  // Z = R + 64 state in byte lanes
+      const uint32_t zb = (KIND == 0 ? acc_b : h_centre + v_cross) + st * kByteK;
+      nw = br.next4(zb);
+      if constexpr (kChecked) {
+        max_h = __vmaxu4(max_h, h_centre & hmask);
+        max_r = __vmaxu4(max_r, zb & ((kByteK - 1) * 0x01010101u) & hmask);
+        bad |= br.negative(zb) & hmask;
+      }
     } else {
-      acc_lo += widen_lo(st) << 11;
-      acc_hi += widen_hi(st) << 11;
-    }
-    const uint32_t nw = next_word(sr.pair(acc_lo), sr.pair(acc_hi));
-    if constexpr (kChecked) {
-      max_h = __vmaxu4(max_h, h_centre & hmask);
-      max_r = __vmaxu2(max_r, acc_lo & sr.r_mask & rmask_lo);
-      max_r = __vmaxu2(max_r, acc_hi & sr.r_mask & rmask_hi);
-      bad |= (sr.negative(acc_lo) & rmask_lo) | (sr.negative(acc_hi) & rmask_hi);
+      if (KIND == 1) {  // R = H + V (centre twice), plus 128 * state: all < 256
+        const uint32_t zb = h_centre + v_cross + (st << 7);
+        acc_lo = widen_lo(zb);
+        acc_hi = widen_hi(zb);
+      } else {
+        acc_lo += widen_lo(st) << 11;
+        acc_hi += widen_hi(st) << 11;
+      }
+      nw = next_word(sr.pair(acc_lo), sr.pair(acc_hi));
+      if constexpr (kChecked) {
+        max_h = __vmaxu4(max_h, h_centre & hmask);
+        max_r = __vmaxu2(max_r, acc_lo & sr.r_mask & rmask_lo);
+        max_r = __vmaxu2(max_r, acc_hi & sr.r_mask & rmask_hi);
+        bad |= (sr.negative(acc_lo) & rmask_lo) | (sr.negative(acc_hi) & rmask_hi);
+      }
     }
     if (full_word) *reinterpret_cast<uint32_t*>(optr) = nw;
     else if (x < in.cols) store_word(out, y0 + y, x, nw);
   }
+  if constexpr (kChecked && kByte)  // byte-lane R maxima -> the 16-bit layout flush_stats reduces
+    max_r = max(max(max_r & 0xFF, (max_r >> 8) & 0xFF), max((max_r >> 16) & 0xFF, max_r >> 24));
   if constexpr (kChecked) flush_stats(stats, max_h, max_r, bad);
 }
 
@@ -354,14 +401,20 @@ __global__ void __launch_bounds__(kThreads)
   const int seg = threadIdx.x >> 5;
   const int x = x_strip + 4 * j;
   constexpr uint32_t K = KIND == 0 ? 2048u : 128u;
+  constexpr bool kByte = byte_rule<R, KIND>();  // R < 64: sums and rule in byte lanes
   const SimdRule sr(rc, K);
+  const ByteRule br(rc);
   const uint32_t rmask_lo = (x < in.cols ? 0xFFFFu : 0u) | (x + 1 < in.cols ? 0xFFFF0000u : 0u);
   const uint32_t rmask_hi = (x + 2 < in.cols ? 0xFFFFu : 0u) | (x + 3 < in.cols ? 0xFFFF0000u : 0u);
+  const uint32_t rmask_b = x + 3 < in.cols ? 0xFFFFFFFFu
+                           : (x >= in.cols ? 0u : (1u << (8 * (in.cols - x))) - 1u);
   constexpr int kSeg = kPackTY / 8;
   const int ys = seg * kSeg;
   const uint32_t* hcol = htile + j;  // H word of H row k: hcol[k * kHStride]
   const uint8_t* ccol = tile + 16 + 4 * j;
-  uint32_t lo = 0, hi = 0;  // Moore: R lanes; VN: V (vertical cell sums) bytes in lo
+  // Moore: R lanes (byte lanes when kByte, else 16-bit lo / hi); VN: V (vertical
+  // cell sums) bytes in lo
+  uint32_t lo = 0, hi = 0;
   if (KIND == 0) {
     // R(ys) = sum of H rows ys .. ys + 2r (H row k = interior row y0 - r + k);
     // byte lanes for up to 7 rows (<= 231), then widened
@@ -369,12 +422,13 @@ __global__ void __launch_bounds__(kThreads)
 #pragma unroll
     for (int k = 0; k <= 2 * R; ++k) {
       g += hcol[(ys + k) * kHStride];
-      if (k % 7 == 6 || k == 2 * R) {
+      if (!kByte && (k % 7 == 6 || k == 2 * R)) {
         lo += widen_lo(g);
         hi += widen_hi(g);
         g = 0;
       }
     }
+    if (kByte) lo = g;  // <= 49
   } else {
 #pragma unroll
     for (int k = -R; k <= R; ++k) lo += *reinterpret_cast<const uint32_t*>(ccol + (kHalo + ys + k) * kTileW);
@@ -390,7 +444,11 @@ __global__ void __launch_bounds__(kThreads)
   const uint8_t* const c_mid = ccol + (kHalo + ys) * kTileW;
   auto row = [&](int yy) {
     if (yy > 0) {
-      if (KIND == 0) {
+      if (KIND == 0 && kByte) {
+        // R += H(y + r) - H(y - r - 1), byte lanes: the sum before the
+        // subtraction is >= the subtrahend in every lane (no borrow)
+        lo = lo + h_in[yy * kHStride] - h_in[(yy - 2 * R - 1) * kHStride];
+      } else if (KIND == 0) {
         // R += H(y + r) - H(y - r - 1): a biased byte difference (31..97), widened
         const uint32_t d = h_in[yy * kHStride] + 0x40404040u - h_in[(yy - 2 * R - 1) * kHStride];
         lo += widen_lo(d) - 0x00400040u;
@@ -401,20 +459,31 @@ __global__ void __launch_bounds__(kThreads)
       }
     }
     const uint32_t st = *reinterpret_cast<const uint32_t*>(c_mid + yy * kTileW);
-    uint32_t zl, zh;
-    if (KIND == 0) {
-      zl = lo + (widen_lo(st) << 11);
-      zh = hi + (widen_hi(st) << 11);
-    } else {  // R = H + V (centre twice), + 128 * state: all < 256 in byte lanes
-      const uint32_t zb = h_mid[yy * kHStride] + lo + (st << 7);
-      zl = widen_lo(zb);
-      zh = widen_hi(zb);
-    }
-    const uint32_t nw = next_word(sr.pair(zl), sr.pair(zh));
-    if constexpr (kChecked) {
-      max_r = __vmaxu2(max_r, zl & sr.r_mask & rmask_lo);
-      max_r = __vmaxu2(max_r, zh & sr.r_mask & rmask_hi);
-      bad |= (sr.negative(zl) & rmask_lo) | (sr.negative(zh) & rmask_hi);
+    uint32_t nw;
+    if constexpr (kByte) {
+      // Z = R + 64 state in byte lanes (R < 64): Moore R = lo, VN R = H + V
+      const uint32_t zb = (KIND == 0 ? lo : h_mid[yy * kHStride] + lo) + st * kByteK;
+      nw = br.next4(zb);
+      if constexpr (kChecked) {
+        max_r = __vmaxu4(max_r, zb & ((kByteK - 1) * 0x01010101u) & rmask_b);
+        bad |= br.negative(zb) & rmask_b;
+      }
+    } else {
+      uint32_t zl, zh;
+      if (KIND == 0) {
+        zl = lo + (widen_lo(st) << 11);
+        zh = hi + (widen_hi(st) << 11);
+      } else {  // R = H + V (centre twice), + 128 * state: all < 256 in byte lanes
+        const uint32_t zb = h_mid[yy * kHStride] + lo + (st << 7);
+        zl = widen_lo(zb);
+        zh = widen_hi(zb);
+      }
+      nw = next_word(sr.pair(zl), sr.pair(zh));
+      if constexpr (kChecked) {
+        max_r = __vmaxu2(max_r, zl & sr.r_mask & rmask_lo);
+        max_r = __vmaxu2(max_r, zh & sr.r_mask & rmask_hi);
+        bad |= (sr.negative(zl) & rmask_lo) | (sr.negative(zh) & rmask_hi);
+      }
     }
     if (full_word) *reinterpret_cast<uint32_t*>(optr + yy * kStrip) = nw;
     else if (x < in.cols) store_word(out, y0 + ys + yy, x, nw);
@@ -425,7 +494,11 @@ __global__ void __launch_bounds__(kThreads)
   } else {
     for (int yy = 0; yy < nrows; ++yy) row(yy);
   }
-  if constexpr (kChecked) flush_stats(stats, max_h, max_r, bad);
+  if constexpr (kChecked) {
+    // byte-lane R maxima -> the 16-bit layout flush_stats reduces
+    if (kByte) max_r = max(max(max_r & 0xFF, (max_r >> 8) & 0xFF), max((max_r >> 16) & 0xFF, max_r >> 24));
+    flush_stats(stats, max_h, max_r, bad);
+  }
 }
 
 template <int R>
@@ -440,7 +513,24 @@ cudaError_t launch_r(const SlabView& in, const SlabView& out, const RuleConsts& 
   const int strips = interior_strips(in.cols);
   const int ty = engine == kEnginePack ? kPackTY : kBaseTY;
   const dim3 grid(strips, (in.rows + ty - 1) / ty);
-  const size_t smem = engine == kEnginePack ? pack_smem_bytes<R>() : 0;
+  // pack: at most four CTAs per SM.  At r = 1 the tile + H rows (45.3 KB)
+  // would let five in, and five run 29 % slower (620 vs 480 us at 32768^2,
+  // same-box A/B: the fifth CTA's row pass floods the shared-memory
+  // instruction queue, ncu stall mio_throttle 10.9 vs 2.0); three or fewer
+  // are slower again (520 / 674 us).
+  constexpr size_t kPackSmemFloor = 47000;
+  size_t smem = engine == kEnginePack ? std::max(pack_smem_bytes<R>(), kPackSmemFloor) : 0;
+  if (engine == kEnginePack)
+    if (const char* e = std::getenv("LTL_PACK_MIN_SMEM"))  // A/B: CTAs per SM
+      smem = std::max<size_t>(pack_smem_bytes<R>(), static_cast<size_t>(std::atol(e)));
+  // base: its 28 KB static tile would let seven CTAs in; 10 KB of unused
+  // dynamic padding keeps five, 1.26x faster at r = 1 (682 -> 541 us at
+  // 32768^2, same-box A/B; r = 2 / 3: 861 -> 749, 1189 -> 1075 us).
+  if (engine == kEngineBase) {
+    smem = 10000;
+    if (const char* e = std::getenv("LTL_BASE_PAD_SMEM"))  // A/B: CTAs per SM
+      smem = static_cast<size_t>(std::atol(e));
+  }
   if (smem > 48 * 1024) {
     // the attribute is per device: set once on each (a per-launch call
     // serialises launches measurably)
