@@ -3,7 +3,7 @@
 "cell updates/sec vs radius r=1..16 at 1/2/4/8 B200; % of roofline").
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--workload c1|c2|c3|c4] [--engine cat|base|pack]
+                    [--workload c1|c2|c3|c4] [--engine cat|base|pack|cat-4bit]
 
 Workloads (BASELINE.json configs; all grids from init_random(n, density,
 seed 1), generated on the device bit-identically to the reference's
@@ -54,6 +54,7 @@ BYTES_PER_CELL = 2   # read 1 B state + write 1 B next state
 OPS_ALG = 192        # the reference's 6 fragment MMAs x 2*16^3 / 16^2
 OPS_EXEC = 800       # tcgen05 kind::i8 ops the kernel issues per cell
 OPS_EXEC_WIDE = 960  # the same for the r = 17..32 boxes (6 x M128.N192.K32 + 12 x M128.N64.K32)
+OPS_EXEC_4BIT = 880  # 4-bit cells: + one bias MMA (M128.N160.K32 kind::f8f6f4) per 128 x 128 unit
 BOSCO = "R5,C2,M1,S34..58,B34..45,NM"
 
 WORKLOADS = {
@@ -348,6 +349,9 @@ def ours_single(args):
     n = workload_side(workload)
     rules = workload_rules(workload)
     engine = args.engine
+    mma_engine = engine in ("cat", "cat-4bit")
+    # algorithmic bytes per cell update: u8 cells 2 (read + write), 4-bit cells 1
+    bpc = 1 if engine == "cat-4bit" else BYTES_PER_CELL
     torus = ltl.DeviceTorus(rows=n, cols=n)
 
     clocks = Clocks(torch.cuda.current_device())
@@ -369,7 +373,7 @@ def ours_single(args):
     hbm = peaks["hbm_gbs"]
     p_mma, mma_src = mma_i8_peak()
     for e in per:
-        e["hbm_frac"] = BYTES_PER_CELL * n * n / (e["ms_per_generation"] / 1e3) / 1e9 / hbm
+        e["hbm_frac"] = bpc * n * n / (e["ms_per_generation"] / 1e3) / 1e9 / hbm
     ms_step = sum(e["ms_per_generation"] for e in per)
     value = min(e["cell_updates_per_s"] for e in per)
     # The timed region launches the step kernel only (gpu_launches = one per
@@ -379,10 +383,11 @@ def ours_single(args):
     # of consecutive launches and reads ~4 % longer.)
     kern_avg_s = statistics.mean(e["ms_per_generation"] for e in per) / 1e3
     kern_iso_s = statistics.mean(e["kernel_ms_isolated"] for e in per) / 1e3
-    achieved = BYTES_PER_CELL * n * n / kern_avg_s / 1e9
-    ceiling_hbm = hbm * 1e9 / BYTES_PER_CELL
-    ops_exec = OPS_EXEC_WIDE if workload == "wide" else OPS_EXEC
-    ceiling_mma = p_mma / ops_exec if engine == "cat" else None
+    achieved = bpc * n * n / kern_avg_s / 1e9
+    ceiling_hbm = hbm * 1e9 / bpc
+    ops_exec = (OPS_EXEC_WIDE if workload == "wide" else
+                OPS_EXEC_4BIT if engine == "cat-4bit" else OPS_EXEC)
+    ceiling_mma = p_mma / ops_exec if mma_engine else None
 
     # e2e through the public C-ABI (ltl_run_interior = run_engine(Cat)):
     # pinned host grids, upload + K generations + download per radius
@@ -407,7 +412,9 @@ def ours_single(args):
         "data": "synthetic (device init_random, splitmix64 grids identical to the reference's)",
         "config": dict(config_dict(workload, 1),
                        engine={"cat": "tcgen05 banded-MMA", "base": "CUDA-core direct-sum stencil",
-                               "pack": "CUDA-core packed sliding-window stencil"}[engine],
+                               "pack": "CUDA-core packed sliding-window stencil",
+                               "cat-4bit": "tcgen05 banded-MMA on 4-bit device cells "
+                                           "(pass 1 kind::f8f6f4 e4m3 x e2m1)"}[engine],
                        step=(f"one generation of each of the {len(rules)} radii"
                              if len(rules) > 1 else "one generation")),
         "aggregate_value": n * n * len(rules) / (ms_step / 1e3),
@@ -422,19 +429,19 @@ def ours_single(args):
         "gpu_launches": launches,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                      "frac": achieved / hbm, "traffic": None, "peak_source": peak_src,
-                     "kernel": "ltl_tc_step_kernel" if engine == "cat" else f"{engine} stencil",
+                     "kernel": "ltl_tc_step_kernel" if mma_engine else f"{engine} stencil",
                      "kernel_ms_per_generation": kern_avg_s * 1e3,
                      "kernel_ms_isolated": kern_iso_s * 1e3,
-                     "algorithmic_bytes_per_generation": BYTES_PER_CELL * n * n,
+                     "algorithmic_bytes_per_generation": bpc * n * n,
                      "per": ("generation: timed-region event time / launches (one step-kernel "
                              "launch per generation), mean over the radii"),
                      "ceiling_cells_per_s_hbm": ceiling_hbm,
                      "ceiling_cells_per_s_mma": ceiling_mma,
-                     "mma_peak_ops": p_mma if engine == "cat" else None,
-                     "mma_peak_source": mma_src if engine == "cat" else None,
+                     "mma_peak_ops": p_mma if mma_engine else None,
+                     "mma_peak_source": mma_src if mma_engine else None,
                      "ops_per_cell_algorithmic": OPS_ALG, "ops_per_cell_executed":
-                         ops_exec if engine == "cat" else None,
-                     "mma_frac": (value * ops_exec / p_mma) if engine == "cat" else None},
+                         ops_exec if mma_engine else None,
+                     "mma_frac": (value * ops_exec / p_mma) if mma_engine else None},
         "clocks": clk,
     }
     ncu_name = f"ncu_tc_step_{'wide_' if workload == 'wide' else ''}{n}.json"
@@ -592,7 +599,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--workload", choices=tuple(WORKLOADS), default=None)
-    ap.add_argument("--engine", choices=("cat", "base", "pack"), default="cat")
+    ap.add_argument("--engine", choices=("cat", "base", "pack", "cat-4bit"), default="cat")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--dist", action="store_true",
                     help="the multi-process slab path even at world size 1 (testing)")

@@ -66,6 +66,16 @@ extern "C" {
  * ltl_parse_rule_ext(text, 32, ...). */
 #define LTL_FLAG_WIDE_RADIUS 0x20u
 #define LTL_MAX_WIDE_RADIUS 32
+/* Cell storage of the Cat engine on the device (opt-in).
+ * LTL_FLAG_4BIT_CELLS: where the geometry allows it -- one whole-torus slab,
+ * cols % 128 == 0, rows % 32 == 0, r <= 16 -- the generations of the call step
+ * a 4-bit copy of the grid (two cells per byte: B_alg = 1 byte per cell update
+ * instead of 2; pass 1 on tcgen05.mma kind::f8f6f4, e4m3 band weights x e2m1
+ * cells, f16 accumulators), converted from / back to the u8 slab at the start /
+ * end of the call; elsewhere the flag is ignored (u8 cells).  Same bytes as the
+ * u8 path.  Not the default: the step is bound by its instruction issue, not
+ * by HBM, so halving the bytes does not pay. */
+#define LTL_FLAG_4BIT_CELLS 0x40u
 
 /* catsim::LtlRule, proj/include/catsim/rule.hpp:17-32 */
 typedef struct ltl_rule_c {

@@ -57,6 +57,20 @@ struct SlabView {
   __host__ __device__ __forceinline__ int64_t bytes() const { return strips * strip_bytes; }
 };
 
+// 4-bit copy of a slab for the packed tcgen05 step: the same strips and padded
+// rows, 64 bytes per strip row, cell x of a row in the low (x even) or high
+// nibble of byte x / 2 (nibble value 1 = alive: e2m1 0.5, the pass-1 B operand
+// as it is).  B_alg = 1 byte per cell update.
+constexpr int kPkRow = kStrip / 2;
+struct PackedView {
+  uint8_t* buf;
+  int32_t rows;
+  int32_t cols;
+  int32_t strips;       // storage strips (as SlabView)
+  int64_t strip_bytes;  // (rows + 2 * kHalo) * kPkRow
+  __host__ __device__ __forceinline__ int64_t bytes() const { return strips * strip_bytes; }
+};
+
 __host__ __device__ inline int32_t interior_strips(int32_t cols) {
   return (cols + kStrip - 1) / kStrip;
 }
@@ -156,15 +170,23 @@ struct TcLaunch {
                        // the loads: wrap_cols and wrap_rows or ring; maps built for 32)
   int32_t grid;        // CTAs (0 = auto)
   long long* trace;    // debug timeline (LTL_TC_TRACE), nullptr = off
+  int32_t packed;      // 4-bit cells: maps over PackedSlab buffers (halo 16, whole-torus
+                       // slab, every wrap by the loads)
 };
 cudaError_t launch_tc_step(const TcLaunch& a, cudaStream_t stream);
 int tc_persistent_ctas(int32_t rows, int32_t cols, int num_sms);  // 0: no multi-generation launch
 int tc_sweep_chunks(int32_t strips, int32_t bands, int ctas);  // chunks per band of a multi-generation launch
-size_t tc_smem_bytes(int halo);
+size_t tc_smem_bytes(int halo, bool packed = false);
 
 // Host-side tensor-map builders (driver entry point fetched at runtime).
 cudaError_t make_load_maps(CUtensorMap* maps, const SlabView& s, int halo = kHalo);
 cudaError_t make_store_map(CUtensorMap* map, const SlabView& s);
+// The same over the 4-bit copy of a slab (PackedView: 64-byte strip rows):
+// loads as 16U4_ALIGN16B boxes (the padded e2m1 operand layout, SWIZZLE_128B),
+// stores of 64 x 64-byte staging tiles (SWIZZLE_64B).
+struct PackedView;
+cudaError_t make_load_maps_packed(CUtensorMap* maps, const PackedView& s);
+cudaError_t make_store_map_packed(CUtensorMap* map, const PackedView& s);
 // halo-row (16 / 32) SWIZZLE_128B pieces over a slab (the ring's rows from a neighbour).
 cudaError_t make_piece_map(CUtensorMap* map, const SlabView& s, int halo = kHalo);
 
@@ -205,6 +227,9 @@ cudaError_t launch_from_strips(const SlabView& s, uint8_t* dense, cudaStream_t s
 // cols multiples of f) <-> strip slab interior.
 cudaError_t launch_frag_relayout(uint8_t* dense, const SlabView& s, int f, bool to_strips,
                                  cudaStream_t stream);
+// u8 slab <-> its 4-bit copy (every padded row of every strip).
+cudaError_t launch_pack_cells(const SlabView& s, const PackedView& pk, cudaStream_t stream);
+cudaError_t launch_unpack_cells(const PackedView& pk, const SlabView& s, cudaStream_t stream);
 // *bad |= 1 if any of dense[0, n) is not 0 / 1 (snapshot payloads).
 cudaError_t launch_check_cells(const uint8_t* dense, int64_t n, int32_t* bad,
                                cudaStream_t stream);

@@ -110,6 +110,32 @@ __global__ void check_cells_kernel(const uint8_t* dense, int64_t n, int32_t* bad
   if (__syncthreads_or(acc != 0) && threadIdx.x == 0) atomicOr(bad, 1);
 }
 
+// u8 strips <-> 4-bit strips: 16 cells per thread (one uint4 <-> one uint2);
+// strip-major in both, so a flat index walks both buffers in order.  Cells
+// 2i, 2i+1 -> low / high nibble of byte i.
+__device__ __forceinline__ uint32_t pack4(uint32_t w) {  // 4 cells -> 2 bytes in bits 0..15
+  const uint32_t t = w | (w >> 4);                      // bytes 0 / 2: c0 | c1 << 4, c2 | c3 << 4
+  return __byte_perm(t, 0, 0x4420);
+}
+__device__ __forceinline__ uint32_t unpack4(uint32_t p) {  // 2 bytes (bits 0..15) -> 4 cells
+  const uint32_t t = __byte_perm(p, 0, 0x1100);              // p0 p0 p1 p1
+  return (t & 0x000F000Fu) | ((t >> 4) & 0x0F000F00u);
+}
+__global__ void pack_cells_kernel(const uint4* u8, uint2* pk, int64_t n16) {
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n16; i += stride) {
+    const uint4 v = u8[i];
+    pk[i] = make_uint2(pack4(v.x) | (pack4(v.y) << 16), pack4(v.z) | (pack4(v.w) << 16));
+  }
+}
+__global__ void unpack_cells_kernel(const uint2* pk, uint4* u8, int64_t n16) {
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n16; i += stride) {
+    const uint2 p = pk[i];
+    u8[i] = make_uint4(unpack4(p.x), unpack4(p.x >> 16), unpack4(p.y), unpack4(p.y >> 16));
+  }
+}
+
 int blocks_for(int64_t work) {
   int64_t b = (work + 255) / 256;
   if (b > 148 * 8) b = 148 * 8;
@@ -146,6 +172,24 @@ cudaError_t launch_frag_relayout(uint8_t* dense, const SlabView& s, int f, bool 
     case 8: frag_relayout_kernel<4, false><<<blocks, 256, 0, stream>>>(dense, s); break;
     default: return cudaErrorInvalidValue;
   }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_pack_cells(const SlabView& s, const PackedView& pk, cudaStream_t stream) {
+  if (s.rows <= 0 || s.cols <= 0) return cudaSuccess;
+  if (pk.bytes() * 2 != s.bytes()) return cudaErrorInvalidValue;
+  const int64_t n16 = s.bytes() / 16;
+  pack_cells_kernel<<<blocks_for(n16), 256, 0, stream>>>(reinterpret_cast<const uint4*>(s.buf),
+                                                         reinterpret_cast<uint2*>(pk.buf), n16);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_unpack_cells(const PackedView& pk, const SlabView& s, cudaStream_t stream) {
+  if (s.rows <= 0 || s.cols <= 0) return cudaSuccess;
+  if (pk.bytes() * 2 != s.bytes()) return cudaErrorInvalidValue;
+  const int64_t n16 = s.bytes() / 16;
+  unpack_cells_kernel<<<blocks_for(n16), 256, 0, stream>>>(reinterpret_cast<const uint2*>(pk.buf),
+                                                           reinterpret_cast<uint4*>(s.buf), n16);
   return cudaGetLastError();
 }
 

@@ -73,9 +73,17 @@ struct Slab {
   bool ring_ready = false;                    // peers wired
   uint32_t ring_gen = 0;                      // steps since the last ring start
   std::vector<void*> ipc_opened;              // IPC mappings to close
+  // 4-bit copy of the two generations (LTL_FLAG_4BIT_CELLS), allocated on
+  // the first packed run, and its tensor maps
+  uint8_t* pbuf[2] = {nullptr, nullptr};
+  CUtensorMap pload_maps[2][ltl::kTcLoadMaps];
+  CUtensorMap pstore_map[2];
 
   ltl::SlabView view(int which, int32_t cols) const {
     return ltl::SlabView{buf[which], rows, cols, strips, strip_bytes};
+  }
+  ltl::PackedView pview(int which, int32_t cols) const {
+    return ltl::PackedView{pbuf[which], rows, cols, strips, strip_bytes / 2};
   }
 };
 
@@ -94,6 +102,11 @@ struct ltl_ctx {
   size_t pinned_bytes = 0;
   std::vector<Slab> slabs;
   std::string err;
+  // 4-bit cells: pk_live = the current generation is pbuf[pk_cur] (buf[cur] is
+  // stale); pk_hold = keep it there between enqueues (inside ltl_time only:
+  // every public call returns with the u8 slab current)
+  bool pk_live = false, pk_hold = false;
+  int pk_cur = 0;
 };
 
 namespace {
@@ -314,6 +327,8 @@ void destroy_ctx(ltl_ctx* ctx) {
     if (s.stream) cudaStreamSynchronize(s.stream);
     for (auto& b : s.buf)
       if (b) cudaFree(b);
+    for (auto& b : s.pbuf)
+      if (b) cudaFree(b);
     if (s.dstats) cudaFree(s.dstats);
     if (s.flags) cudaFree(s.flags);
     for (void* ptr : s.ipc_opened) cudaIpcCloseMemHandle(ptr);
@@ -432,11 +447,97 @@ bool persistent_ok(const ltl_ctx* ctx, uint32_t flags) {
   return true;
 }
 
+// 4-bit cells (LTL_FLAG_4BIT_CELLS): the Cat engine on one whole-torus slab
+// whose every wrap the step loads itself, r <= 16.
+bool packed_ok(const ltl_ctx* ctx, uint32_t flags, const ltl::RuleConsts& rc) {
+  if (stencil_engine(flags) || !(flags & LTL_FLAG_4BIT_CELLS)) return false;
+  return rc.r <= kHalo && ctx->slabs.size() == 1 && wrap_cols(ctx) && wrap_rows(ctx) &&
+         ctx->slabs[0].rows > 0;
+}
+
+// The 4-bit copy back into the u8 slab (buf[cur]) if it holds the current generation.
+void settle_packed(ltl_ctx* ctx) {
+  if (!ctx->pk_live) return;
+  Slab& s = ctx->slabs[0];
+  ck(cudaSetDevice(s.dev), "cudaSetDevice");
+  ck(ltl::launch_unpack_cells(s.pview(ctx->pk_cur, ctx->cols), s.view(ctx->cur, ctx->cols),
+                              s.stream),
+     "unpack cells");
+  ++ctx->launches;
+  ctx->pk_live = false;
+  enqueue_halo(ctx, ctx->cur, true);  // (the wraps are the loads': marks the halo stale)
+}
+
+// `gens` generations of the packed Cat step: pack buf[cur] (unless the copy is
+// live), one persistent launch or one launch per generation ping-ponging the
+// two 4-bit buffers, unpack into buf[cur] (unless pk_hold).
+void enqueue_step_packed(ltl_ctx* ctx, const ltl::RuleConsts& rc, uint32_t flags,
+                         bool want_stats, cudaEvent_t* kt0, cudaEvent_t* kt1, int32_t gens) {
+  Slab& s = ctx->slabs[0];
+  ck(cudaSetDevice(s.dev), "cudaSetDevice");
+  if (!s.pbuf[0]) {
+    const size_t bytes = static_cast<size_t>(s.strips) * (s.strip_bytes / 2);
+    for (int b = 0; b < 2; ++b) {
+      ck(cudaMalloc(&s.pbuf[b], bytes), "cudaMalloc 4-bit slab");
+      ck(cudaMemsetAsync(s.pbuf[b], 0, bytes, s.stream), "memset 4-bit slab");
+      ck(ltl::make_load_maps_packed(s.pload_maps[b], s.pview(b, ctx->cols)), "tensor map (load)");
+      ck(ltl::make_store_map_packed(&s.pstore_map[b], s.pview(b, ctx->cols)), "tensor map (store)");
+    }
+  }
+  if (!ctx->pk_live) {
+    ck(ltl::launch_pack_cells(s.view(ctx->cur, ctx->cols), s.pview(ctx->pk_cur, ctx->cols),
+                              s.stream),
+       "pack cells");
+    ++ctx->launches;
+    ctx->pk_live = true;
+  }
+  const bool persist = gens > 1 && persistent_ok(ctx, flags);
+  if (kt0) ck(cudaEventRecord(kt0[0], s.stream), "event");
+  for (int32_t g = 0; g < (persist ? 1 : gens); ++g) {
+    const int pc = ctx->pk_cur;
+    ltl::TcLaunch a{};
+    a.packed = 1;
+    a.halo = kHalo;
+    a.load_maps = s.pload_maps[pc];
+    a.store_map = &s.pstore_map[1 - pc];
+    a.wrap_cols = 1;
+    a.wrap_rows = 1;
+    if (persist) {
+      a.load_maps_b = s.pload_maps[1 - pc];
+      a.store_map_b = &s.pstore_map[pc];
+      a.gens = gens;
+      a.flags = s.flags;
+      a.flag_base = s.flag_base;
+      s.flag_base += 2u * static_cast<uint32_t>(gens);
+    }
+    a.rows = s.rows;
+    a.cols = ctx->cols;
+    a.rule = rc;
+    a.inject_fault = (flags & LTL_FLAG_INJECT_FAULT) != 0;
+    a.fault_f = ctx->f;
+    a.fault_row_phase = s.row0 % ctx->f;
+    a.gen_base = ctx->gen_counter + g;
+    a.row0 = s.row0;
+    a.stats = want_stats ? s.dstats : nullptr;
+    ck(ltl::launch_tc_step(a, s.stream), "tcgen05 kernel (4-bit cells)");
+    ++ctx->launches;
+    if (!persist || (gens & 1)) ctx->pk_cur = 1 - pc;
+  }
+  if (kt1) ck(cudaEventRecord(kt1[0], s.stream), "event");
+  ctx->gen_counter += gens;
+  if (!ctx->pk_hold) settle_packed(ctx);
+}
+
 // `gens` generations (cur -> nxt -> ...): one persistent launch when
 // persistent_ok (gens > 1), else gens x (main kernel per slab + halo of nxt).
 void enqueue_step(ltl_ctx* ctx, const ltl::RuleConsts& rc, uint32_t flags, bool want_stats,
                   cudaEvent_t* kt0, cudaEvent_t* kt1, int32_t gens = 1) {
   if (gens <= 0) return;
+  if (packed_ok(ctx, flags, rc)) {
+    enqueue_step_packed(ctx, rc, flags, want_stats, kt0, kt1, gens);
+    return;
+  }
+  settle_packed(ctx);
   const bool persist = gens > 1 && persistent_ok(ctx, flags);
   if (gens > 1 && !persist) {
     for (int32_t t = 0; t < gens; ++t) enqueue_step(ctx, rc, flags, want_stats, nullptr, nullptr);
@@ -1084,6 +1185,21 @@ int ltl_time(ltl_ctx* ctx, const ltl_rule_c* rule, int32_t steps, int32_t warmup
     check_run_args(ctx, rule, steps, flags);
     const ltl::RuleConsts rc = rule_consts(*rule);
     const size_t G = ctx->slabs.size();
+    // 4-bit cells: the copy stays current across the warm-up, timed and
+    // sampled generations (converted once, outside the timed region); the
+    // u8 slab is brought back up to date before the call returns
+    struct Hold {
+      ltl_ctx* c;
+      ~Hold() {
+        c->pk_hold = false;
+        try {
+          settle_packed(c);
+          sync_all(c);
+        } catch (...) {
+        }
+      }
+    } hold{ctx};
+    ctx->pk_hold = true;
     enqueue_step(ctx, rc, flags, false, nullptr, nullptr, warmup);
     sync_all(ctx);
     // one persistent launch for all timed generations when possible
@@ -1139,6 +1255,9 @@ int ltl_time(ltl_ctx* ctx, const ltl_rule_c* rule, int32_t steps, int32_t warmup
         ker = std::max(ker, acc * steps / sample);
       }
     }
+    ctx->pk_hold = false;
+    settle_packed(ctx);
+    sync_all(ctx);
     if (total_ms) *total_ms = tot;
     if (kernel_ms) *kernel_ms = ker;
   });

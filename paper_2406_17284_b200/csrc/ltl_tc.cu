@@ -92,7 +92,6 @@ constexpr int kWarpOut0 = 2 + kConvWarps;
 constexpr int kWarpP2 = kWarpOut0 + kOutWarps;  // 14
 constexpr int kWarpStore = kWarpP2 + 1;           // 15
 constexpr uint32_t kTileBytes = kSub * 32;        // 2 KB pass-2 B tile [64 n][32 k]
-constexpr uint32_t kStageBytes = kSub * kStrip;   // 64 x 128 B = 8 KB output staging tile
 constexpr uint32_t kTmemCols = 512;               // all of the SM's TMEM
 static_assert(kSubs == 2 && kSlots == kSubs, "one output group per sub-block; barrier arrays sized kSubs");
 
@@ -104,15 +103,28 @@ static_assert(kSubs == 2 && kSlots == kSubs, "one output group per sub-block; ba
 //            band chunks, one D2 buffer shared by the two output groups
 //            (TMEM), 7 box stages and 2 staging slots per group (SMEM).
 // The pass-1 K range [-32, 160) already covers a horizontal radius of 32.
-template <int kH>
+template <int kH, bool kPk = false>
 struct Geo {
   static_assert(kH == 16 || kH == 32, "halo rows");
+  static_assert(!kPk || kH == 16, "4-bit cells: r <= 16 boxes only");
   static constexpr int kBox = kBand + 2 * kH;              // 160 / 192 box rows (one TMA box)
   static constexpr int kRowOff = kHalo - kH;               // padded row of box row 0, minus 128 b
   static constexpr int kBandChunks = (kSub + 2 * kH) / 32;  // pass-2 band K chunks: 3 / 4
   static constexpr int kNumTiles = kBandChunks + 4;         // + Iv0..1, W*Iv0..1
-  static constexpr int kXStages = kH == 16 ? 8 : 7;         // 3 boxes in use + prefetched
-  static constexpr int kStageSlots = kH == 16 ? 3 : 2;      // staging tiles per output group
+#ifndef LTL_PK_XSTAGES
+#define LTL_PK_XSTAGES 9
+#endif
+  static constexpr int kXStages = kPk ? LTL_PK_XSTAGES : kH == 16 ? 8 : 7;  // 3 in use + prefetched
+#ifndef LTL_PK_STAGE_SLOTS
+#define LTL_PK_STAGE_SLOTS 3
+#endif
+  static constexpr int kStageSlots = kPk ? LTL_PK_STAGE_SLOTS : kH == 16 ? 3 : 2;  // per output group
+  // 4-bit cells (kPk): HBM rows of a strip are 64 B (two cells per byte, cell
+  // 2i in the low nibble); a TMA box lands in the padded 16U4_ALIGN16B SMEM
+  // layout (8 bytes of nibbles + 8 unused per 16 cells: the same 128-byte SMEM
+  // rows as u8 cells), the output staging tile is 64 rows x 64 B.
+  static constexpr uint32_t kRowBytes = kPk ? kStrip / 2 : kStrip;   // HBM bytes per strip row
+  static constexpr uint32_t kStageBytes = kSub * kRowBytes;           // 8 / 4 KB staging tile
   // D2 buffers (64 columns each).  kH = 32: sub-block 1's only; sub-block 0's
   // D2 goes into the free columns [kD2InSlot, +64) of the unit's D1 slot
   // (the planes use [0, 80)), so the slot is free once pass 2 is done AND
@@ -124,15 +136,21 @@ struct Geo {
 #endif
   static constexpr uint32_t kD2InSlot = kBox - kSub;       // 128 (kH = 32)
   // centre weight W of pass 2 (Moore: Z = R + 128 W state must clear R <= (2r+1)^2)
-  static constexpr uint32_t kCentreW = kH == 16 ? 16u : 64u;   // K = 2048 / 8192
+  // (4-bit cells, Moore: pass 2 sums 2 H, Z = 2 R + 4096 state, R <= 1089)
+  static constexpr uint32_t kCentreW = kPk ? 32u : kH == 16 ? 16u : 64u;   // K = 2048 / 8192 / 4096
   static constexpr uint32_t kVnK = kH == 16 ? 128u : 256u;     // VN: R <= 2(2r+1)
-  static constexpr uint32_t kBoxBytes = kBox * kStrip;      // 20 / 24 KB
+  static constexpr uint32_t kBoxBytes = kBox * kStrip;      // 20 / 24 KB of SMEM
+  static constexpr uint32_t kBoxTx = kBox * kRowBytes;      // HBM bytes of one box
   static_assert(kBox % 32 == 0 && kBox <= 256, "box rows: whole K chunks, one TMA box");
 
   // Shared-memory carve-up (offsets from a 1024-aligned base).
   static constexpr uint32_t kSmemX = 0;
   static constexpr uint32_t kSmemBand = kSmemX + kXStages * kBoxBytes;
-  static constexpr uint32_t kSmemStage = kSmemBand + kNumTiles * kTileBytes;
+  // 4-bit cells: a resident B tile of e2m1 1.0 (160 rows x 32 cells, SW32,
+  // 5 KB) for pass 1's bias MMA, D1 += 1024 (A = e4m3 32.0 x 32 k)
+  static constexpr uint32_t kOnesBytes = kPk ? kBox * 32 : 0;
+  static constexpr uint32_t kSmemOnes = kSmemBand + kNumTiles * kTileBytes;
+  static constexpr uint32_t kSmemStage = kSmemOnes + kOnesBytes;
   static constexpr uint32_t kSmemBars = kSmemStage + kSubs * kStageSlots * kStageBytes;
   static constexpr uint32_t kNumBars =
       2 * kXStages + 4 * kSlots + 2 * kSubs + 2 * kSubs * kStageSlots;
@@ -152,12 +170,17 @@ struct Geo {
   static constexpr uint32_t kPiOff = kPbCols;
   static constexpr uint32_t kTmemD2 = kTmemSlot + kSlots * kSlotCols;
   static constexpr uint32_t kTmemA1 = kTmemD2 + kD2Bufs * kSub;  // pass-1 A: 192 k / 4 = 48
+  static constexpr uint32_t kTmemBias = kTmemA1 + kKChunks * 8;  // 4-bit cells: bias A chunk (8)
   static_assert(kPiOff + kPiCols <= kSlotCols, "planes fit in the D1 slot");
   static_assert(kD2Bufs == kSubs || kPiOff + kPiCols <= kD2InSlot, "slot D2 clear of the planes");
-  static_assert(kTmemA1 + kKChunks * 8 <= kTmemCols, "TMEM budget");
+  static_assert(kTmemBias + (kPk ? 8 : 0) <= kTmemCols, "TMEM budget");
+  static_assert(kSmemStage % 1024 == 0, "staging tiles: swizzle-atom aligned");
   static_assert(kSlotCols % 8 == 0 && kPiOff % 8 == 0 && kTmemD2 % 8 == 0, "A operand alignment");
 
-  static constexpr uint32_t kIdesc1 = idesc_i8_u8u8_s32(128, kBox);
+  // pass 1: u8 cells -> kind::i8 (s32 D1); 4-bit cells -> kind::f8f6f4 with
+  // e4m3 band weights x e2m1 cells (nibble 1 = 0.5), f16 D1 (exact: <= 67)
+  static constexpr uint32_t kIdesc1 =
+      kPk ? idesc_f8f6f4_e4m3_e2m1_f16(128, kBox) : idesc_i8_u8u8_s32(128, kBox);
   static constexpr uint32_t kIdesc2 = idesc_i8_u8u8_s32(128, kSub);
 };
 
@@ -352,10 +375,20 @@ __device__ __forceinline__ uint32_t rule_pair(uint32_t z, const SimdRule& k) {
   return lop3<0x70>(e, c, d);             // e & ~(c & d)
 }
 
-template <int kH, bool kChecked, bool kRing>
+// TMEM lane (= pass-1 A row = D1 / D2 lane) of strip column x: the identity
+// for u8 cells; for 4-bit cells lanes 16j + i and 16j + 8 + i hold columns
+// 16j + 2i and 16j + 2i + 1, so the 16x256b loads of the output warps hand
+// every thread the two cells of one output byte.
+template <bool kPk>
+__host__ __device__ constexpr int lane_x(int lane) {
+  return kPk ? (lane & ~15) | ((lane & 7) << 1) | ((lane >> 3) & 1) : lane;
+}
+
+template <int kH, bool kChecked, bool kRing, bool kPk>
 __global__ void __launch_bounds__(kThreads, 1)
     ltl_tc_step_kernel(const __grid_constant__ TcMaps maps, const Params p) {
-  using G = Geo<kH>;
+  using G = Geo<kH, kPk>;
+  constexpr uint32_t kStageBytes = G::kStageBytes;
   constexpr int kBox = G::kBox;
   constexpr int kXStages = G::kXStages;
   constexpr int kStageSlots = G::kStageSlots;
@@ -417,6 +450,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     *reinterpret_cast<uint32_t*>(smem + kSmemBand + t * kTileBytes + sw32_offset(j, k0)) = word;
   }
+  if constexpr (kPk) {  // e2m1 1.0 = nibble 2 everywhere (data and padding: layout-free)
+    for (uint32_t w = threadIdx.x; w < G::kOnesBytes / 4; w += kThreads)
+      reinterpret_cast<uint32_t*>(smem + G::kSmemOnes)[w] = 0x22222222u;
+  }
   fence_proxy_async_smem();
   if (warp == 0 && lane == 0) {
     // Prefetch every load / store map of the grid (all four load maps even
@@ -456,7 +493,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   // A1[x][k] = [|k-32-x| <= r] + 128*[k == x+32], four k per column; warps
   // 2..5 write their lane quarter.
   if (warp >= 2 && warp < 2 + kConvWarps) {
-    const int m = 32 * static_cast<int>(warp & 3) + static_cast<int>(lane);
+    const int m = lane_x<kPk>(32 * static_cast<int>(warp & 3) + static_cast<int>(lane));
     uint32_t a1[kKChunks * 8];
 #pragma unroll
     for (int c = 0; c < kKChunks * 8; ++c) {
@@ -464,10 +501,17 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
       for (int b = 0; b < 4; ++b) {
         const int d = 4 * c + b - 32 - m;
-        uint32_t v = (d >= -r && d <= r) ? 1u : 0u;
-        if (d == 0) {
-          v += 128u;  // state marker
-          if (p.inject_fault && m % p.fault_f == 0) v = 128u;  // pi2(0,0) flipped: no centre term
+        const bool in = d >= -r && d <= r;
+        const bool drop = d == 0 && p.inject_fault && m % p.fault_f == 0;  // pi2(0,0) flipped
+        uint32_t v;
+        if constexpr (kPk) {
+          // e4m3 weights on cells of 0.5: window 4.0 (0x48) -> 2 per live
+          // cell, centre 6.0 (0x4C) -> 3: D1 = 2 H + state; faulted centre
+          // 2.0 (0x40) -> the state marker only
+          v = d == 0 ? (drop ? 0x40u : 0x4Cu) : in ? 0x48u : 0u;
+        } else {
+          // D1 = H + 128 state (the state marker in bit 7)
+          v = d == 0 ? (drop ? 128u : 129u) : in ? 1u : 0u;
         }
         word |= v << (8 * b);
       }
@@ -480,6 +524,11 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
       for (int i = 0; i < 8; ++i) v8[i] = a1[8 * c + i];
       tmem_st_32x32b_x8(trow + 8 * c, v8);
+    }
+    if constexpr (kPk) {  // e4m3 32.0 (0x60) x 32 k: the bias MMA adds 1024
+      const uint32_t v8[8] = {0x60606060u, 0x60606060u, 0x60606060u, 0x60606060u,
+                              0x60606060u, 0x60606060u, 0x60606060u, 0x60606060u};
+      tmem_st_32x32b_x8(trow + (G::kTmemBias - kTmemA1), v8);
     }
     tmem_st_wait();
   }
@@ -579,7 +628,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               const int strip = storage_strip(k);
               uint8_t* dst = smem + kSmemX + s * kBoxBytes;
               if (!first && !last) {
-                mbar_arrive_expect_tx(&x_full[s], kBoxBytes);
+                mbar_arrive_expect_tx(&x_full[s], G::kBoxTx);
 #ifdef LTL_DIAG_L2_READS  // timing probe only (wrong results): every box from band 1 (L2-resident)
                 tma_load_3d(dst, &lm[0], &x_full[s], 0, kBand + G::kRowOff, strip);
 #else
@@ -589,7 +638,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 // first / last band of a whole torus: the kH rows beyond the
                 // edge are loaded from the other end of the strip (padded row 16 + y)
                 const int body = last ? last_rows : kBand;  // interior rows in the box body
-                mbar_arrive_expect_tx(&x_full[s], (last ? last_rows + 2 * kH : kBox) * kStrip);
+                mbar_arrive_expect_tx(&x_full[s], (last ? last_rows + 2 * kH : kBox) * G::kRowBytes);
                 int row = 0;  // box row being filled
                 if (kRing && first && !up_ready) {
                   wait_flag_geq_sys(p.up_done, p.ring_gen);
@@ -648,11 +697,22 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc_fence_after();
         if (elect_one()) {
           const uint32_t dcol = tmem + kTmemSlot + kSlotCols * sl;
-          mma_i8_ts(dcol, a1, box(gl) + (96 >> 4), G::kIdesc1, 0);
+          auto mma1 = [&](uint32_t a, uint64_t b, uint32_t acc) {
+            if constexpr (kPk) mma_f8f6f4_ts(dcol, a, b, G::kIdesc1, acc);
+            else mma_i8_ts(dcol, a, b, G::kIdesc1, acc);
+          };
+          // (the padded 4-bit SMEM layout keeps 32 cells per 32 bytes: the
+          // same K-chunk offsets as u8 cells)
+          if constexpr (kPk) {
+            // D1 = 1024 + 2 H + state (f16): each f16's low byte is 2 H + state
+            mma1(tmem + G::kTmemBias, smem_desc_sw32_kmajor(smem_u32(smem + G::kSmemOnes)), 0);
+            mma1(a1, box(gl) + (96 >> 4), 1);
+          } else {
+            mma1(a1, box(gl) + (96 >> 4), 0);
+          }
 #pragma unroll
-          for (int q = 1; q <= 4; ++q)
-            mma_i8_ts(dcol, a1 + 8 * q, box(go) + ((32 * (q - 1)) >> 4), G::kIdesc1, 1);
-          mma_i8_ts(dcol, a1 + 40, box(gr), G::kIdesc1, 1);
+          for (int q = 1; q <= 4; ++q) mma1(a1 + 8 * q, box(go) + ((32 * (q - 1)) >> 4), 1);
+          mma1(a1 + 40, box(gr), 1);
           mma_commit(&d1_full[sl]);
           mma_commit(&x_empty[gl % kXStages]);  // box t-1 is done
           if (t == t1 - 1) {
@@ -694,8 +754,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           return pack_pairs(reg(2 * i), reg(2 * i + 1));
         };
         if constexpr (kChecked) {
-          const bool x_ok = (t % p.strips) * kStrip + 32 * static_cast<int>(q) +
-                                static_cast<int>(lane) < p.cols;
+          const bool x_ok = (t % p.strips) * kStrip +
+                                lane_x<kPk>(32 * static_cast<int>(q) + static_cast<int>(lane)) < p.cols;
           const int prow0 = band * kBand + G::kRowOff;  // padded row of box row 0
 #pragma unroll
           for (int i = 0; i < kBox / 2; ++i) {
@@ -703,7 +763,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int hh = 0; hh < 2; ++hh) {
               const int prow = prow0 + 2 * i + hh;
-              const uint32_t hv = (pr >> (16 * hh)) & 0x7Fu;
+              const uint32_t hv = kPk ? ((pr >> (16 * hh)) & 0xFFu) >> 1 : (pr >> (16 * hh)) & 0x7Fu;
               if (x_ok && prow >= kHalo && prow < p.rows + kHalo) max_h = max(max_h, hv);
             }
           }
@@ -718,8 +778,16 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
             const uint32_t raw = raw_word(8 * c + i);
-            pb[i] = vn ? (raw >> 7) & 0x01010101u : raw & 0x7F7F7F7Fu;
-            pi[i] = vn ? raw : raw & 0x80808080u;
+            if constexpr (kPk) {  // bytes 2 H + state (the f16 D1 + 1024's low bytes)
+              // Moore: Pb = 2 H (pass 2 sums 2 R), Pi = 128 state;
+              // VN: Pb = state, Pi = H + 128 state
+              const uint32_t sb = (raw << 7) & 0x80808080u;
+              pb[i] = vn ? raw & 0x01010101u : raw & 0xFEFEFEFEu;
+              pi[i] = vn ? ((raw >> 1) & 0x7F7F7F7Fu) | sb : sb;
+            } else {  // bytes H + 128 state
+              pb[i] = vn ? (raw >> 7) & 0x01010101u : raw & 0x7F7F7F7Fu;
+              pi[i] = vn ? raw : raw & 0x80808080u;
+            }
           }
           tmem_st_32x32b_x8(pb_col + 8 * c, pb);
           if constexpr (kH == 16) {
@@ -870,14 +938,15 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t trow_base = tmem + ((q * 32) << 16);
     const uint32_t trow_fixed = trow_base + kTmemD2 + (G::kD2Bufs == kSubs ? kSub * grp : 0);
     const RuleConsts rc = p.rule;
-    const uint32_t K = vn ? G::kVnK : 128u * G::kCentreW;  // Z = R + K state
+    const uint32_t K = vn ? G::kVnK : 128u * G::kCentreW;  // Z = zs R + K state
+    const uint32_t zs = kPk && !vn ? 2u : 1u;                  // 4-bit cells, Moore: 2 R
     SimdRule sr;
-    sr.ca = (0x8000u - rc.lo_dead) * 0x10001u;
-    sr.cb = (0x7FFFu - (rc.lo_dead + rc.w_dead)) * 0x10001u;
-    sr.cc = (0x8000u - (K + rc.lo_live)) * 0x10001u;
-    sr.cd = (0x7FFFu - (K + rc.lo_live + rc.w_live)) * 0x10001u;
+    sr.ca = (0x8000u - zs * rc.lo_dead) * 0x10001u;
+    sr.cb = (0x7FFFu - zs * (rc.lo_dead + rc.w_dead)) * 0x10001u;
+    sr.cc = (0x8000u - (K + zs * rc.lo_live)) * 0x10001u;
+    sr.cd = (0x7FFFu - (K + zs * (rc.lo_live + rc.w_live))) * 0x10001u;
     const uint32_t g_live = (0x8000u - K) * 0x10001u;
-    const uint32_t g_neg = (0x8000u - (K + rc.neg_live)) * 0x10001u;
+    const uint32_t g_neg = (0x8000u - (K + zs * rc.neg_live)) * 0x10001u;
     const uint32_t r_mask = (K - 1) * 0x10001u;
     uint32_t max_r = 0, bad = 0;
     // staging: the group's whole 64-row x 128-column sub-block in one
@@ -894,7 +963,10 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
       for (int hh = 0; hh < 2; ++hh) {
         const uint32_t y = 32 * tt + lane, c = 2 * q + hh;
-        st_off[tt][hh] = y * kStrip + ((c ^ (y & 7)) << 4);
+        // 4-bit cells: 64-byte rows, SWIZZLE_64B (chunk q ^ ((y >> 1) & 3)),
+        // one 16-byte chunk (32 cells) per warp
+        st_off[tt][hh] = kPk ? y * G::kRowBytes + ((q ^ ((y >> 1) & 3)) << 4)
+                             : y * kStrip + ((c ^ (y & 7)) << 4);
       }
     uint32_t h = 0;
     for (int gg = 0; gg < p.gens; ++gg) {
@@ -923,15 +995,34 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint32_t w[2][2][4];  // [tile][lane half][stmatrix register]
 #pragma unroll
         for (int tt = 0; tt < 2; ++tt) {
+          if constexpr (kPk) {
+            // registers jj (even column 2i) and jj + 2 (odd column 2i + 1)
+            // of lane half hh make output byte 8 hh + i of the warp's 16:
+            // register 2v + e = [rows (c, c+1) of half 0, of half 1]
 #pragma unroll
-          for (int hh = 0; hh < 2; ++hh) {
-            const uint32_t* zz = z[tt][hh];
+            for (int v = 0; v < 2; ++v)
 #pragma unroll
-            for (int v = 0; v < 2; ++v) {
-              const uint32_t a0 = rule_pair(zz[4 * v + 0], sr), b0 = rule_pair(zz[4 * v + 1], sr);
-              const uint32_t a2 = rule_pair(zz[4 * v + 2], sr), b2 = rule_pair(zz[4 * v + 3], sr);
-              w[tt][hh][2 * v + 0] = prmt(a0, a2, 0xFDB9) & 0x01010101u;
-              w[tt][hh][2 * v + 1] = prmt(b0, b2, 0xFDB9) & 0x01010101u;
+              for (int e = 0; e < 2; ++e) {
+                const uint32_t ra0 = rule_pair(z[tt][0][4 * v + e], sr);
+                const uint32_t ra1 = rule_pair(z[tt][1][4 * v + e], sr);
+                const uint32_t rb0 = rule_pair(z[tt][0][4 * v + e + 2], sr);
+                const uint32_t rb1 = rule_pair(z[tt][1][4 * v + e + 2], sr);
+                // bytes [row c, row c+1] x [half 0, half 1]: even column 0x01, odd 0x10
+                const uint32_t even = prmt(ra0, ra1, 0xFDB9) & 0x01010101u;
+                const uint32_t odd = prmt(rb0, rb1, 0xFDB9);  // 0x00 / 0xFF bytes
+                w[tt][0][2 * v + e] = lop3<0xF8>(even, odd, 0x10101010u);  // even | (odd & C)
+              }
+          } else {
+#pragma unroll
+            for (int hh = 0; hh < 2; ++hh) {
+              const uint32_t* zz = z[tt][hh];
+#pragma unroll
+              for (int v = 0; v < 2; ++v) {
+                const uint32_t a0 = rule_pair(zz[4 * v + 0], sr), b0 = rule_pair(zz[4 * v + 1], sr);
+                const uint32_t a2 = rule_pair(zz[4 * v + 2], sr), b2 = rule_pair(zz[4 * v + 3], sr);
+                w[tt][hh][2 * v + 0] = prmt(a0, a2, 0xFDB9) & 0x01010101u;
+                w[tt][hh][2 * v + 1] = prmt(b0, b2, 0xFDB9) & 0x01010101u;
+              }
             }
           }
         }
@@ -945,7 +1036,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int hh = 0; hh < 2; ++hh) {
 #pragma unroll
               for (int jj = 0; jj < 8; ++jj) {
-                const int xl = 16 * hh + static_cast<int>(lane >> 2) + 8 * ((jj >> 1) & 1);
+                const int xl = lane_x<kPk>(32 * static_cast<int>(q) + 16 * hh +
+                                           static_cast<int>(lane >> 2) + 8 * ((jj >> 1) & 1)) -
+                               32 * static_cast<int>(q);
                 const int c = 4 * static_cast<int>(lane & 3) + 2 * (jj & 1) + 16 * (jj >> 2);
                 const int y0 = ybase + 32 * tt;
                 const bool xv = (t % p.strips) * kStrip + 32 * static_cast<int>(q) + xl < p.cols;
@@ -961,7 +1054,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                   for (int e = 0; e < 2; ++e) {
                     if (!((neg >> (16 * e)) & 0x8000u)) continue;
                     const int zl = static_cast<int>((zz >> (16 * e)) & 0xFFFFu);
-                    const int cnt = zl - static_cast<int>(K) - rc.neg_live;  // < 0
+                    const int cnt = (zl - static_cast<int>(K)) / static_cast<int>(zs) - rc.neg_live;  // < 0
                     const int y = p.row0 + y0 + out_row_of_col(c + e);
                     const int x = (t % p.strips) * kStrip + 32 * static_cast<int>(q) + xl;
                     atomicMin(&p.stats->first_negative,
@@ -979,7 +1072,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int tt = 0; tt < 2; ++tt) {
           stmatrix_x4_trans_b8(sa + st_off[tt][0], w[tt][0][0], w[tt][0][1], w[tt][0][2], w[tt][0][3]);
-          stmatrix_x4_trans_b8(sa + st_off[tt][1], w[tt][1][0], w[tt][1][1], w[tt][1][2], w[tt][1][3]);
+          if constexpr (!kPk)
+            stmatrix_x4_trans_b8(sa + st_off[tt][1], w[tt][1][0], w[tt][1][1], w[tt][1][2], w[tt][1][3]);
         }
         fence_proxy_async_smem();
         named_barrier(1 + grp, kGroupThreads);
@@ -989,7 +1083,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     }
     if constexpr (kChecked) {
-      int32_t mr = static_cast<int32_t>(max(max_r & 0xFFFF, max_r >> 16));
+      int32_t mr = static_cast<int32_t>(max(max_r & 0xFFFF, max_r >> 16) / zs);
 #pragma unroll
       for (int off = 16; off > 0; off >>= 1) mr = max(mr, __shfl_xor_sync(0xffffffffu, mr, off));
       if (lane == 0) atomicMax(&p.stats->max_r, mr);
@@ -1018,7 +1112,9 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 }  // namespace
 
-size_t tc_smem_bytes(int halo) { return halo == 32 ? Geo<32>::kSmemAlloc : Geo<16>::kSmemAlloc; }
+size_t tc_smem_bytes(int halo, bool packed) {
+  return packed ? Geo<16, true>::kSmemAlloc : halo == 32 ? Geo<32>::kSmemAlloc : Geo<16>::kSmemAlloc;
+}
 
 // Multi-generation launches (SegIter's sweep): one CTA per SM, all resident.
 // A generation boundary of one-launch-per-generation costs ~12.7 us (grid
@@ -1069,14 +1165,16 @@ cudaError_t launch_tc_step(const TcLaunch& a, cudaStream_t stream) {
       return cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(bytes));
     };
-    for (cudaError_t r : {set_smem(ltl_tc_step_kernel<16, false, false>, Geo<16>::kSmemAlloc),
-                          set_smem(ltl_tc_step_kernel<16, true, false>, Geo<16>::kSmemAlloc),
-                          set_smem(ltl_tc_step_kernel<16, false, true>, Geo<16>::kSmemAlloc),
-                          set_smem(ltl_tc_step_kernel<16, true, true>, Geo<16>::kSmemAlloc),
-                          set_smem(ltl_tc_step_kernel<32, false, false>, Geo<32>::kSmemAlloc),
-                          set_smem(ltl_tc_step_kernel<32, true, false>, Geo<32>::kSmemAlloc),
-                          set_smem(ltl_tc_step_kernel<32, false, true>, Geo<32>::kSmemAlloc),
-                          set_smem(ltl_tc_step_kernel<32, true, true>, Geo<32>::kSmemAlloc)})
+    for (cudaError_t r : {set_smem(ltl_tc_step_kernel<16, false, false, false>, Geo<16>::kSmemAlloc),
+                          set_smem(ltl_tc_step_kernel<16, true, false, false>, Geo<16>::kSmemAlloc),
+                          set_smem(ltl_tc_step_kernel<16, false, true, false>, Geo<16>::kSmemAlloc),
+                          set_smem(ltl_tc_step_kernel<16, true, true, false>, Geo<16>::kSmemAlloc),
+                          set_smem(ltl_tc_step_kernel<32, false, false, false>, Geo<32>::kSmemAlloc),
+                          set_smem(ltl_tc_step_kernel<32, true, false, false>, Geo<32>::kSmemAlloc),
+                          set_smem(ltl_tc_step_kernel<32, false, true, false>, Geo<32>::kSmemAlloc),
+                          set_smem(ltl_tc_step_kernel<32, true, true, false>, Geo<32>::kSmemAlloc),
+                          set_smem(ltl_tc_step_kernel<16, false, false, true>, Geo<16, true>::kSmemAlloc),
+                          set_smem(ltl_tc_step_kernel<16, true, false, true>, Geo<16, true>::kSmemAlloc)})
       if (r != cudaSuccess) return r;
     int sms = 0;
     e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -1106,6 +1204,8 @@ cudaError_t launch_tc_step(const TcLaunch& a, cudaStream_t stream) {
   // 16-row HBM halo cannot hold 32 rows / columns
   if (a.halo != 0 && a.halo != 16 && a.halo != 32) return cudaErrorInvalidValue;
   if (halo == 32 && !(p.wrap_cols && (p.wrap_rows || p.ring))) return cudaErrorInvalidValue;
+  // 4-bit cells: one whole-torus slab whose every wrap the loads do, r <= 16
+  if (a.packed && (halo != 16 || p.ring || !(p.wrap_cols && p.wrap_rows))) return cudaErrorInvalidValue;
   if (p.ring) {
     p.wrap_rows = 0;
     p.up_flags = a.up_flags ? a.up_flags : a.flags;
@@ -1137,7 +1237,7 @@ cudaError_t launch_tc_step(const TcLaunch& a, cudaStream_t stream) {
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(static_cast<unsigned>(grid));
   cfg.blockDim = dim3(kThreads);
-  cfg.dynamicSmemBytes = tc_smem_bytes(halo);
+  cfg.dynamicSmemBytes = tc_smem_bytes(halo, a.packed != 0);
   cfg.stream = stream;
   cudaLaunchAttribute attr[2];
   int nattr = 0;
@@ -1170,18 +1270,21 @@ cudaError_t launch_tc_step(const TcLaunch& a, cudaStream_t stream) {
   }
   // the ring's peer-memory paths are compiled only into the ring kernels
   const bool st = a.stats != nullptr;
+  if (a.packed)
+    return st ? cudaLaunchKernelEx(&cfg, ltl_tc_step_kernel<16, true, false, true>, maps, p)
+              : cudaLaunchKernelEx(&cfg, ltl_tc_step_kernel<16, false, false, true>, maps, p);
   if (halo == 32) {
     if (p.ring)
-      return st ? cudaLaunchKernelEx(&cfg, ltl_tc_step_kernel<32, true, true>, maps, p)
-                : cudaLaunchKernelEx(&cfg, ltl_tc_step_kernel<32, false, true>, maps, p);
-    return st ? cudaLaunchKernelEx(&cfg, ltl_tc_step_kernel<32, true, false>, maps, p)
-              : cudaLaunchKernelEx(&cfg, ltl_tc_step_kernel<32, false, false>, maps, p);
+      return st ? cudaLaunchKernelEx(&cfg, ltl_tc_step_kernel<32, true, true, false>, maps, p)
+                : cudaLaunchKernelEx(&cfg, ltl_tc_step_kernel<32, false, true, false>, maps, p);
+    return st ? cudaLaunchKernelEx(&cfg, ltl_tc_step_kernel<32, true, false, false>, maps, p)
+              : cudaLaunchKernelEx(&cfg, ltl_tc_step_kernel<32, false, false, false>, maps, p);
   }
   if (p.ring)
-    return st ? cudaLaunchKernelEx(&cfg, ltl_tc_step_kernel<16, true, true>, maps, p)
-              : cudaLaunchKernelEx(&cfg, ltl_tc_step_kernel<16, false, true>, maps, p);
-  return st ? cudaLaunchKernelEx(&cfg, ltl_tc_step_kernel<16, true, false>, maps, p)
-            : cudaLaunchKernelEx(&cfg, ltl_tc_step_kernel<16, false, false>, maps, p);
+    return st ? cudaLaunchKernelEx(&cfg, ltl_tc_step_kernel<16, true, true, false>, maps, p)
+              : cudaLaunchKernelEx(&cfg, ltl_tc_step_kernel<16, false, true, false>, maps, p);
+  return st ? cudaLaunchKernelEx(&cfg, ltl_tc_step_kernel<16, true, false, false>, maps, p)
+            : cudaLaunchKernelEx(&cfg, ltl_tc_step_kernel<16, false, false, false>, maps, p);
 }
 
 }  // namespace ltl

@@ -34,17 +34,20 @@ cudaError_t get_encode(EncodeFn* fn) {
   return cudaSuccess;
 }
 
+// {row_elems, rows, strips} over strips of `row_bytes`-byte rows
 cudaError_t encode3(CUtensorMap* map, void* base, uint64_t rows, uint64_t strips,
                     uint64_t strip_bytes, uint32_t box_w, uint32_t box_h,
-                    CUtensorMapSwizzle swz) {
+                    CUtensorMapSwizzle swz,
+                    CUtensorMapDataType type = CU_TENSOR_MAP_DATA_TYPE_UINT8,
+                    uint64_t row_elems = kStrip, uint64_t row_bytes = kStrip) {
   EncodeFn fn;
   cudaError_t e = get_encode(&fn);
   if (e != cudaSuccess) return e;
-  const cuuint64_t dims[3] = {static_cast<cuuint64_t>(kStrip), rows, strips};
-  const cuuint64_t strides[2] = {static_cast<cuuint64_t>(kStrip), strip_bytes};
+  const cuuint64_t dims[3] = {row_elems, rows, strips};
+  const cuuint64_t strides[2] = {row_bytes, strip_bytes};
   const cuuint32_t box[3] = {box_w, box_h, 1};
   const cuuint32_t estr[3] = {1, 1, 1};
-  const CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, base, dims, strides, box, estr,
+  const CUresult r = fn(map, type, 3, base, dims, strides, box, estr,
                         CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
@@ -91,6 +94,37 @@ cudaError_t make_piece_map(CUtensorMap* map, const SlabView& s, int halo) {
   return encode3(map, s.buf, static_cast<uint64_t>(s.rows) + 2 * kHalo,
                  static_cast<uint64_t>(s.strips), static_cast<uint64_t>(s.strip_bytes), kStrip,
                  static_cast<uint32_t>(halo), CU_TENSOR_MAP_SWIZZLE_128B);
+}
+
+// The 4-bit copy of a slab (PackedView): load boxes of 128 cells per row as
+// 16U4_ALIGN16B -- in SMEM every 16 cells take 16 bytes (8 of nibbles, 8
+// unused), the e2m1 operand layout of tcgen05.mma kind::f8f6f4, SWIZZLE_128B
+// like the u8 boxes (tools/ubench_fp4.cu) -- with the same four box shapes.
+cudaError_t make_load_maps_packed(CUtensorMap* maps, const PackedView& s) {
+  if (s.rows <= 0 || s.cols <= 0) return cudaSuccess;
+  const int last = s.rows - kTcBand * ((s.rows - 1) / kTcBand);
+  const bool one_band = s.rows <= kTcBand;
+  const uint32_t h = kHalo;
+  const uint32_t box[kTcLoadMaps] = {kTcBand + 2 * h, h, kTcBand + h,
+                                     static_cast<uint32_t>(last) + (one_band ? 0 : h)};
+  for (int i = 0; i < kTcLoadMaps; ++i) {
+    const cudaError_t e = encode3(&maps[i], s.buf, static_cast<uint64_t>(s.rows) + 2 * kHalo,
+                                  static_cast<uint64_t>(s.strips),
+                                  static_cast<uint64_t>(s.strip_bytes), kStrip, box[i],
+                                  CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_DATA_TYPE_16U4_ALIGN16B,
+                                  kStrip, kPkRow);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
+// Interior rows of the 4-bit copy: 64-row x 64-byte staging tiles (4 KB),
+// SWIZZLE_64B so the output warps' stmatrix rows land conflict-free.
+cudaError_t make_store_map_packed(CUtensorMap* map, const PackedView& s) {
+  if (s.rows <= 0 || s.cols <= 0) return cudaSuccess;
+  return encode3(map, s.buf + kHalo * kPkRow, static_cast<uint64_t>(s.rows),
+                 static_cast<uint64_t>(s.strips), static_cast<uint64_t>(s.strip_bytes), kPkRow, 64,
+                 CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_DATA_TYPE_UINT8, kPkRow, kPkRow);
 }
 
 }  // namespace ltl

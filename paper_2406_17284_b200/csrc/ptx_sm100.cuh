@@ -249,6 +249,18 @@ __device__ __forceinline__ void mma_i8_ts(uint32_t d_tmem, uint32_t a_tmem, uint
       : "memory");
 }
 
+// D[tmem] (+)= A[tmem] * B[smem desc], kind::f8f6f4 (A e4m3 K-major in TMEM, 4
+// per column; B e2m1 in the padded 16U4_ALIGN16B SMEM layout; D per idesc).
+__device__ __forceinline__ void mma_f8f6f4_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc,
+                                              uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f8f6f4 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
 // Arrive on an mbarrier once every previously issued tcgen05.mma of this thread completes.
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
   asm volatile(
@@ -402,6 +414,15 @@ __device__ __forceinline__ uint64_t smem_desc_sw128_kmajor(uint32_t smem_addr) {
 __host__ __device__ constexpr uint32_t idesc_i8_u8u8_s32(int m, int n) {
   return (2u << 4)                                  // D format S32
          | (0u << 7) | (0u << 10)                   // A, B unsigned 8-bit
+         | (static_cast<uint32_t>(n >> 3) << 17)    // N >> 3
+         | (static_cast<uint32_t>(m >> 4) << 24);   // M >> 4
+}
+
+// Instruction descriptor, kind::f8f6f4: A e4m3 x B e2m1 -> D f16 (one f16 per
+// 32-bit TMEM column, low half), both K-major, shape M x N.
+__host__ __device__ constexpr uint32_t idesc_f8f6f4_e4m3_e2m1_f16(int m, int n) {
+  return (0u << 4)                                  // D format F16
+         | (0u << 7) | (5u << 10)                   // A E4M3, B E2M1
          | (static_cast<uint32_t>(n >> 3) << 17)    // N >> 3
          | (static_cast<uint32_t>(m >> 4) << 24);   // M >> 4
 }

@@ -33,7 +33,11 @@ FLAG_WIDE_RADIUS = 0x20
 MAX_RADIUS, MAX_WIDE_RADIUS = 16, 32
 FLAG_STENCIL = FLAG_ENGINE_BASE
 # engine name -> ltl_run flag (catsim::EngineKind; proj/src/engines.cpp:9-15)
-ENGINE_FLAGS = {"cat": 0, "base": FLAG_ENGINE_BASE, "pack": FLAG_ENGINE_PACK}
+# the Cat engine on 4-bit device cells where the geometry allows (opt-in,
+# include/ltl_b200.h LTL_FLAG_4BIT_CELLS; same bytes as "cat")
+FLAG_4BIT_CELLS = 0x40
+ENGINE_FLAGS = {"cat": 0, "base": FLAG_ENGINE_BASE, "pack": FLAG_ENGINE_PACK,
+                "cat-4bit": FLAG_4BIT_CELLS}
 
 
 class LtlLogicError(RuntimeError):
@@ -339,7 +343,7 @@ class DeviceTorus:
             engine = "base"
         if engine not in ENGINE_FLAGS:
             raise ValueError(f"config error: unknown engine '{engine}' (cat, base, pack)")
-        wide = engine == "cat" and rule is not None and rule.r > MAX_RADIUS
+        wide = engine in ("cat", "cat-4bit") and rule is not None and rule.r > MAX_RADIUS
         return (ENGINE_FLAGS[engine] | (FLAG_INJECT_FAULT if inject_fault else 0)
                 | (FLAG_WIDE_RADIUS if wide else 0))
 
@@ -451,7 +455,7 @@ class DeviceTorus:
                                              ctypes.c_void_p(bot_ptr)))
 
 
-ENGINES = ("cat", "base", "pack")
+ENGINES = ("cat", "base", "pack", "cat-4bit")  # cat-4bit: the Cat engine on 4-bit device cells
 
 
 def snapshot_probe(path: str):
