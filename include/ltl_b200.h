@@ -190,6 +190,11 @@ int ltl_time(ltl_ctx* ctx, const ltl_rule_c* rule, int32_t steps, int32_t warmup
              uint32_t flags, double* total_ms, double* kernel_ms);
 /* Kernels launched inside the last ltl_time's timed loop (total_ms region). */
 int64_t ltl_time_launches(const ltl_ctx* ctx);
+/* Bytes this context has moved between host and device memory so far
+ * (dir 0: host -> device, 1: device -> host) by its uploads / downloads: one
+ * bit per cell where the bit-packed transfers ran (>= 4 MB of rows of a
+ * multiple of 32 cells, all 0 / 1), one byte per cell elsewhere. */
+int64_t ltl_transfer_bytes(const ltl_ctx* ctx, int32_t dir);
 
 /* End-to-end: upload interior from host memory, run `steps` generations,
  * download the interior into `interior_out` -- the whole run_engine(Cat)

@@ -2,6 +2,9 @@
 // of libltl_b200.so (not part of the public API).
 #pragma once
 
+#include <cstddef>
+#include <cstdint>
+
 #include "catsim/rule.hpp"
 #include "ltl_b200.h"
 
@@ -38,3 +41,16 @@ inline ltl_rule_c to_c(const LtlRule& r) {
 }
 
 }  // namespace catsim
+
+// Bit-packed host <-> device transfers (host/xfer_bits.cpp): rows of
+// row_bytes (% 32 == 0) cells at host `pitch` <-> contiguous rows of
+// row_bytes / 8 bytes of bits (cell x of a row = bit x % 8 of byte x / 8).
+namespace ltl_host {
+bool bits_available();  // AVX-512BW or AVX2 on this CPU
+int xfer_threads();     // host threads for the packing (<= 16)
+// false if a byte is neither 0 nor 1 (the caller then copies bytes)
+bool cells_to_bits(const uint8_t* src, size_t pitch, size_t row_bytes, int64_t nrows, uint8_t* dst,
+                   int threads);
+void bits_to_cells(const uint8_t* src, uint8_t* dst, size_t pitch, size_t row_bytes, int64_t nrows,
+                   int threads);
+}  // namespace ltl_host

@@ -227,6 +227,12 @@ cudaError_t launch_from_strips(const SlabView& s, uint8_t* dense, cudaStream_t s
 // cols multiples of f) <-> strip slab interior.
 cudaError_t launch_frag_relayout(uint8_t* dense, const SlabView& s, int f, bool to_strips,
                                  cudaStream_t stream);
+// dense {0, 1} bytes <-> bits (bit k % 8 of byte k / 8 = byte k), n % 32 == 0:
+// the device side of the bit-packed host transfers.
+cudaError_t launch_bits_to_cells(const uint8_t* bits, uint8_t* cells, int64_t n, cudaStream_t stream);
+// (*bad |= 1 if a byte is neither 0 nor 1)
+cudaError_t launch_cells_to_bits(const uint8_t* cells, uint8_t* bits, int64_t n, int32_t* bad,
+                                 cudaStream_t stream);
 // u8 slab <-> its 4-bit copy (every padded row of every strip).
 cudaError_t launch_pack_cells(const SlabView& s, const PackedView& pk, cudaStream_t stream);
 cudaError_t launch_unpack_cells(const PackedView& pk, const SlabView& s, cudaStream_t stream);

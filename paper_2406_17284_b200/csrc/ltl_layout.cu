@@ -136,6 +136,36 @@ __global__ void unpack_cells_kernel(const uint2* pk, uint4* u8, int64_t n16) {
   }
 }
 
+// 32 cells <-> one 32-bit word of bits per thread.
+__global__ void bits_to_cells_kernel(const uint32_t* bits, uint4* cells, int64_t words) {
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < words; i += stride) {
+    const uint32_t w = bits[i];
+    uint32_t c[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k)  // nibble k -> 4 bytes: b0..b3 at bits 0, 8, 16, 24
+      c[k] = (((w >> (4 * k)) & 0xFu) * 0x00204081u) & 0x01010101u;
+    cells[2 * i] = make_uint4(c[0], c[1], c[2], c[3]);
+    cells[2 * i + 1] = make_uint4(c[4], c[5], c[6], c[7]);
+  }
+}
+__global__ void cells_to_bits_kernel(const uint4* cells, uint32_t* bits, int64_t words, int32_t* bad) {
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  uint32_t acc = 0;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < words; i += stride) {
+    const uint4 a = cells[2 * i], b = cells[2 * i + 1];
+    const uint32_t c[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+    uint32_t w = 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {  // 4 bytes of {0, 1} -> 4 bits (bits 24..27 of the product)
+      acc |= c[k] & 0xFEFEFEFEu;
+      w |= (((c[k] & 0x01010101u) * 0x01020408u) >> 24 & 0xFu) << (4 * k);
+    }
+    bits[i] = w;
+  }
+  if (__syncthreads_or(acc != 0) && threadIdx.x == 0) atomicOr(bad, 1);
+}
+
 int blocks_for(int64_t work) {
   int64_t b = (work + 255) / 256;
   if (b > 148 * 8) b = 148 * 8;
@@ -172,6 +202,23 @@ cudaError_t launch_frag_relayout(uint8_t* dense, const SlabView& s, int f, bool 
     case 8: frag_relayout_kernel<4, false><<<blocks, 256, 0, stream>>>(dense, s); break;
     default: return cudaErrorInvalidValue;
   }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_bits_to_cells(const uint8_t* bits, uint8_t* cells, int64_t n, cudaStream_t stream) {
+  if (n <= 0) return cudaSuccess;
+  if (n % 32) return cudaErrorInvalidValue;
+  bits_to_cells_kernel<<<blocks_for(n / 32), 256, 0, stream>>>(
+      reinterpret_cast<const uint32_t*>(bits), reinterpret_cast<uint4*>(cells), n / 32);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_cells_to_bits(const uint8_t* cells, uint8_t* bits, int64_t n, int32_t* bad,
+                                 cudaStream_t stream) {
+  if (n <= 0) return cudaSuccess;
+  if (n % 32) return cudaErrorInvalidValue;
+  cells_to_bits_kernel<<<blocks_for(n / 32), 256, 0, stream>>>(
+      reinterpret_cast<const uint4*>(cells), reinterpret_cast<uint32_t*>(bits), n / 32, bad);
   return cudaGetLastError();
 }
 

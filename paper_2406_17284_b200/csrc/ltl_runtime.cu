@@ -100,6 +100,9 @@ struct ltl_ctx {
   int64_t timed_launches = 0;  // inside the last ltl_time's timed loop
   uint8_t* pinned[2] = {nullptr, nullptr};  // snapshot streaming buffers (lazy)
   size_t pinned_bytes = 0;
+  // bit-packed transfers: a device buffer of bits per device (lazy, grown)
+  std::vector<std::pair<uint8_t*, size_t>> xbits;
+  int64_t moved[2] = {0, 0};  // host -> device, device -> host bytes (ltl_transfer_bytes)
   std::vector<Slab> slabs;
   std::string err;
   // 4-bit cells: pk_live = the current generation is pbuf[pk_cur] (buf[cur] is
@@ -337,6 +340,12 @@ void destroy_ctx(ltl_ctx* ctx) {
     for (cudaEvent_t e : s.timing) cudaEventDestroy(e);
     if (s.stream && s.own_stream) cudaStreamDestroy(s.stream);
   }
+  for (size_t d = 0; d < ctx->xbits.size(); ++d)
+    if (ctx->xbits[d].first) {
+      cudaSetDevice(static_cast<int>(d));
+      cudaFree(ctx->xbits[d].first);
+    }
+  ctx->xbits.clear();
   ctx->slabs.clear();
 }
 
@@ -792,9 +801,107 @@ void parallel_rows(int64_t nrows, size_t row_bytes, Fn&& fn) {
 // `nrows` rows of `row_bytes` at host pitch `pitch` -> dense device rows.
 // Returns with the copies enqueued on `st` (pageable: completed up to the
 // last chunk's DMA, which the caller's stream sync covers).
+// ---- bit-packed transfers (host/xfer_bits.cpp): a grid crosses PCIe as one
+// bit per cell.  The host packs / unpacks a 256 MB-of-cells chunk on all its
+// cores (AVX-512BW / AVX2) while the previous chunk is in flight through the
+// context's pinned chunks; the device expands / packs (ltl_layout.cu).  Used
+// for >= 4 MB of rows of a multiple of 32 cells whose bytes are all 0 / 1
+// (else the byte copies below run: the same bytes land either way).
+// LTL_BYTE_TRANSFERS=1 keeps the byte copies (A/B).
+constexpr size_t kBitsChunk = 8u << 20;  // bits per pipelined chunk (64 MB of cells)
+bool use_bits(int64_t nrows, size_t row_bytes) {
+  return row_bytes % 32 == 0 && row_bytes <= kStageChunk &&
+         nrows * static_cast<int64_t>(row_bytes) >= (4LL << 20) &&
+         ltl_host::bits_available() && !std::getenv("LTL_BYTE_TRANSFERS");
+}
+
+// `bytes` of bits + a flag word at device_bits_flag(.., bytes)
+constexpr size_t bits_flag_offset(size_t bytes) { return (bytes + 255) / 256 * 256; }
+uint8_t* device_bits(ltl_ctx* ctx, size_t bytes) {
+  bytes = bits_flag_offset(bytes) + 256;
+  int dev = 0;
+  ck(cudaGetDevice(&dev), "cudaGetDevice");
+  if (ctx->xbits.size() <= static_cast<size_t>(dev)) ctx->xbits.resize(dev + 1, {nullptr, 0});
+  auto& b = ctx->xbits[dev];
+  if (b.second < bytes) {
+    if (b.first) ck(cudaFree(b.first), "cudaFree (bits)");
+    b.first = nullptr;
+    ck(cudaMalloc(&b.first, bytes), "cudaMalloc (bits)");
+    b.second = bytes;
+  }
+  return b.first;
+}
+
+// false: a byte was not 0 / 1 (nothing usable written; copy bytes instead)
+bool h2d_bits(ltl_ctx* ctx, uint8_t* dev, const uint8_t* host, int64_t nrows, size_t row_bytes,
+              size_t pitch, cudaStream_t st) {
+  const size_t brow = row_bytes / 8;
+  uint8_t* bits = device_bits(ctx, static_cast<size_t>(nrows) * brow);
+  ensure_stage(ctx);
+  const int64_t per = std::max<int64_t>(1, static_cast<int64_t>(kBitsChunk / brow));
+  const int T = ltl_host::xfer_threads();
+  cudaEvent_t ev[2];
+  for (auto& e : ev) ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+  bool ok = true;
+  for (int64_t r0 = 0, k = 0; r0 < nrows && ok; r0 += per, ++k) {
+    const int64_t cnt = std::min(per, nrows - r0);
+    if (k >= 2) ck(cudaEventSynchronize(ev[k % 2]), "staging");  // chunk buffer free again
+    uint8_t* stage = ctx->pinned[k % 2];
+    ok = ltl_host::cells_to_bits(host + r0 * pitch, pitch, row_bytes, cnt, stage, T);
+    if (!ok) break;
+    ck(cudaMemcpyAsync(bits + r0 * brow, stage, cnt * brow, cudaMemcpyHostToDevice, st), "upload");
+    ctx->moved[0] += cnt * static_cast<int64_t>(brow);
+    ck(cudaEventRecord(ev[k % 2], st), "event");
+  }
+  if (ok) ck(ltl::launch_bits_to_cells(bits, dev, nrows * static_cast<int64_t>(row_bytes), st),
+             "bits -> cells");
+  ck(cudaStreamSynchronize(st), "staging");
+  for (auto& e : ev) cudaEventDestroy(e);
+  return ok;
+}
+
+// false: a device byte was not 0 / 1 (nothing written; copy bytes instead)
+bool d2h_bits(ltl_ctx* ctx, uint8_t* host, const uint8_t* dev, int64_t nrows, size_t row_bytes,
+              size_t pitch, cudaStream_t st) {
+  const size_t brow = row_bytes / 8;
+  uint8_t* bits = device_bits(ctx, static_cast<size_t>(nrows) * brow);
+  int32_t* dbad = reinterpret_cast<int32_t*>(bits + bits_flag_offset(static_cast<size_t>(nrows) * brow));
+  ensure_stage(ctx);
+  ck(cudaMemsetAsync(dbad, 0, sizeof(int32_t), st), "memset flag");
+  ck(ltl::launch_cells_to_bits(dev, bits, nrows * static_cast<int64_t>(row_bytes), dbad, st),
+     "cells -> bits");
+  int32_t hbad = 0;
+  ck(cudaMemcpyAsync(&hbad, dbad, sizeof hbad, cudaMemcpyDeviceToHost, st), "flag");
+  ck(cudaStreamSynchronize(st), "flag");
+  if (hbad) return false;
+  const int64_t per = std::max<int64_t>(1, static_cast<int64_t>(kBitsChunk / brow));
+  const int64_t chunks = (nrows + per - 1) / per;
+  const int T = ltl_host::xfer_threads();
+  cudaEvent_t ev[2];
+  for (auto& e : ev) ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+  auto issue = [&](int64_t k) {
+    const int64_t r0 = k * per, cnt = std::min(per, nrows - r0);
+    ck(cudaMemcpyAsync(ctx->pinned[k % 2], bits + r0 * brow, cnt * brow, cudaMemcpyDeviceToHost, st),
+       "download");
+    ctx->moved[1] += cnt * static_cast<int64_t>(brow);
+    ck(cudaEventRecord(ev[k % 2], st), "event");
+  };
+  issue(0);
+  for (int64_t k = 0; k < chunks; ++k) {
+    if (k + 1 < chunks) issue(k + 1);  // its buffer's unpack (chunk k-1) is done
+    ck(cudaEventSynchronize(ev[k % 2]), "staging");
+    const int64_t r0 = k * per, cnt = std::min(per, nrows - r0);
+    ltl_host::bits_to_cells(ctx->pinned[k % 2], host + r0 * pitch, pitch, row_bytes, cnt, T);
+  }
+  for (auto& e : ev) cudaEventDestroy(e);
+  return true;
+}
+
 void h2d_rows(ltl_ctx* ctx, uint8_t* dev, const uint8_t* host, int64_t nrows, size_t row_bytes,
               size_t pitch, cudaStream_t st) {
   if (nrows <= 0 || row_bytes == 0) return;
+  if (use_bits(nrows, row_bytes) && h2d_bits(ctx, dev, host, nrows, row_bytes, pitch, st)) return;
+  ctx->moved[0] += nrows * static_cast<int64_t>(row_bytes);
   if (host_pinned(host) || row_bytes > kStageChunk) {
     ck(cudaMemcpy2DAsync(dev, row_bytes, host, pitch, row_bytes, nrows, cudaMemcpyHostToDevice, st),
        "upload");
@@ -823,6 +930,8 @@ void h2d_rows(ltl_ctx* ctx, uint8_t* dev, const uint8_t* host, int64_t nrows, si
 void d2h_rows(ltl_ctx* ctx, uint8_t* host, const uint8_t* dev, int64_t nrows, size_t row_bytes,
               size_t pitch, cudaStream_t st) {
   if (nrows <= 0 || row_bytes == 0) return;
+  if (use_bits(nrows, row_bytes) && d2h_bits(ctx, host, dev, nrows, row_bytes, pitch, st)) return;
+  ctx->moved[1] += nrows * static_cast<int64_t>(row_bytes);
   if (host_pinned(host) || row_bytes > kStageChunk) {
     ck(cudaMemcpy2DAsync(host, pitch, dev, row_bytes, row_bytes, nrows, cudaMemcpyDeviceToHost, st),
        "download");
@@ -1095,6 +1204,10 @@ void ltl_destroy(ltl_ctx* ctx) {
 int64_t ltl_kernel_launches(const ltl_ctx* ctx) { return ctx ? ctx->launches : -1; }
 
 int64_t ltl_time_launches(const ltl_ctx* ctx) { return ctx ? ctx->timed_launches : 0; }
+
+int64_t ltl_transfer_bytes(const ltl_ctx* ctx, int32_t dir) {
+  return ctx && (dir == 0 || dir == 1) ? ctx->moved[dir] : 0;
+}
 
 const char* ltl_last_error(const ltl_ctx* ctx) {
   return ctx ? ctx->err.c_str() : g_last_error.c_str();

@@ -397,6 +397,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                      kSmemBars = G::kSmemBars;
   constexpr uint32_t kSlotCols = G::kSlotCols, kTmemSlot = G::kTmemSlot, kTmemD2 = G::kTmemD2,
                      kTmemA1 = G::kTmemA1, kPbOff = G::kPbOff, kPiOff = G::kPiOff;
+  LTL_TRACE_CTA(10);  // kernel entry (trace build)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
@@ -494,6 +495,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   // 2..5 write their lane quarter.
   if (warp >= 2 && warp < 2 + kConvWarps) {
     const int m = lane_x<kPk>(32 * static_cast<int>(warp & 3) + static_cast<int>(lane));
+    // pi2(0,0) flipped in this column's fragment (one modulo per thread: the
+    // table below is fully unrolled, and this prologue sits on the critical
+    // path of the last SM at every generation boundary)
+    const bool fault_col = p.inject_fault && m % p.fault_f == 0;
     uint32_t a1[kKChunks * 8];
 #pragma unroll
     for (int c = 0; c < kKChunks * 8; ++c) {
@@ -502,7 +507,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int b = 0; b < 4; ++b) {
         const int d = 4 * c + b - 32 - m;
         const bool in = d >= -r && d <= r;
-        const bool drop = d == 0 && p.inject_fault && m % p.fault_f == 0;  // pi2(0,0) flipped
+        const bool drop = d == 0 && fault_col;
         uint32_t v;
         if constexpr (kPk) {
           // e4m3 weights on cells of 0.5: window 4.0 (0x48) -> 2 per live
@@ -537,6 +542,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_after();
   // Everything above only touched this CTA's SMEM/TMEM, so it overlapped the
   // previous kernel's tail (PDL).  The grid is read from here on.
+  LTL_TRACE_CTA(12);  // prologue done
   pdl_launch_dependents();
   pdl_wait_prerequisites();
   LTL_TRACE_CTA(14);

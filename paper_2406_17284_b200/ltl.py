@@ -69,7 +69,7 @@ class ltl_stats_c(ctypes.Structure):
 # Every symbol include/ltl_b200.h declares (tests check the .so exports them all).
 EXPORTS = (
     "ltl_create", "ltl_create_torus", "ltl_create_grid", "ltl_destroy", "ltl_last_error", "ltl_rows", "ltl_cols",
-    "ltl_num_slabs", "ltl_kernel_launches", "ltl_time_launches", "ltl_upload", "ltl_download",
+    "ltl_num_slabs", "ltl_kernel_launches", "ltl_time_launches", "ltl_transfer_bytes", "ltl_upload", "ltl_download",
     "ltl_upload_interior", "ltl_download_interior", "ltl_run", "ltl_run_async", "ltl_synchronize", "ltl_time",
     "ltl_run_interior", "ltl_create_part", "ltl_set_stream", "ltl_step_part", "ltl_fill_halo",
     "ltl_slab_buffer", "ltl_pack_edges", "ltl_unpack_halo", "ltl_ring_export",
@@ -109,6 +109,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
         "ltl_num_slabs": ([vp], ctypes.c_int32),
         "ltl_kernel_launches": ([vp], ctypes.c_int64),
         "ltl_time_launches": ([vp], ctypes.c_int64),
+        "ltl_transfer_bytes": ([vp, ctypes.c_int32], ctypes.c_int64),
         "ltl_upload": ([vp, u8p, ctypes.c_int32], ctypes.c_int),
         "ltl_download": ([vp, u8p, ctypes.c_int32], ctypes.c_int),
         "ltl_download_padded": ([vp, u8p, ctypes.c_int32, ctypes.c_int32], ctypes.c_int),
@@ -160,6 +161,8 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
         "ltl_build_info": ([], ctypes.c_char_p),
     }
     for name, (args, res) in sig.items():
+        if "LTL_LIB" in os.environ and not hasattr(lib, name):
+            continue  # A/B against an older build: entry points it predates stay unbound
         fn = getattr(lib, name)
         fn.argtypes = args
         fn.restype = res
@@ -409,6 +412,11 @@ class DeviceTorus:
     def time_launches(self) -> int:
         """Kernels launched inside the last time() call's timed loop."""
         return int(self.lib.ltl_time_launches(self._ctx))
+
+    def transfer_bytes(self) -> tuple[int, int]:
+        """(host -> device, device -> host) bytes moved so far (ltl_transfer_bytes)."""
+        return (int(self.lib.ltl_transfer_bytes(self._ctx, 0)),
+                int(self.lib.ltl_transfer_bytes(self._ctx, 1)))
 
     def slab_buffer(self, slab: int = 0, which: int = 0):
         """(device pointer, strip bytes, interior rows) of a generation buffer
