@@ -1143,7 +1143,10 @@ int tc_persistent_ctas(int32_t rows, int32_t cols, int num_sms) {
   // profiles/small_torus_r02.txt).
   if (units <= 2LL * num_sms && !std::getenv("LTL_NO_SMALL_PERSIST"))
     return static_cast<int>(units < num_sms ? units : num_sms);
-  return bands >= 16 && units >= 8LL * num_sms && units <= 190LL * num_sms ? num_sms : 0;
+  // Middle sizes: 8192^2 (28 units per SM) runs 34.5 us per generation with
+  // one launch each vs 38.3 in the sweep, 16384^2 (111 per SM) 95.5 vs 94.3
+  // (same box, after the prologue fix; tools/gpu_r02ah.sh).
+  return bands >= 16 && units >= 48LL * num_sms && units <= 190LL * num_sms ? num_sms : 0;
 }
 
 // Chunks per band of the multi-generation sweep: <= 12 units per chunk
