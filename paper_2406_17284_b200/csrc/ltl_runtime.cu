@@ -22,6 +22,7 @@
 #include "host/internal.hpp"
 #include "ltl_b200.h"
 #include "ltl_kernels.cuh"
+#include "ptx_sm100.cuh"
 
 using ltl::kHalo;
 
@@ -963,7 +964,38 @@ void d2h_rows(ltl_ctx* ctx, uint8_t* host, const uint8_t* dev, int64_t nrows, si
   for (auto& e : ev) cudaEventDestroy(e);
 }
 
+// Ring readers of our "dead" buffer.  Between steps the other generation
+// buffer of a slab holds generation g-1 -- but a ring neighbour still running
+// its step g-1 reads that buffer's edge rows (and a neighbour running step g
+// reads the current one).  Uploads / downloads / snapshots use the dead
+// buffer as their dense staging area and an upload rewrites the current one,
+// so before them every ring neighbour must be past every step that reads our
+// buffers: neighbours in this process -- all slabs' streams drained; in other
+// processes -- a one-thread kernel on the slab's stream waits until their
+// step counters reach ours (the steps read our buffers up to generation
+// ring_gen - 1; a neighbour ahead is blocked on our counter before it reads
+// generation ring_gen).
+__global__ void ring_quiesce_kernel(const uint32_t* up_done, const uint32_t* down_done,
+                                    uint32_t target) {
+  ltl::ptx::wait_flag_geq_sys(up_done, target);
+  ltl::ptx::wait_flag_geq_sys(down_done, target);
+}
+
+void quiesce_ring_readers(ltl_ctx* ctx) {
+  if (!ring_ok(ctx)) return;
+  if (ctx->slabs.size() > 1) sync_all(ctx);
+  if (!ctx->external_row_halo) return;  // in-process ring: the streams are the order
+  for (Slab& s : ctx->slabs) {
+    if (!s.up_done || !s.down_done) continue;
+    ck(cudaSetDevice(s.dev), "cudaSetDevice");
+    ring_quiesce_kernel<<<1, 1, 0, s.stream>>>(s.up_done, s.down_done, s.ring_gen);
+    ck(cudaGetLastError(), "ring quiesce");
+    ++ctx->launches;
+  }
+}
+
 void upload_interior(ltl_ctx* ctx, const uint8_t* interior) {
+  quiesce_ring_readers(ctx);
   const int cur = ctx->cur;
   for (Slab& s : ctx->slabs) {
     ck(cudaSetDevice(s.dev), "cudaSetDevice");
@@ -980,6 +1012,7 @@ void upload_interior(ltl_ctx* ctx, const uint8_t* interior) {
 }
 
 void download_interior(ltl_ctx* ctx, uint8_t* interior) {
+  quiesce_ring_readers(ctx);
   const int cur = ctx->cur;
   for (Slab& s : ctx->slabs) {
     ck(cudaSetDevice(s.dev), "cudaSetDevice");
@@ -1039,6 +1072,7 @@ void host_fill_halo(uint8_t* padded, int32_t n, int32_t f, int32_t layout) {
 // f (n + 2f)) into the slab's dead generation buffer, and a relayout kernel
 // scatters it into strips.  No host pass over the cells.
 void upload_padded(ltl_ctx* ctx, const uint8_t* padded, int32_t layout) {
+  quiesce_ring_readers(ctx);
   const int32_t n = ctx->rows, f = ctx->f;
   const size_t p = static_cast<size_t>(n) + 2 * f;
   const int cur = ctx->cur;
@@ -1082,6 +1116,7 @@ void upload_padded(ltl_ctx* ctx, const uint8_t* padded, int32_t layout) {
 // interior of `padded`; the halo bytes are untouched unless fill_halo (then
 // the periodic images are written on the host: 4fn + 4f^2 cells).
 void download_padded(ltl_ctx* ctx, uint8_t* padded, int32_t layout, bool fill_halo) {
+  quiesce_ring_readers(ctx);
   const int32_t n = ctx->rows, f = ctx->f;
   const size_t p = static_cast<size_t>(n) + 2 * f;
   const int cur = ctx->cur;
@@ -1683,6 +1718,7 @@ void check_square(const ltl_ctx* ctx) {
 }
 
 void snapshot_write_ctx(ltl_ctx* ctx, const char* path, int32_t layout) {
+  quiesce_ring_readers(ctx);
   check_layout(layout);
   check_square(ctx);
   std::FILE* fh = std::fopen(path, "wb");
@@ -1727,6 +1763,7 @@ void snapshot_write_ctx(ltl_ctx* ctx, const char* path, int32_t layout) {
 }
 
 int32_t snapshot_read_ctx(ltl_ctx* ctx, const char* path) {
+  quiesce_ring_readers(ctx);
   std::FILE* fh = std::fopen(path, "rb");
   if (!fh) snap_fail(std::string("cannot open '") + path + "' for reading");
   FileCloser closer{fh};

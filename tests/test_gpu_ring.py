@@ -26,7 +26,8 @@ def _free_port():
     return port
 
 
-def _worker(rank, world, port, global_rows, cols, steps, text, q, multi=False, own_gpu=False):
+def _worker(rank, world, port, global_rows, cols, steps, text, q, multi=False, own_gpu=False,
+            race=False):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     if multi:  # multi-generation launches even on small slabs (world 1: self-ring)
         os.environ["LTL_FORCE_PERSIST"] = "1"
@@ -40,7 +41,15 @@ def _worker(rank, world, port, global_rows, cols, steps, text, q, multi=False, o
         rng = np.random.default_rng(7)
         full = (rng.random((global_rows, cols)) < 0.3).astype(np.uint8)
         part.upload(np.ascontiguousarray(full[part.row0:part.row0 + part.rows]))
-        if multi:
+        if race:
+            # downloads with no barrier around them, right before and right
+            # after the steps: a neighbour may still be reading this rank's
+            # buffers (ltl_download must wait for it, never race it)
+            part.torus.download()
+            part.run(text, 2)
+            part.torus.download()
+            part.run(text, steps - 2)
+        elif multi:
             part.run(text, steps - 2)  # all generations in one call ...
             part.run(text, 2)          # ... and a second call continuing the counters
         else:
@@ -56,15 +65,19 @@ def _worker(rank, world, port, global_rows, cols, steps, text, q, multi=False, o
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,global_rows,cols,multi,own_gpu", [
-    (2, 256, 256, False, False), (4, 512, 128, False, False), (1, 96, 384, False, False),
-    (2, 256, 256, True, False),               # same GPU: one launch per generation
-    (1, 512, 384, True, False),               # self-ring: persistent ring kernel
+@pytest.mark.parametrize("world,global_rows,cols,multi,own_gpu,race", [
+    (2, 256, 256, False, False, False), (4, 512, 128, False, False, False),
+    (1, 96, 384, False, False, False),
+    (2, 256, 256, True, False, False),        # same GPU: one launch per generation
+    (1, 512, 384, True, False, False),        # self-ring: persistent ring kernel
+    # unsynchronised downloads between steps, multi-band slabs
+    (2, 2048, 1024, False, False, True), (4, 2048, 512, False, False, True),
     # one process per GPU (needs >= 2 / 4 GPUs): the cross-device persistent
     # ring kernel, rows pulled over NVLink through CUDA IPC
-    (2, 1024, 512, True, True), (2, 512, 256, False, True), (4, 2048, 256, True, True),
+    (2, 1024, 512, True, True, False), (2, 512, 256, False, True, False),
+    (4, 2048, 256, True, True, False), (2, 4096, 1024, True, True, True),
 ])
-def test_ring_processes_match_oracle(orc, world, global_rows, cols, multi, own_gpu):
+def test_ring_processes_match_oracle(orc, world, global_rows, cols, multi, own_gpu, race):
     if not torch.cuda.is_available():
         pytest.skip("no GPU")
     if own_gpu and torch.cuda.device_count() < world:
@@ -75,7 +88,8 @@ def test_ring_processes_match_oracle(orc, world, global_rows, cols, multi, own_g
     q = ctx.Queue()
     port = _free_port()
     procs = [ctx.Process(target=_worker,
-                         args=(r, world, port, global_rows, cols, steps, text, q, multi, own_gpu))
+                         args=(r, world, port, global_rows, cols, steps, text, q, multi, own_gpu,
+                               race))
              for r in range(world)]
     for p in procs:
         p.start()
