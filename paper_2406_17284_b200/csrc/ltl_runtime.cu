@@ -1468,6 +1468,7 @@ int ltl_init_random(ltl_ctx* ctx, double density, uint64_t seed, int32_t fill_n)
         throw std::invalid_argument("init_random: fill_n exceeds n");
       fill_rows = fill_cols = fill_n;
     }
+    quiesce_ring_readers(ctx);  // rewrites the current generation neighbours may read
     for (Slab& s : ctx->slabs) {
       ck(cudaSetDevice(s.dev), "cudaSetDevice");
       ck(ltl::launch_init_random(s.view(ctx->cur, ctx->cols), s.row0, fill_rows, fill_cols,
