@@ -253,6 +253,19 @@ def reference_arm(args, rank, world):
         n = 16384
         note = f" (bounded sample: {n}^2 torus of the same rule; the GPU arm's torus is " \
                f"{'N*' if workload == 'c4' else ''}65536 x 65536)"
+    else:
+        # each step a bounded sample so the whole run ends within minutes: the
+        # reference CAT engine does ~5.5e7 cell updates/s on 16 cores, flat in
+        # n and r (profiles/bench_ref_c2_r02a.json: 19.4 s per 32768^2
+        # generation); the largest square torus whose W + K generations fit
+        # in ~5 min
+        full = n
+        while n > 4096 and (args.warmup + args.steps) * n * n / 5.5e7 > 300:
+            n //= 2
+        if n != full:
+            note = (f" (bounded sample: {n}^2 torus of the same rules and densities, so that the "
+                    f"{args.warmup} + {args.steps} generations end within minutes; the GPU arm's "
+                    f"torus is {full} x {full})")
     # the initial grids, built by the reference's init_random in parallel threads
     grids = [None] * len(rules)
 
