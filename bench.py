@@ -130,7 +130,8 @@ def workload_side(workload):
 
 class Clocks:
     """SM clock / throttle sampler running during the timed region: NVML every
-    5 ms (nvidia_ml_py), else nvidia-smi every 100 ms."""
+    20 ms (nvidia_ml_py; light enough not to disturb the timed launches), else
+    nvidia-smi every 100 ms."""
 
     REASONS = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20,
                "sw_power_cap": 0x4}
@@ -160,7 +161,7 @@ class Clocks:
                         self.watts.append(pynvml.nvmlDeviceGetPowerUsage(h) / 1000.0)
                     except Exception:  # noqa: BLE001
                         pass
-                    time.sleep(0.005)
+                    time.sleep(0.020)
             self.thread = threading.Thread(target=loop, daemon=True)
             self.thread.start()
             return
