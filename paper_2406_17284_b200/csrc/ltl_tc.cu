@@ -430,26 +430,63 @@ __global__ void __launch_bounds__(kThreads, 1)
   // (nb = G::kBandChunks).  kH = 32, VN: the band's centre entry also carries
   // 128 (Pb = state there), so Z = R + 256 state clears R <= 2 (2r + 1).
   constexpr int nb = G::kBandChunks;
-  for (uint32_t w = threadIdx.x; w < G::kNumTiles * kSub * 8u; w += kThreads) {
-    const int t = static_cast<int>(w / (kSub * 8)), j = static_cast<int>((w / 8) % kSub),
-              k0 = 4 * static_cast<int>(w % 8);
-    const int rho = out_row_of_col(j);
-    uint32_t word = 0;
+  // The twelve warps outside 2..5 build the band tiles while warps 2..5
+  // compute the pass-1 A table in registers (the prologue sits on the
+  // critical path of the last SM at every generation boundary).
+  constexpr uint32_t kTileThreads = kThreads - 32 * kConvWarps;
+  const bool a_warp = warp >= 2 && warp < 2 + kConvWarps;
+  uint32_t a1[kKChunks * 8];
+  if (a_warp) {
+    const int m = lane_x<kPk>(32 * static_cast<int>(warp & 3) + static_cast<int>(lane));
+    // pi2(0,0) flipped in this column's fragment (one modulo per thread: the
+    // table below is fully unrolled, and this prologue sits on the critical
+    // path of the last SM at every generation boundary)
+    const bool fault_col = p.inject_fault && m % p.fault_f == 0;
 #pragma unroll
-    for (int b = 0; b < 4; ++b) {
-      int v;
-      if (t < nb) {
-        const int d = 32 * t + k0 + b - kH - rho;
-        v = (d >= -r && d <= r);
-        if (p.inject_fault && d == 0 && (rho + p.fault_row_phase) % p.fault_f == 0) v = 0;
-        if (kH == 32 && vn && d == 0) v += 128;
-      } else {
-        const int c = (t - nb) % 2;
-        v = (32 * c + k0 + b == rho) ? (t >= nb + 2 ? static_cast<int>(G::kCentreW) : 1) : 0;
+    for (int c = 0; c < kKChunks * 8; ++c) {
+      uint32_t word = 0;
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {
+        const int d = 4 * c + b - 32 - m;
+        const bool in = d >= -r && d <= r;
+        const bool drop = d == 0 && fault_col;
+        uint32_t v;
+        if constexpr (kPk) {
+          // e4m3 weights on cells of 0.5: window 4.0 (0x48) -> 2 per live
+          // cell, centre 6.0 (0x4C) -> 3: D1 = 2 H + state; faulted centre
+          // 2.0 (0x40) -> the state marker only
+          v = d == 0 ? (drop ? 0x40u : 0x4Cu) : in ? 0x48u : 0u;
+        } else {
+          // D1 = H + 128 state (the state marker in bit 7)
+          v = d == 0 ? (drop ? 128u : 129u) : in ? 1u : 0u;
+        }
+        word |= v << (8 * b);
       }
-      word |= static_cast<uint32_t>(v) << (8 * b);
+      a1[c] = word;
     }
-    *reinterpret_cast<uint32_t*>(smem + kSmemBand + t * kTileBytes + sw32_offset(j, k0)) = word;
+  } else {
+    const uint32_t tid_t = threadIdx.x < 64 ? threadIdx.x : threadIdx.x - 32 * kConvWarps;
+    for (uint32_t w = tid_t; w < G::kNumTiles * kSub * 8u; w += kTileThreads) {
+      const int t = static_cast<int>(w / (kSub * 8)), j = static_cast<int>((w / 8) % kSub),
+                k0 = 4 * static_cast<int>(w % 8);
+      const int rho = out_row_of_col(j);
+      uint32_t word = 0;
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {
+        int v;
+        if (t < nb) {
+          const int d = 32 * t + k0 + b - kH - rho;
+          v = (d >= -r && d <= r);
+          if (p.inject_fault && d == 0 && (rho + p.fault_row_phase) % p.fault_f == 0) v = 0;
+          if (kH == 32 && vn && d == 0) v += 128;
+        } else {
+          const int c = (t - nb) % 2;
+          v = (32 * c + k0 + b == rho) ? (t >= nb + 2 ? static_cast<int>(G::kCentreW) : 1) : 0;
+        }
+        word |= static_cast<uint32_t>(v) << (8 * b);
+      }
+      *reinterpret_cast<uint32_t*>(smem + kSmemBand + t * kTileBytes + sw32_offset(j, k0)) = word;
+    }
   }
   if constexpr (kPk) {  // e2m1 1.0 = nibble 2 everywhere (data and padding: layout-free)
     for (uint32_t w = threadIdx.x; w < G::kOnesBytes / 4; w += kThreads)
@@ -493,35 +530,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   // cheaper than an SMEM descriptor one, tools/ubench_mma.cu): lane x holds
   // A1[x][k] = [|k-32-x| <= r] + 128*[k == x+32], four k per column; warps
   // 2..5 write their lane quarter.
-  if (warp >= 2 && warp < 2 + kConvWarps) {
-    const int m = lane_x<kPk>(32 * static_cast<int>(warp & 3) + static_cast<int>(lane));
-    // pi2(0,0) flipped in this column's fragment (one modulo per thread: the
-    // table below is fully unrolled, and this prologue sits on the critical
-    // path of the last SM at every generation boundary)
-    const bool fault_col = p.inject_fault && m % p.fault_f == 0;
-    uint32_t a1[kKChunks * 8];
-#pragma unroll
-    for (int c = 0; c < kKChunks * 8; ++c) {
-      uint32_t word = 0;
-#pragma unroll
-      for (int b = 0; b < 4; ++b) {
-        const int d = 4 * c + b - 32 - m;
-        const bool in = d >= -r && d <= r;
-        const bool drop = d == 0 && fault_col;
-        uint32_t v;
-        if constexpr (kPk) {
-          // e4m3 weights on cells of 0.5: window 4.0 (0x48) -> 2 per live
-          // cell, centre 6.0 (0x4C) -> 3: D1 = 2 H + state; faulted centre
-          // 2.0 (0x40) -> the state marker only
-          v = d == 0 ? (drop ? 0x40u : 0x4Cu) : in ? 0x48u : 0u;
-        } else {
-          // D1 = H + 128 state (the state marker in bit 7)
-          v = d == 0 ? (drop ? 128u : 129u) : in ? 1u : 0u;
-        }
-        word |= v << (8 * b);
-      }
-      a1[c] = word;
-    }
+  if (a_warp) {
     const uint32_t trow = tmem + ((32u * (warp & 3)) << 16) + kTmemA1;
 #pragma unroll
     for (int c = 0; c < kKChunks; ++c) {
