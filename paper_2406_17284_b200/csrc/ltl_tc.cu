@@ -1158,13 +1158,14 @@ int tc_persistent_ctas(int32_t rows, int32_t cols, int num_sms) {
   return bands >= 16 && units >= 48LL * num_sms && units <= 190LL * num_sms ? num_sms : 0;
 }
 
-// Chunks per band of the multi-generation sweep: <= 12 units per chunk
-// (16384^2 A/B: 12 -> 93.7 us, 16 -> 94.3, 20 -> 97.0, 8 -> ~101), and no
+// Chunks per band of the multi-generation sweep: <= 16 units per chunk
+// (16384^2, current kernel, tools/gpu_r02al.sh: 8 / 12 / 16 / 24 / 32 / 64 /
+// 128 units -> 100.8 / 94.4 / 93.4 / 95.0 / 96.2 / 94.4 / 136.5 us), and no
 // more units per chunk than units per CTA (a tiny torus: one unit per chunk,
 // so every CTA gets one).
 int tc_sweep_chunks(int32_t strips, int32_t bands, int ctas) {
-  const int64_t per_cta = ctas > 0 ? static_cast<int64_t>(strips) * bands / ctas : 12;
-  int per = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(12, per_cta)));
+  const int64_t per_cta = ctas > 0 ? static_cast<int64_t>(strips) * bands / ctas : 16;
+  int per = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(16, per_cta)));
   if (const char* e = std::getenv("LTL_SWEEP_UNITS")) per = std::max(1, std::atoi(e));  // tuning
   return (strips + per - 1) / per;
 }
