@@ -123,48 +123,38 @@ __device__ __forceinline__ uint32_t next_word(uint32_t a, uint32_t b) {
 // of the slab into tile[TY + 32][kTileW] (rows past the slab read as 0).
 // The strip's own 128 columns are ONE contiguous block of the strip layout
 // (16-byte chunk i at byte 16 i); the 16 side columns are one chunk per row
-// of the neighbour strips.  Every thread first issues ALL its loads (ncu:
-// with one load in flight per thread the loop stalled ~30 % of the kernel on
-// the store waiting for it), then stores them.
+// of the neighbour strips.  16-byte cp.async copies (LDGSTS): the data goes
+// global -> SMEM without a register round trip or an SMEM store instruction
+// (ncu of the register-staged version: the tile stores waited on their loads
+// and crowded the shared-memory instruction queue of the compute phase).
+__device__ __forceinline__ void cp_async16(uint8_t* dst, const void* src, bool valid) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;"
+               ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(dst))), "l"(src),
+               "r"(valid ? 16 : 0)
+               : "memory");
+}
+
 template <int TY>
 __device__ __forceinline__ void load_tile(const SlabView& in, int strip, int y0, uint8_t* tile) {
   constexpr int kRows = TY + 2 * kHalo;
   constexpr int kMain = kRows * 8, kSide = kRows * 2;
-  constexpr int kPerMain = (kMain + kThreads - 1) / kThreads;
-  constexpr int kPerSide = (kSide + kThreads - 1) / kThreads;
   const int valid_rows = min(kRows, in.rows + 2 * kHalo - y0);
   const uint8_t* mid = in.buf + static_cast<int64_t>(strip + 1) * in.strip_bytes +
                        static_cast<int64_t>(y0) * kStrip;
   const uint8_t* left = mid - in.strip_bytes + (kStrip - kHalo);
   const uint8_t* right = mid + in.strip_bytes;
-  uint4 vm[kPerMain], vs[kPerSide];
-#pragma unroll
-  for (int u = 0; u < kPerMain; ++u) {
-    const int i = static_cast<int>(threadIdx.x) + u * kThreads;
-    vm[u] = (i < kMain && (i >> 3) < valid_rows)
-                ? __ldg(reinterpret_cast<const uint4*>(mid) + i) : make_uint4(0, 0, 0, 0);
+  for (int i = static_cast<int>(threadIdx.x); i < kMain; i += kThreads) {
+    const bool v = (i >> 3) < valid_rows;  // zero-filled past the slab
+    cp_async16(tile + (i >> 3) * kTileW + kHalo + 16 * (i & 7),
+               v ? mid + 16 * i : in.buf, v);
   }
-#pragma unroll
-  for (int u = 0; u < kPerSide; ++u) {
-    const int i = static_cast<int>(threadIdx.x) + u * kThreads;
+  for (int i = static_cast<int>(threadIdx.x); i < kSide; i += kThreads) {
     const int row = i >> 1;
-    vs[u] = (i < kSide && row < valid_rows)
-                ? __ldg(reinterpret_cast<const uint4*>((i & 1 ? right : left) + row * kStrip))
-                : make_uint4(0, 0, 0, 0);
+    const bool v = row < valid_rows;
+    cp_async16(tile + row * kTileW + ((i & 1) ? kHalo + kStrip : 0),
+               v ? (i & 1 ? right : left) + row * kStrip : in.buf, v);
   }
-  auto put = [&](int row, int col, const uint4& v) {
-    *reinterpret_cast<uint4*>(tile + row * kTileW + col) = v;  // 16-byte aligned
-  };
-#pragma unroll
-  for (int u = 0; u < kPerMain; ++u) {
-    const int i = static_cast<int>(threadIdx.x) + u * kThreads;
-    if (i < kMain) put(i >> 3, kHalo + 16 * (i & 7), vm[u]);
-  }
-#pragma unroll
-  for (int u = 0; u < kPerSide; ++u) {
-    const int i = static_cast<int>(threadIdx.x) + u * kThreads;
-    if (i < kSide) put(i >> 1, (i & 1) ? kHalo + kStrip : 0, vs[u]);
-  }
+  asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
 }
 
 // store four next states at interior row y, columns x .. x+3 (clipped to cols)
@@ -513,40 +503,35 @@ cudaError_t launch_r(const SlabView& in, const SlabView& out, const RuleConsts& 
   const int strips = interior_strips(in.cols);
   const int ty = engine == kEnginePack ? kPackTY : kBaseTY;
   const dim3 grid(strips, (in.rows + ty - 1) / ty);
-  // pack: at most four CTAs per SM.  At r = 1 the tile + H rows (45.3 KB)
-  // would let five in, and five run 29 % slower (620 vs 480 us at 32768^2,
-  // same-box A/B: the fifth CTA's row pass floods the shared-memory
-  // instruction queue, ncu stall mio_throttle 10.9 vs 2.0); three or fewer
-  // are slower again (520 / 674 us).
-  constexpr size_t kPackSmemFloor = 47000;
-  size_t smem = engine == kEnginePack ? std::max(pack_smem_bytes<R>(), kPackSmemFloor) : 0;
+  // CTAs per SM: with the cp.async tile loads as many as the SMEM allows
+  // (same-box A/B at 32768^2, tools/gpu_r02ao.sh: pack r = 1 with five CTAs
+  // 2.84e12 vs four 2.73e12 vs three 2.45e12; base r = 1 with seven 2.24e12
+  // vs five 2.12e12).  The register-staged loads of round 1 wanted caps (the
+  // fifth pack CTA's tile stores flooded the shared-memory instruction queue);
+  // the A/B knobs stay.
+  size_t smem = engine == kEnginePack ? pack_smem_bytes<R>() : 0;
   if (engine == kEnginePack)
     if (const char* e = std::getenv("LTL_PACK_MIN_SMEM"))  // A/B: CTAs per SM
       smem = std::max<size_t>(pack_smem_bytes<R>(), static_cast<size_t>(std::atol(e)));
-  // base: its 28 KB static tile would let seven CTAs in; 10 KB of unused
-  // dynamic padding keeps five, 1.26x faster at r = 1 (682 -> 541 us at
-  // 32768^2, same-box A/B; r = 2 / 3: 861 -> 749, 1189 -> 1075 us).
-  if (engine == kEngineBase) {
-    smem = 10000;
+  if (engine == kEngineBase)
     if (const char* e = std::getenv("LTL_BASE_PAD_SMEM"))  // A/B: CTAs per SM
       smem = static_cast<size_t>(std::atol(e));
-  }
   if (smem > 48 * 1024) {
-    // the attribute is per device: set once on each (a per-launch call
-    // serialises launches measurably)
-    static bool done[64] = {};
+    // the attribute is per device: set on each when a launch needs more than
+    // it was set to (a per-launch call serialises launches measurably)
+    static size_t set_to[64] = {};
     int dev = 0;
     cudaError_t e = cudaGetDevice(&dev);
     if (e != cudaSuccess) return e;
     if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
-    if (!done[dev]) {
+    if (set_to[dev] < smem) {
       for (auto fn : {pack_kernel<R, 0, true>, pack_kernel<R, 0, false>, pack_kernel<R, 1, true>,
                       pack_kernel<R, 1, false>}) {
         e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(smem));
         if (e != cudaSuccess) return e;
       }
-      done[dev] = true;
+      set_to[dev] = smem;
     }
   }
 #define LTL_STENCIL_LAUNCH(KERNEL, KIND)                                                   \
