@@ -26,7 +26,7 @@ def main():
         rule = parse_rule_text(text)
         init = (np.random.default_rng(rows + cols).random((rows, cols)) < 0.3).astype(np.uint8)
         want = orc.simulate(init, rule, 3)
-        for engine in ("cat", "base", "pack"):
+        for engine in ("cat", "base", "pack", "cat-4bit"):
             with ltl.DeviceTorus(rows=rows, cols=cols) as t:
                 t.upload(init)
                 t.run(text, 3, engine=engine, stats=True)
@@ -47,6 +47,12 @@ def main():
         t.init_random(0.4, 2)
         p = t.download_padded(ltl.LAYOUT_FRAGMENT)
         t.upload_padded(p, ltl.LAYOUT_FRAGMENT)
+    with ltl.DeviceTorus(n=2048) as t:  # bit-packed host <-> device transfers (>= 4 MB)
+        g = (np.random.default_rng(9).random((2048, 2048)) < 0.3).astype(np.uint8)
+        t.upload(g)
+        assert np.array_equal(t.download(), g)
+        t.run("R1,C2,M0,S2..3,B3..3,NM", 1, engine="cat-4bit")
+        assert np.array_equal(t.download(), orc.simulate(g, parse_rule_text("R1,C2,M0,S2..3,B3..3,NM"), 1))
     print("sanitize cases done")
 
 
