@@ -29,7 +29,7 @@
 extern "C" {
 #endif
 
-#define LTL_ABI_VERSION 4
+#define LTL_ABI_VERSION 5
 
 /* status codes <-> reference exception classes */
 #define LTL_OK 0

@@ -1159,9 +1159,10 @@ void download_padded(ltl_ctx* ctx, uint8_t* padded, int32_t layout, bool fill_ha
 extern "C" {
 
 const char* ltl_build_info(void) {
-  return "ltl_b200 abi=4 arch=sm_100a layout=column-strips-128 "
-         "engines=cat(tcgen05-banded-i8:sweep,ring),base(cuda-core-direct),pack(cuda-core-sliding) "
-         "kernels=halo,relayout,fragment-relayout,init,snapshot";
+  return "ltl_b200 abi=5 arch=sm_100a layout=column-strips-128 "
+         "engines=cat(tcgen05-banded-i8:sweep,ring;4bit:tcgen05-f8f6f4),base(cuda-core-direct),"
+         "pack(cuda-core-sliding) "
+         "kernels=halo,relayout,fragment-relayout,init,snapshot,cell-pack,bit-transfer";
 }
 
 int ltl_create_torus(ltl_ctx** out, int32_t rows, int32_t cols, int32_t num_slabs,
