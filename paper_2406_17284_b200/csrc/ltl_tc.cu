@@ -103,6 +103,18 @@ static_assert(kSubs == 2 && kSlots == kSubs, "one output group per sub-block; ba
 //            band chunks, one D2 buffer shared by the two output groups
 //            (TMEM), 7 box stages and 2 staging slots per group (SMEM).
 // The pass-1 K range [-32, 160) already covers a horizontal radius of 32.
+// 4-bit cells: the f16 D1 is moved into the binade [1024, 2048) (bit pattern
+// 0x6400 + D1) by a 7th pass-1 MMA (1, default) or by an add.f16x2 per
+// register in the convert (0, A/B).
+#ifndef LTL_PK_BIAS_MMA
+#define LTL_PK_BIAS_MMA 1
+#endif
+__device__ __forceinline__ uint32_t hadd2_u32(uint32_t a, uint32_t b) {
+  uint32_t d;
+  asm("add.rn.f16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
+  return d;
+}
+
 template <int kH, bool kPk = false>
 struct Geo {
   static_assert(kH == 16 || kH == 32, "halo rows");
@@ -718,7 +730,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           };
           // (the padded 4-bit SMEM layout keeps 32 cells per 32 bytes: the
           // same K-chunk offsets as u8 cells)
-          if constexpr (kPk) {
+          if constexpr (kPk && LTL_PK_BIAS_MMA) {
             // D1 = 1024 + 2 H + state (f16): each f16's low byte is 2 H + state
             mma1(tmem + G::kTmemBias, smem_desc_sw32_kmajor(smem_u32(smem + G::kSmemOnes)), 0);
             mma1(a1, box(gl) + (96 >> 4), 1);
@@ -764,6 +776,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         else
           tmem_ld_32x32b_x16_pack16(slot_col + 128, *reinterpret_cast<uint32_t(*)[16]>(vc));
         tmem_ld_wait();
+        if constexpr (kPk && !LTL_PK_BIAS_MMA) {
+#pragma unroll
+          for (int k = 0; k < 32; ++k) va[k] = hadd2_u32(va[k], 0x64006400u);
+#pragma unroll
+          for (int k = 0; k < 32; ++k) vb[k] = hadd2_u32(vb[k], 0x64006400u);
+#pragma unroll
+          for (int k = 0; k < kBox / 2 - 64; ++k) vc[k] = hadd2_u32(vc[k], 0x64006400u);
+        }
         auto reg = [&](int k) -> uint32_t { return k < 32 ? va[k] : k < 64 ? vb[k - 32] : vc[k - 64]; };
         auto raw_word = [&](int i) -> uint32_t {  // box rows 4i .. 4i+3 as bytes
           return pack_pairs(reg(2 * i), reg(2 * i + 1));
