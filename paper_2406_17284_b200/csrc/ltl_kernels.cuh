@@ -172,6 +172,8 @@ struct TcLaunch {
   long long* trace;    // debug timeline (LTL_TC_TRACE), nullptr = off
   int32_t packed;      // 4-bit cells: maps over PackedSlab buffers (halo 16, whole-torus
                        // slab, every wrap by the loads)
+  uint32_t* dyn;       // one launch per generation: 2 zeroed words (remainder cursor,
+                       // exit ticket) for the dynamic schedule; nullptr = static
 };
 cudaError_t launch_tc_step(const TcLaunch& a, cudaStream_t stream);
 int tc_persistent_ctas(int32_t rows, int32_t cols, int num_sms);  // 0: no multi-generation launch

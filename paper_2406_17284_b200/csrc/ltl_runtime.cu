@@ -51,6 +51,7 @@ struct Slab {
   CUtensorMap store_map[2];
   ltl::DeviceStats* dstats = nullptr;
   uint32_t* flags = nullptr;   // per-unit completion counters (multi-generation launches)
+  uint32_t* dyn = nullptr;     // dynamic schedule of one-generation launches (cursor, ticket)
   uint32_t flag_base = 0;      // their value between launches
   cudaStream_t stream = nullptr;
   bool own_stream = true;
@@ -284,6 +285,8 @@ void create_slabs(ltl_ctx* ctx, int32_t num_slabs, const int32_t* dev_ids) {
       ck(cudaMalloc(&s.flags, std::max<size_t>(units, 1) * sizeof(uint32_t)), "cudaMalloc flags");
       ck(cudaMemsetAsync(s.flags, 0, std::max<size_t>(units, 1) * sizeof(uint32_t), s.stream),
          "memset flags");
+      ck(cudaMalloc(&s.dyn, 2 * sizeof(uint32_t)), "cudaMalloc schedule cursor");
+      ck(cudaMemsetAsync(s.dyn, 0, 2 * sizeof(uint32_t), s.stream), "memset schedule cursor");
       ck(cudaMalloc(&s.ring_sync, 2 * sizeof(uint32_t)), "cudaMalloc ring counters");
       ck(cudaMemsetAsync(s.ring_sync, 0, 2 * sizeof(uint32_t), s.stream), "memset ring counters");
     }
@@ -335,6 +338,7 @@ void destroy_ctx(ltl_ctx* ctx) {
       if (b) cudaFree(b);
     if (s.dstats) cudaFree(s.dstats);
     if (s.flags) cudaFree(s.flags);
+    if (s.dyn) cudaFree(s.dyn);
     for (void* ptr : s.ipc_opened) cudaIpcCloseMemHandle(ptr);
     if (s.ring_sync) cudaFree(s.ring_sync);
     if (s.ev_step) cudaEventDestroy(s.ev_step);
@@ -523,6 +527,7 @@ void enqueue_step_packed(ltl_ctx* ctx, const ltl::RuleConsts& rc, uint32_t flags
     a.rows = s.rows;
     a.cols = ctx->cols;
     a.rule = rc;
+    a.dyn = s.dyn;
     a.inject_fault = (flags & LTL_FLAG_INJECT_FAULT) != 0;
     a.fault_f = ctx->f;
     a.fault_row_phase = s.row0 % ctx->f;
@@ -633,6 +638,7 @@ void enqueue_step(ltl_ctx* ctx, const ltl::RuleConsts& rc, uint32_t flags, bool 
       a.rows = s.rows;
       a.cols = ctx->cols;
       a.rule = rc;
+      a.dyn = s.dyn;
       a.inject_fault = fault;
       // the reference's fault flips pi2(0,0) of every f x f fragment
       // (src/cat_engine.cpp:277): columns / rows == 0 mod f of the global torus

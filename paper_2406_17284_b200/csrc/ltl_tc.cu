@@ -93,6 +93,8 @@ constexpr int kWarpP2 = kWarpOut0 + kOutWarps;  // 14
 constexpr int kWarpStore = kWarpP2 + 1;           // 15
 constexpr uint32_t kTileBytes = kSub * 32;        // 2 KB pass-2 B tile [64 n][32 k]
 constexpr uint32_t kTmemCols = 512;               // all of the SM's TMEM
+constexpr uint32_t kSegSlots = 8;                 // dynamic-schedule segment ring
+constexpr uint32_t kSegReaders = 15;              // warps that read it: all but the producer
 static_assert(kSubs == 2 && kSlots == kSubs, "one output group per sub-block; barrier arrays sized kSubs");
 
 // Geometry of one kernel variant, by the halo rows kH its boxes carry:
@@ -166,7 +168,10 @@ struct Geo {
   static constexpr uint32_t kSmemBars = kSmemStage + kSubs * kStageSlots * kStageBytes;
   static constexpr uint32_t kNumBars =
       2 * kXStages + 4 * kSlots + 2 * kSubs + 2 * kSubs * kStageSlots;
-  static constexpr uint32_t kSmemTotal = kSmemBars + kNumBars * 8 + 16;
+  // dynamic remainder schedule (SegIter): a ring of segment descriptors
+  // handed from the producer warp to the other roles
+  static constexpr uint32_t kSmemSeg = (kSmemBars + kNumBars * 8 + 16 + 15) & ~15u;
+  static constexpr uint32_t kSmemTotal = kSmemSeg + kSegSlots * (16 + 2 * 8);
   static constexpr uint32_t kSmemAlloc = kSmemTotal + 1024;  // alignment slack
   static_assert(kSmemAlloc <= 227 * 1024, "shared memory budget");
 
@@ -248,6 +253,10 @@ struct Params {
   uint32_t flag_base;            // their common value when the launch starts
   DeviceStats* stats;
   long long* trace;  // debug timeline of CTA 0 (only with -DLTL_TC_TRACE_BUILD)
+  // one launch per generation: the remainder after the whole-band rounds is
+  // handed out at run time ([0] unit cursor, [1] CTA exit ticket; zero
+  // between launches), nullptr = the static remainder runs
+  uint32_t* dyn;
 };
 
 #ifdef LTL_TC_TRACE_BUILD
@@ -299,6 +308,19 @@ __device__ __forceinline__ long long global_ns() {
 // order: no unit waits in steady state, whatever the CTA count, and no CTA
 // holds units of a generation before all of its units of the previous one
 // (deadlock-free with all CTAs resident).
+// Segment descriptors of the dynamic remainder (one launch per generation):
+// the producer warp takes unit ranges from a global cursor (guided: about
+// half of the remainder's fair share per CTA, at least 8 units, never past a
+// band's end) and hands each to the 15 other warps through this SMEM ring.
+// CTAs on slower SMs (measured: a few % longer per unit on some of them)
+// then take fewer units instead of finishing last.
+struct SegRing {
+  int4* e;
+  uint64_t* full;
+  uint64_t* empty;
+};
+
+template <bool kDyn>
 struct SegIter {
   int64_t u, u_end, U;  // remainder part: linear unit range of this CTA
   int32_t S, G, B0, round, rounds;
@@ -306,9 +328,21 @@ struct SegIter {
   // sweep (multi-generation) mode: global chunk index, this generation's end
   int64_t ci, c_base, c_end;
   int32_t C, B, gen;
-  __device__ SegIter(const Params& p, int gen_)
+  // dynamic remainder
+  uint32_t* dyn;
+  SegRing ring;
+  uint32_t seq;
+  bool producer;
+  uint32_t pend_u, pend_e;  // producer: the part of its last grab past a band's end
+  __device__ SegIter(const Params& p, int gen_, const SegRing& ring_ = SegRing{}, bool producer_ = false)
       : S(p.strips), G(static_cast<int32_t>(gridDim.x)), round(0), rotate(p.wrap_cols != 0),
-        C(p.gens > 1 ? p.sweep_chunks : 0), B(p.bands), gen(gen_) {
+        C(p.gens > 1 ? p.sweep_chunks : 0), B(p.bands), gen(gen_),
+        // (only after whole-band rounds: with none -- 8192^2, 16384^2 per launch --
+        // the all-dynamic order loses the rotated remainder's L2 locality:
+        // 34.0 -> 35.7 us; at 32768^2 345 -> 338 us, tools/gpu_r02au.sh)
+        dyn(!kDyn || p.gens > 1 || p.bands < static_cast<int32_t>(gridDim.x) ? nullptr : p.dyn),
+        ring(ring_), seq(0), producer(producer_),
+        pend_u(0), pend_e(0) {
     if (C > 0) {
       c_base = static_cast<int64_t>(gen) * B * C;
       c_end = c_base + static_cast<int64_t>(B) * C;
@@ -341,6 +375,9 @@ struct SegIter {
       t1 = S;
       return true;
     }
+    if constexpr (kDyn) {
+      if (dyn) return dyn_next(band, t0, t1);
+    }
     if (u >= u_end) return false;
     const int k = static_cast<int>(u / S);  // band within the remainder
     band = B0 + k;
@@ -356,6 +393,53 @@ struct SegIter {
       t0 += r;
       t1 += r;
     }
+    return true;
+  }
+  __device__ bool dyn_next(int& band, int& t0, int& t1) {
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t slot = seq % kSegSlots, par = (seq / kSegSlots) & 1;
+    ++seq;
+    int4 sg = make_int4(-1, 0, 0, 0);
+    if (producer) {
+      if (lane == 0) {
+        // one atomicAdd per grab (a CAS loop over 148 producers serialises),
+        // taken when the previous one is used up -- not earlier: a CTA that
+        // reserves its next range ahead of time keeps it while it is slow
+        // (measured: 347 vs 339 us at 32768^2).  A grab past a band's end is
+        // published as two segments.
+        const uint32_t total = static_cast<uint32_t>(U), su = static_cast<uint32_t>(S);
+        if (pend_u >= pend_e) {
+          const uint32_t c = *reinterpret_cast<volatile uint32_t*>(dyn);
+          const uint32_t rem = c < total ? total - c : 0u;
+          const uint32_t want = min(su, max(8u, rem / (2u * static_cast<uint32_t>(G))));
+          const uint32_t u0 = atomicAdd(dyn, want);
+          pend_u = min(u0, total);
+          pend_e = min(u0 + want, total);
+        }
+        if (pend_u < pend_e) {
+          const uint32_t e = min(pend_e, (pend_u / su + 1) * su);  // this band's part
+          sg = make_int4(B0 + static_cast<int>(pend_u / su), static_cast<int>(pend_u % su),
+                         static_cast<int>(pend_u % su + (e - pend_u)), 0);
+          pend_u = e;
+        }
+        mbar_wait(&ring.empty[slot], par ^ 1);
+        ring.e[slot] = sg;
+        mbar_arrive(&ring.full[slot]);
+      }
+      sg.x = __shfl_sync(0xffffffffu, sg.x, 0);
+      sg.y = __shfl_sync(0xffffffffu, sg.y, 0);
+      sg.z = __shfl_sync(0xffffffffu, sg.z, 0);
+    } else {
+      mbar_wait(&ring.full[slot], par);
+      const volatile int* ve = reinterpret_cast<const volatile int*>(&ring.e[slot]);
+      sg = make_int4(ve[0], ve[1], ve[2], 0);
+      __syncwarp(__activemask());
+      if (lane == 0) mbar_arrive(&ring.empty[slot]);
+    }
+    if (sg.x < 0) return false;
+    band = sg.x;
+    t0 = sg.y;
+    t1 = sg.z;
     return true;
   }
 };
@@ -396,7 +480,7 @@ __host__ __device__ constexpr int lane_x(int lane) {
   return kPk ? (lane & ~15) | ((lane & 7) << 1) | ((lane >> 3) & 1) : lane;
 }
 
-template <int kH, bool kChecked, bool kRing, bool kPk>
+template <int kH, bool kChecked, bool kRing, bool kPk, bool kDyn>
 __global__ void __launch_bounds__(kThreads, 1)
     ltl_tc_step_kernel(const __grid_constant__ TcMaps maps, const Params p) {
   using G = Geo<kH, kPk>;
@@ -428,6 +512,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   // two units ahead of output group 0 -- one "D2 written" barrier per slot
   uint64_t* d2_slot_full = st_empty + kSubs * kStageSlots;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(d2_slot_full + kSlots);
+  SegRing seg;
+  seg.e = reinterpret_cast<int4*>(smem + G::kSmemSeg);
+  seg.full = reinterpret_cast<uint64_t*>(smem + G::kSmemSeg + kSegSlots * 16);
+  seg.empty = seg.full + kSegSlots;
 
   const uint32_t warp = warp_id();
   const uint32_t lane = threadIdx.x & 31;
@@ -531,6 +619,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&st_full[i], 1);
       mbar_init(&st_empty[i], 1);
     }
+    if constexpr (kDyn) {
+      for (uint32_t i = 0; i < kSegSlots; ++i) {
+        mbar_init(&seg.full[i], 1);
+        mbar_init(&seg.empty[i], kSegReaders);
+      }
+    }
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc(tmem_slot, kTmemCols);
@@ -580,7 +674,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int gg = 0; gg < p.gens; ++gg) {
       const CUtensorMap* lm = maps.load[gg & 1];
       const uint32_t target = p.flag_base + 2u * static_cast<uint32_t>(gg);
-      SegIter it(p, gg);
+      SegIter<kDyn> it(p, gg, seg, true);
       int band, t0, t1;
       while (it.next(band, t0, t1)) {
         const bool edge_rows = p.wrap_rows || kRing;  // rows beyond the slab by piece loads
@@ -710,7 +804,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     auto box = [&](uint32_t idx) { return x_desc + (((idx % kXStages) * kBoxBytes) >> 4); };
     uint32_t g = 0, h = 0;
     for (int gg = 0; gg < p.gens; ++gg) {
-    SegIter it(p, gg);
+    SegIter<kDyn> it(p, gg, seg);
     int band, t0, t1;
     while (it.next(band, t0, t1)) {
       for (int t = t0; t < t1; ++t, ++h) {
@@ -758,7 +852,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t trow = tmem + ((q * 32) << 16);
     uint32_t max_h = 0, h = 0;
     for (int gg = 0; gg < p.gens; ++gg) {
-    SegIter it(p, gg);
+    SegIter<kDyn> it(p, gg, seg);
     int band, t0, t1;
     while (it.next(band, t0, t1)) {
       for (int t = t0; t < t1; ++t, ++h) {
@@ -859,7 +953,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int ti = vn ? nb : nb + 2;
     uint32_t h = 0;
     for (int gg = 0; gg < p.gens; ++gg) {
-    SegIter it(p, gg);
+    SegIter<kDyn> it(p, gg, seg);
     int band, t0, t1;
     while (it.next(band, t0, t1)) {
       for (int t = t0; t < t1; ++t, ++h) {
@@ -907,7 +1001,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t npend = 0, h = 0, n_open = 0;  // n_open: committed, slot not yet freed
       int open_slot[2] = {0, 0};
       for (int gg = 0; gg < p.gens; ++gg) {
-        SegIter it(p, gg);
+        SegIter<kDyn> it(p, gg, seg);
         int band, t0, t1;
         while (it.next(band, t0, t1)) {
           for (int t = t0; t < t1; ++t, ++h) {
@@ -1005,7 +1099,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     uint32_t h = 0;
     for (int gg = 0; gg < p.gens; ++gg) {
-    SegIter it(p, gg);
+    SegIter<kDyn> it(p, gg, seg);
     int band, t0, t1;
     while (it.next(band, t0, t1)) {
       for (int t = t0; t < t1; ++t, ++h) {
@@ -1142,6 +1236,17 @@ __global__ void __launch_bounds__(kThreads, 1)
       red_relaxed_add_sys(p.my_done, static_cast<uint32_t>(p.gens));  // generations completed
     }
   }
+  if (kDyn && p.dyn && p.gens == 1 && p.bands >= static_cast<int32_t>(gridDim.x) &&
+      threadIdx.x == 0) {
+    // every segment of this CTA has been taken: the launch's last CTA rearms
+    // the cursor for the next launch (which reads it after griddepcontrol.wait)
+    __threadfence();
+    if (atomicAdd(p.dyn + 1, 1u) + 1u == gridDim.x) {
+      p.dyn[0] = 0u;
+      p.dyn[1] = 0u;
+      __threadfence();
+    }
+  }
   if (warp == 1) tmem_dealloc(tmem, kTmemCols);
 }
 
@@ -1204,16 +1309,18 @@ cudaError_t launch_tc_step(const TcLaunch& a, cudaStream_t stream) {
       return cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(bytes));
     };
-    for (cudaError_t r : {set_smem(ltl_tc_step_kernel<16, false, false, false>, Geo<16>::kSmemAlloc),
-                          set_smem(ltl_tc_step_kernel<16, true, false, false>, Geo<16>::kSmemAlloc),
-                          set_smem(ltl_tc_step_kernel<16, false, true, false>, Geo<16>::kSmemAlloc),
-                          set_smem(ltl_tc_step_kernel<16, true, true, false>, Geo<16>::kSmemAlloc),
-                          set_smem(ltl_tc_step_kernel<32, false, false, false>, Geo<32>::kSmemAlloc),
-                          set_smem(ltl_tc_step_kernel<32, true, false, false>, Geo<32>::kSmemAlloc),
-                          set_smem(ltl_tc_step_kernel<32, false, true, false>, Geo<32>::kSmemAlloc),
-                          set_smem(ltl_tc_step_kernel<32, true, true, false>, Geo<32>::kSmemAlloc),
-                          set_smem(ltl_tc_step_kernel<16, false, false, true>, Geo<16, true>::kSmemAlloc),
-                          set_smem(ltl_tc_step_kernel<16, true, false, true>, Geo<16, true>::kSmemAlloc)})
+    for (cudaError_t r : {set_smem(ltl_tc_step_kernel<16, false, false, false, false>, Geo<16>::kSmemAlloc),
+                          set_smem(ltl_tc_step_kernel<16, true, false, false, false>, Geo<16>::kSmemAlloc),
+                          set_smem(ltl_tc_step_kernel<16, false, true, false, false>, Geo<16>::kSmemAlloc),
+                          set_smem(ltl_tc_step_kernel<16, true, true, false, false>, Geo<16>::kSmemAlloc),
+                          set_smem(ltl_tc_step_kernel<32, false, false, false, false>, Geo<32>::kSmemAlloc),
+                          set_smem(ltl_tc_step_kernel<32, true, false, false, false>, Geo<32>::kSmemAlloc),
+                          set_smem(ltl_tc_step_kernel<32, false, true, false, false>, Geo<32>::kSmemAlloc),
+                          set_smem(ltl_tc_step_kernel<32, true, true, false, false>, Geo<32>::kSmemAlloc),
+                          set_smem(ltl_tc_step_kernel<16, false, false, true, false>, Geo<16, true>::kSmemAlloc),
+                          set_smem(ltl_tc_step_kernel<16, true, false, true, false>, Geo<16, true>::kSmemAlloc),
+                          set_smem(ltl_tc_step_kernel<16, false, false, false, true>, Geo<16>::kSmemAlloc),
+                          set_smem(ltl_tc_step_kernel<16, true, false, false, true>, Geo<16>::kSmemAlloc)})
       if (r != cudaSuccess) return r;
     int sms = 0;
     e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -1260,6 +1367,7 @@ cudaError_t launch_tc_step(const TcLaunch& a, cudaStream_t stream) {
   p.flag_base = a.flag_base;
   p.stats = a.stats;
   p.trace = a.trace;
+  p.dyn = p.gens == 1 && !std::getenv("LTL_STATIC_SCHED") ? a.dyn : nullptr;  // env: A/B
   // One persistent CTA per SM over the units (fewer for small grids).
   const int64_t units = static_cast<int64_t>(p.bands) * p.strips;
   int64_t grid = units < num_sms ? units : num_sms;
@@ -1310,20 +1418,26 @@ cudaError_t launch_tc_step(const TcLaunch& a, cudaStream_t stream) {
   // the ring's peer-memory paths are compiled only into the ring kernels
   const bool st = a.stats != nullptr;
   if (a.packed)
-    return st ? cudaLaunchKernelEx(&cfg, ltl_tc_step_kernel<16, true, false, true>, maps, p)
-              : cudaLaunchKernelEx(&cfg, ltl_tc_step_kernel<16, false, false, true>, maps, p);
+    return st ? cudaLaunchKernelEx(&cfg, ltl_tc_step_kernel<16, true, false, true, false>, maps, p)
+              : cudaLaunchKernelEx(&cfg, ltl_tc_step_kernel<16, false, false, true, false>, maps, p);
   if (halo == 32) {
     if (p.ring)
-      return st ? cudaLaunchKernelEx(&cfg, ltl_tc_step_kernel<32, true, true, false>, maps, p)
-                : cudaLaunchKernelEx(&cfg, ltl_tc_step_kernel<32, false, true, false>, maps, p);
-    return st ? cudaLaunchKernelEx(&cfg, ltl_tc_step_kernel<32, true, false, false>, maps, p)
-              : cudaLaunchKernelEx(&cfg, ltl_tc_step_kernel<32, false, false, false>, maps, p);
+      return st ? cudaLaunchKernelEx(&cfg, ltl_tc_step_kernel<32, true, true, false, false>, maps, p)
+                : cudaLaunchKernelEx(&cfg, ltl_tc_step_kernel<32, false, true, false, false>, maps, p);
+    return st ? cudaLaunchKernelEx(&cfg, ltl_tc_step_kernel<32, true, false, false, false>, maps, p)
+              : cudaLaunchKernelEx(&cfg, ltl_tc_step_kernel<32, false, false, false, false>, maps, p);
   }
   if (p.ring)
-    return st ? cudaLaunchKernelEx(&cfg, ltl_tc_step_kernel<16, true, true, false>, maps, p)
-              : cudaLaunchKernelEx(&cfg, ltl_tc_step_kernel<16, false, true, false>, maps, p);
-  return st ? cudaLaunchKernelEx(&cfg, ltl_tc_step_kernel<16, true, false, false>, maps, p)
-            : cudaLaunchKernelEx(&cfg, ltl_tc_step_kernel<16, false, false, false>, maps, p);
+    return st ? cudaLaunchKernelEx(&cfg, ltl_tc_step_kernel<16, true, true, false, false>, maps, p)
+              : cudaLaunchKernelEx(&cfg, ltl_tc_step_kernel<16, false, true, false, false>, maps, p);
+  // the dynamic remainder schedule: u8 cells, one launch per generation with
+  // whole-band rounds (32768^2 345 -> 339 us; elsewhere it does not pay,
+  // tools/gpu_r02au/av.sh), compiled only into its own instantiations
+  if (p.dyn && p.gens == 1 && p.bands >= grid)
+    return st ? cudaLaunchKernelEx(&cfg, ltl_tc_step_kernel<16, true, false, false, true>, maps, p)
+              : cudaLaunchKernelEx(&cfg, ltl_tc_step_kernel<16, false, false, false, true>, maps, p);
+  return st ? cudaLaunchKernelEx(&cfg, ltl_tc_step_kernel<16, true, false, false, false>, maps, p)
+            : cudaLaunchKernelEx(&cfg, ltl_tc_step_kernel<16, false, false, false, false>, maps, p);
 }
 
 }  // namespace ltl
