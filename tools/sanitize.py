@@ -47,6 +47,14 @@ def main():
         t.init_random(0.4, 2)
         p = t.download_padded(ltl.LAYOUT_FRAGMENT)
         t.upload_padded(p, ltl.LAYOUT_FRAGMENT)
+    os.environ["LTL_TC_GRID"] = "3"  # 8 bands >= 3 CTAs: the dynamic remainder schedule
+    os.environ["LTL_NO_PERSIST"] = "1"
+    g = (np.random.default_rng(5).random((1024, 512)) < 0.3).astype(np.uint8)
+    with ltl.DeviceTorus(rows=1024, cols=512) as t:
+        t.upload(g)
+        t.run("R5,C2,M1,S34..58,B34..45,NM", 3)
+        assert np.array_equal(t.download(), orc.simulate(g, parse_rule_text("R5,C2,M1,S34..58,B34..45,NM"), 3))
+    del os.environ["LTL_TC_GRID"], os.environ["LTL_NO_PERSIST"]
     with ltl.DeviceTorus(n=2048) as t:  # bit-packed host <-> device transfers (>= 4 MB)
         g = (np.random.default_rng(9).random((2048, 2048)) < 0.3).astype(np.uint8)
         t.upload(g)
