@@ -367,3 +367,34 @@ def test_determinism_matrix(ltl, orc, kind, monkeypatch):
                 assert np.array_equal(got, expect), (kind, persist, grid, units)
                 if persist == "0":
                     break  # the chunk length only matters to the sweep
+
+
+@pytest.mark.parametrize("grid", ["3", "5", "7"])
+def test_dynamic_schedule_matches_static(ltl, orc, grid, monkeypatch):
+    """One launch per generation with whole-band rounds hands the remainder out
+    at run time (ltl_tc.cu SegIter<kDyn>); CTA counts that leave a remainder of
+    1..3 bands: the same bytes, H / R maxima and faulted grids as the static
+    schedule and the oracle."""
+    n, text = 1024, "R7,C2,M1,S60..140,B50..110,NM"
+    init = orc.init_random(n, 0.3, 4)
+    monkeypatch.setenv("LTL_NO_PERSIST", "1")
+    monkeypatch.setenv("LTL_TC_GRID", grid)
+    outs = []
+    for static in (False, True):
+        if static:
+            monkeypatch.setenv("LTL_STATIC_SCHED", "1")
+        with ltl.DeviceTorus(n=n) as t:
+            t.upload(init)
+            st = t.run(text, 3, stats=True)
+            got = t.download()
+            t.upload(init)
+            try:
+                t.run(text, 2, inject_fault=True)
+                faulted = t.download()
+            except ltl.LtlLogicError as e:
+                faulted = str(e)
+        outs.append((got, st["max_h"], st["max_r"], faulted))
+    assert np.array_equal(outs[0][0], orc.simulate(init, parse_rule_text(text), 3))
+    assert np.array_equal(outs[0][0], outs[1][0]) and outs[0][1:3] == outs[1][1:3]
+    f0, f1 = outs[0][3], outs[1][3]
+    assert (isinstance(f0, str) and f0 == f1) or np.array_equal(f0, f1)
