@@ -320,6 +320,12 @@ struct SegRing {
   uint64_t* empty;
 };
 
+#ifndef LTL_DYN_MIN  // dynamic remainder: smallest grab (units), fair-share divisor
+#define LTL_DYN_MIN 8
+#endif
+#ifndef LTL_DYN_DIV
+#define LTL_DYN_DIV 2
+#endif
 template <bool kDyn>
 struct SegIter {
   int64_t u, u_end, U;  // remainder part: linear unit range of this CTA
@@ -411,7 +417,9 @@ struct SegIter {
         if (pend_u >= pend_e) {
           const uint32_t c = *reinterpret_cast<volatile uint32_t*>(dyn);
           const uint32_t rem = c < total ? total - c : 0u;
-          const uint32_t want = min(su, max(8u, rem / (2u * static_cast<uint32_t>(G))));
+          const uint32_t want =
+              min(su, max(static_cast<uint32_t>(LTL_DYN_MIN),
+                          rem / (static_cast<uint32_t>(LTL_DYN_DIV) * static_cast<uint32_t>(G))));
           const uint32_t u0 = atomicAdd(dyn, want);
           pend_u = min(u0, total);
           pend_e = min(u0 + want, total);
