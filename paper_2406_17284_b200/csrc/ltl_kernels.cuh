@@ -235,6 +235,9 @@ cudaError_t launch_bits_to_cells(const uint8_t* bits, uint8_t* cells, int64_t n,
 // (*bad |= 1 if a byte is neither 0 nor 1)
 cudaError_t launch_cells_to_bits(const uint8_t* cells, uint8_t* bits, int64_t n, int32_t* bad,
                                  cudaStream_t stream);
+// bits (row-major, cols % 32 == 0) <-> the interior of a slab's strips.
+cudaError_t launch_bits_to_strips(const uint8_t* bits, const SlabView& s, cudaStream_t stream);
+cudaError_t launch_strips_to_bits(const SlabView& s, uint8_t* bits, int32_t* bad, cudaStream_t stream);
 // u8 slab <-> its 4-bit copy (every padded row of every strip).
 cudaError_t launch_pack_cells(const SlabView& s, const PackedView& pk, cudaStream_t stream);
 cudaError_t launch_unpack_cells(const PackedView& pk, const SlabView& s, cudaStream_t stream);

@@ -166,6 +166,43 @@ __global__ void cells_to_bits_kernel(const uint4* cells, uint32_t* bits, int64_t
   if (__syncthreads_or(acc != 0) && threadIdx.x == 0) atomicOr(bad, 1);
 }
 
+// The same straight between bits and the strips of a slab interior (cols %
+// 32 == 0: 32 cells of a row never straddle a strip), one word per thread:
+// uploads and downloads of dense interiors skip the dense staging pass.
+__global__ void bits_to_strips_kernel(const uint32_t* bits, SlabView s, int64_t words) {
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  const int64_t wpr = s.cols / 32;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < words; i += stride) {
+    const uint32_t w = bits[i];
+    uint32_t c[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) c[k] = (((w >> (4 * k)) & 0xFu) * 0x00204081u) & 0x01010101u;
+    const int y = static_cast<int>(i / wpr), x = 32 * static_cast<int>(i % wpr);
+    uint4* d = reinterpret_cast<uint4*>(s.buf + s.offset(y + kHalo, x));
+    d[0] = make_uint4(c[0], c[1], c[2], c[3]);
+    d[1] = make_uint4(c[4], c[5], c[6], c[7]);
+  }
+}
+__global__ void strips_to_bits_kernel(SlabView s, uint32_t* bits, int64_t words, int32_t* bad) {
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  const int64_t wpr = s.cols / 32;
+  uint32_t acc = 0;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < words; i += stride) {
+    const int y = static_cast<int>(i / wpr), x = 32 * static_cast<int>(i % wpr);
+    const uint4* src = reinterpret_cast<const uint4*>(s.buf + s.offset(y + kHalo, x));
+    const uint4 a = src[0], b = src[1];
+    const uint32_t c[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+    uint32_t w = 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      acc |= c[k] & 0xFEFEFEFEu;
+      w |= (((c[k] & 0x01010101u) * 0x01020408u) >> 24 & 0xFu) << (4 * k);
+    }
+    bits[i] = w;
+  }
+  if (__syncthreads_or(acc != 0) && threadIdx.x == 0) atomicOr(bad, 1);
+}
+
 int blocks_for(int64_t work) {
   int64_t b = (work + 255) / 256;
   if (b > 148 * 8) b = 148 * 8;
@@ -219,6 +256,24 @@ cudaError_t launch_cells_to_bits(const uint8_t* cells, uint8_t* bits, int64_t n,
   if (n % 32) return cudaErrorInvalidValue;
   cells_to_bits_kernel<<<blocks_for(n / 32), 256, 0, stream>>>(
       reinterpret_cast<const uint4*>(cells), reinterpret_cast<uint32_t*>(bits), n / 32, bad);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_bits_to_strips(const uint8_t* bits, const SlabView& s, cudaStream_t stream) {
+  if (s.rows <= 0 || s.cols <= 0) return cudaSuccess;
+  if (s.cols % 32) return cudaErrorInvalidValue;
+  const int64_t words = static_cast<int64_t>(s.rows) * (s.cols / 32);
+  bits_to_strips_kernel<<<blocks_for(words), 256, 0, stream>>>(reinterpret_cast<const uint32_t*>(bits), s,
+                                                               words);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_strips_to_bits(const SlabView& s, uint8_t* bits, int32_t* bad, cudaStream_t stream) {
+  if (s.rows <= 0 || s.cols <= 0) return cudaSuccess;
+  if (s.cols % 32) return cudaErrorInvalidValue;
+  const int64_t words = static_cast<int64_t>(s.rows) * (s.cols / 32);
+  strips_to_bits_kernel<<<blocks_for(words), 256, 0, stream>>>(s, reinterpret_cast<uint32_t*>(bits), words,
+                                                               bad);
   return cudaGetLastError();
 }
 

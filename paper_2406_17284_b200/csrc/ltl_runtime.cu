@@ -840,8 +840,10 @@ uint8_t* device_bits(ltl_ctx* ctx, size_t bytes) {
 }
 
 // false: a byte was not 0 / 1 (nothing usable written; copy bytes instead)
+// strips != nullptr: the bits go straight into that slab view's interior
+// (dense rows of the slab: row_bytes == its cols) instead of `dev`
 bool h2d_bits(ltl_ctx* ctx, uint8_t* dev, const uint8_t* host, int64_t nrows, size_t row_bytes,
-              size_t pitch, cudaStream_t st) {
+              size_t pitch, cudaStream_t st, const ltl::SlabView* strips = nullptr) {
   const size_t brow = row_bytes / 8;
   uint8_t* bits = device_bits(ctx, static_cast<size_t>(nrows) * brow);
   ensure_stage(ctx);
@@ -860,8 +862,10 @@ bool h2d_bits(ltl_ctx* ctx, uint8_t* dev, const uint8_t* host, int64_t nrows, si
     ctx->moved[0] += cnt * static_cast<int64_t>(brow);
     ck(cudaEventRecord(ev[k % 2], st), "event");
   }
-  if (ok) ck(ltl::launch_bits_to_cells(bits, dev, nrows * static_cast<int64_t>(row_bytes), st),
-             "bits -> cells");
+  if (ok && strips) ck(ltl::launch_bits_to_strips(bits, *strips, st), "bits -> strips");
+  else if (ok)
+    ck(ltl::launch_bits_to_cells(bits, dev, nrows * static_cast<int64_t>(row_bytes), st),
+       "bits -> cells");
   ck(cudaStreamSynchronize(st), "staging");
   for (auto& e : ev) cudaEventDestroy(e);
   return ok;
@@ -869,14 +873,16 @@ bool h2d_bits(ltl_ctx* ctx, uint8_t* dev, const uint8_t* host, int64_t nrows, si
 
 // false: a device byte was not 0 / 1 (nothing written; copy bytes instead)
 bool d2h_bits(ltl_ctx* ctx, uint8_t* host, const uint8_t* dev, int64_t nrows, size_t row_bytes,
-              size_t pitch, cudaStream_t st) {
+              size_t pitch, cudaStream_t st, const ltl::SlabView* strips = nullptr) {
   const size_t brow = row_bytes / 8;
   uint8_t* bits = device_bits(ctx, static_cast<size_t>(nrows) * brow);
   int32_t* dbad = reinterpret_cast<int32_t*>(bits + bits_flag_offset(static_cast<size_t>(nrows) * brow));
   ensure_stage(ctx);
   ck(cudaMemsetAsync(dbad, 0, sizeof(int32_t), st), "memset flag");
-  ck(ltl::launch_cells_to_bits(dev, bits, nrows * static_cast<int64_t>(row_bytes), dbad, st),
-     "cells -> bits");
+  if (strips) ck(ltl::launch_strips_to_bits(*strips, bits, dbad, st), "strips -> bits");
+  else
+    ck(ltl::launch_cells_to_bits(dev, bits, nrows * static_cast<int64_t>(row_bytes), dbad, st),
+       "cells -> bits");
   int32_t hbad = 0;
   ck(cudaMemcpyAsync(&hbad, dbad, sizeof hbad, cudaMemcpyDeviceToHost, st), "flag");
   ck(cudaStreamSynchronize(st), "flag");
@@ -1006,10 +1012,16 @@ void upload_interior(ltl_ctx* ctx, const uint8_t* interior) {
   for (Slab& s : ctx->slabs) {
     ck(cudaSetDevice(s.dev), "cudaSetDevice");
     if (s.rows == 0 || ctx->cols == 0) continue;
-    h2d_rows(ctx, s.buf[1 - cur], interior + static_cast<size_t>(s.host_row0) * ctx->cols, s.rows,
-             ctx->cols, ctx->cols, s.stream);
-    ck(ltl::launch_to_strips(s.buf[1 - cur], s.view(cur, ctx->cols), s.stream), "to_strips");
-    ++ctx->launches;
+    const uint8_t* src = interior + static_cast<size_t>(s.host_row0) * ctx->cols;
+    const ltl::SlabView v = s.view(cur, ctx->cols);
+    if (use_bits(s.rows, ctx->cols) &&
+        h2d_bits(ctx, nullptr, src, s.rows, ctx->cols, ctx->cols, s.stream, &v)) {
+      ++ctx->launches;     // bits -> strips
+    } else {
+      h2d_rows(ctx, s.buf[1 - cur], src, s.rows, ctx->cols, ctx->cols, s.stream);
+      ck(ltl::launch_to_strips(s.buf[1 - cur], v, s.stream), "to_strips");
+      ++ctx->launches;
+    }
     if (ctx->slabs.size() > 1) ck(cudaEventRecord(s.ev_step, s.stream), "event");
   }
   enqueue_halo(ctx, cur);
@@ -1024,10 +1036,17 @@ void download_interior(ltl_ctx* ctx, uint8_t* interior) {
     ck(cudaSetDevice(s.dev), "cudaSetDevice");
     if (s.rows == 0 || ctx->cols == 0) continue;
     const size_t n = static_cast<size_t>(s.rows) * ctx->cols;
-    ck(ltl::launch_from_strips(s.view(cur, ctx->cols), s.buf[1 - cur], s.stream), "from_strips");
+    uint8_t* dst = interior + static_cast<size_t>(s.host_row0) * ctx->cols;
+    const ltl::SlabView v = s.view(cur, ctx->cols);
+    if (use_bits(s.rows, ctx->cols) &&
+        d2h_bits(ctx, dst, nullptr, s.rows, ctx->cols, ctx->cols, s.stream, &v)) {
+      ++ctx->launches;  // strips -> bits
+      continue;
+    }
+    ck(ltl::launch_from_strips(v, s.buf[1 - cur], s.stream), "from_strips");
     ++ctx->launches;
-    d2h_rows(ctx, interior + static_cast<size_t>(s.host_row0) * ctx->cols, s.buf[1 - cur],
-             static_cast<int64_t>(n / ctx->cols), ctx->cols, ctx->cols, s.stream);
+    d2h_rows(ctx, dst, s.buf[1 - cur], static_cast<int64_t>(n / ctx->cols), ctx->cols, ctx->cols,
+             s.stream);
   }
   sync_all(ctx);
 }
