@@ -53,7 +53,9 @@
 //
 // One CTA per SM (all 512 TMEM columns), 16 warps:
 //   warp 0        TMA producer (+ unit flags of multi-generation launches,
-//                 ring counters of slabs)
+//                 ring counters of slabs, the run-time remainder schedule of
+//                 the kDyn instantiations: it takes unit ranges from a global
+//                 cursor and hands them to the other warps, SegIter)
 //   warp 1        pass-1 MMA issuer, TMEM owner
 //   warps 2..5    convert D1 (warp w: TMEM lane quarter w%4 = 32 strip columns)
 //   warps 6..13   rule + stage D2: group g = 0 / 1 takes sub-block g of every unit
@@ -61,8 +63,10 @@
 //   warp 15       TMA stores, unit publication (multi-generation launches)
 // Every stage hands over through mbarrier rings, so TMA, both MMA passes and
 // both epilogue groups overlap across sub-blocks and units.  Measured limit
-// (DESIGN.md §6): this on-SM pipeline, ~1400 cycles per unit, just above the
-// HBM time of a unit.
+// (DESIGN.md §3.1): ~1450 cycles per unit, where the kernel's instruction
+// issue (~4000 warp instructions per unit at IPC ~2.6) and its HBM share at
+// 2 B/cell coincide.  kPk: the same step on 4-bit cells (pass 1 on
+// kind::f8f6f4).
 #include <cuda.h>
 #include <cuda_runtime.h>
 
